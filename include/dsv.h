@@ -1,0 +1,114 @@
+/*
+ * dsv.h — C ABI of the B200-native DSV dynamic-sparsity attention path.
+ *
+ * Every entry point is `extern "C"`, takes plain device pointers, element
+ * strides and a cudaStream_t (as void*), launches asynchronously on that
+ * stream and returns an int status (DSV_OK or DSV_E*). Nothing here allocates
+ * device memory or throws; callers own every buffer. Pointers are device
+ * pointers unless stated otherwise.
+ *
+ * Reference interfaces replaced (reference = /root/reference/pkg/src/dynsparse):
+ *   dsv_project          predictor.py:94-100   project(x, w)            (X W, both sides, all heads)
+ *   dsv_gemm_bf16        predictor.py:238-239  + selection.py:149 tile product (tcgen05 GEMM)
+ *   dsv_scores_f32       selection.py:149/204/222 q_lr @ k_lr.T (fp32, small inner width)
+ *   dsv_topk             selection.py:118-175  streaming_topk / :178-242 twopass_select
+ *                        (exact top-k, ties -> lower index, ascending emit, k-th threshold)
+ *   dsv_sparse_fwd       attention.py:153-187  sparse_attention (uniform/group-shared sets)
+ *                        grouping.py:196-216   grouped_sparse_attention
+ *   dsv_sparse_bwd       trainer.py:110-117    autograd of the sparse attention (dQ, dK, dV)
+ *   dsv_rows_fwd/_bwd    attention.py:176-183  ragged per-query index sets (CSR)
+ *   dsv_gather_rows      cpsim.py:147-156/195-216 pack/unpack of head slices and KV rows
+ */
+#ifndef DSV_H_
+#define DSV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DSV_OK 0
+#define DSV_EINVAL 1       /* invalid argument: shape, k outside [1, L], alignment      */
+#define DSV_EUNSUPPORTED 2 /* outside the kernels' envelope (e.g. head dim not 64/128) */
+#define DSV_ECUDA 3        /* CUDA runtime / launch failure                             */
+
+#define DSV_DTYPE_F32 0
+#define DSV_DTYPE_BF16 1
+
+/* Library version (major*10000 + minor*100 + patch) and last error text (thread-local). */
+int dsv_version(void);
+const char* dsv_last_error(void);
+
+/* Number of streaming multiprocessors of the current device (0 if none). */
+int dsv_device_sm_count(void);
+
+/* C[b] = A[b] . B[b]^T on tcgen05 (bf16 in, fp32 accumulate).
+ * A: [nbatch][M][K] bf16, row stride lda (elements), batch stride a_bs;
+ * B: [nbatch][N][K] bf16, row stride ldb, batch stride b_bs;
+ * C: [nbatch][M][N], dtype DSV_DTYPE_F32 or DSV_DTYPE_BF16, row stride ldc, batch stride c_bs.
+ * Strides in bytes must be multiples of 16; K is zero-padded to 64 internally. */
+int dsv_gemm_bf16(const void* A, long long lda, long long a_bs, const void* B, long long ldb,
+                  long long b_bs, void* C, int c_dtype, long long ldc, long long c_bs,
+                  int M, int N, int K, int nbatch, void* stream);
+
+/* Predictor projection (K1a): out[L][n_out] = X[L][d_model] . Wt[n_out][d_model]^T, bf16.
+ * Wt stacks the per-head W_q^T then W_k^T rows: row (side*H + h)*r + j. */
+int dsv_project(const void* X, const void* Wt, void* out, int L, int d_model, int n_out,
+                void* stream);
+
+/* fp32 scores C[b][i][j] = sum_t A[b][i][t] * B[b][j][t] (t < r <= 64), deterministic
+ * fmaf order t = 0..r-1. a_dtype: DSV_DTYPE_F32 or DSV_DTYPE_BF16 (for both A and B). */
+int dsv_scores_f32(const void* A, long long lda, long long a_bs, const void* B, long long ldb,
+                   long long b_bs, float* C, long long ldc, long long c_bs, int nbatch, int R,
+                   int Lk, int r, int in_dtype, void* stream);
+
+/* Exact top-k per row of an fp32 score matrix (K2).
+ * scores: [rows][ld] fp32; row r uses k = k_per_head[r / rows_per_head] (1 <= k <= L).
+ * out_idx: [rows][out_ld] int32 ascending column ids (first k entries written);
+ * out_thr: [rows] fp32 k-th largest score. Ties at the threshold keep lower ids;
+ * -0.0 == +0.0. */
+int dsv_topk(const float* scores, long long ld, int rows, int L, const int* k_per_head,
+             int rows_per_head, int* out_idx, long long out_ld, float* out_thr, void* stream);
+
+/* Group-tiled sparse attention forward (K3f), bf16, head dim D in {64, 128}.
+ * q: [H][Lq][D], k, v: [H][Lk][D]; grp_rows: [G][128] int32 member token ids (entries past
+ * grp_size[g] repeat a member); idx: [H][G][ldk] int32 ascending key ids, kcount[H] valid
+ * per head (1..ldk). out: [H][Lq][D] bf16; lse: [H][Lq] fp32, log2 domain of the scaled
+ * logits. flags bit0: keep P in shared memory instead of TMEM. */
+int dsv_sparse_fwd(const void* q, const void* k, const void* v, const int* grp_rows,
+                   const int* grp_size, const int* idx, long long ldk, const int* kcount, int H,
+                   int G, int Lq, int Lk, int D, float scale, void* out, float* lse, int flags,
+                   void* stream);
+
+/* Backward (K3b). dout: [H][Lq][D] bf16, out/lse from dsv_sparse_fwd. dq: [H][Lq][D] bf16
+ * (every query of a group is written); dk_acc, dv_acc: [H][Lk][D] fp32 accumulators that the
+ * caller zeroes; contributions are added atomically. */
+int dsv_sparse_bwd(const void* q, const void* k, const void* v, const void* out,
+                   const void* dout, const float* lse, const int* grp_rows, const int* grp_size,
+                   const int* idx, long long ldk, const int* kcount, int H, int G, int Lq, int Lk,
+                   int D, float scale, void* dq, float* dk_acc, float* dv_acc, void* stream);
+
+/* Ragged per-(head, query) CSR sparse attention on CUDA cores (fp32 math), any D <= 256.
+ * ptr: [H*Lq + 1] int64 offsets into cols (int32 key ids). out: [H][Lq][D] fp32,
+ * lse: [H][Lq] fp32 natural log of the scaled logits. in_dtype: F32 or BF16 (q/k/v/dout). */
+int dsv_rows_fwd(const void* q, const void* k, const void* v, const long long* ptr,
+                 const int* cols, int H, int Lq, int Lk, int D, float scale, int in_dtype,
+                 float* out, float* lse, void* stream);
+int dsv_rows_bwd(const void* q, const void* k, const void* v, const float* out, const float* lse,
+                 const void* dout, const long long* ptr, const int* cols, int H, int Lq, int Lk,
+                 int D, float scale, int in_dtype, float* dq, float* dk_acc, float* dv_acc,
+                 void* stream);
+
+/* out[i] = src[rows[i]] for n rows of row_bytes bytes (row strides in bytes, multiples of 4). */
+int dsv_gather_rows(const void* src, long long src_stride, const int* rows, int n,
+                    int row_bytes, void* out, long long out_stride, void* stream);
+
+/* fp32 -> bf16 conversion of n contiguous elements. */
+int dsv_f32_to_bf16(const float* in, void* out, long long n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DSV_H_ */

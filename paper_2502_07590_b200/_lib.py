@@ -1,0 +1,93 @@
+"""ctypes binding of libdsv.so (the C ABI in include/dsv.h).
+
+The shared library is the product: every hot-path call goes through it. There
+is no CPU fallback — if the library is missing or no CUDA device is present,
+the calls raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import c_float, c_int, c_longlong, c_void_p
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libdsv.so"
+
+DSV_OK, DSV_EINVAL, DSV_EUNSUPPORTED, DSV_ECUDA = 0, 1, 2, 3
+DTYPE_F32, DTYPE_BF16 = 0, 1
+
+# name -> argtypes (restype is int unless listed in _RESTYPES)
+SIGNATURES = {
+    "dsv_version": [],
+    "dsv_last_error": [],
+    "dsv_device_sm_count": [],
+    "dsv_gemm_bf16": [c_void_p, c_longlong, c_longlong, c_void_p, c_longlong, c_longlong,
+                      c_void_p, c_int, c_longlong, c_longlong, c_int, c_int, c_int, c_int,
+                      c_void_p],
+    "dsv_project": [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p],
+    "dsv_scores_f32": [c_void_p, c_longlong, c_longlong, c_void_p, c_longlong, c_longlong,
+                       c_void_p, c_longlong, c_longlong, c_int, c_int, c_int, c_int, c_int,
+                       c_void_p],
+    "dsv_topk": [c_void_p, c_longlong, c_int, c_int, c_void_p, c_int, c_void_p, c_longlong,
+                 c_void_p, c_void_p],
+    "dsv_sparse_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_longlong,
+                       c_void_p, c_int, c_int, c_int, c_int, c_int, c_float, c_void_p, c_void_p,
+                       c_int, c_void_p],
+    "dsv_sparse_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                       c_void_p, c_void_p, c_longlong, c_void_p, c_int, c_int, c_int, c_int,
+                       c_int, c_float, c_void_p, c_void_p, c_void_p, c_void_p],
+    "dsv_rows_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int,
+                     c_int, c_float, c_int, c_void_p, c_void_p, c_void_p],
+    "dsv_rows_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                     c_void_p, c_int, c_int, c_int, c_int, c_float, c_int, c_void_p, c_void_p,
+                     c_void_p, c_void_p],
+    "dsv_gather_rows": [c_void_p, c_longlong, c_void_p, c_int, c_int, c_void_p, c_longlong,
+                        c_void_p],
+    "dsv_f32_to_bf16": [c_void_p, c_void_p, c_longlong, c_void_p],
+}
+_RESTYPES = {"dsv_last_error": ctypes.c_char_p}
+
+_lib = None
+
+
+class DSVError(RuntimeError):
+    """A CUDA-side failure reported by libdsv (status DSV_ECUDA / DSV_EUNSUPPORTED)."""
+
+
+def load(build_if_missing: bool = True) -> ctypes.CDLL:
+    """Load (building first if needed and possible) the in-tree libdsv.so."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if build_if_missing and os.environ.get("DSV_NO_BUILD") != "1":
+        from . import build as _build
+        try:
+            if not _build.up_to_date():
+                _build.build()
+        except RuntimeError:
+            if not LIB_PATH.exists():
+                raise
+    if not LIB_PATH.exists():
+        raise DSVError(f"{LIB_PATH} is missing: build it with `python -m paper_2502_07590_b200.build`")
+    lib = ctypes.CDLL(str(LIB_PATH))
+    for name, args in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = _RESTYPES.get(name, c_int)
+    _lib = lib
+    return lib
+
+
+def check(status: int, what: str) -> None:
+    if status == DSV_OK:
+        return
+    msg = load().dsv_last_error().decode(errors="replace")
+    if status == DSV_EINVAL:
+        raise ValueError(f"{what}: {msg}")
+    raise DSVError(f"{what} failed (status {status}): {msg}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)

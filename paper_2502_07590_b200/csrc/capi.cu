@@ -1,0 +1,259 @@
+// capi.cu — the extern "C" boundary (include/dsv.h): argument validation, TMA
+// descriptor encoding and kernel dispatch. No allocation, no exceptions.
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/dsv.h"
+#include "dsv_common.cuh"
+
+// kernels (defined in the other translation units)
+size_t dsv_topk_smem_bytes(int L);
+int dsv_topk_launch(const float*, long long, int, int, const int*, int, int*, long long, float*,
+                    cudaStream_t);
+int dsv_scores_f32_launch(const void*, long long, long long, const void*, long long, long long,
+                          float*, long long, long long, int, int, int, int, int, cudaStream_t);
+int dsv_rows_fwd_launch(const void*, const void*, const void*, const long long*, const int*, int,
+                        int, int, int, float, int, float*, float*, cudaStream_t);
+int dsv_rows_bwd_launch(const void*, const void*, const void*, const float*, const float*,
+                        const void*, const long long*, const int*, int, int, int, int, float, int,
+                        float*, float*, float*, cudaStream_t);
+int dsv_gemm_launch(const CUtensorMap*, const CUtensorMap*, void*, int, int, int, long long,
+                    long long, int, int, int, cudaStream_t);
+int dsv_attn_fwd_tc_launch(const CUtensorMap*, const CUtensorMap*, const CUtensorMap*, const int*,
+                           const int*, const int*, long long, const int*, int, int, int, int, int,
+                           float, int, void*, float*, cudaStream_t);
+int dsv_attn_bwd_tc_launch(const CUtensorMap*, const CUtensorMap*, const CUtensorMap*,
+                           const CUtensorMap*, const void*, const void*, const float*, const int*,
+                           const int*, const int*, long long, const int*, int, int, int, int, int,
+                           float, float, void*, float*, float*, cudaStream_t);
+int dsv_f32_to_bf16_launch(const float*, void*, long long, cudaStream_t);
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_status(int rc, const char* what) {
+  if (rc == 0) return DSV_OK;
+  return fail(DSV_ECUDA, "%s: %s", what, cudaGetErrorString((cudaError_t)rc));
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// bf16 tensor map with up to 3 dims: dims[0] innermost (elements), strides in bytes for
+// dims 1..rank-1, 128B swizzle.
+bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
+              const uint64_t* strides_bytes, const uint32_t* box) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t gd[5];
+  cuuint64_t gs[4];
+  cuuint32_t bx[5], es[5];
+  for (int i = 0; i < rank; ++i) { gd[i] = dims[i]; bx[i] = box[i]; es[i] = 1; }
+  for (int i = 0; i + 1 < rank; ++i) gs[i] = strides_bytes[i];
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), gd, gs, bx,
+                  es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// Row-gather map over a [rows][D] bf16 matrix (contiguous rows): box = 64 columns x 1 row.
+bool make_gather_map(CUtensorMap* m, const void* base, long long rows, int D) {
+  const uint64_t dims[2] = {(uint64_t)D, (uint64_t)rows};
+  const uint64_t strides[1] = {(uint64_t)D * 2};
+  const uint32_t box[2] = {64, 1};
+  return make_map(m, base, 2, dims, strides, box);
+}
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+int dsv_version(void) { return 100; }
+const char* dsv_last_error(void) { return g_err; }
+
+int dsv_device_sm_count(void) {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  return n;
+}
+
+int dsv_gemm_bf16(const void* A, long long lda, long long a_bs, const void* B, long long ldb,
+                  long long b_bs, void* C, int c_dtype, long long ldc, long long c_bs, int M,
+                  int N, int K, int nbatch, void* stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || nbatch <= 0) return fail(DSV_EINVAL, "gemm: empty shape");
+  if (!al16(A) || !al16(B)) return fail(DSV_EINVAL, "gemm: operands must be 16-byte aligned");
+  if ((lda * 2) % 16 || (ldb * 2) % 16 || (a_bs * 2) % 16 || (b_bs * 2) % 16)
+    return fail(DSV_EINVAL, "gemm: operand strides must be multiples of 16 bytes");
+  if (c_dtype != DSV_DTYPE_F32 && c_dtype != DSV_DTYPE_BF16)
+    return fail(DSV_EINVAL, "gemm: bad output dtype");
+  const int bn = N >= 256 ? 256 : 128;
+  CUtensorMap ta, tb;
+  {
+    const uint64_t dims[3] = {(uint64_t)K, (uint64_t)M, (uint64_t)nbatch};
+    const uint64_t st[2] = {(uint64_t)lda * 2, (uint64_t)(nbatch > 1 ? a_bs : (long long)M * lda) * 2};
+    const uint32_t box[3] = {64, 128, 1};
+    if (!make_map(&ta, A, 3, dims, st, box)) return fail(DSV_EINVAL, "gemm: tensor map A");
+  }
+  {
+    const uint64_t dims[3] = {(uint64_t)K, (uint64_t)N, (uint64_t)nbatch};
+    const uint64_t st[2] = {(uint64_t)ldb * 2, (uint64_t)(nbatch > 1 ? b_bs : (long long)N * ldb) * 2};
+    const uint32_t box[3] = {64, (uint32_t)bn, 1};
+    if (!make_map(&tb, B, 3, dims, st, box)) return fail(DSV_EINVAL, "gemm: tensor map B");
+  }
+  return cuda_status(dsv_gemm_launch(&ta, &tb, C, M, N, K, ldc, c_bs, nbatch,
+                                     c_dtype == DSV_DTYPE_F32, bn, S(stream)),
+                     "gemm launch");
+}
+
+int dsv_project(const void* X, const void* Wt, void* out, int L, int d_model, int n_out,
+                void* stream) {
+  if (L <= 0 || d_model <= 0 || n_out <= 0) return fail(DSV_EINVAL, "project: empty shape");
+  return dsv_gemm_bf16(X, d_model, 0, Wt, d_model, 0, out, DSV_DTYPE_BF16, n_out, 0, L, n_out,
+                       d_model, 1, stream);
+}
+
+int dsv_scores_f32(const void* A, long long lda, long long a_bs, const void* B, long long ldb,
+                   long long b_bs, float* C, long long ldc, long long c_bs, int nbatch, int R,
+                   int Lk, int r, int in_dtype, void* stream) {
+  if (R <= 0 || Lk <= 0 || nbatch <= 0) return fail(DSV_EINVAL, "scores: empty shape");
+  if (r < 1 || r > 64) return fail(DSV_EUNSUPPORTED, "scores: inner width %d outside [1, 64]", r);
+  return cuda_status(dsv_scores_f32_launch(A, lda, a_bs, B, ldb, b_bs, C, ldc, c_bs, nbatch, R,
+                                           Lk, r, in_dtype == DSV_DTYPE_BF16, S(stream)),
+                     "scores launch");
+}
+
+int dsv_topk(const float* scores, long long ld, int rows, int L, const int* k_per_head,
+             int rows_per_head, int* out_idx, long long out_ld, float* out_thr, void* stream) {
+  if (rows < 0 || L < 1 || rows_per_head < 1) return fail(DSV_EINVAL, "topk: bad shape");
+  if (ld < L) return fail(DSV_EINVAL, "topk: row stride %lld < L=%d", ld, L);
+  return cuda_status(dsv_topk_launch(scores, ld, rows, L, k_per_head, rows_per_head, out_idx,
+                                     out_ld, out_thr, S(stream)),
+                     "topk launch");
+}
+
+int dsv_sparse_fwd(const void* q, const void* k, const void* v, const int* grp_rows,
+                   const int* grp_size, const int* idx, long long ldk, const int* kcount, int H,
+                   int G, int Lq, int Lk, int D, float scale, void* out, float* lse, int flags,
+                   void* stream) {
+  if (D != 64 && D != 128) return fail(DSV_EUNSUPPORTED, "sparse_fwd: head dim %d not 64/128", D);
+  if (H <= 0 || G <= 0 || Lq <= 0 || Lk <= 0 || ldk <= 0)
+    return fail(DSV_EINVAL, "sparse_fwd: empty shape");
+  if (!al16(q) || !al16(k) || !al16(v) || !al16(out) || !al16(grp_rows))
+    return fail(DSV_EINVAL, "sparse_fwd: pointers must be 16-byte aligned");
+  CUtensorMap tq, tk, tv;
+  if (!make_gather_map(&tq, q, (long long)H * Lq, D) || !make_gather_map(&tk, k, (long long)H * Lk, D) ||
+      !make_gather_map(&tv, v, (long long)H * Lk, D))
+    return fail(DSV_ECUDA, "sparse_fwd: tensor map encode failed");
+  const float scale_log2 = scale * 1.4426950408889634f;
+  return cuda_status(dsv_attn_fwd_tc_launch(&tq, &tk, &tv, grp_rows, grp_size, idx, ldk, kcount,
+                                            H, G, Lq, Lk, D, scale_log2, (flags & 1) ? 0 : 1,
+                                            out, lse, S(stream)),
+                     "sparse_fwd launch");
+}
+
+int dsv_sparse_bwd(const void* q, const void* k, const void* v, const void* out,
+                   const void* dout, const float* lse, const int* grp_rows, const int* grp_size,
+                   const int* idx, long long ldk, const int* kcount, int H, int G, int Lq, int Lk,
+                   int D, float scale, void* dq, float* dk_acc, float* dv_acc, void* stream) {
+  if (D != 64 && D != 128) return fail(DSV_EUNSUPPORTED, "sparse_bwd: head dim %d not 64/128", D);
+  if (H <= 0 || G <= 0 || Lq <= 0 || Lk <= 0 || ldk <= 0)
+    return fail(DSV_EINVAL, "sparse_bwd: empty shape");
+  if (!al16(q) || !al16(k) || !al16(v) || !al16(out) || !al16(dout) || !al16(dq) ||
+      !al16(dk_acc) || !al16(dv_acc) || !al16(grp_rows))
+    return fail(DSV_EINVAL, "sparse_bwd: pointers must be 16-byte aligned");
+  CUtensorMap tq, tdo, tk, tv;
+  if (!make_gather_map(&tq, q, (long long)H * Lq, D) ||
+      !make_gather_map(&tdo, dout, (long long)H * Lq, D) ||
+      !make_gather_map(&tk, k, (long long)H * Lk, D) || !make_gather_map(&tv, v, (long long)H * Lk, D))
+    return fail(DSV_ECUDA, "sparse_bwd: tensor map encode failed");
+  const float scale_log2 = scale * 1.4426950408889634f;
+  return cuda_status(dsv_attn_bwd_tc_launch(&tq, &tdo, &tk, &tv, out, dout, lse, grp_rows,
+                                            grp_size, idx, ldk, kcount, H, G, Lq, Lk, D, scale,
+                                            scale_log2, dq, dk_acc, dv_acc, S(stream)),
+                     "sparse_bwd launch");
+}
+
+int dsv_rows_fwd(const void* q, const void* k, const void* v, const long long* ptr,
+                 const int* cols, int H, int Lq, int Lk, int D, float scale, int in_dtype,
+                 float* out, float* lse, void* stream) {
+  if (D < 1 || D > 256) return fail(DSV_EUNSUPPORTED, "rows_fwd: head dim %d outside [1, 256]", D);
+  if (H <= 0 || Lq <= 0 || Lk <= 0) return fail(DSV_EINVAL, "rows_fwd: empty shape");
+  return cuda_status(dsv_rows_fwd_launch(q, k, v, ptr, cols, H, Lq, Lk, D, scale,
+                                         in_dtype == DSV_DTYPE_BF16, out, lse, S(stream)),
+                     "rows_fwd launch");
+}
+
+int dsv_rows_bwd(const void* q, const void* k, const void* v, const float* out, const float* lse,
+                 const void* dout, const long long* ptr, const int* cols, int H, int Lq, int Lk,
+                 int D, float scale, int in_dtype, float* dq, float* dk_acc, float* dv_acc,
+                 void* stream) {
+  if (D < 1 || D > 256) return fail(DSV_EUNSUPPORTED, "rows_bwd: head dim %d outside [1, 256]", D);
+  if (H <= 0 || Lq <= 0 || Lk <= 0) return fail(DSV_EINVAL, "rows_bwd: empty shape");
+  return cuda_status(dsv_rows_bwd_launch(q, k, v, out, lse, dout, ptr, cols, H, Lq, Lk, D, scale,
+                                         in_dtype == DSV_DTYPE_BF16, dq, dk_acc, dv_acc, S(stream)),
+                     "rows_bwd launch");
+}
+
+int dsv_f32_to_bf16(const float* in, void* out, long long n, void* stream) {
+  return cuda_status(dsv_f32_to_bf16_launch(in, out, n, S(stream)), "f32_to_bf16 launch");
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ gather rows
+namespace {
+__global__ void gather_rows_kernel(const uint8_t* __restrict__ src, long long sstride,
+                                   const int* __restrict__ rows, int n, int words,
+                                   uint8_t* __restrict__ out, long long ostride) {
+  const int i = blockIdx.x;
+  if (i >= n) return;
+  const uint32_t* s = reinterpret_cast<const uint32_t*>(src + (long long)rows[i] * sstride);
+  uint32_t* o = reinterpret_cast<uint32_t*>(out + (long long)i * ostride);
+  for (int w = threadIdx.x; w < words; w += blockDim.x) o[w] = s[w];
+}
+}  // namespace
+
+extern "C" int dsv_gather_rows(const void* src, long long src_stride, const int* rows, int n,
+                               int row_bytes, void* out, long long out_stride, void* stream) {
+  if (n <= 0) return DSV_OK;
+  if (row_bytes % 4 || src_stride % 4 || out_stride % 4)
+    return fail(DSV_EINVAL, "gather_rows: byte sizes must be multiples of 4");
+  gather_rows_kernel<<<n, 128, 0, S(stream)>>>((const uint8_t*)src, src_stride, rows, n,
+                                               row_bytes / 4, (uint8_t*)out, out_stride);
+  return cuda_status((int)cudaGetLastError(), "gather_rows launch");
+}

@@ -1,0 +1,171 @@
+// gemm_tc.cu — K1: tcgen05/TMEM GEMM for the low-rank predictor.
+//
+//   C[b, m, n] = sum_k A[b, m, k] * B[b, n, k]     (bf16 in, fp32 accumulate)
+//
+// Used twice on the hot path:
+//  * K1a projection  X[L, H*d] . Wt[2*r*H, H*d]^T -> [Q_lr | K_lr] (reference
+//    pkg/src/dynsparse/predictor.py:94-100 `project`, applied at :238-239 for
+//    both W_q and W_k, batched over all heads in one GEMM);
+//  * K1b proxy scores Q_lr[proxies] . K_lr^T per head (K = r = 16; reference
+//    pkg/src/dynsparse/selection.py:149), fp32 out for K2.
+//
+// Structure: one 128 x BN output tile per CTA; warp 0 (one elected lane) is the
+// TMA producer over a STAGES-deep ring of 128B-swizzled K-major A/B tiles,
+// warp 1 (one elected lane) issues tcgen05.mma (M=128, N=BN, K=16) into a TMEM
+// accumulator, then all four warps drain TMEM (tcgen05.ld 32x32b) and store.
+
+#include <cuda.h>
+#include "dsv_common.cuh"
+
+namespace dsv {
+namespace gemm {
+
+constexpr int BM = 128, BK = 64;
+
+template <int BN, int STAGES>
+struct SmemLayout {
+  static constexpr int kA = BM * BK * 2;
+  static constexpr int kB = BN * BK * 2;
+  static constexpr int kStage = kA + kB;
+  static constexpr int kBytes = STAGES * kStage + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int BN, int STAGES, bool kF32Out>
+__global__ void __launch_bounds__(128, 1)
+gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+            void* __restrict__ C, int M, int N, int K, long long ldc, long long c_bs) {
+  using SL = SmemLayout<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SL::kStage);
+  uint64_t* empty = full + STAGES;
+  uint64_t* accum = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN, b = blockIdx.z;
+  const int nk = (K + BK - 1) / BK;
+  constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      prefetch_tmap(&tmA);
+      prefetch_tmap(&tmB);
+      for (int s = 0; s < STAGES; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
+      mbar_init(accum, 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    tmem_alloc(tmem_slot, kTmemCols);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (kb / STAGES) & 1;
+      mbar_wait(empty + s, ph ^ 1);
+      uint8_t* sa = smem + s * SL::kStage;
+      uint8_t* sb = sa + SL::kA;
+      mbar_arrive_expect_tx(full + s, SL::kStage);
+      tma_load_3d(sa, &tmA, full + s, kb * BK, m0, b);
+      tma_load_3d(sb, &tmB, full + s, kb * BK, n0, b);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, 0, 0);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (kb / STAGES) & 1;
+      mbar_wait(full + s, ph);
+      tc_fence_after();
+      const uint32_t sa = smem_u32(smem + s * SL::kStage);
+      const uint32_t sb = sa + SL::kA;
+#pragma unroll
+      for (int kk = 0; kk < BK / 16; ++kk) {
+        const uint64_t ad = sdesc_sw128(sa + kk * 32, 16, 1024);
+        const uint64_t bd = sdesc_sw128(sb + kk * 32, 16, 1024);
+        mma_ss(tmem, ad, bd, idesc, (kb | kk) != 0);
+      }
+      mma_commit(empty + s);
+    }
+    mma_commit(accum);
+  }
+  __syncwarp();
+
+  // ---------------- epilogue: TMEM -> registers -> global
+  mbar_wait(accum, 0);
+  tc_fence_after();
+  const int row = m0 + warp * 32 + lane;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  const bool vec_ok = kF32Out ? ((ldc & 3) == 0) : ((ldc & 7) == 0);
+#pragma unroll 1
+  for (int c = 0; c < BN; c += 32) {
+    uint32_t r[32];
+    tmem_ld32(trow + c, r);
+    tmem_ld_wait();
+    if (row >= M) continue;
+    const int col = n0 + c;
+    if constexpr (kF32Out) {
+      float* out = reinterpret_cast<float*>(C) + (long long)b * c_bs + (long long)row * ldc + col;
+      if (vec_ok && col + 32 <= N) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(out + j) =
+              make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                          __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+      } else {
+        for (int j = 0; j < 32; ++j)
+          if (col + j < N) out[j] = __uint_as_float(r[j]);
+      }
+    } else {
+      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(C) + (long long)b * c_bs +
+                           (long long)row * ldc + col;
+      if (vec_ok && col + 32 <= N) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 8)
+          *reinterpret_cast<uint4*>(out + j) = make_uint4(
+              pack_bf16(__uint_as_float(r[j]), __uint_as_float(r[j + 1])),
+              pack_bf16(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])),
+              pack_bf16(__uint_as_float(r[j + 4]), __uint_as_float(r[j + 5])),
+              pack_bf16(__uint_as_float(r[j + 6]), __uint_as_float(r[j + 7])));
+      } else {
+        for (int j = 0; j < 32; ++j)
+          if (col + j < N) out[j] = __float2bfloat16_rn(__uint_as_float(r[j]));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, kTmemCols);
+}
+
+}  // namespace gemm
+}  // namespace dsv
+
+template <int BN, int STAGES, bool F32>
+static int launch_gemm(const CUtensorMap* ta, const CUtensorMap* tb, void* C, int M, int N, int K,
+                       long long ldc, long long c_bs, int nbatch, cudaStream_t st) {
+  using namespace dsv::gemm;
+  const int smem = SmemLayout<BN, STAGES>::kBytes;
+  auto kern = gemm_kernel<BN, STAGES, F32>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  dim3 grid((M + BM - 1) / BM, (N + BN - 1) / BN, nbatch);
+  kern<<<grid, 128, smem, st>>>(*ta, *tb, C, M, N, K, ldc, c_bs);
+  return (int)cudaGetLastError();
+}
+
+int dsv_gemm_launch(const CUtensorMap* ta, const CUtensorMap* tb, void* C, int M, int N, int K,
+                    long long ldc, long long c_bs, int nbatch, int f32_out, int bn,
+                    cudaStream_t st) {
+  if (bn == 256) {
+    return f32_out ? launch_gemm<256, 4, true>(ta, tb, C, M, N, K, ldc, c_bs, nbatch, st)
+                   : launch_gemm<256, 4, false>(ta, tb, C, M, N, K, ldc, c_bs, nbatch, st);
+  }
+  return f32_out ? launch_gemm<128, 4, true>(ta, tb, C, M, N, K, ldc, c_bs, nbatch, st)
+                 : launch_gemm<128, 4, false>(ta, tb, C, M, N, K, ldc, c_bs, nbatch, st);
+}

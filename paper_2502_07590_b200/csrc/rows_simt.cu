@@ -1,0 +1,253 @@
+// rows_simt.cu — CUDA-core kernels for the general (ragged / per-query) case.
+//
+// * dsv_scores_f32: batched fp32 score product C[b] = A[b] . B[b]^T for small
+//   inner width r (the low-rank predictor scores, reference
+//   pkg/src/dynsparse/selection.py:149 `q_block @ k_lr[c0:c1].T`). Summation
+//   runs t = 0..r-1 with fmaf, so the result is deterministic; it feeds K2.
+// * sparse attention over arbitrary per-(head, query) CSR index lists
+//   (reference pkg/src/dynsparse/attention.py:176-183, the ragged per-row
+//   loop, and the autograd of pkg/src/dynsparse/trainer.py:110-117).
+//   One warp per (head, query); fp32 math; online softmax; LSE saved for the
+//   backward, which recomputes P and scatter-adds dK/dV with fp32 atomics.
+// These are the GPU correctness path for index sets the tensor-core kernels do
+// not tile (per-query lists, theta-oracle sets, groups < 64 queries).
+
+#include "dsv_common.cuh"
+
+namespace dsv {
+namespace simt {
+
+template <typename T> DSV_DEV float ld_f(const T* p);
+template <> DSV_DEV float ld_f<float>(const float* p) { return __ldg(p); }
+template <> DSV_DEV float ld_f<__nv_bfloat16>(const __nv_bfloat16* p) {
+  return __bfloat162float(*p);
+}
+
+// C[b, i, j] = sum_t A[b, i, t] * B[b, j, t]; A: [nb, R, r] (row stride lda),
+// B: [nb, Lk, r] (row stride ldb), C: [nb, R, Lk] (row stride ldc).
+template <typename T>
+__global__ void __launch_bounds__(256)
+scores_kernel(const T* __restrict__ A, long long lda, long long a_bs,
+              const T* __restrict__ B, long long ldb, long long b_bs,
+              float* __restrict__ C, long long ldc, long long c_bs, int R, int Lk, int r) {
+  extern __shared__ float sA[];  // [32][r]
+  const int b = blockIdx.z;
+  const int i0 = blockIdx.y * 32;
+  const int j = blockIdx.x * 256 + threadIdx.x;
+  const T* Ab = A + b * a_bs;
+  const T* Bb = B + b * b_bs;
+  for (int e = threadIdx.x; e < 32 * r; e += 256) {
+    const int ii = e / r, t = e - ii * r;
+    sA[e] = (i0 + ii < R) ? ld_f(Ab + (long long)(i0 + ii) * lda + t) : 0.f;
+  }
+  __syncthreads();
+  if (j >= Lk) return;
+  float bj[64];
+#pragma unroll
+  for (int t = 0; t < 64; ++t) bj[t] = (t < r) ? ld_f(Bb + (long long)j * ldb + t) : 0.f;
+  float* Cb = C + b * c_bs;
+  const int iend = min(32, R - i0);
+  for (int ii = 0; ii < iend; ++ii) {
+    float acc = 0.f;
+#pragma unroll
+    for (int t = 0; t < 64; ++t)
+      if (t < r) acc = fmaf(sA[ii * r + t], bj[t], acc);
+    Cb[(long long)(i0 + ii) * ldc + j] = acc;
+  }
+}
+
+// ---------------------------------------------------------------- attention
+// q: [H, Lq, d], k/v: [H, Lk, d]; ptr: [H*Lq + 1] (int64), cols: int32 key ids.
+template <typename T, int NE>  // NE = ceil(d / 32) elements per lane
+__global__ void __launch_bounds__(256)
+attn_rows_fwd_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
+                     const long long* __restrict__ ptr, const int* __restrict__ cols,
+                     int H, int Lq, int Lk, int d, float scale,
+                     float* __restrict__ o, float* __restrict__ lse) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= H * Lq) return;
+  const int h = gw / Lq;
+  const T* qr = q + (long long)gw * d;
+  float qv[NE], acc[NE];
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const int c = lane + 32 * e;
+    qv[e] = (c < d) ? ld_f(qr + c) * scale : 0.f;
+    acc[e] = 0.f;
+  }
+  float m = -INFINITY, l = 0.f;
+  const long long p0 = ptr[gw], p1 = ptr[gw + 1];
+  const T* kh = k + (long long)h * Lk * d;
+  const T* vh = v + (long long)h * Lk * d;
+  for (long long p = p0; p < p1; ++p) {
+    const int key = cols[p];
+    const T* kr = kh + (long long)key * d;
+    float s = 0.f;
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const int c = lane + 32 * e;
+      if (c < d) s = fmaf(qv[e], ld_f(kr + c), s);
+    }
+#pragma unroll
+    for (int o2 = 16; o2; o2 >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o2);
+    const float mn = fmaxf(m, s);
+    const float alpha = __expf(m - mn);
+    const float pw = __expf(s - mn);
+    l = l * alpha + pw;
+    const T* vr = vh + (long long)key * d;
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const int c = lane + 32 * e;
+      acc[e] = acc[e] * alpha + ((c < d) ? pw * ld_f(vr + c) : 0.f);
+    }
+    m = mn;
+  }
+  const float inv = 1.f / l;
+  float* orow = o + (long long)gw * d;
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const int c = lane + 32 * e;
+    if (c < d) orow[c] = acc[e] * inv;
+  }
+  if (lane == 0) lse[gw] = m + logf(l);
+}
+
+template <typename T, int NE>
+__global__ void __launch_bounds__(256)
+attn_rows_bwd_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
+                     const float* __restrict__ o, const float* __restrict__ lse,
+                     const T* __restrict__ dout,
+                     const long long* __restrict__ ptr, const int* __restrict__ cols,
+                     int H, int Lq, int Lk, int d, float scale,
+                     float* __restrict__ dq, float* __restrict__ dk, float* __restrict__ dv) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= H * Lq) return;
+  const int h = gw / Lq;
+  float qv[NE], dov[NE], dqa[NE];
+  float delta = 0.f;
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const int c = lane + 32 * e;
+    const bool ok = c < d;
+    qv[e] = ok ? ld_f(q + (long long)gw * d + c) : 0.f;
+    dov[e] = ok ? ld_f(dout + (long long)gw * d + c) : 0.f;
+    delta += ok ? dov[e] * o[(long long)gw * d + c] : 0.f;
+    dqa[e] = 0.f;
+  }
+#pragma unroll
+  for (int o2 = 16; o2; o2 >>= 1) delta += __shfl_xor_sync(0xffffffffu, delta, o2);
+  const float lrow = lse[gw];
+  const long long p0 = ptr[gw], p1 = ptr[gw + 1];
+  const long long hoff = (long long)h * Lk * d;
+  for (long long p = p0; p < p1; ++p) {
+    const int key = cols[p];
+    const T* kr = k + hoff + (long long)key * d;
+    const T* vr = v + hoff + (long long)key * d;
+    float s = 0.f, dp = 0.f;
+    float kv[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const int c = lane + 32 * e;
+      kv[e] = (c < d) ? ld_f(kr + c) : 0.f;
+      s = fmaf(qv[e], kv[e], s);
+      dp = fmaf(dov[e], (c < d) ? ld_f(vr + c) : 0.f, dp);
+    }
+#pragma unroll
+    for (int o2 = 16; o2; o2 >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, o2);
+      dp += __shfl_xor_sync(0xffffffffu, dp, o2);
+    }
+    const float pw = __expf(s * scale - lrow);
+    const float ds = pw * (dp - delta) * scale;
+    float* dkr = dk + hoff + (long long)key * d;
+    float* dvr = dv + hoff + (long long)key * d;
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const int c = lane + 32 * e;
+      if (c < d) {
+        dqa[e] = fmaf(ds, kv[e], dqa[e]);
+        atomicAdd(dkr + c, ds * qv[e]);
+        atomicAdd(dvr + c, pw * dov[e]);
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const int c = lane + 32 * e;
+    if (c < d) dq[(long long)gw * d + c] = dqa[e];
+  }
+}
+
+}  // namespace simt
+}  // namespace dsv
+
+using namespace dsv::simt;
+
+int dsv_scores_f32_launch(const void* A, long long lda, long long a_bs, const void* B,
+                          long long ldb, long long b_bs, float* C, long long ldc, long long c_bs,
+                          int nbatch, int R, int Lk, int r, int bf16_in, cudaStream_t st) {
+  if (r < 1 || r > 64) return 1;
+  dim3 grid((Lk + 255) / 256, (R + 31) / 32, nbatch);
+  const size_t sm = 32 * r * sizeof(float);
+  if (bf16_in)
+    scores_kernel<__nv_bfloat16><<<grid, 256, sm, st>>>(
+        (const __nv_bfloat16*)A, lda, a_bs, (const __nv_bfloat16*)B, ldb, b_bs, C, ldc, c_bs, R,
+        Lk, r);
+  else
+    scores_kernel<float><<<grid, 256, sm, st>>>((const float*)A, lda, a_bs, (const float*)B, ldb,
+                                                b_bs, C, ldc, c_bs, R, Lk, r);
+  return (int)cudaGetLastError();
+}
+
+template <typename T>
+static int rows_fwd(const void* q, const void* k, const void* v, const long long* ptr,
+                    const int* cols, int H, int Lq, int Lk, int d, float scale, float* o,
+                    float* lse, cudaStream_t st) {
+  const long long warps = (long long)H * Lq;
+  const int blocks = (int)((warps * 32 + 255) / 256);
+  const T *Q = (const T*)q, *K = (const T*)k, *V = (const T*)v;
+  switch ((d + 31) / 32) {
+    case 1: attn_rows_fwd_kernel<T, 1><<<blocks, 256, 0, st>>>(Q, K, V, ptr, cols, H, Lq, Lk, d, scale, o, lse); break;
+    case 2: attn_rows_fwd_kernel<T, 2><<<blocks, 256, 0, st>>>(Q, K, V, ptr, cols, H, Lq, Lk, d, scale, o, lse); break;
+    case 3: case 4: attn_rows_fwd_kernel<T, 4><<<blocks, 256, 0, st>>>(Q, K, V, ptr, cols, H, Lq, Lk, d, scale, o, lse); break;
+    case 5: case 6: case 7: case 8: attn_rows_fwd_kernel<T, 8><<<blocks, 256, 0, st>>>(Q, K, V, ptr, cols, H, Lq, Lk, d, scale, o, lse); break;
+    default: return 1;
+  }
+  return (int)cudaGetLastError();
+}
+
+template <typename T>
+static int rows_bwd(const void* q, const void* k, const void* v, const float* o, const float* lse,
+                    const void* dout, const long long* ptr, const int* cols, int H, int Lq, int Lk,
+                    int d, float scale, float* dq, float* dk, float* dv, cudaStream_t st) {
+  const long long warps = (long long)H * Lq;
+  const int blocks = (int)((warps * 32 + 255) / 256);
+  const T *Q = (const T*)q, *K = (const T*)k, *V = (const T*)v, *DO = (const T*)dout;
+  switch ((d + 31) / 32) {
+    case 1: attn_rows_bwd_kernel<T, 1><<<blocks, 256, 0, st>>>(Q, K, V, o, lse, DO, ptr, cols, H, Lq, Lk, d, scale, dq, dk, dv); break;
+    case 2: attn_rows_bwd_kernel<T, 2><<<blocks, 256, 0, st>>>(Q, K, V, o, lse, DO, ptr, cols, H, Lq, Lk, d, scale, dq, dk, dv); break;
+    case 3: case 4: attn_rows_bwd_kernel<T, 4><<<blocks, 256, 0, st>>>(Q, K, V, o, lse, DO, ptr, cols, H, Lq, Lk, d, scale, dq, dk, dv); break;
+    case 5: case 6: case 7: case 8: attn_rows_bwd_kernel<T, 8><<<blocks, 256, 0, st>>>(Q, K, V, o, lse, DO, ptr, cols, H, Lq, Lk, d, scale, dq, dk, dv); break;
+    default: return 1;
+  }
+  return (int)cudaGetLastError();
+}
+
+int dsv_rows_fwd_launch(const void* q, const void* k, const void* v, const long long* ptr,
+                        const int* cols, int H, int Lq, int Lk, int d, float scale, int bf16_in,
+                        float* o, float* lse, cudaStream_t st) {
+  return bf16_in ? rows_fwd<__nv_bfloat16>(q, k, v, ptr, cols, H, Lq, Lk, d, scale, o, lse, st)
+                 : rows_fwd<float>(q, k, v, ptr, cols, H, Lq, Lk, d, scale, o, lse, st);
+}
+
+int dsv_rows_bwd_launch(const void* q, const void* k, const void* v, const float* o,
+                        const float* lse, const void* dout, const long long* ptr, const int* cols,
+                        int H, int Lq, int Lk, int d, float scale, int bf16_in, float* dq,
+                        float* dk, float* dv, cudaStream_t st) {
+  return bf16_in ? rows_bwd<__nv_bfloat16>(q, k, v, o, lse, dout, ptr, cols, H, Lq, Lk, d, scale,
+                                           dq, dk, dv, st)
+                 : rows_bwd<float>(q, k, v, o, lse, dout, ptr, cols, H, Lq, Lk, d, scale, dq, dk,
+                                   dv, st);
+}

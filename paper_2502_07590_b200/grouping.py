@@ -1,0 +1,131 @@
+"""Voxel query grouping (reference pkg/src/dynsparse/grouping.py).
+
+A voxel group is the tensor-core query tile: its members (<= 128 queries) share
+one critical-KV index list, selected by the group's proxy query. The plan is
+built on the host (cheap integer work) and uploaded once as two small device
+tables consumed by the K3 kernels:
+
+    grp_rows int32 [G, 128]  member token ids, padded by repeating the last member
+    grp_size int32 [G]       live members per group
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .grid import TokenGrid
+
+# Candidate voxel shapes, smallest to largest (grouping.py:22-32).
+SIZE_LADDER = (
+    (1, 1, 1), (2, 2, 1), (2, 2, 2), (4, 2, 2), (4, 4, 2),
+    (4, 4, 4), (8, 4, 4), (8, 8, 4), (8, 8, 8),
+)
+
+TILE = 128
+
+
+@dataclass
+class VoxelGroupPlan:
+    """Tiling partition of the grid plus one proxy per group (grouping.py:35-61)."""
+
+    grid: TokenGrid
+    dims: tuple
+    members: list
+    proxies: np.ndarray
+    _device: dict = field(default_factory=dict, repr=False)
+
+    @property
+    def n_groups(self) -> int:
+        return len(self.members)
+
+    @property
+    def max_group(self) -> int:
+        return max(m.size for m in self.members)
+
+    def to_json(self) -> dict:
+        return {"grid": list(self.grid.dims), "dims": list(self.dims),
+                "proxies": self.proxies.tolist()}
+
+    @classmethod
+    def from_json(cls, data: dict) -> "VoxelGroupPlan":
+        plan = build_groups(TokenGrid(*data["grid"]), tuple(data["dims"]))
+        if plan.proxies.tolist() != list(data["proxies"]):
+            raise ValueError("stored proxies do not match the deterministic tiling")
+        return plan
+
+    def tables(self, device) -> tuple[torch.Tensor, torch.Tensor]:
+        """(grp_rows [G, 128], grp_size [G]) int32 on `device` (cached)."""
+        key = str(device)
+        if key not in self._device:
+            rows, size = group_tables(self.members)
+            self._device[key] = (torch.from_numpy(rows).to(device),
+                                 torch.from_numpy(size).to(device))
+        return self._device[key]
+
+    def proxies_tensor(self, device) -> torch.Tensor:
+        key = "proxies:" + str(device)
+        if key not in self._device:
+            self._device[key] = torch.from_numpy(self.proxies.astype(np.int32)).to(device)
+        return self._device[key]
+
+
+def build_groups(grid: TokenGrid, dims) -> VoxelGroupPlan:
+    """Tile the grid into voxels of shape dims, clipped at boundaries (grouping.py:64-90).
+
+    Enumeration is t-outer, h, w-inner; the proxy of a voxel is the member at
+    floor(len / 2) of its clipped extent along every axis.
+    """
+    gt, gh, gw = (int(d) for d in dims)
+    if min(gt, gh, gw) < 1:
+        raise ValueError(f"voxel dims must be positive, got {dims}")
+    if gt > grid.frames or gh > grid.height or gw > grid.width:
+        raise ValueError(f"voxel dims {dims} exceed grid {grid.dims}")
+    T, H, W = grid.dims
+    members, proxies = [], []
+    for t0 in range(0, T, gt):
+        ts = np.arange(t0, min(t0 + gt, T))
+        for h0 in range(0, H, gh):
+            hs = np.arange(h0, min(h0 + gh, H))
+            for w0 in range(0, W, gw):
+                ws = np.arange(w0, min(w0 + gw, W))
+                flat = (ts[:, None, None] * H + hs[None, :, None]) * W + ws[None, None, :]
+                members.append(np.sort(flat.reshape(-1)).astype(np.int64))
+                proxies.append(int((ts[ts.size // 2] * H + hs[hs.size // 2]) * W + ws[ws.size // 2]))
+    return VoxelGroupPlan(grid=grid, dims=(gt, gh, gw), members=members,
+                          proxies=np.asarray(proxies, dtype=np.int64))
+
+
+def group_tables(members) -> tuple[np.ndarray, np.ndarray]:
+    """Pad member lists to the 128-query tile (host-side)."""
+    G = len(members)
+    rows = np.empty((G, TILE), dtype=np.int32)
+    size = np.empty(G, dtype=np.int32)
+    for g, m in enumerate(members):
+        m = np.asarray(m, dtype=np.int64)
+        if m.size == 0 or m.size > TILE:
+            raise ValueError(f"group {g} has {m.size} members; tiles hold 1..{TILE}")
+        rows[g, : m.size] = m
+        rows[g, m.size:] = m[-1]
+        size[g] = m.size
+    return rows, size
+
+
+def overlap_ratio(member_sets: list, proxy_pos: int) -> float:
+    """Mean over non-proxy members of |I_m & I_proxy| / |I_m| (grouping.py:93-114)."""
+    if not 0 <= proxy_pos < len(member_sets):
+        raise ValueError("proxy position outside the member list")
+    if len(member_sets) == 1:
+        return 1.0
+    proxy = np.asarray(member_sets[proxy_pos], dtype=np.int64)
+    ratios = []
+    for pos, m in enumerate(member_sets):
+        if pos == proxy_pos:
+            continue
+        m = np.asarray(m, dtype=np.int64)
+        if m.size == 0:
+            raise ValueError("member sets must be nonempty")
+        ratios.append(np.intersect1d(m, proxy, assume_unique=True).size / m.size)
+    return float(np.mean(ratios))

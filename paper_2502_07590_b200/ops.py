@@ -1,0 +1,202 @@
+"""Device-tensor wrappers over the C ABI (one function per libdsv entry point).
+
+All tensors must already live on the current CUDA device; outputs are
+allocated here with torch (device memory plumbing only) and filled by the
+libdsv kernels on the current stream. There is no CPU path: a missing CUDA
+device or library raises.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _lib
+
+_F32, _BF16 = _lib.DTYPE_F32, _lib.DTYPE_BF16
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _require_cuda(*ts: torch.Tensor) -> None:
+    for t in ts:
+        if not t.is_cuda:
+            raise _lib.DSVError("libdsv kernels need CUDA tensors (no CPU fallback exists)")
+
+
+def _ptr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+# ------------------------------------------------------------------- K1 GEMM
+def gemm_bf16(a: torch.Tensor, b: torch.Tensor, out_dtype=torch.float32) -> torch.Tensor:
+    """Batched C = A . B^T on tcgen05. a: [nb, M, K] or [M, K] bf16, b: [nb, N, K] or [N, K]."""
+    _require_cuda(a, b)
+    squeeze = a.dim() == 2
+    if squeeze:
+        a, b = a.unsqueeze(0), b.unsqueeze(0)
+    if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16:
+        raise ValueError("gemm_bf16 expects bf16 operands")
+    nb, M, K = a.shape
+    _, N, K2 = b.shape
+    if K != K2 or b.shape[0] != nb:
+        raise ValueError(f"gemm shape mismatch {tuple(a.shape)} x {tuple(b.shape)}")
+    if a.stride(2) != 1 or b.stride(2) != 1:
+        raise ValueError("gemm operands need unit stride along K")
+    c = torch.empty((nb, M, N), device=a.device, dtype=out_dtype)
+    _lib.call("dsv_gemm_bf16", _ptr(a), a.stride(1), a.stride(0), _ptr(b), b.stride(1), b.stride(0),
+              _ptr(c), _F32 if out_dtype == torch.float32 else _BF16, c.stride(1), c.stride(0),
+              M, N, K, nb, _stream())
+    return c[0] if squeeze else c
+
+
+def project(x: torch.Tensor, wt: torch.Tensor) -> torch.Tensor:
+    """K1a: [L, d_model] . wt[n_out, d_model]^T -> [L, n_out] bf16."""
+    _require_cuda(x, wt)
+    x = x.contiguous()
+    wt = wt.contiguous()
+    L, dm = x.shape
+    n_out = wt.shape[0]
+    out = torch.empty((L, n_out), device=x.device, dtype=torch.bfloat16)
+    _lib.call("dsv_project", _ptr(x), _ptr(wt), _ptr(out), L, dm, n_out, _stream())
+    return out
+
+
+def scores_f32(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """fp32 scores C[nb, R, Lk] = A[nb, R, r] . B[nb, Lk, r]^T (A, B fp32 or bf16)."""
+    _require_cuda(a, b)
+    squeeze = a.dim() == 2
+    if squeeze:
+        a, b = a.unsqueeze(0), b.unsqueeze(0)
+    if a.dtype != b.dtype or a.dtype not in (torch.float32, torch.bfloat16):
+        raise ValueError("scores_f32 expects matching fp32 or bf16 operands")
+    if a.stride(2) != 1 or b.stride(2) != 1:
+        a, b = a.contiguous(), b.contiguous()
+    nb, R, r = a.shape
+    Lk = b.shape[1]
+    if out is None:
+        out = torch.empty((nb, R, Lk), device=a.device, dtype=torch.float32)
+    _lib.call("dsv_scores_f32", _ptr(a), a.stride(1), a.stride(0), _ptr(b), b.stride(1),
+              b.stride(0), _ptr(out), out.stride(1), out.stride(0), nb, R, Lk, r,
+              _BF16 if a.dtype == torch.bfloat16 else _F32, _stream())
+    return out[0] if squeeze else out
+
+
+# ------------------------------------------------------------------- K2 top-k
+def topk_rows(scores: torch.Tensor, k_per_head: torch.Tensor, rows_per_head: int,
+              k_max: int | None = None):
+    """Exact top-k per row of fp32 scores [R, L] (row r uses k_per_head[r // rows_per_head]).
+
+    Returns (idx int32 [R, k_max] ascending — entries past a row's k are
+    undefined, thresholds fp32 [R]).
+    """
+    _require_cuda(scores, k_per_head)
+    if scores.dtype != torch.float32 or scores.dim() != 2 or scores.stride(1) != 1:
+        raise ValueError("scores must be a row-major fp32 matrix")
+    R, L = scores.shape
+    kp = k_per_head.to(device=scores.device, dtype=torch.int32).contiguous()
+    if k_max is None:
+        k_max = int(kp.max().item())
+    idx = torch.empty((R, k_max), device=scores.device, dtype=torch.int32)
+    thr = torch.empty((R,), device=scores.device, dtype=torch.float32)
+    _lib.call("dsv_topk", _ptr(scores), scores.stride(0), R, L, _ptr(kp), rows_per_head, _ptr(idx),
+              idx.stride(0), _ptr(thr), _stream())
+    return idx, thr
+
+
+# ------------------------------------------------------------------- K3 attention
+def sparse_fwd(q, k, v, grp_rows, grp_size, idx, kcount, scale=None, p_in_tmem=True):
+    """Group-tiled sparse attention forward. q: [H, Lq, D], k/v: [H, Lk, D] bf16.
+
+    grp_rows int32 [G, 128], grp_size int32 [G], idx int32 [H, G, ldk], kcount int32 [H].
+    Returns (out bf16 [H, Lq, D], lse2 fp32 [H, Lq]).
+    """
+    _require_cuda(q, k, v, grp_rows, grp_size, idx, kcount)
+    H, Lq, D = q.shape
+    Lk = k.shape[1]
+    G = grp_rows.shape[0]
+    if scale is None:
+        scale = 1.0 / math.sqrt(D)
+    out = torch.empty_like(q)
+    lse = torch.empty((H, Lq), device=q.device, dtype=torch.float32)
+    _lib.call("dsv_sparse_fwd", _ptr(q), _ptr(k), _ptr(v), _ptr(grp_rows), _ptr(grp_size),
+              _ptr(idx), idx.stride(1), _ptr(kcount), H, G, Lq, Lk, D, float(scale), _ptr(out),
+              _ptr(lse), 0 if p_in_tmem else 1, _stream())
+    return out, lse
+
+
+def sparse_bwd(q, k, v, out, dout, lse, grp_rows, grp_size, idx, kcount, scale=None,
+               dk_acc=None, dv_acc=None):
+    """Backward of sparse_fwd. Returns (dq bf16, dk_acc fp32, dv_acc fp32)."""
+    _require_cuda(q, k, v, out, dout, lse)
+    H, Lq, D = q.shape
+    Lk = k.shape[1]
+    G = grp_rows.shape[0]
+    if scale is None:
+        scale = 1.0 / math.sqrt(D)
+    dq = torch.empty_like(q)
+    if dk_acc is None:
+        dk_acc = torch.zeros((H, Lk, D), device=q.device, dtype=torch.float32)
+    if dv_acc is None:
+        dv_acc = torch.zeros((H, Lk, D), device=q.device, dtype=torch.float32)
+    _lib.call("dsv_sparse_bwd", _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(dout), _ptr(lse),
+              _ptr(grp_rows), _ptr(grp_size), _ptr(idx), idx.stride(1), _ptr(kcount), H, G, Lq,
+              Lk, D, float(scale), _ptr(dq), _ptr(dk_acc), _ptr(dv_acc), _stream())
+    return dq, dk_acc, dv_acc
+
+
+def rows_fwd(q, k, v, ptr, cols, scale=None):
+    """Ragged CSR sparse attention forward on CUDA cores. Returns (out fp32, lse fp32 natural)."""
+    _require_cuda(q, k, v, ptr, cols)
+    H, Lq, D = q.shape
+    Lk = k.shape[1]
+    if scale is None:
+        scale = 1.0 / math.sqrt(D)
+    out = torch.empty((H, Lq, D), device=q.device, dtype=torch.float32)
+    lse = torch.empty((H, Lq), device=q.device, dtype=torch.float32)
+    _lib.call("dsv_rows_fwd", _ptr(q), _ptr(k), _ptr(v), _ptr(ptr), _ptr(cols), H, Lq, Lk, D,
+              float(scale), _BF16 if q.dtype == torch.bfloat16 else _F32, _ptr(out), _ptr(lse),
+              _stream())
+    return out, lse
+
+
+def rows_bwd(q, k, v, out, lse, dout, ptr, cols, scale=None):
+    """Backward of rows_fwd. Returns fp32 (dq, dk, dv)."""
+    _require_cuda(q, k, v, out, lse, dout, ptr, cols)
+    H, Lq, D = q.shape
+    Lk = k.shape[1]
+    if scale is None:
+        scale = 1.0 / math.sqrt(D)
+    dq = torch.empty((H, Lq, D), device=q.device, dtype=torch.float32)
+    dk = torch.zeros((H, Lk, D), device=q.device, dtype=torch.float32)
+    dv = torch.zeros((H, Lk, D), device=q.device, dtype=torch.float32)
+    _lib.call("dsv_rows_bwd", _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), _ptr(dout),
+              _ptr(ptr), _ptr(cols), H, Lq, Lk, D, float(scale),
+              _BF16 if q.dtype == torch.bfloat16 else _F32, _ptr(dq), _ptr(dk), _ptr(dv),
+              _stream())
+    return dq, dk, dv
+
+
+def gather_rows(src: torch.Tensor, rows: torch.Tensor, out: torch.Tensor | None = None):
+    """out[i] = src[rows[i]] for a 2-D src (row-major rows)."""
+    _require_cuda(src, rows)
+    rows = rows.to(torch.int32).contiguous()
+    n = rows.numel()
+    if out is None:
+        out = torch.empty((n, src.shape[1]), device=src.device, dtype=src.dtype)
+    es = src.element_size()
+    _lib.call("dsv_gather_rows", _ptr(src), src.stride(0) * es, _ptr(rows), n, src.shape[1] * es,
+              _ptr(out), out.stride(0) * es, _stream())
+    return out
+
+
+def f32_to_bf16(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    _require_cuda(x)
+    x = x.contiguous()
+    if out is None:
+        out = torch.empty(x.shape, device=x.device, dtype=torch.bfloat16)
+    _lib.call("dsv_f32_to_bf16", _ptr(x), _ptr(out), x.numel(), _stream())
+    return out
