@@ -13,22 +13,23 @@
 // [H, G, ldk] ascending, k per head int32 [H]; LSE fp32 [H, L] in the log2
 // domain of the scaled logits (lse2 = max + log2(sum)).
 //
-// Forward CTA (one per (head, group); 192 threads):
-//   warp 0   : TMA producer — Q tile via tile::gather4 on the member rows, then
-//              per 128-key block the selected K and V rows via gather4 into a
-//              2-stage ring (128B swizzle, two 64-column atoms for D=128);
-//   warp 1   : tcgen05.mma issuer — S_j = Q K_j^T into one of two TMEM S
-//              buffers, then O += P_{j-1} V_{j-1} (P read from TMEM aliased over
-//              S, or from shared memory in the kPTmem=false variant);
-//   warps 2-5: softmax — one query row per thread: tcgen05.ld of S, online
-//              max with lazy rescale (only when the max grows by > 2^8), P to
-//              TMEM/smem as bf16, O correction in TMEM when rescaling, and the
-//              final O/l epilogue + LSE.
-// Backward CTA (transposed formulation, keys in TMEM lanes):
-//   S^T = K_j Q^T and dP^T = V_j dO^T (M = keys), workers (one key row per
-//   thread) form P^T and dS^T in TMEM, dV_j = P^T dO and dK_j = dS^T Q read
-//   their A operand from TMEM, dQ += dS K_j reads dS from shared memory;
-//   dK_j / dV_j rows are scatter-added into fp32 accumulators with red.v4.
+// Both kernels run one CTA per (head, group), head-major so the K/V of the two
+// or three heads in flight stay L2-resident, 416 threads:
+//   warps 0-3  : row workers (one TMEM lane = one row per thread)
+//   warp  4    : tcgen05.mma issuer (one elected lane) + TMEM owner
+//   warps 5-12 : gather producers — 256 threads issue 16-byte cp.async copies of
+//                the selected K/V rows straight into 128B-swizzled UMMA tiles
+//                (measured on B200: ~50 B/clk/SM for random 256 B rows, vs ~8 for
+//                TMA tile::gather4), a 3-deep (fwd) / 2-deep (bwd) ring.
+// Forward: S_j = Q K_j^T into one of two TMEM S buffers; softmax workers take
+// the row max in a first TMEM pass, write P (bf16) over S in a second, rescale
+// O in TMEM only when the max grows by > 2^8; O += P_{j-1} V_{j-1} reads P from
+// TMEM (A operand) and V from shared memory (MN-major B).
+// Backward (transposed, keys in TMEM lanes): S^T = K_j Q^T, dP^T = V_j dO^T;
+// workers (one key per thread) form P^T, dS^T in TMEM and dS in smem; then
+// dQ += dS K_j, dV_j = P^T dO, dK_j = dS^T Q; dV_j / dK_j rows are staged per
+// warp through shared memory and scatter-added with row-contiguous red.v4
+// (coalesced: 2x the L2 reduction rate of row-per-thread atomics).
 
 #include <cuda.h>
 #include "dsv_common.cuh"
@@ -38,54 +39,84 @@ namespace attn {
 
 constexpr int BQ = 128;   // queries per tile
 constexpr int BKV = 128;  // keys per block
-constexpr int kThreads = 192;
-constexpr int kStages = 2;
+constexpr int kWorkWarps = 4;
+constexpr int kMmaWarp = 4;
+constexpr int kProdWarp0 = 5;
+constexpr int kProdWarps = 8;
+constexpr int kProdThreads = kProdWarps * 32;
+constexpr int kThreads = (kWorkWarps + 1 + kProdWarps) * 32;
+
+template <int D>
+struct Gather {
+  static constexpr int kCPR = D / 8;                          // 16-byte chunks per row
+  static constexpr int kPer = 128 * kCPR / kProdThreads;      // chunks per thread per tile
+  static constexpr int kRowStep = kProdThreads / kCPR;        // rows between a thread's chunks
+  static constexpr int kTile = 128 * D * 2;
+};
+
+// Issue the cp.async copies of one 128-row tile (rows[i] = absolute row id of
+// this thread's i-th chunk) into a 128B-swizzled K-major tile (atom = 64 cols).
+template <int D>
+DSV_DEV void issue_tile(uint8_t* tile, const __nv_bfloat16* base,
+                        const int (&rows)[Gather<D>::kPer], int ptid) {
+  using G = Gather<D>;
+  const int q = ptid % G::kCPR, r0 = ptid / G::kCPR;
+  const uint32_t t0 = smem_u32(tile) + (q >> 3) * (128 * 128);
+#pragma unroll
+  for (int i = 0; i < G::kPer; ++i)
+    cp_async16(t0 + sw128_off(r0 + i * G::kRowStep, q & 7), base + (long long)rows[i] * D + q * 8);
+}
+
+// Producer-side bookkeeping: cp.async groups are retired in order; retiring a
+// group makes its bytes visible to the tensor core (proxy fence) and arrives on
+// the group's "full" barrier (one arrival per producer warp).
+template <int kAllow, typename BarOf>
+DSV_DEV void retire_groups(int committed, int& retired, BarOf bar_of) {
+  if (committed - retired <= kAllow) return;
+  cp_async_wait<kAllow>();
+  fence_proxy_async_smem();
+  __syncwarp();
+  for (; retired < committed - kAllow; ++retired)
+    if ((threadIdx.x & 31) == 0) mbar_arrive(bar_of(retired));
+}
+
+// ====================================================================== fwd
+constexpr int kFwdStages = 3;
 
 template <int D>
 struct FwdSmem {
-  static constexpr int kAtoms = D / 64;
-  static constexpr int kTile = 128 * D * 2;          // one 128-row operand tile
+  static constexpr int kTile = 128 * D * 2;
   static constexpr int kQ = 0;
   static constexpr int kK = kQ + kTile;
-  static constexpr int kV = kK + kStages * kTile;
-  static constexpr int kP = kV + kStages * kTile;     // only used when P lives in smem
-  static constexpr int kBar = kP + 128 * 128 * 2;
+  static constexpr int kV = kK + kFwdStages * kTile;
+  static constexpr int kBar = kV + kFwdStages * kTile;
   static constexpr int kBytes = kBar + 256 + 1024;
 };
 
 struct FwdBars {
   uint64_t q_full;
-  uint64_t k_full[kStages], v_full[kStages], kv_empty[kStages];
+  uint64_t kv_full[kFwdStages], kv_empty[kFwdStages];
   uint64_t s_full[2], p_full[2];
   uint64_t o_ready, o_final;
   uint32_t tmem;
 };
 
-// Gather 128 rows (row ids from `rows`, 4 per lane) of a [*, D] bf16 tensor
-// into a 128B-swizzled tile: atom a holds columns [64a, 64a+64).
 template <int D>
-DSV_DEV void gather_tile(uint8_t* tile, const CUtensorMap* tm, uint64_t* bar, int lane,
-                         int r0, int r1, int r2, int r3) {
-#pragma unroll
-  for (int a = 0; a < D / 64; ++a)
-    tma_gather4(tile + a * (128 * 128) + lane * 512, tm, bar, a * 64, r0, r1, r2, r3);
-}
-
-template <int D, bool kPTmem>
 __global__ void __launch_bounds__(kThreads, 1)
-sparse_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                  const __grid_constant__ CUtensorMap tmV, const int* __restrict__ grp_rows,
+sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __restrict__ Kg,
+                  const __nv_bfloat16* __restrict__ Vg, const int* __restrict__ grp_rows,
                   const int* __restrict__ grp_size, const int* __restrict__ idx, long long ldk,
                   const int* __restrict__ kcount, int G, int Lq, int Lk, float scale_log2,
                   __nv_bfloat16* __restrict__ O, float* __restrict__ lse) {
   using SL = FwdSmem<D>;
+  using GT = Gather<D>;
+  constexpr int ST = kFwdStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   FwdBars& B = *reinterpret_cast<FwdBars*>(smem + SL::kBar);
   uint8_t* sQ = smem + SL::kQ;
   uint8_t* sK = smem + SL::kK;
   uint8_t* sV = smem + SL::kV;
-  uint8_t* sP = smem + SL::kP;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = blockIdx.x / G, g = blockIdx.x - h * G;
@@ -94,19 +125,16 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
   const int* irow = idx + ((long long)h * G + g) * ldk;
   const int* mrow = grp_rows + (long long)g * BQ;
 
-  if (warp == 0) {
+  if (warp == kMmaWarp) {
     if (lane == 0) {
-      prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmV);
-      mbar_init(&B.q_full, 1);
-      for (int s = 0; s < kStages; ++s) {
-        mbar_init(&B.k_full[s], 1); mbar_init(&B.v_full[s], 1); mbar_init(&B.kv_empty[s], 1);
-      }
+      mbar_init(&B.q_full, kProdWarps);
+      for (int s = 0; s < ST; ++s) { mbar_init(&B.kv_full[s], kProdWarps); mbar_init(&B.kv_empty[s], 1); }
       for (int s = 0; s < 2; ++s) { mbar_init(&B.s_full[s], 1); mbar_init(&B.p_full[s], 128); }
       mbar_init(&B.o_ready, 1);
       mbar_init(&B.o_final, 1);
       fence_barrier_init();
     }
-  } else if (warp == 1) {
+    __syncwarp();
     tmem_alloc(&B.tmem, 512);
   }
   tc_fence_before();
@@ -115,32 +143,35 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
   const uint32_t tmem = B.tmem;
   const uint32_t tS0 = tmem, tO = tmem + 256;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ producer
-    {
-      const int4 m4 = *reinterpret_cast<const int4*>(mrow + lane * 4);
-      const int base = h * Lq;
-      if (lane == 0) mbar_arrive_expect_tx(&B.q_full, SL::kTile);
-      __syncwarp();
-      gather_tile<D>(sQ, &tmQ, &B.q_full, lane, base + m4.x, base + m4.y, base + m4.z, base + m4.w);
-    }
+  if (warp >= kProdWarp0) {
+    // ------------------------------------------------------------ producers
+    const int ptid = threadIdx.x - kProdWarp0 * 32;
+    const int r0 = ptid / GT::kCPR;
+    auto bar_of = [&](int grp) { return grp == 0 ? &B.q_full : &B.kv_full[(grp - 1) % ST]; };
+    int rows[GT::kPer];
+    const int qbase = h * Lq;
+#pragma unroll
+    for (int i = 0; i < GT::kPer; ++i) rows[i] = qbase + __ldg(mrow + r0 + i * GT::kRowStep);
+    issue_tile<D>(sQ, Qg, rows, ptid);
+    cp_async_commit();
+    int committed = 1, retired = 0;
     const int kbase = h * Lk;
     for (int j = 0; j < nblk; ++j) {
-      const int st = j % kStages;
-      if (j >= kStages) mbar_wait(&B.kv_empty[st], ((j / kStages) - 1) & 1);
-      const int p = j * BKV + lane * 4;
-      int r[4];
+      const int st = j % ST;
+      if (j >= ST) mbar_wait(&B.kv_empty[st], ((j / ST) - 1) & 1);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) r[i] = kbase + __ldg(irow + min(p + i, kh - 1));
-      if (lane == 0) {
-        mbar_arrive_expect_tx(&B.k_full[st], SL::kTile);
-        mbar_arrive_expect_tx(&B.v_full[st], SL::kTile);
-      }
-      __syncwarp();
-      gather_tile<D>(sK + st * SL::kTile, &tmK, &B.k_full[st], lane, r[0], r[1], r[2], r[3]);
-      gather_tile<D>(sV + st * SL::kTile, &tmV, &B.v_full[st], lane, r[0], r[1], r[2], r[3]);
+      for (int i = 0; i < GT::kPer; ++i)
+        rows[i] = kbase + __ldg(irow + min(j * BKV + r0 + i * GT::kRowStep, kh - 1));
+      issue_tile<D>(sK + st * SL::kTile, Kg, rows, ptid);
+      issue_tile<D>(sV + st * SL::kTile, Vg, rows, ptid);
+      cp_async_commit();
+      ++committed;
+      // the MMA issues S_{j+1} before PV_j, so block j+1 must be visible before
+      // this thread can block on kv_empty for block j+ST: keep <= ST-2 in flight
+      retire_groups<ST - 2>(committed, retired, bar_of);
     }
-  } else if (warp == 1) {
+    retire_groups<0>(committed, retired, bar_of);
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idS = idesc_bf16_f32(128, BKV, 0, 0);
     constexpr uint32_t idO = idesc_bf16_f32(128, D, 0, 1);
@@ -148,8 +179,8 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
     mbar_wait(&B.q_full, 0);
     for (int j = 0; j <= nblk; ++j) {
       if (j < nblk) {
-        const int st = j % kStages;
-        mbar_wait(&B.k_full[st], (j / kStages) & 1);
+        const int st = j % ST;
+        mbar_wait(&B.kv_full[st], (j / ST) & 1);
         tc_fence_after();
         if (elect_one()) {
           const uint32_t aK = smem_u32(sK + st * SL::kTile);
@@ -165,22 +196,15 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         __syncwarp();
       }
       if (j >= 1) {
-        const int jp = j - 1, st = jp % kStages;
+        const int jp = j - 1, st = jp % ST;
         mbar_wait(&B.p_full[jp & 1], (jp >> 1) & 1);
-        mbar_wait(&B.v_full[st], (jp / kStages) & 1);
         tc_fence_after();
         if (elect_one()) {
           const uint32_t aV = smem_u32(sV + st * SL::kTile);
 #pragma unroll
-          for (int kk = 0; kk < BKV / 16; ++kk) {
-            const uint64_t bd = sdesc_sw128(aV + kk * 2048, 128 * 128, 1024);
-            if constexpr (kPTmem) {
-              mma_ts(tO, tS0 + (jp & 1) * 128 + kk * 8, bd, idO, (jp | kk) != 0);
-            } else {
-              const uint32_t aP = smem_u32(sP) + (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-              mma_ss(tO, sdesc_sw128(aP, 16, 1024), bd, idO, (jp | kk) != 0);
-            }
-          }
+          for (int kk = 0; kk < BKV / 16; ++kk)
+            mma_ts(tO, tS0 + (jp & 1) * 128 + kk * 8,
+                   sdesc_sw128(aV + kk * 2048, 128 * 128, 1024), idO, (jp | kk) != 0);
           mma_commit(&B.kv_empty[st]);
           mma_commit(&B.o_ready);
           if (jp == nblk - 1) mma_commit(&B.o_final);
@@ -190,29 +214,25 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
     }
   } else {
     // ------------------------------------------------------------ softmax
-    const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const int row = warp * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     float m_run = -INFINITY, l_run = 0.f;
     for (int j = 0; j < nblk; ++j) {
       const int sb = j & 1;
       const int kv = min(BKV, kh - j * BKV);
+      const uint32_t tS = tS0 + sb * 128 + lane_off;
       mbar_wait(&B.s_full[sb], (j >> 1) & 1);
       tc_fence_after();
-      float sv[BKV];
-#pragma unroll
+      // pass 1: block row max
+      float mx = -INFINITY;
+#pragma unroll 1
       for (int c = 0; c < BKV / 32; ++c) {
         uint32_t r[32];
-        tmem_ld32(tS0 + sb * 128 + lane_off + c * 32, r);
+        tmem_ld32(tS + c * 32, r);
         tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(r[i]);
-      }
-      float mx = -INFINITY;
-#pragma unroll
-      for (int i = 0; i < BKV; ++i) {
-        if (i >= kv) sv[i] = -INFINITY;
-        mx = fmaxf(mx, sv[i]);
+        for (int i = 0; i < 32; ++i)
+          if (c * 32 + i < kv) mx = fmaxf(mx, __uint_as_float(r[i]));
       }
       mx *= scale_log2;
       if (j == 0) {
@@ -235,36 +255,26 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         tmem_st_wait();
         m_run = mx;
       }
-      if constexpr (!kPTmem) {
-        // single smem P buffer: PV_{j-1} must have consumed it
-        if (j >= 1) mbar_wait(&B.o_ready, (j - 1) & 1);
-      }
+      // pass 2: P = 2^(s*scale_log2 - m) in bf16 over the S columns already read
       float lsum = 0.f;
-#pragma unroll
+#pragma unroll 1
       for (int c = 0; c < BKV / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tS + c * 32, r);
+        tmem_ld_wait();
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float p0 = fast_exp2(fmaf(sv[c * 32 + 2 * i], scale_log2, -m_run));
-          const float p1 = fast_exp2(fmaf(sv[c * 32 + 2 * i + 1], scale_log2, -m_run));
+          const int col = c * 32 + 2 * i;
+          const float p0 = col < kv ? fast_exp2(fmaf(__uint_as_float(r[2 * i]), scale_log2, -m_run)) : 0.f;
+          const float p1 = col + 1 < kv ? fast_exp2(fmaf(__uint_as_float(r[2 * i + 1]), scale_log2, -m_run)) : 0.f;
           pk[i] = pack_bf16(p0, p1);
           lsum += bf16lo(pk[i]) + bf16hi(pk[i]);
         }
-        if constexpr (kPTmem) {
-          tmem_st16(tS0 + sb * 128 + lane_off + c * 16, pk);
-        } else {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int chunk = c * 4 + q;  // 16-byte chunk index along keys (0..15)
-            uint8_t* dst = sP + (chunk >> 3) * (128 * 128) + sw128_off(row, chunk & 7);
-            *reinterpret_cast<uint4*>(dst) =
-                make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-          }
-        }
+        tmem_st16(tS + c * 16, pk);
       }
       l_run += lsum;
-      if constexpr (kPTmem) tmem_st_wait();
-      else fence_proxy_async_smem();
+      tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&B.p_full[sb]);
     }
@@ -294,20 +304,21 @@ sparse_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, 512);
+  if (warp == kMmaWarp) tmem_dealloc(tmem, 512);
 }
 
 // ====================================================================== bwd
+constexpr int kBwdStages = 2;
+
 template <int D>
 struct BwdSmem {
   static constexpr int kTile = 128 * D * 2;
   static constexpr int kQ = 0;
   static constexpr int kdO = kQ + kTile;
-  static constexpr int kdS = kdO + kTile;                 // [128 keys][128 q] bf16
+  static constexpr int kdS = kdO + kTile;                 // [128 keys][128 q] bf16; scatter staging
   static constexpr int kK = kdS + 128 * 128 * 2;
-  static constexpr int kStagesB = (kK + 4 * kTile + 1024 + 256 + 1024 <= 232448) ? 2 : 1;
-  static constexpr int kV = kK + kStagesB * kTile;
-  static constexpr int kLse = kV + kStagesB * kTile;
+  static constexpr int kV = kK + kBwdStages * kTile;
+  static constexpr int kLse = kV + kBwdStages * kTile;
   static constexpr int kDelta = kLse + 512;
   static constexpr int kBar = kDelta + 512;
   static constexpr int kBytes = kBar + 256 + 1024;
@@ -315,23 +326,23 @@ struct BwdSmem {
 
 struct BwdBars {
   uint64_t q_full;
-  uint64_t k_full[2], v_full[2], kv_empty[2];
-  uint64_t sdp_full, pds_full, dvdk_full, tmem_free, dq_done;
+  uint64_t kv_full[kBwdStages], kv_empty[kBwdStages];
+  uint64_t sdp_full, pds_full, mma_done, tmem_free;
   uint32_t tmem;
 };
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
-sparse_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
-                  const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-                  const __nv_bfloat16* __restrict__ Og, const __nv_bfloat16* __restrict__ dOg,
-                  const float* __restrict__ lse, const int* __restrict__ grp_rows,
-                  const int* __restrict__ grp_size, const int* __restrict__ idx, long long ldk,
-                  const int* __restrict__ kcount, int G, int Lq, int Lk, float scale,
-                  float scale_log2, __nv_bfloat16* __restrict__ dQ, float* __restrict__ dK,
-                  float* __restrict__ dV) {
+sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __restrict__ dOg,
+                  const __nv_bfloat16* __restrict__ Kg, const __nv_bfloat16* __restrict__ Vg,
+                  const __nv_bfloat16* __restrict__ Og, const float* __restrict__ lse,
+                  const int* __restrict__ grp_rows, const int* __restrict__ grp_size,
+                  const int* __restrict__ idx, long long ldk, const int* __restrict__ kcount,
+                  int G, int Lq, int Lk, float scale, float scale_log2,
+                  __nv_bfloat16* __restrict__ dQ, float* __restrict__ dK, float* __restrict__ dV) {
   using SL = BwdSmem<D>;
-  constexpr int ST = SL::kStagesB;
+  using GT = Gather<D>;
+  constexpr int ST = kBwdStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   BwdBars& B = *reinterpret_cast<BwdBars*>(smem + SL::kBar);
@@ -350,21 +361,17 @@ sparse_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
   const int* irow = idx + ((long long)h * G + g) * ldk;
   const int* mrow = grp_rows + (long long)g * BQ;
 
-  if (warp == 0) {
+  if (warp == kMmaWarp) {
     if (lane == 0) {
-      prefetch_tmap(&tmQ); prefetch_tmap(&tmdO); prefetch_tmap(&tmK); prefetch_tmap(&tmV);
-      mbar_init(&B.q_full, 1);
-      for (int s = 0; s < 2; ++s) {
-        mbar_init(&B.k_full[s], 1); mbar_init(&B.v_full[s], 1); mbar_init(&B.kv_empty[s], 1);
-      }
+      mbar_init(&B.q_full, kProdWarps);
+      for (int s = 0; s < ST; ++s) { mbar_init(&B.kv_full[s], kProdWarps); mbar_init(&B.kv_empty[s], 1); }
       mbar_init(&B.sdp_full, 1);
       mbar_init(&B.pds_full, 128);
-      mbar_init(&B.dvdk_full, 1);
+      mbar_init(&B.mma_done, 1);
       mbar_init(&B.tmem_free, 128);
-      mbar_init(&B.dq_done, 1);
       fence_barrier_init();
     }
-  } else if (warp == 1) {
+    __syncwarp();
     tmem_alloc(&B.tmem, 512);
   }
   tc_fence_before();
@@ -373,33 +380,34 @@ sparse_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
   const uint32_t tmem = B.tmem;
   const uint32_t tA = tmem, tB = tmem + 128, tC = tmem + 256, tDq = tmem + 384;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ producer
-    {
-      const int4 m4 = *reinterpret_cast<const int4*>(mrow + lane * 4);
-      const int base = h * Lq;
-      if (lane == 0) mbar_arrive_expect_tx(&B.q_full, 2 * SL::kTile);
-      __syncwarp();
-      gather_tile<D>(sQ, &tmQ, &B.q_full, lane, base + m4.x, base + m4.y, base + m4.z, base + m4.w);
-      gather_tile<D>(sdO, &tmdO, &B.q_full, lane, base + m4.x, base + m4.y, base + m4.z, base + m4.w);
-    }
+  if (warp >= kProdWarp0) {
+    // ------------------------------------------------------------ producers
+    const int ptid = threadIdx.x - kProdWarp0 * 32;
+    const int r0 = ptid / GT::kCPR;
+    auto bar_of = [&](int grp) { return grp == 0 ? &B.q_full : &B.kv_full[(grp - 1) % ST]; };
+    int rows[GT::kPer];
+    const int qbase = h * Lq;
+#pragma unroll
+    for (int i = 0; i < GT::kPer; ++i) rows[i] = qbase + __ldg(mrow + r0 + i * GT::kRowStep);
+    issue_tile<D>(sQ, Qg, rows, ptid);
+    issue_tile<D>(sdO, dOg, rows, ptid);
+    cp_async_commit();
+    int committed = 1, retired = 0;
     const int kbase = h * Lk;
     for (int j = 0; j < nblk; ++j) {
       const int st = j % ST;
       if (j >= ST) mbar_wait(&B.kv_empty[st], ((j / ST) - 1) & 1);
-      const int p = j * BKV + lane * 4;
-      int r[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) r[i] = kbase + __ldg(irow + min(p + i, kh - 1));
-      if (lane == 0) {
-        mbar_arrive_expect_tx(&B.k_full[st], SL::kTile);
-        mbar_arrive_expect_tx(&B.v_full[st], SL::kTile);
-      }
-      __syncwarp();
-      gather_tile<D>(sK + st * SL::kTile, &tmK, &B.k_full[st], lane, r[0], r[1], r[2], r[3]);
-      gather_tile<D>(sV + st * SL::kTile, &tmV, &B.v_full[st], lane, r[0], r[1], r[2], r[3]);
+      for (int i = 0; i < GT::kPer; ++i)
+        rows[i] = kbase + __ldg(irow + min(j * BKV + r0 + i * GT::kRowStep, kh - 1));
+      issue_tile<D>(sK + st * SL::kTile, Kg, rows, ptid);
+      issue_tile<D>(sV + st * SL::kTile, Vg, rows, ptid);
+      cp_async_commit();
+      ++committed;
+      retire_groups<ST - 1>(committed, retired, bar_of);
     }
-  } else if (warp == 1) {
+    retire_groups<0>(committed, retired, bar_of);
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idST = idesc_bf16_f32(128, 128, 0, 0);   // K_j . Q^T, V_j . dO^T
     constexpr uint32_t idDV = idesc_bf16_f32(128, D, 0, 1);     // P^T(tmem) . dO(MN)
@@ -410,8 +418,7 @@ sparse_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
     for (int j = 0; j < nblk; ++j) {
       const int st = j % ST;
       const uint32_t aK = smem_u32(sK + st * SL::kTile), aV = smem_u32(sV + st * SL::kTile);
-      mbar_wait(&B.k_full[st], (j / ST) & 1);
-      mbar_wait(&B.v_full[st], (j / ST) & 1);
+      mbar_wait(&B.kv_full[st], (j / ST) & 1);
       if (j > 0) mbar_wait(&B.tmem_free, (j - 1) & 1);
       tc_fence_after();
       if (elect_one()) {
@@ -431,6 +438,11 @@ sparse_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
       mbar_wait(&B.pds_full, j & 1);
       tc_fence_after();
       if (elect_one()) {
+        // dQ += dS K_j    (A = dS MN-major in smem, B = K_j MN-major)
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ss(tDq, sdesc_sw128(adS + kk * 2048, 128 * 128, 1024),
+                 sdesc_sw128(aK + kk * 2048, 128 * 128, 1024), idDQ, (j | kk) != 0);
         // dV_j = P^T dO   (A = P^T in TMEM cols tA[0,64), K = 128 queries)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
@@ -443,22 +455,15 @@ sparse_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             mma_ts(tB + 64, tB + kk * 8, sdesc_sw128(aQ + 128 * 128 + kk * 2048, 128 * 128, 1024),
                    idDK, kk > 0);
         }
-        mma_commit(&B.dvdk_full);
-        // dQ += dS K_j    (A = dS MN-major in smem, B = K_j MN-major)
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          mma_ss(tDq, sdesc_sw128(adS + kk * 2048, 128 * 128, 1024),
-                 sdesc_sw128(aK + kk * 2048, 128 * 128, 1024), idDQ, (j | kk) != 0);
-        mma_commit(&B.dq_done);
+        mma_commit(&B.mma_done);
         mma_commit(&B.kv_empty[st]);
       }
       __syncwarp();
     }
   } else {
     // ------------------------------------------------------------ workers
-    const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;   // query row in prologue/epilogue; key row per block
-    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const int row = warp * 32 + lane;   // query row in prologue/epilogue; key row per block
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     const int gsz = grp_size[g];
     const int tok = mrow[row];
     {
@@ -481,13 +486,13 @@ sparse_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
       sDelta[row] = dlt;
       named_bar_sync(1, 128);
     }
+    uint8_t* stg = sdS + warp * 8192;   // per-warp scatter staging (2 x 4 KB), reuses the dS tile
     for (int j = 0; j < nblk; ++j) {
       const int kv = min(BKV, kh - j * BKV);
       const bool kvalid = row < kv;
       const int key = kvalid ? __ldg(irow + j * BKV + row) : 0;
       mbar_wait(&B.sdp_full, j & 1);
       tc_fence_after();
-      if (j > 0) mbar_wait(&B.dq_done, (j - 1) & 1);   // dQ_{j-1} done reading sdS
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         uint32_t rs[32], rd[32];
@@ -519,34 +524,40 @@ sparse_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&B.pds_full);
-      // ---- scatter dV_j, dK_j rows of this key into the fp32 accumulators
-      mbar_wait(&B.dvdk_full, j & 1);
+      // ---- scatter dV_j, dK_j: per-warp smem transpose, then row-contiguous red.v4
+      mbar_wait(&B.mma_done, j & 1);
       tc_fence_after();
-      float* dvrow = dV + ((long long)h * Lk + key) * D;
-      float* dkrow = dK + ((long long)h * Lk + key) * D;
+      const long long hoff = (long long)h * Lk * D;
 #pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t rv[32], rk[32];
-        tmem_ld32(tC + lane_off + c * 32, rv);
-        // dK columns [0,64) live in tA[64,128), [64,128) in tB[64,128)
-        tmem_ld32((c < 2 ? tA : tB) + 64 + lane_off + (c & 1) * 32, rk);
+      for (int n = 0; n < 2 * (D / 32); ++n) {
+        const int t = n / (D / 32), c = n % (D / 32);
+        const uint32_t taddr = t == 0 ? tC + c * 32 : (c < 2 ? tA : tB) + 64 + (c & 1) * 32;
+        uint32_t r[32];
+        tmem_ld32(taddr + lane_off, r);
         tmem_ld_wait();
-        if (kvalid) {
+        uint8_t* buf = stg + (n & 1) * 4096;
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            red_add_v4(dvrow + c * 32 + i, __uint_as_float(rv[i]), __uint_as_float(rv[i + 1]),
-                       __uint_as_float(rv[i + 2]), __uint_as_float(rv[i + 3]));
-            red_add_v4(dkrow + c * 32 + i, __uint_as_float(rk[i]), __uint_as_float(rk[i + 1]),
-                       __uint_as_float(rk[i + 2]), __uint_as_float(rk[i + 3]));
-          }
+        for (int qd = 0; qd < 8; ++qd)
+          *reinterpret_cast<uint4*>(buf + lane * 128 + ((qd ^ (lane & 7)) << 4)) =
+              make_uint4(r[4 * qd], r[4 * qd + 1], r[4 * qd + 2], r[4 * qd + 3]);
+        __syncwarp();
+        float* acc = (t == 0 ? dV : dK) + hoff + c * 32 + (lane & 7) * 4;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int rr = (lane >> 3) + 4 * i;
+          const uint4 v = *reinterpret_cast<const uint4*>(buf + rr * 128 + (((lane & 7) ^ (rr & 7)) << 4));
+          const int krr = __shfl_sync(0xffffffffu, key, rr);
+          const int okr = __shfl_sync(0xffffffffu, (int)kvalid, rr);
+          if (okr)
+            red_add_v4(acc + (long long)krr * D, __uint_as_float(v.x), __uint_as_float(v.y),
+                       __uint_as_float(v.z), __uint_as_float(v.w));
         }
+        __syncwarp();
       }
       tc_fence_before();
       mbar_arrive(&B.tmem_free);
     }
-    // ---------------- dQ epilogue (query rows)
-    mbar_wait(&B.dq_done, (nblk - 1) & 1);
-    tc_fence_after();
+    // ---------------- dQ epilogue (query rows); the last mma_done covered dQ
     __nv_bfloat16* qrow = dQ + ((long long)h * Lq + tok) * D;
 #pragma unroll 1
     for (int c = 0; c < D / 32; ++c) {
@@ -566,7 +577,7 @@ sparse_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, 512);
+  if (warp == kMmaWarp) tmem_dealloc(tmem, 512);
 }
 
 __global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
@@ -585,61 +596,57 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* 
 
 using namespace dsv::attn;
 
-template <int D, bool PT>
-static int fwd_launch(const CUtensorMap* tq, const CUtensorMap* tk, const CUtensorMap* tv,
-                      const int* grp_rows, const int* grp_size, const int* idx, long long ldk,
-                      const int* kcount, int H, int G, int Lq, int Lk, float scale_log2,
-                      void* O, float* lse, cudaStream_t st) {
-  auto kern = sparse_fwd_kernel<D, PT>;
+template <int D>
+static int fwd_launch(const void* q, const void* k, const void* v, const int* grp_rows,
+                      const int* grp_size, const int* idx, long long ldk, const int* kcount, int H,
+                      int G, int Lq, int Lk, float scale_log2, void* O, float* lse, cudaStream_t st) {
+  auto kern = sparse_fwd_kernel<D>;
   const int smem = FwdSmem<D>::kBytes;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  kern<<<H * G, kThreads, smem, st>>>(*tq, *tk, *tv, grp_rows, grp_size, idx, ldk, kcount, G, Lq,
-                                      Lk, scale_log2, (__nv_bfloat16*)O, lse);
+  kern<<<H * G, kThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
+                                      (const __nv_bfloat16*)v, grp_rows, grp_size, idx, ldk,
+                                      kcount, G, Lq, Lk, scale_log2, (__nv_bfloat16*)O, lse);
   return (int)cudaGetLastError();
 }
 
-int dsv_attn_fwd_tc_launch(const CUtensorMap* tq, const CUtensorMap* tk, const CUtensorMap* tv,
-                           const int* grp_rows, const int* grp_size, const int* idx,
-                           long long ldk, const int* kcount, int H, int G, int Lq, int Lk, int D,
-                           float scale_log2, int p_in_tmem, void* O, float* lse,
-                           cudaStream_t st) {
+int dsv_attn_fwd_tc_launch(const void* q, const void* k, const void* v, const int* grp_rows,
+                           const int* grp_size, const int* idx, long long ldk, const int* kcount,
+                           int H, int G, int Lq, int Lk, int D, float scale_log2, void* O,
+                           float* lse, cudaStream_t st) {
   if (D == 128)
-    return p_in_tmem ? fwd_launch<128, true>(tq, tk, tv, grp_rows, grp_size, idx, ldk, kcount, H, G, Lq, Lk, scale_log2, O, lse, st)
-                     : fwd_launch<128, false>(tq, tk, tv, grp_rows, grp_size, idx, ldk, kcount, H, G, Lq, Lk, scale_log2, O, lse, st);
+    return fwd_launch<128>(q, k, v, grp_rows, grp_size, idx, ldk, kcount, H, G, Lq, Lk, scale_log2, O, lse, st);
   if (D == 64)
-    return p_in_tmem ? fwd_launch<64, true>(tq, tk, tv, grp_rows, grp_size, idx, ldk, kcount, H, G, Lq, Lk, scale_log2, O, lse, st)
-                     : fwd_launch<64, false>(tq, tk, tv, grp_rows, grp_size, idx, ldk, kcount, H, G, Lq, Lk, scale_log2, O, lse, st);
+    return fwd_launch<64>(q, k, v, grp_rows, grp_size, idx, ldk, kcount, H, G, Lq, Lk, scale_log2, O, lse, st);
   return 1;
 }
 
 template <int D>
-static int bwd_launch(const CUtensorMap* tq, const CUtensorMap* tdo, const CUtensorMap* tk,
-                      const CUtensorMap* tv, const void* O, const void* dO, const float* lse,
-                      const int* grp_rows, const int* grp_size, const int* idx, long long ldk,
-                      const int* kcount, int H, int G, int Lq, int Lk, float scale,
+static int bwd_launch(const void* q, const void* k, const void* v, const void* O, const void* dO,
+                      const float* lse, const int* grp_rows, const int* grp_size, const int* idx,
+                      long long ldk, const int* kcount, int H, int G, int Lq, int Lk, float scale,
                       float scale_log2, void* dQ, float* dK, float* dV, cudaStream_t st) {
   auto kern = sparse_bwd_kernel<D>;
   const int smem = BwdSmem<D>::kBytes;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  kern<<<H * G, kThreads, smem, st>>>(*tq, *tdo, *tk, *tv, (const __nv_bfloat16*)O,
-                                      (const __nv_bfloat16*)dO, lse, grp_rows, grp_size, idx, ldk,
+  kern<<<H * G, kThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)dO,
+                                      (const __nv_bfloat16*)k, (const __nv_bfloat16*)v,
+                                      (const __nv_bfloat16*)O, lse, grp_rows, grp_size, idx, ldk,
                                       kcount, G, Lq, Lk, scale, scale_log2, (__nv_bfloat16*)dQ,
                                       dK, dV);
   return (int)cudaGetLastError();
 }
 
-int dsv_attn_bwd_tc_launch(const CUtensorMap* tq, const CUtensorMap* tdo, const CUtensorMap* tk,
-                           const CUtensorMap* tv, const void* O, const void* dO, const float* lse,
-                           const int* grp_rows, const int* grp_size, const int* idx,
-                           long long ldk, const int* kcount, int H, int G, int Lq, int Lk, int D,
-                           float scale, float scale_log2, void* dQ, float* dK, float* dV,
-                           cudaStream_t st) {
+int dsv_attn_bwd_tc_launch(const void* q, const void* k, const void* v, const void* O,
+                           const void* dO, const float* lse, const int* grp_rows,
+                           const int* grp_size, const int* idx, long long ldk, const int* kcount,
+                           int H, int G, int Lq, int Lk, int D, float scale, float scale_log2,
+                           void* dQ, float* dK, float* dV, cudaStream_t st) {
   if (D == 128)
-    return bwd_launch<128>(tq, tdo, tk, tv, O, dO, lse, grp_rows, grp_size, idx, ldk, kcount, H, G,
-                           Lq, Lk, scale, scale_log2, dQ, dK, dV, st);
+    return bwd_launch<128>(q, k, v, O, dO, lse, grp_rows, grp_size, idx, ldk, kcount, H, G, Lq, Lk,
+                           scale, scale_log2, dQ, dK, dV, st);
   if (D == 64)
-    return bwd_launch<64>(tq, tdo, tk, tv, O, dO, lse, grp_rows, grp_size, idx, ldk, kcount, H, G,
-                          Lq, Lk, scale, scale_log2, dQ, dK, dV, st);
+    return bwd_launch<64>(q, k, v, O, dO, lse, grp_rows, grp_size, idx, ldk, kcount, H, G, Lq, Lk,
+                          scale, scale_log2, dQ, dK, dV, st);
   return 1;
 }
 

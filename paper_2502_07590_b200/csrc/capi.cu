@@ -25,13 +25,13 @@ int dsv_rows_bwd_launch(const void*, const void*, const void*, const float*, con
                         float*, float*, float*, cudaStream_t);
 int dsv_gemm_launch(const CUtensorMap*, const CUtensorMap*, void*, int, int, int, long long,
                     long long, int, int, int, cudaStream_t);
-int dsv_attn_fwd_tc_launch(const CUtensorMap*, const CUtensorMap*, const CUtensorMap*, const int*,
-                           const int*, const int*, long long, const int*, int, int, int, int, int,
-                           float, int, void*, float*, cudaStream_t);
-int dsv_attn_bwd_tc_launch(const CUtensorMap*, const CUtensorMap*, const CUtensorMap*,
-                           const CUtensorMap*, const void*, const void*, const float*, const int*,
-                           const int*, const int*, long long, const int*, int, int, int, int, int,
-                           float, float, void*, float*, float*, cudaStream_t);
+int dsv_attn_fwd_tc_launch(const void*, const void*, const void*, const int*, const int*,
+                           const int*, long long, const int*, int, int, int, int, int, float,
+                           void*, float*, cudaStream_t);
+int dsv_attn_bwd_tc_launch(const void*, const void*, const void*, const void*, const void*,
+                           const float*, const int*, const int*, const int*, long long,
+                           const int*, int, int, int, int, int, float, float, void*, float*,
+                           float*, cudaStream_t);
 int dsv_f32_to_bf16_launch(const float*, void*, long long, cudaStream_t);
 
 namespace {
@@ -85,14 +85,6 @@ bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
-}
-
-// Row-gather map over a [rows][D] bf16 matrix (contiguous rows): box = 64 columns x 1 row.
-bool make_gather_map(CUtensorMap* m, const void* base, long long rows, int D) {
-  const uint64_t dims[2] = {(uint64_t)D, (uint64_t)rows};
-  const uint64_t strides[1] = {(uint64_t)D * 2};
-  const uint32_t box[2] = {64, 1};
-  return make_map(m, base, 2, dims, strides, box);
 }
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -175,14 +167,10 @@ int dsv_sparse_fwd(const void* q, const void* k, const void* v, const int* grp_r
     return fail(DSV_EINVAL, "sparse_fwd: empty shape");
   if (!al16(q) || !al16(k) || !al16(v) || !al16(out) || !al16(grp_rows))
     return fail(DSV_EINVAL, "sparse_fwd: pointers must be 16-byte aligned");
-  CUtensorMap tq, tk, tv;
-  if (!make_gather_map(&tq, q, (long long)H * Lq, D) || !make_gather_map(&tk, k, (long long)H * Lk, D) ||
-      !make_gather_map(&tv, v, (long long)H * Lk, D))
-    return fail(DSV_ECUDA, "sparse_fwd: tensor map encode failed");
+  (void)flags;
   const float scale_log2 = scale * 1.4426950408889634f;
-  return cuda_status(dsv_attn_fwd_tc_launch(&tq, &tk, &tv, grp_rows, grp_size, idx, ldk, kcount,
-                                            H, G, Lq, Lk, D, scale_log2, (flags & 1) ? 0 : 1,
-                                            out, lse, S(stream)),
+  return cuda_status(dsv_attn_fwd_tc_launch(q, k, v, grp_rows, grp_size, idx, ldk, kcount, H, G,
+                                            Lq, Lk, D, scale_log2, out, lse, S(stream)),
                      "sparse_fwd launch");
 }
 
@@ -196,15 +184,10 @@ int dsv_sparse_bwd(const void* q, const void* k, const void* v, const void* out,
   if (!al16(q) || !al16(k) || !al16(v) || !al16(out) || !al16(dout) || !al16(dq) ||
       !al16(dk_acc) || !al16(dv_acc) || !al16(grp_rows))
     return fail(DSV_EINVAL, "sparse_bwd: pointers must be 16-byte aligned");
-  CUtensorMap tq, tdo, tk, tv;
-  if (!make_gather_map(&tq, q, (long long)H * Lq, D) ||
-      !make_gather_map(&tdo, dout, (long long)H * Lq, D) ||
-      !make_gather_map(&tk, k, (long long)H * Lk, D) || !make_gather_map(&tv, v, (long long)H * Lk, D))
-    return fail(DSV_ECUDA, "sparse_bwd: tensor map encode failed");
   const float scale_log2 = scale * 1.4426950408889634f;
-  return cuda_status(dsv_attn_bwd_tc_launch(&tq, &tdo, &tk, &tv, out, dout, lse, grp_rows,
-                                            grp_size, idx, ldk, kcount, H, G, Lq, Lk, D, scale,
-                                            scale_log2, dq, dk_acc, dv_acc, S(stream)),
+  return cuda_status(dsv_attn_bwd_tc_launch(q, k, v, out, dout, lse, grp_rows, grp_size, idx, ldk,
+                                            kcount, H, G, Lq, Lk, D, scale, scale_log2, dq, dk_acc,
+                                            dv_acc, S(stream)),
                      "sparse_bwd launch");
 }
 

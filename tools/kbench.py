@@ -61,9 +61,8 @@ def main():
     q, kk, v, do = (torch.randn((H, L, D), device=dev, generator=g).to(torch.bfloat16) for _ in range(4))
     rows, size = plan.tables(dev)
     fl_f = 4 * L * k * D * H
-    for pt in (True, False):
-        t = timeit(lambda: ops.sparse_fwd(q, kk, v, rows, size, idx, kp, p_in_tmem=pt))
-        print(f"fwd(ptmem={int(pt)}) {t:8.3f} ms  {fl_f / t / 1e9:8.1f} TFLOP/s")
+    t = timeit(lambda: ops.sparse_fwd(q, kk, v, rows, size, idx, kp))
+    print(f"fwd       {t:8.3f} ms  {fl_f / t / 1e9:8.1f} TFLOP/s")
     o, lse = ops.sparse_fwd(q, kk, v, rows, size, idx, kp)
     dk = torch.zeros((H, L, D), device=dev, dtype=torch.float32)
     dv = torch.zeros_like(dk)
