@@ -82,6 +82,10 @@ DSV_DEV void retire_groups(int committed, int& retired, BarOf bar_of) {
 
 // ====================================================================== fwd
 constexpr int kFwdStages = 3;
+constexpr int kFwdSoftWGs = 2;                                   // warps 0-7
+constexpr int kFwdMmaWarp = 8;
+constexpr int kFwdProdWarp0 = 9;
+constexpr int kFwdThreads = (kFwdSoftWGs * 4 + 1 + kProdWarps) * 32;   // 544
 
 template <int D>
 struct FwdSmem {
@@ -89,6 +93,7 @@ struct FwdSmem {
   static constexpr int kQ = 0;
   static constexpr int kK = kQ + kTile;
   static constexpr int kV = kK + kFwdStages * kTile;
+  static constexpr int kML = kQ;   // [2 WG][2][128] floats, reuses Q once all MMAs are done
   static constexpr int kBar = kV + kFwdStages * kTile;
   static constexpr int kBytes = kBar + 256 + 1024;
 };
@@ -97,12 +102,44 @@ struct FwdBars {
   uint64_t q_full;
   uint64_t kv_full[kFwdStages], kv_empty[kFwdStages];
   uint64_t s_full[2], p_full[2];
-  uint64_t o_ready, o_final;
+  uint64_t o_final;
   uint32_t tmem;
 };
 
+// Shared-memory base aligned to 1024 B without leaving the shared address space.
+DSV_DEV uint8_t* aligned_smem(uint8_t* raw) {
+  return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+}
+
+// Softmax pass 2 over one S buffer: P = 2^(s*scale_log2 - m) (bf16) written over
+// the S columns already read; returns the row sum of P.
+template <bool kMasked>
+DSV_DEV float softmax_p_pass(uint32_t tS, float scale_log2, float m, int kv) {
+  float lsum = 0.f;
+#pragma unroll 1
+  for (int c = 0; c < BKV / 32; ++c) {
+    uint32_t r[32];
+    tmem_ld32(tS + c * 32, r);
+    tmem_ld_wait();
+    uint32_t pk[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      float p0 = fast_exp2(fmaf(__uint_as_float(r[2 * i]), scale_log2, -m));
+      float p1 = fast_exp2(fmaf(__uint_as_float(r[2 * i + 1]), scale_log2, -m));
+      if constexpr (kMasked) {
+        if (c * 32 + 2 * i >= kv) p0 = 0.f;
+        if (c * 32 + 2 * i + 1 >= kv) p1 = 0.f;
+      }
+      lsum += p0 + p1;
+      pk[i] = pack_bf16(p0, p1);
+    }
+    tmem_st16(tS + c * 16, pk);
+  }
+  return lsum;
+}
+
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kFwdThreads, 1)
 sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __restrict__ Kg,
                   const __nv_bfloat16* __restrict__ Vg, const int* __restrict__ grp_rows,
                   const int* __restrict__ grp_size, const int* __restrict__ idx, long long ldk,
@@ -111,12 +148,13 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   using SL = FwdSmem<D>;
   using GT = Gather<D>;
   constexpr int ST = kFwdStages;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = aligned_smem(smem_raw);
   FwdBars& B = *reinterpret_cast<FwdBars*>(smem + SL::kBar);
   uint8_t* sQ = smem + SL::kQ;
   uint8_t* sK = smem + SL::kK;
   uint8_t* sV = smem + SL::kV;
+  float* sML = reinterpret_cast<float*>(smem + SL::kML);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = blockIdx.x / G, g = blockIdx.x - h * G;
@@ -125,12 +163,11 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   const int* irow = idx + ((long long)h * G + g) * ldk;
   const int* mrow = grp_rows + (long long)g * BQ;
 
-  if (warp == kMmaWarp) {
+  if (warp == kFwdMmaWarp) {
     if (lane == 0) {
       mbar_init(&B.q_full, kProdWarps);
       for (int s = 0; s < ST; ++s) { mbar_init(&B.kv_full[s], kProdWarps); mbar_init(&B.kv_empty[s], 1); }
       for (int s = 0; s < 2; ++s) { mbar_init(&B.s_full[s], 1); mbar_init(&B.p_full[s], 128); }
-      mbar_init(&B.o_ready, 1);
       mbar_init(&B.o_final, 1);
       fence_barrier_init();
     }
@@ -141,11 +178,11 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = B.tmem;
-  const uint32_t tS0 = tmem, tO = tmem + 256;
+  const uint32_t tS0 = tmem, tO0 = tmem + 256;   // S_b at tS0 + 128 b, O_w at tO0 + 128 w
 
-  if (warp >= kProdWarp0) {
+  if (warp >= kFwdProdWarp0) {
     // ------------------------------------------------------------ producers
-    const int ptid = threadIdx.x - kProdWarp0 * 32;
+    const int ptid = threadIdx.x - kFwdProdWarp0 * 32;
     const int r0 = ptid / GT::kCPR;
     auto bar_of = [&](int grp) { return grp == 0 ? &B.q_full : &B.kv_full[(grp - 1) % ST]; };
     int rows[GT::kPer];
@@ -158,10 +195,10 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
     const int kbase = h * Lk;
     for (int j = 0; j < nblk; ++j) {
       const int st = j % ST;
-      if (j >= ST) mbar_wait(&B.kv_empty[st], ((j / ST) - 1) & 1);
 #pragma unroll
       for (int i = 0; i < GT::kPer; ++i)
         rows[i] = kbase + __ldg(irow + min(j * BKV + r0 + i * GT::kRowStep, kh - 1));
+      if (j >= ST) mbar_wait(&B.kv_empty[st], ((j / ST) - 1) & 1);
       issue_tile<D>(sK + st * SL::kTile, Kg, rows, ptid);
       issue_tile<D>(sV + st * SL::kTile, Vg, rows, ptid);
       cp_async_commit();
@@ -171,7 +208,7 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
       retire_groups<ST - 2>(committed, retired, bar_of);
     }
     retire_groups<0>(committed, retired, bar_of);
-  } else if (warp == kMmaWarp) {
+  } else if (warp == kFwdMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idS = idesc_bf16_f32(128, BKV, 0, 0);
     constexpr uint32_t idO = idesc_bf16_f32(128, D, 0, 1);
@@ -196,115 +233,117 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
         __syncwarp();
       }
       if (j >= 1) {
-        const int jp = j - 1, st = jp % ST;
-        mbar_wait(&B.p_full[jp & 1], (jp >> 1) & 1);
+        const int jp = j - 1, st = jp % ST, w = jp & 1;
+        mbar_wait(&B.p_full[w], (jp >> 1) & 1);
         tc_fence_after();
         if (elect_one()) {
           const uint32_t aV = smem_u32(sV + st * SL::kTile);
 #pragma unroll
           for (int kk = 0; kk < BKV / 16; ++kk)
-            mma_ts(tO, tS0 + (jp & 1) * 128 + kk * 8,
-                   sdesc_sw128(aV + kk * 2048, 128 * 128, 1024), idO, (jp | kk) != 0);
+            mma_ts(tO0 + w * 128, tS0 + w * 128 + kk * 8,
+                   sdesc_sw128(aV + kk * 2048, 128 * 128, 1024), idO, (jp >= 2 || kk > 0));
           mma_commit(&B.kv_empty[st]);
-          mma_commit(&B.o_ready);
           if (jp == nblk - 1) mma_commit(&B.o_final);
         }
         __syncwarp();
       }
     }
   } else {
-    // ------------------------------------------------------------ softmax
-    const int row = warp * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    // ------------------------------------------------------------ softmax WGs
+    // WG w takes blocks j = w, w+2, ... with its own (m, l) and O_w accumulator.
+    // When it sees S_j, PV_{j-2} (the last writer of O_w) has completed: the
+    // MMA issued S_j after PV_{j-2}, and S_j's commit covers all prior MMAs.
+    const int wg = warp >> 2, wq = warp & 3;
+    const int row = wq * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    const uint32_t tS = tS0 + wg * 128 + lane_off;
+    const uint32_t tO = tO0 + wg * 128 + lane_off;
     float m_run = -INFINITY, l_run = 0.f;
-    for (int j = 0; j < nblk; ++j) {
-      const int sb = j & 1;
+    for (int j = wg; j < nblk; j += 2) {
       const int kv = min(BKV, kh - j * BKV);
-      const uint32_t tS = tS0 + sb * 128 + lane_off;
-      mbar_wait(&B.s_full[sb], (j >> 1) & 1);
+      mbar_wait(&B.s_full[wg], (j >> 1) & 1);
       tc_fence_after();
-      // pass 1: block row max
       float mx = -INFINITY;
 #pragma unroll 1
       for (int c = 0; c < BKV / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(tS + c * 32, r);
         tmem_ld_wait();
+        if (kv == BKV) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c * 32 + i < kv) mx = fmaxf(mx, __uint_as_float(r[i]));
+          for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c * 32 + i < kv) mx = fmaxf(mx, __uint_as_float(r[i]));
+        }
       }
       mx *= scale_log2;
-      if (j == 0) {
+      if (j == wg) {
         m_run = mx;
       } else if (mx > m_run + 8.f) {
-        // O correction: wait for PV_{j-1}, rescale O and l by 2^(m_run - mx)
-        mbar_wait(&B.o_ready, (j - 1) & 1);
-        tc_fence_after();
         const float alpha = fast_exp2(m_run - mx);
         l_run *= alpha;
 #pragma unroll 1
         for (int c = 0; c < D / 16; ++c) {
           uint32_t r[16];
-          tmem_ld16(tO + lane_off + c * 16, r);
+          tmem_ld16(tO + c * 16, r);
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-          tmem_st16(tO + lane_off + c * 16, r);
+          tmem_st16(tO + c * 16, r);
         }
         tmem_st_wait();
         m_run = mx;
       }
-      // pass 2: P = 2^(s*scale_log2 - m) in bf16 over the S columns already read
-      float lsum = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < BKV / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tS + c * 32, r);
-        tmem_ld_wait();
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int col = c * 32 + 2 * i;
-          const float p0 = col < kv ? fast_exp2(fmaf(__uint_as_float(r[2 * i]), scale_log2, -m_run)) : 0.f;
-          const float p1 = col + 1 < kv ? fast_exp2(fmaf(__uint_as_float(r[2 * i + 1]), scale_log2, -m_run)) : 0.f;
-          pk[i] = pack_bf16(p0, p1);
-          lsum += bf16lo(pk[i]) + bf16hi(pk[i]);
-        }
-        tmem_st16(tS + c * 16, pk);
-      }
-      l_run += lsum;
+      l_run += (kv == BKV) ? softmax_p_pass<false>(tS, scale_log2, m_run, kv)
+                           : softmax_p_pass<true>(tS, scale_log2, m_run, kv);
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&B.p_full[sb]);
+      mbar_arrive(&B.p_full[wg]);
     }
-    // ---------------- epilogue
+    // ---------------- epilogue: merge the two WGs' partial softmax states
     mbar_wait(&B.o_final, 0);
     tc_fence_after();
+    sML[(wg * 2 + 0) * 128 + row] = m_run;
+    sML[(wg * 2 + 1) * 128 + row] = l_run;
+    named_bar_sync(1, 256);
+    const float m0 = sML[0 * 128 + row], l0 = sML[1 * 128 + row];
+    const float m1 = sML[2 * 128 + row], l1 = sML[3 * 128 + row];
+    const float m = fmaxf(m0, m1);
+    const float a0 = l0 > 0.f ? fast_exp2(m0 - m) : 0.f;
+    const float a1 = l1 > 0.f ? fast_exp2(m1 - m) : 0.f;
+    const float denom = l0 * a0 + l1 * a1;
+    const float inv = 1.f / denom;
+    const float c0 = a0 * inv, c1 = a1 * inv;
     const int gsz = grp_size[g];
     const int tok = mrow[row];
-    const float inv = 1.f / l_run;
     __nv_bfloat16* orow = O + ((long long)h * Lq + tok) * D;
+    constexpr int kChunks = D / 32;
 #pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t r[32];
-      tmem_ld32(tO + lane_off + c * 32, r);
+    for (int c = wg * (kChunks / 2); c < (wg + 1) * (kChunks / 2); ++c) {
+      uint32_t r0[32], r1[32];
+      tmem_ld32(tO0 + lane_off + c * 32, r0);
+      tmem_ld32(tO0 + 128 + lane_off + c * 32, r1);
       tmem_ld_wait();
       if (row < gsz) {
+        float o[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          o[i] = (a0 > 0.f ? __uint_as_float(r0[i]) * c0 : 0.f) +
+                 (a1 > 0.f ? __uint_as_float(r1[i]) * c1 : 0.f);
 #pragma unroll
         for (int i = 0; i < 32; i += 8)
-          *reinterpret_cast<uint4*>(orow + c * 32 + i) = make_uint4(
-              pack_bf16(__uint_as_float(r[i]) * inv, __uint_as_float(r[i + 1]) * inv),
-              pack_bf16(__uint_as_float(r[i + 2]) * inv, __uint_as_float(r[i + 3]) * inv),
-              pack_bf16(__uint_as_float(r[i + 4]) * inv, __uint_as_float(r[i + 5]) * inv),
-              pack_bf16(__uint_as_float(r[i + 6]) * inv, __uint_as_float(r[i + 7]) * inv));
+          *reinterpret_cast<uint4*>(orow + c * 32 + i) =
+              make_uint4(pack_bf16(o[i], o[i + 1]), pack_bf16(o[i + 2], o[i + 3]),
+                         pack_bf16(o[i + 4], o[i + 5]), pack_bf16(o[i + 6], o[i + 7]));
       }
     }
-    if (row < gsz) lse[(long long)h * Lq + tok] = m_run + __log2f(l_run);
+    if (wg == 0 && row < gsz) lse[(long long)h * Lq + tok] = m + __log2f(denom);
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == kMmaWarp) tmem_dealloc(tmem, 512);
+  if (warp == kFwdMmaWarp) tmem_dealloc(tmem, 512);
 }
 
 // ====================================================================== bwd
@@ -343,8 +382,8 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   using SL = BwdSmem<D>;
   using GT = Gather<D>;
   constexpr int ST = kBwdStages;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = aligned_smem(smem_raw);
   BwdBars& B = *reinterpret_cast<BwdBars*>(smem + SL::kBar);
   uint8_t* sQ = smem + SL::kQ;
   uint8_t* sdO = smem + SL::kdO;
@@ -603,7 +642,7 @@ static int fwd_launch(const void* q, const void* k, const void* v, const int* gr
   auto kern = sparse_fwd_kernel<D>;
   const int smem = FwdSmem<D>::kBytes;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  kern<<<H * G, kThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
+  kern<<<H * G, kFwdThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
                                       (const __nv_bfloat16*)v, grp_rows, grp_size, idx, ldk,
                                       kcount, G, Lq, Lk, scale_log2, (__nv_bfloat16*)O, lse);
   return (int)cudaGetLastError();
