@@ -67,19 +67,6 @@ DSV_DEV void issue_tile(uint8_t* tile, const __nv_bfloat16* base,
     cp_async16(t0 + sw128_off(r0 + i * G::kRowStep, q & 7), base + (long long)rows[i] * D + q * 8);
 }
 
-// Producer-side bookkeeping: cp.async groups are retired in order; retiring a
-// group makes its bytes visible to the tensor core (proxy fence) and arrives on
-// the group's "full" barrier (one arrival per producer warp).
-template <int kAllow, typename BarOf>
-DSV_DEV void retire_groups(int committed, int& retired, BarOf bar_of) {
-  if (committed - retired <= kAllow) return;
-  cp_async_wait<kAllow>();
-  fence_proxy_async_smem();
-  __syncwarp();
-  for (; retired < committed - kAllow; ++retired)
-    if ((threadIdx.x & 31) == 0) mbar_arrive(bar_of(retired));
-}
-
 // ====================================================================== fwd
 constexpr int kFwdStages = 3;
 constexpr int kFwdSoftWGs = 2;                                   // warps 0-7
@@ -165,8 +152,8 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
 
   if (warp == kFwdMmaWarp) {
     if (lane == 0) {
-      mbar_init(&B.q_full, kProdWarps);
-      for (int s = 0; s < ST; ++s) { mbar_init(&B.kv_full[s], kProdWarps); mbar_init(&B.kv_empty[s], 1); }
+      mbar_init(&B.q_full, kProdThreads);
+      for (int s = 0; s < ST; ++s) { mbar_init(&B.kv_full[s], kProdThreads); mbar_init(&B.kv_empty[s], 1); }
       for (int s = 0; s < 2; ++s) { mbar_init(&B.s_full[s], 1); mbar_init(&B.p_full[s], 128); }
       mbar_init(&B.o_final, 1);
       fence_barrier_init();
@@ -182,16 +169,16 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
 
   if (warp >= kFwdProdWarp0) {
     // ------------------------------------------------------------ producers
+    // cp.async copies arrive on the stage's "full" barrier asynchronously
+    // (cp.async.mbarrier.arrive.noinc: one arrival per producer thread).
     const int ptid = threadIdx.x - kFwdProdWarp0 * 32;
     const int r0 = ptid / GT::kCPR;
-    auto bar_of = [&](int grp) { return grp == 0 ? &B.q_full : &B.kv_full[(grp - 1) % ST]; };
     int rows[GT::kPer];
     const int qbase = h * Lq;
 #pragma unroll
     for (int i = 0; i < GT::kPer; ++i) rows[i] = qbase + __ldg(mrow + r0 + i * GT::kRowStep);
     issue_tile<D>(sQ, Qg, rows, ptid);
-    cp_async_commit();
-    int committed = 1, retired = 0;
+    cp_async_arrive_noinc(&B.q_full);
     const int kbase = h * Lk;
     for (int j = 0; j < nblk; ++j) {
       const int st = j % ST;
@@ -201,13 +188,9 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
       if (j >= ST) mbar_wait(&B.kv_empty[st], ((j / ST) - 1) & 1);
       issue_tile<D>(sK + st * SL::kTile, Kg, rows, ptid);
       issue_tile<D>(sV + st * SL::kTile, Vg, rows, ptid);
-      cp_async_commit();
-      ++committed;
-      // the MMA issues S_{j+1} before PV_j, so block j+1 must be visible before
-      // this thread can block on kv_empty for block j+ST: keep <= ST-2 in flight
-      retire_groups<ST - 2>(committed, retired, bar_of);
+      cp_async_arrive_noinc(&B.kv_full[st]);
     }
-    retire_groups<0>(committed, retired, bar_of);
+    cp_async_wait<0>();
   } else if (warp == kFwdMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idS = idesc_bf16_f32(128, BKV, 0, 0);
@@ -347,28 +330,42 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
 }
 
 // ====================================================================== bwd
-constexpr int kBwdStages = 2;
-
+// Per KV block j (keys in TMEM lanes):
+//   A_j  MMA   S^T = K_j Q^T -> tA, dP^T = V_j dO^T -> tB          (V_j free after)
+//   B_j  work  P^T, dS^T (bf16) over tA/tB, dS -> smem
+//   C_j  MMA   dQ += dS K_j -> tDq (K_j free), dV_j -> tC, dK_j -> tA[64:] | tB[64:]
+//   C'_j work  dV_j, dK_j rows -> bf16 staging in smem; TMEM released
+//   D_j  prod  staging -> coalesced red.v4 into the fp32 dK/dV accumulators
+// D_j (bounded by the L2 reduction rate) overlaps A..C' of block j+1. Staging the
+// per-block contributions in bf16 rounds each contribution like P and dS already
+// are; the accumulation itself stays fp32.
 template <int D>
 struct BwdSmem {
   static constexpr int kTile = 128 * D * 2;
   static constexpr int kQ = 0;
   static constexpr int kdO = kQ + kTile;
-  static constexpr int kdS = kdO + kTile;                 // [128 keys][128 q] bf16; scatter staging
+  static constexpr int kdS = kdO + kTile;                 // [128 keys][128 q] bf16 (MN-major A)
   static constexpr int kK = kdS + 128 * 128 * 2;
-  static constexpr int kV = kK + kBwdStages * kTile;
-  static constexpr int kLse = kV + kBwdStages * kTile;
+  static constexpr int kV = kK + kTile;
+  static constexpr int kStg = kV + kTile;                 // [2 tensors][128 rows][D] bf16
+  static constexpr int kLse = kStg + 2 * 128 * D * 2;
   static constexpr int kDelta = kLse + 512;
   static constexpr int kBar = kDelta + 512;
   static constexpr int kBytes = kBar + 256 + 1024;
 };
 
 struct BwdBars {
-  uint64_t q_full;
-  uint64_t kv_full[kBwdStages], kv_empty[kBwdStages];
-  uint64_t sdp_full, pds_full, mma_done, tmem_free;
+  uint64_t q_full, k_full, v_full, k_empty, v_empty;
+  uint64_t sdp_full, pds_full, mma_done, tmem_free, stg_full, stg_free;
   uint32_t tmem;
 };
+
+// byte offset of 16-byte chunk q of staging row p (rows of D bf16, XOR-swizzled)
+template <int D>
+DSV_DEV uint32_t stg_off(int p, int q) {
+  constexpr int kC = D / 8;   // chunks per row
+  return (uint32_t)(p * (D * 2) + ((q ^ (p & (kC - 1))) << 4));
+}
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -381,7 +378,6 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
                   __nv_bfloat16* __restrict__ dQ, float* __restrict__ dK, float* __restrict__ dV) {
   using SL = BwdSmem<D>;
   using GT = Gather<D>;
-  constexpr int ST = kBwdStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = aligned_smem(smem_raw);
   BwdBars& B = *reinterpret_cast<BwdBars*>(smem + SL::kBar);
@@ -390,6 +386,7 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   uint8_t* sdS = smem + SL::kdS;
   uint8_t* sK = smem + SL::kK;
   uint8_t* sV = smem + SL::kV;
+  uint8_t* sStg = smem + SL::kStg;
   float* sLse = reinterpret_cast<float*>(smem + SL::kLse);
   float* sDelta = reinterpret_cast<float*>(smem + SL::kDelta);
 
@@ -402,12 +399,17 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
 
   if (warp == kMmaWarp) {
     if (lane == 0) {
-      mbar_init(&B.q_full, kProdWarps);
-      for (int s = 0; s < ST; ++s) { mbar_init(&B.kv_full[s], kProdWarps); mbar_init(&B.kv_empty[s], 1); }
+      mbar_init(&B.q_full, kProdThreads);
+      mbar_init(&B.k_full, kProdThreads);
+      mbar_init(&B.v_full, kProdThreads);
+      mbar_init(&B.k_empty, 1);
+      mbar_init(&B.v_empty, 1);
       mbar_init(&B.sdp_full, 1);
       mbar_init(&B.pds_full, 128);
       mbar_init(&B.mma_done, 1);
       mbar_init(&B.tmem_free, 128);
+      mbar_init(&B.stg_full, 128);
+      mbar_init(&B.stg_free, kProdThreads);
       fence_barrier_init();
     }
     __syncwarp();
@@ -418,34 +420,75 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   tc_fence_after();
   const uint32_t tmem = B.tmem;
   const uint32_t tA = tmem, tB = tmem + 128, tC = tmem + 256, tDq = tmem + 384;
+  const long long hoff = (long long)h * Lk * D;
 
   if (warp >= kProdWarp0) {
-    // ------------------------------------------------------------ producers
+    // ------------------------------------------------------------ producers + scatter
     const int ptid = threadIdx.x - kProdWarp0 * 32;
+    const int pw = ptid >> 5;
     const int r0 = ptid / GT::kCPR;
-    auto bar_of = [&](int grp) { return grp == 0 ? &B.q_full : &B.kv_full[(grp - 1) % ST]; };
     int rows[GT::kPer];
     const int qbase = h * Lq;
 #pragma unroll
     for (int i = 0; i < GT::kPer; ++i) rows[i] = qbase + __ldg(mrow + r0 + i * GT::kRowStep);
     issue_tile<D>(sQ, Qg, rows, ptid);
     issue_tile<D>(sdO, dOg, rows, ptid);
-    cp_async_commit();
-    int committed = 1, retired = 0;
+    cp_async_arrive_noinc(&B.q_full);
     const int kbase = h * Lk;
+    // scatter of block jb: warp pw owns rows [16 pw, 16 pw + 16) of both tensors
+    auto scatter = [&](int jb) {
+      const int kv = min(BKV, kh - jb * BKV);
+      const int myrow = pw * 16 + (lane & 15);
+      const int mykey = myrow < kv ? __ldg(irow + jb * BKV + myrow) : 0;
+      mbar_wait(&B.stg_full, jb & 1);
+      if constexpr (D == 128) {
+#pragma unroll 4
+        for (int rr = 0; rr < 16; ++rr) {
+          const int p = pw * 16 + rr;
+          const int key = __shfl_sync(0xffffffffu, mykey, rr);
+          if (p < kv) {
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              const uint2 v = *reinterpret_cast<const uint2*>(
+                  sStg + t * (128 * D * 2) + stg_off<D>(p, lane >> 1) + (lane & 1) * 8);
+              red_add_v4((t == 0 ? dV : dK) + hoff + (long long)key * D + lane * 4,
+                         bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y));
+            }
+          }
+        }
+      } else {
+#pragma unroll 4
+        for (int rr = 0; rr < 16; rr += 2) {
+          const int p = pw * 16 + rr + (lane >> 4);
+          const int key = __shfl_sync(0xffffffffu, mykey, rr + (lane >> 4));
+          if (p < kv) {
+            const int e = (lane & 15) * 4;
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              const uint2 v = *reinterpret_cast<const uint2*>(
+                  sStg + t * (128 * D * 2) + stg_off<D>(p, e >> 3) + ((e >> 2) & 1) * 8);
+              red_add_v4((t == 0 ? dV : dK) + hoff + (long long)key * D + e,
+                         bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y));
+            }
+          }
+        }
+      }
+      mbar_arrive(&B.stg_free);
+    };
     for (int j = 0; j < nblk; ++j) {
-      const int st = j % ST;
-      if (j >= ST) mbar_wait(&B.kv_empty[st], ((j / ST) - 1) & 1);
 #pragma unroll
       for (int i = 0; i < GT::kPer; ++i)
         rows[i] = kbase + __ldg(irow + min(j * BKV + r0 + i * GT::kRowStep, kh - 1));
-      issue_tile<D>(sK + st * SL::kTile, Kg, rows, ptid);
-      issue_tile<D>(sV + st * SL::kTile, Vg, rows, ptid);
-      cp_async_commit();
-      ++committed;
-      retire_groups<ST - 1>(committed, retired, bar_of);
+      if (j > 0) mbar_wait(&B.v_empty, (j - 1) & 1);
+      issue_tile<D>(sV, Vg, rows, ptid);
+      cp_async_arrive_noinc(&B.v_full);
+      if (j > 0) mbar_wait(&B.k_empty, (j - 1) & 1);
+      issue_tile<D>(sK, Kg, rows, ptid);
+      cp_async_arrive_noinc(&B.k_full);
+      if (j > 0) scatter(j - 1);
     }
-    retire_groups<0>(committed, retired, bar_of);
+    scatter(nblk - 1);
+    cp_async_wait<0>();
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idST = idesc_bf16_f32(128, 128, 0, 0);   // K_j . Q^T, V_j . dO^T
@@ -453,11 +496,11 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
     constexpr uint32_t idDK = idesc_bf16_f32(128, 64, 0, 1);    // dS^T(tmem) . Q(MN), 64 cols
     constexpr uint32_t idDQ = idesc_bf16_f32(128, D, 1, 1);     // dS(MN smem) . K_j(MN)
     const uint32_t aQ = smem_u32(sQ), adO = smem_u32(sdO), adS = smem_u32(sdS);
+    const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
     mbar_wait(&B.q_full, 0);
     for (int j = 0; j < nblk; ++j) {
-      const int st = j % ST;
-      const uint32_t aK = smem_u32(sK + st * SL::kTile), aV = smem_u32(sV + st * SL::kTile);
-      mbar_wait(&B.kv_full[st], (j / ST) & 1);
+      mbar_wait(&B.k_full, j & 1);
+      mbar_wait(&B.v_full, j & 1);
       if (j > 0) mbar_wait(&B.tmem_free, (j - 1) & 1);
       tc_fence_after();
       if (elect_one()) {
@@ -472,6 +515,7 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
           mma_ss(tB, sdesc_sw128(aV + off, 16, 1024), sdesc_sw128(adO + off, 16, 1024), idST, kk > 0);
         }
         mma_commit(&B.sdp_full);
+        mma_commit(&B.v_empty);
       }
       __syncwarp();
       mbar_wait(&B.pds_full, j & 1);
@@ -482,6 +526,7 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
         for (int kk = 0; kk < 8; ++kk)
           mma_ss(tDq, sdesc_sw128(adS + kk * 2048, 128 * 128, 1024),
                  sdesc_sw128(aK + kk * 2048, 128 * 128, 1024), idDQ, (j | kk) != 0);
+        mma_commit(&B.k_empty);
         // dV_j = P^T dO   (A = P^T in TMEM cols tA[0,64), K = 128 queries)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
@@ -495,7 +540,6 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
                    idDK, kk > 0);
         }
         mma_commit(&B.mma_done);
-        mma_commit(&B.kv_empty[st]);
       }
       __syncwarp();
     }
@@ -525,11 +569,9 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
       sDelta[row] = dlt;
       named_bar_sync(1, 128);
     }
-    uint8_t* stg = sdS + warp * 8192;   // per-warp scatter staging (2 x 4 KB), reuses the dS tile
     for (int j = 0; j < nblk; ++j) {
       const int kv = min(BKV, kh - j * BKV);
       const bool kvalid = row < kv;
-      const int key = kvalid ? __ldg(irow + j * BKV + row) : 0;
       mbar_wait(&B.sdp_full, j & 1);
       tc_fence_after();
 #pragma unroll 1
@@ -563,10 +605,10 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&B.pds_full);
-      // ---- scatter dV_j, dK_j: per-warp smem transpose, then row-contiguous red.v4
+      // ---- C': dV_j / dK_j rows -> bf16 staging (after the previous scatter drained it)
       mbar_wait(&B.mma_done, j & 1);
       tc_fence_after();
-      const long long hoff = (long long)h * Lk * D;
+      if (j > 0) mbar_wait(&B.stg_free, (j - 1) & 1);
 #pragma unroll 1
       for (int n = 0; n < 2 * (D / 32); ++n) {
         const int t = n / (D / 32), c = n % (D / 32);
@@ -574,27 +616,18 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
         uint32_t r[32];
         tmem_ld32(taddr + lane_off, r);
         tmem_ld_wait();
-        uint8_t* buf = stg + (n & 1) * 4096;
+        uint8_t* srow = sStg + t * (128 * D * 2);
 #pragma unroll
-        for (int qd = 0; qd < 8; ++qd)
-          *reinterpret_cast<uint4*>(buf + lane * 128 + ((qd ^ (lane & 7)) << 4)) =
-              make_uint4(r[4 * qd], r[4 * qd + 1], r[4 * qd + 2], r[4 * qd + 3]);
-        __syncwarp();
-        float* acc = (t == 0 ? dV : dK) + hoff + c * 32 + (lane & 7) * 4;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int rr = (lane >> 3) + 4 * i;
-          const uint4 v = *reinterpret_cast<const uint4*>(buf + rr * 128 + (((lane & 7) ^ (rr & 7)) << 4));
-          const int krr = __shfl_sync(0xffffffffu, key, rr);
-          const int okr = __shfl_sync(0xffffffffu, (int)kvalid, rr);
-          if (okr)
-            red_add_v4(acc + (long long)krr * D, __uint_as_float(v.x), __uint_as_float(v.y),
-                       __uint_as_float(v.z), __uint_as_float(v.w));
-        }
-        __syncwarp();
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<uint4*>(srow + stg_off<D>(row, c * 4 + q)) = make_uint4(
+              pack_bf16(__uint_as_float(r[8 * q + 0]), __uint_as_float(r[8 * q + 1])),
+              pack_bf16(__uint_as_float(r[8 * q + 2]), __uint_as_float(r[8 * q + 3])),
+              pack_bf16(__uint_as_float(r[8 * q + 4]), __uint_as_float(r[8 * q + 5])),
+              pack_bf16(__uint_as_float(r[8 * q + 6]), __uint_as_float(r[8 * q + 7])));
       }
       tc_fence_before();
       mbar_arrive(&B.tmem_free);
+      mbar_arrive(&B.stg_full);
     }
     // ---------------- dQ epilogue (query rows); the last mma_done covered dQ
     __nv_bfloat16* qrow = dQ + ((long long)h * Lq + tok) * D;

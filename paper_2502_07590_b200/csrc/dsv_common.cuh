@@ -127,6 +127,11 @@ DSV_DEV void cp_async16(uint32_t dst, const void* src) {
 DSV_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 DSV_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
+// Arrive on `bar` (asynchronously) once all cp.async copies this thread issued so
+// far have landed; .noinc: the arrival counts against the barrier's init count.
+DSV_DEV void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
 
 // ----------------------------------------------------------------- tcgen05
 DSV_DEV void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
