@@ -58,7 +58,7 @@ int dsv_gemm_bf16(const void* A, long long lda, long long a_bs, const void* B, l
 int dsv_project(const void* X, const void* Wt, void* out, int L, int d_model, int n_out,
                 void* stream);
 
-/* fp32 scores C[b][i][j] = sum_t A[b][i][t] * B[b][j][t] (t < r <= 64), deterministic
+/* fp32 scores C[b][i][j] = sum_t A[b][i][t] * B[b][j][t] (any r >= 1), deterministic
  * fmaf order t = 0..r-1. a_dtype: DSV_DTYPE_F32 or DSV_DTYPE_BF16 (for both A and B). */
 int dsv_scores_f32(const void* A, long long lda, long long a_bs, const void* B, long long ldb,
                    long long b_bs, float* C, long long ldc, long long c_bs, int nbatch, int R,
@@ -74,24 +74,26 @@ int dsv_topk(const float* scores, long long ld, int rows, int L, const int* k_pe
 
 /* Group-tiled sparse attention forward (K3f), bf16, head dim D in {64, 128}.
  * q: [H][Lq][D], k, v: [H][Lk][D]; grp_rows: [G][128] int32 member token ids (entries past
- * grp_size[g] repeat a member); idx: [H][G][ldk] int32 ascending key ids, kcount[H] valid
- * per head (1..ldk). out: [H][Lq][D] bf16; lse: [H][Lq] fp32, log2 domain of the scaled
- * logits. flags bit0: keep P in shared memory instead of TMEM. */
+ * grp_size[g] repeat a member); idx: [H][G][ldk] int32 ascending key ids with kcount[h] valid
+ * entries per row (1..ldk), or, when kcount_hg != NULL, kcount_hg[h*G + g] valid entries.
+ * out: [H][Lq][D] bf16; lse: [H][Lq] fp32, log2 domain of the scaled logits. */
 int dsv_sparse_fwd(const void* q, const void* k, const void* v, const int* grp_rows,
-                   const int* grp_size, const int* idx, long long ldk, const int* kcount, int H,
-                   int G, int Lq, int Lk, int D, float scale, void* out, float* lse, int flags,
-                   void* stream);
+                   const int* grp_size, const int* idx, long long ldk, const int* kcount,
+                   const int* kcount_hg, int H, int G, int Lq, int Lk, int D, float scale,
+                   void* out, float* lse, void* stream);
 
 /* Backward (K3b). dout: [H][Lq][D] bf16, out/lse from dsv_sparse_fwd. dq: [H][Lq][D] bf16
  * (every query of a group is written); dk_acc, dv_acc: [H][Lk][D] fp32 accumulators that the
  * caller zeroes; contributions are added atomically. */
 int dsv_sparse_bwd(const void* q, const void* k, const void* v, const void* out,
                    const void* dout, const float* lse, const int* grp_rows, const int* grp_size,
-                   const int* idx, long long ldk, const int* kcount, int H, int G, int Lq, int Lk,
-                   int D, float scale, void* dq, float* dk_acc, float* dv_acc, void* stream);
+                   const int* idx, long long ldk, const int* kcount, const int* kcount_hg, int H,
+                   int G, int Lq, int Lk, int D, float scale, void* dq, float* dk_acc,
+                   float* dv_acc, void* stream);
 
 /* Ragged per-(head, query) CSR sparse attention on CUDA cores (fp32 math), any D <= 256.
- * ptr: [H*Lq + 1] int64 offsets into cols (int32 key ids). out: [H][Lq][D] fp32,
+ * ptr: [H*Lq + 1] int64 offsets into cols (int32 key ids); cols == NULL selects every key
+ * (dense attention, ptr unused). out: [H][Lq][D] fp32,
  * lse: [H][Lq] fp32 natural log of the scaled logits. in_dtype: F32 or BF16 (q/k/v/dout). */
 int dsv_rows_fwd(const void* q, const void* k, const void* v, const long long* ptr,
                  const int* cols, int H, int Lq, int Lk, int D, float scale, int in_dtype,

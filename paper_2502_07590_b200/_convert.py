@@ -1,0 +1,69 @@
+"""Argument coercion shared by the reference-compatible API.
+
+Mirrors the reference's validation contract (pkg/src/dynsparse/validate.py:10-25
+`as_matrix`): inputs must be 2-D (per head) and finite, otherwise ValueError.
+Host inputs (numpy / lists) are moved to the CUDA device; results go back to
+the caller's world (numpy in -> numpy out, torch in -> torch out).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+
+class NumericalError(Exception):
+    """A computation produced a non-finite result (validate.py:6-7)."""
+
+
+def device() -> torch.device:
+    if not torch.cuda.is_available():
+        from ._lib import DSVError
+
+        raise DSVError("the DSV kernels need a CUDA device; there is no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def is_torch(x) -> bool:
+    return isinstance(x, torch.Tensor)
+
+
+def as_matrix(name: str, x, dtype=None):
+    """validate.py:10-25 — 2-D, finite; float32 kept, anything else float64."""
+    if is_torch(x):
+        if x.dim() != 2:
+            raise ValueError(f"{name} must be 2D, got shape {tuple(x.shape)}")
+        if not bool(torch.isfinite(x).all()):
+            raise ValueError(f"{name} contains NaN or Inf")
+        return x
+    arr = np.asarray(x)
+    if dtype is not None:
+        arr = arr.astype(dtype, copy=False)
+    elif arr.dtype not in (np.float32, np.float64):
+        arr = arr.astype(np.float64)
+    if arr.ndim != 2:
+        raise ValueError(f"{name} must be 2D, got shape {arr.shape}")
+    if not np.all(np.isfinite(arr)):
+        raise ValueError(f"{name} contains NaN or Inf")
+    return arr
+
+
+def check_same_cols(name_a, a, name_b, b) -> None:
+    if a.shape[1] != b.shape[1]:
+        raise ValueError(f"{name_a} and {name_b} must share the inner dimension: "
+                         f"{a.shape[1]} != {b.shape[1]}")
+
+
+def to_device(x, dtype: torch.dtype) -> torch.Tensor:
+    dev = device()
+    if is_torch(x):
+        return x.to(device=dev, dtype=dtype).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x)).to(device=dev, dtype=dtype)
+
+
+def back(t: torch.Tensor, like, np_dtype=None):
+    """Return `t` in the caller's world: numpy (with np_dtype) if `like` is host data."""
+    if is_torch(like):
+        return t
+    out = t.detach().cpu().numpy()
+    return out.astype(np_dtype, copy=False) if np_dtype is not None else out

@@ -130,8 +130,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __restrict__ Kg,
                   const __nv_bfloat16* __restrict__ Vg, const int* __restrict__ grp_rows,
                   const int* __restrict__ grp_size, const int* __restrict__ idx, long long ldk,
-                  const int* __restrict__ kcount, int G, int Lq, int Lk, float scale_log2,
-                  __nv_bfloat16* __restrict__ O, float* __restrict__ lse) {
+                  const int* __restrict__ kcount, const int* __restrict__ kcount_hg, int G,
+                  int Lq, int Lk, float scale_log2, __nv_bfloat16* __restrict__ O,
+                  float* __restrict__ lse) {
   using SL = FwdSmem<D>;
   using GT = Gather<D>;
   constexpr int ST = kFwdStages;
@@ -145,7 +146,7 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = blockIdx.x / G, g = blockIdx.x - h * G;
-  const int kh = kcount[h];
+  const int kh = kcount_hg ? kcount_hg[blockIdx.x] : kcount[h];
   const int nblk = (kh + BKV - 1) / BKV;
   const int* irow = idx + ((long long)h * G + g) * ldk;
   const int* mrow = grp_rows + (long long)g * BQ;
@@ -374,7 +375,8 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
                   const __nv_bfloat16* __restrict__ Og, const float* __restrict__ lse,
                   const int* __restrict__ grp_rows, const int* __restrict__ grp_size,
                   const int* __restrict__ idx, long long ldk, const int* __restrict__ kcount,
-                  int G, int Lq, int Lk, float scale, float scale_log2,
+                  const int* __restrict__ kcount_hg, int G, int Lq, int Lk, float scale,
+                  float scale_log2,
                   __nv_bfloat16* __restrict__ dQ, float* __restrict__ dK, float* __restrict__ dV) {
   using SL = BwdSmem<D>;
   using GT = Gather<D>;
@@ -392,7 +394,7 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = blockIdx.x / G, g = blockIdx.x - h * G;
-  const int kh = kcount[h];
+  const int kh = kcount_hg ? kcount_hg[blockIdx.x] : kcount[h];
   const int nblk = (kh + BKV - 1) / BKV;
   const int* irow = idx + ((long long)h * G + g) * ldk;
   const int* mrow = grp_rows + (long long)g * BQ;
@@ -670,32 +672,35 @@ using namespace dsv::attn;
 
 template <int D>
 static int fwd_launch(const void* q, const void* k, const void* v, const int* grp_rows,
-                      const int* grp_size, const int* idx, long long ldk, const int* kcount, int H,
-                      int G, int Lq, int Lk, float scale_log2, void* O, float* lse, cudaStream_t st) {
+                      const int* grp_size, const int* idx, long long ldk, const int* kcount,
+                      const int* kcount_hg, int H, int G, int Lq, int Lk, float scale_log2, void* O,
+                      float* lse, cudaStream_t st) {
   auto kern = sparse_fwd_kernel<D>;
   const int smem = FwdSmem<D>::kBytes;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   kern<<<H * G, kFwdThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
                                       (const __nv_bfloat16*)v, grp_rows, grp_size, idx, ldk,
-                                      kcount, G, Lq, Lk, scale_log2, (__nv_bfloat16*)O, lse);
+                                      kcount, kcount_hg, G, Lq, Lk, scale_log2,
+                                      (__nv_bfloat16*)O, lse);
   return (int)cudaGetLastError();
 }
 
 int dsv_attn_fwd_tc_launch(const void* q, const void* k, const void* v, const int* grp_rows,
                            const int* grp_size, const int* idx, long long ldk, const int* kcount,
-                           int H, int G, int Lq, int Lk, int D, float scale_log2, void* O,
-                           float* lse, cudaStream_t st) {
+                           const int* kcount_hg, int H, int G, int Lq, int Lk, int D,
+                           float scale_log2, void* O, float* lse, cudaStream_t st) {
   if (D == 128)
-    return fwd_launch<128>(q, k, v, grp_rows, grp_size, idx, ldk, kcount, H, G, Lq, Lk, scale_log2, O, lse, st);
+    return fwd_launch<128>(q, k, v, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H, G, Lq, Lk, scale_log2, O, lse, st);
   if (D == 64)
-    return fwd_launch<64>(q, k, v, grp_rows, grp_size, idx, ldk, kcount, H, G, Lq, Lk, scale_log2, O, lse, st);
+    return fwd_launch<64>(q, k, v, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H, G, Lq, Lk, scale_log2, O, lse, st);
   return 1;
 }
 
 template <int D>
 static int bwd_launch(const void* q, const void* k, const void* v, const void* O, const void* dO,
                       const float* lse, const int* grp_rows, const int* grp_size, const int* idx,
-                      long long ldk, const int* kcount, int H, int G, int Lq, int Lk, float scale,
+                      long long ldk, const int* kcount, const int* kcount_hg, int H, int G, int Lq,
+                      int Lk, float scale,
                       float scale_log2, void* dQ, float* dK, float* dV, cudaStream_t st) {
   auto kern = sparse_bwd_kernel<D>;
   const int smem = BwdSmem<D>::kBytes;
@@ -703,22 +708,22 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* O
   kern<<<H * G, kThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)dO,
                                       (const __nv_bfloat16*)k, (const __nv_bfloat16*)v,
                                       (const __nv_bfloat16*)O, lse, grp_rows, grp_size, idx, ldk,
-                                      kcount, G, Lq, Lk, scale, scale_log2, (__nv_bfloat16*)dQ,
-                                      dK, dV);
+                                      kcount, kcount_hg, G, Lq, Lk, scale, scale_log2,
+                                      (__nv_bfloat16*)dQ, dK, dV);
   return (int)cudaGetLastError();
 }
 
 int dsv_attn_bwd_tc_launch(const void* q, const void* k, const void* v, const void* O,
                            const void* dO, const float* lse, const int* grp_rows,
                            const int* grp_size, const int* idx, long long ldk, const int* kcount,
-                           int H, int G, int Lq, int Lk, int D, float scale, float scale_log2,
-                           void* dQ, float* dK, float* dV, cudaStream_t st) {
+                           const int* kcount_hg, int H, int G, int Lq, int Lk, int D, float scale,
+                           float scale_log2, void* dQ, float* dK, float* dV, cudaStream_t st) {
   if (D == 128)
-    return bwd_launch<128>(q, k, v, O, dO, lse, grp_rows, grp_size, idx, ldk, kcount, H, G, Lq, Lk,
-                           scale, scale_log2, dQ, dK, dV, st);
+    return bwd_launch<128>(q, k, v, O, dO, lse, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H,
+                           G, Lq, Lk, scale, scale_log2, dQ, dK, dV, st);
   if (D == 64)
-    return bwd_launch<64>(q, k, v, O, dO, lse, grp_rows, grp_size, idx, ldk, kcount, H, G, Lq, Lk,
-                          scale, scale_log2, dQ, dK, dV, st);
+    return bwd_launch<64>(q, k, v, O, dO, lse, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H,
+                          G, Lq, Lk, scale, scale_log2, dQ, dK, dV, st);
   return 1;
 }
 

@@ -26,12 +26,12 @@ int dsv_rows_bwd_launch(const void*, const void*, const void*, const float*, con
 int dsv_gemm_launch(const CUtensorMap*, const CUtensorMap*, void*, int, int, int, long long,
                     long long, int, int, int, cudaStream_t);
 int dsv_attn_fwd_tc_launch(const void*, const void*, const void*, const int*, const int*,
-                           const int*, long long, const int*, int, int, int, int, int, float,
-                           void*, float*, cudaStream_t);
+                           const int*, long long, const int*, const int*, int, int, int, int, int,
+                           float, void*, float*, cudaStream_t);
 int dsv_attn_bwd_tc_launch(const void*, const void*, const void*, const void*, const void*,
                            const float*, const int*, const int*, const int*, long long,
-                           const int*, int, int, int, int, int, float, float, void*, float*,
-                           float*, cudaStream_t);
+                           const int*, const int*, int, int, int, int, int, float, float, void*,
+                           float*, float*, cudaStream_t);
 int dsv_f32_to_bf16_launch(const float*, void*, long long, cudaStream_t);
 
 namespace {
@@ -143,7 +143,7 @@ int dsv_scores_f32(const void* A, long long lda, long long a_bs, const void* B, 
                    long long b_bs, float* C, long long ldc, long long c_bs, int nbatch, int R,
                    int Lk, int r, int in_dtype, void* stream) {
   if (R <= 0 || Lk <= 0 || nbatch <= 0) return fail(DSV_EINVAL, "scores: empty shape");
-  if (r < 1 || r > 64) return fail(DSV_EUNSUPPORTED, "scores: inner width %d outside [1, 64]", r);
+  if (r < 1) return fail(DSV_EINVAL, "scores: inner width %d < 1", r);
   return cuda_status(dsv_scores_f32_launch(A, lda, a_bs, B, ldb, b_bs, C, ldc, c_bs, nbatch, R,
                                            Lk, r, in_dtype == DSV_DTYPE_BF16, S(stream)),
                      "scores launch");
@@ -159,25 +159,26 @@ int dsv_topk(const float* scores, long long ld, int rows, int L, const int* k_pe
 }
 
 int dsv_sparse_fwd(const void* q, const void* k, const void* v, const int* grp_rows,
-                   const int* grp_size, const int* idx, long long ldk, const int* kcount, int H,
-                   int G, int Lq, int Lk, int D, float scale, void* out, float* lse, int flags,
-                   void* stream) {
+                   const int* grp_size, const int* idx, long long ldk, const int* kcount,
+                   const int* kcount_hg, int H, int G, int Lq, int Lk, int D, float scale,
+                   void* out, float* lse, void* stream) {
   if (D != 64 && D != 128) return fail(DSV_EUNSUPPORTED, "sparse_fwd: head dim %d not 64/128", D);
   if (H <= 0 || G <= 0 || Lq <= 0 || Lk <= 0 || ldk <= 0)
     return fail(DSV_EINVAL, "sparse_fwd: empty shape");
   if (!al16(q) || !al16(k) || !al16(v) || !al16(out) || !al16(grp_rows))
     return fail(DSV_EINVAL, "sparse_fwd: pointers must be 16-byte aligned");
-  (void)flags;
   const float scale_log2 = scale * 1.4426950408889634f;
-  return cuda_status(dsv_attn_fwd_tc_launch(q, k, v, grp_rows, grp_size, idx, ldk, kcount, H, G,
-                                            Lq, Lk, D, scale_log2, out, lse, S(stream)),
+  return cuda_status(dsv_attn_fwd_tc_launch(q, k, v, grp_rows, grp_size, idx, ldk, kcount,
+                                            kcount_hg, H, G, Lq, Lk, D, scale_log2, out, lse,
+                                            S(stream)),
                      "sparse_fwd launch");
 }
 
 int dsv_sparse_bwd(const void* q, const void* k, const void* v, const void* out,
                    const void* dout, const float* lse, const int* grp_rows, const int* grp_size,
-                   const int* idx, long long ldk, const int* kcount, int H, int G, int Lq, int Lk,
-                   int D, float scale, void* dq, float* dk_acc, float* dv_acc, void* stream) {
+                   const int* idx, long long ldk, const int* kcount, const int* kcount_hg, int H,
+                   int G, int Lq, int Lk, int D, float scale, void* dq, float* dk_acc,
+                   float* dv_acc, void* stream) {
   if (D != 64 && D != 128) return fail(DSV_EUNSUPPORTED, "sparse_bwd: head dim %d not 64/128", D);
   if (H <= 0 || G <= 0 || Lq <= 0 || Lk <= 0 || ldk <= 0)
     return fail(DSV_EINVAL, "sparse_bwd: empty shape");
@@ -186,8 +187,8 @@ int dsv_sparse_bwd(const void* q, const void* k, const void* v, const void* out,
     return fail(DSV_EINVAL, "sparse_bwd: pointers must be 16-byte aligned");
   const float scale_log2 = scale * 1.4426950408889634f;
   return cuda_status(dsv_attn_bwd_tc_launch(q, k, v, out, dout, lse, grp_rows, grp_size, idx, ldk,
-                                            kcount, H, G, Lq, Lk, D, scale, scale_log2, dq, dk_acc,
-                                            dv_acc, S(stream)),
+                                            kcount, kcount_hg, H, G, Lq, Lk, D, scale, scale_log2,
+                                            dq, dk_acc, dv_acc, S(stream)),
                      "sparse_bwd launch");
 }
 

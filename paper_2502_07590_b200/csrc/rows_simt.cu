@@ -24,36 +24,49 @@ template <> DSV_DEV float ld_f<__nv_bfloat16>(const __nv_bfloat16* p) {
 }
 
 // C[b, i, j] = sum_t A[b, i, t] * B[b, j, t]; A: [nb, R, r] (row stride lda),
-// B: [nb, Lk, r] (row stride ldb), C: [nb, R, Lk] (row stride ldc).
+// B: [nb, Lk, r] (row stride ldb), C: [nb, R, Lk] (row stride ldc). Any r: the
+// inner loop runs in chunks of 64 but always in t order 0..r-1 (fmaf).
+constexpr int kScRows = 16, kScT = 32;
 template <typename T>
 __global__ void __launch_bounds__(256)
 scores_kernel(const T* __restrict__ A, long long lda, long long a_bs,
               const T* __restrict__ B, long long ldb, long long b_bs,
               float* __restrict__ C, long long ldc, long long c_bs, int R, int Lk, int r) {
-  extern __shared__ float sA[];  // [32][r]
+  __shared__ float sA[kScRows * kScT];
   const int b = blockIdx.z;
-  const int i0 = blockIdx.y * 32;
+  const int i0 = blockIdx.y * kScRows;
   const int j = blockIdx.x * 256 + threadIdx.x;
   const T* Ab = A + b * a_bs;
   const T* Bb = B + b * b_bs;
-  for (int e = threadIdx.x; e < 32 * r; e += 256) {
-    const int ii = e / r, t = e - ii * r;
-    sA[e] = (i0 + ii < R) ? ld_f(Ab + (long long)(i0 + ii) * lda + t) : 0.f;
+  float acc[kScRows];
+#pragma unroll
+  for (int ii = 0; ii < kScRows; ++ii) acc[ii] = 0.f;
+  for (int t0 = 0; t0 < r; t0 += kScT) {
+    const int tn = min(kScT, r - t0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kScRows * kScT; e += 256) {
+      const int ii = e / kScT, t = e % kScT;
+      sA[e] = (i0 + ii < R && t < tn) ? ld_f(Ab + (long long)(i0 + ii) * lda + t0 + t) : 0.f;
+    }
+    __syncthreads();
+    if (j < Lk) {
+      float bj[kScT];
+#pragma unroll
+      for (int t = 0; t < kScT; ++t) bj[t] = (t < tn) ? ld_f(Bb + (long long)j * ldb + t0 + t) : 0.f;
+#pragma unroll
+      for (int ii = 0; ii < kScRows; ++ii) {
+#pragma unroll
+        for (int t = 0; t < kScT; ++t)
+          if (t < tn) acc[ii] = fmaf(sA[ii * kScT + t], bj[t], acc[ii]);
+      }
+    }
   }
-  __syncthreads();
   if (j >= Lk) return;
-  float bj[64];
-#pragma unroll
-  for (int t = 0; t < 64; ++t) bj[t] = (t < r) ? ld_f(Bb + (long long)j * ldb + t) : 0.f;
   float* Cb = C + b * c_bs;
-  const int iend = min(32, R - i0);
-  for (int ii = 0; ii < iend; ++ii) {
-    float acc = 0.f;
+  const int iend = min(kScRows, R - i0);
 #pragma unroll
-    for (int t = 0; t < 64; ++t)
-      if (t < r) acc = fmaf(sA[ii * r + t], bj[t], acc);
-    Cb[(long long)(i0 + ii) * ldc + j] = acc;
-  }
+  for (int ii = 0; ii < kScRows; ++ii)
+    if (ii < iend) Cb[(long long)(i0 + ii) * ldc + j] = acc[ii];
 }
 
 // ---------------------------------------------------------------- attention
@@ -77,11 +90,11 @@ attn_rows_fwd_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* 
     acc[e] = 0.f;
   }
   float m = -INFINITY, l = 0.f;
-  const long long p0 = ptr[gw], p1 = ptr[gw + 1];
+  const long long p0 = cols ? ptr[gw] : 0, p1 = cols ? ptr[gw + 1] : Lk;
   const T* kh = k + (long long)h * Lk * d;
   const T* vh = v + (long long)h * Lk * d;
   for (long long p = p0; p < p1; ++p) {
-    const int key = cols[p];
+    const int key = cols ? cols[p] : (int)p;
     const T* kr = kh + (long long)key * d;
     float s = 0.f;
 #pragma unroll
@@ -139,10 +152,10 @@ attn_rows_bwd_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* 
 #pragma unroll
   for (int o2 = 16; o2; o2 >>= 1) delta += __shfl_xor_sync(0xffffffffu, delta, o2);
   const float lrow = lse[gw];
-  const long long p0 = ptr[gw], p1 = ptr[gw + 1];
+  const long long p0 = cols ? ptr[gw] : 0, p1 = cols ? ptr[gw + 1] : Lk;
   const long long hoff = (long long)h * Lk * d;
   for (long long p = p0; p < p1; ++p) {
-    const int key = cols[p];
+    const int key = cols ? cols[p] : (int)p;
     const T* kr = k + hoff + (long long)key * d;
     const T* vr = v + hoff + (long long)key * d;
     float s = 0.f, dp = 0.f;
@@ -188,9 +201,9 @@ using namespace dsv::simt;
 int dsv_scores_f32_launch(const void* A, long long lda, long long a_bs, const void* B,
                           long long ldb, long long b_bs, float* C, long long ldc, long long c_bs,
                           int nbatch, int R, int Lk, int r, int bf16_in, cudaStream_t st) {
-  if (r < 1 || r > 64) return 1;
-  dim3 grid((Lk + 255) / 256, (R + 31) / 32, nbatch);
-  const size_t sm = 32 * r * sizeof(float);
+  if (r < 1) return 1;
+  dim3 grid((Lk + 255) / 256, (R + kScRows - 1) / kScRows, nbatch);
+  const size_t sm = 0;
   if (bf16_in)
     scores_kernel<__nv_bfloat16><<<grid, 256, sm, st>>>(
         (const __nv_bfloat16*)A, lda, a_bs, (const __nv_bfloat16*)B, ldb, b_bs, C, ldc, c_bs, R,

@@ -129,3 +129,52 @@ def overlap_ratio(member_sets: list, proxy_pos: int) -> float:
             raise ValueError("member sets must be nonempty")
         ratios.append(np.intersect1d(m, proxy, assume_unique=True).size / m.size)
     return float(np.mean(ratios))
+
+
+def grouped_sparse_attention(q, k, v, plan: VoxelGroupPlan, group_sets: list, *, flops=None):
+    """Sparse attention where each group's members share one index set (grouping.py:196-216).
+
+    bf16 CUDA tensors with head dim 64/128 run the group-tiled tcgen05 kernel
+    directly (one 128-query tile per group, ragged per-group set sizes); other
+    inputs (numpy / fp32) run the fp32 CUDA-core kernel on the expanded per-query
+    lists, matching the reference's expansion (grouping.py:209-216).
+    """
+    from . import _convert as cv
+    from . import ops
+    from .attention import CriticalIndexSet, sparse_attention
+
+    if len(group_sets) != plan.n_groups:
+        raise ValueError(f"need {plan.n_groups} group index sets, got {len(group_sets)}")
+    sets = []
+    for g, gs in enumerate(group_sets):
+        a = np.asarray(gs.cpu() if isinstance(gs, torch.Tensor) else gs, dtype=np.int64)
+        if a.size == 0:
+            raise ValueError(f"group {g} has an empty index set")
+        sets.append(a)
+    tc_ok = (cv.is_torch(q) and q.dtype == torch.bfloat16 and q.dim() == 2 and q.shape[1] in (64, 128)
+             and plan.max_group <= TILE)
+    if not tc_ok:
+        per_query = [None] * plan.grid.size
+        for g, members in enumerate(plan.members):
+            for m in members:
+                per_query[m] = sets[g]
+        return sparse_attention(q, k, v, CriticalIndexSet(per_query), flops=flops)
+    q = cv.as_matrix("Q", q)
+    dev = q.device
+    k_max = max(s.size for s in sets)
+    idx = np.zeros((1, plan.n_groups, k_max), dtype=np.int32)
+    counts = np.zeros((1, plan.n_groups), dtype=np.int32)
+    for g, s in enumerate(sets):
+        if np.any(np.diff(s) <= 0) or s[0] < 0 or s[-1] >= k.shape[0]:
+            raise ValueError(f"group {g}: indices must be sorted, unique and inside K")
+        idx[0, g, : s.size] = s
+        counts[0, g] = s.size
+    rows, size = plan.tables(dev)
+    out, _ = ops.sparse_fwd(q.unsqueeze(0).contiguous(), k.unsqueeze(0).contiguous(),
+                            v.unsqueeze(0).contiguous(), rows, size, torch.from_numpy(idx).to(dev),
+                            torch.tensor([k_max], dtype=torch.int32, device=dev),
+                            kcount_hg=torch.from_numpy(counts).to(dev))
+    if flops is not None:
+        flops.add_pairs(int(sum(s.size * m.size for s, m in zip(sets, plan.members))), q.shape[1])
+        flops.add_per_query(q.shape[0])
+    return out[0]

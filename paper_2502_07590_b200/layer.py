@@ -1,0 +1,142 @@
+"""One DSV dynamic-sparsity attention layer on a single B200.
+
+The hot path of BASELINE.json's north_star, end to end on device:
+
+  K1a  project      P = X . Wt^T          [L, 2*H*r]  (Q_lr | K_lr for all heads)   tcgen05
+  K1b  scores       S_h = Q_lr[proxies] . K_lr^T  [H, G, L] fp32                 tcgen05
+  K2   select       exact top-k_h per (head, group) row -> idx [H, G, k_max]      CUDA cores
+  K3f  sparse fwd   O, LSE over the selected KV of each group tile                 tcgen05/TMEM
+  K3b  sparse bwd   dQ, dK, dV (dK/dV scatter-added in fp32)                       tcgen05/TMEM
+
+Reference mapping (pkg/src/dynsparse): predictor.py:217-259 estimate_critical
+(per head: project + top-k on the proxy rows, grouping.py:184-193), then
+grouping.py:196-216 grouped_sparse_attention and its autograd
+(trainer.py:110-117). Per-head k = k_from_sparsity(s_h, L)
+(selection.py:60-67); heads may use different sparsities.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import ops
+from .grid import TokenGrid
+from .grouping import VoxelGroupPlan, build_groups
+from .selection import k_from_sparsity
+
+
+@dataclass
+class SelectedKV:
+    """Device index lists: idx int32 [H, G, k_max] ascending, kcount int32 [H]."""
+
+    idx: torch.Tensor
+    kcount: torch.Tensor
+    thresholds: torch.Tensor   # fp32 [H, G], k-th largest approximate score
+    ks: list
+
+
+class DSVAttentionLayer:
+    """Predictor + selection + sparse attention for one layer, device resident."""
+
+    def __init__(self, grid: TokenGrid, heads: int, head_dim: int, d_lr: int = 16,
+                 voxel=(8, 4, 4), sparsity=0.9, device="cuda"):
+        self.grid = grid
+        self.H = int(heads)
+        self.D = int(head_dim)
+        self.r = int(d_lr)
+        self.device = torch.device(device)
+        self.plan: VoxelGroupPlan = build_groups(grid, voxel)
+        self.L = grid.size
+        sp = np.broadcast_to(np.asarray(sparsity, dtype=np.float64), (self.H,))
+        self.ks = [k_from_sparsity(float(s), self.L) for s in sp]
+        self.kcount = torch.tensor(self.ks, dtype=torch.int32, device=self.device)
+        self.k_max = max(self.ks)
+        self.grp_rows, self.grp_size = self.plan.tables(self.device)
+        self.proxies = self.plan.proxies_tensor(self.device)
+        self.scale = 1.0 / math.sqrt(self.D)
+
+    @property
+    def G(self) -> int:
+        return self.plan.n_groups
+
+    # ------------------------------------------------------------- predictor
+    def predictor_weights(self, seed: int = 0) -> torch.Tensor:
+        """Random per-head W_q, W_k (PredictorParams.initialize: N(0, 1/sqrt(d)))
+        stacked transposed as Wt [2*H*r, H*D] bf16."""
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        d_model = self.H * self.D
+        wt = torch.randn((2 * self.H * self.r, d_model), generator=g) / math.sqrt(d_model)
+        return wt.to(torch.bfloat16).to(self.device)
+
+    def select(self, x: torch.Tensor, wt: torch.Tensor, return_scores: bool = False):
+        """K1a + K1b + K2: critical-KV index lists per (head, group)."""
+        H, r, L = self.H, self.r, self.L
+        p = ops.project(x, wt)                                   # [L, 2 H r] bf16
+        qp = ops.gather_rows(p[:, : H * r], self.proxies)        # [G, H r] proxy rows
+        qp = qp.view(self.G, H, r).permute(1, 0, 2)              # [H, G, r] (strided view)
+        k_lr = p[:, H * r:].view(L, H, r).permute(1, 0, 2)       # [H, L, r] (strided view)
+        return self._scores_topk(qp, k_lr, return_scores)
+
+    def select_from_lowrank(self, q_lr: torch.Tensor, k_lr: torch.Tensor,
+                            return_scores: bool = False):
+        """K1b + K2 from per-head low-rank projections q_lr, k_lr [H, L, r] (bf16)."""
+        H, r, L, G = self.H, self.r, self.L, self.G
+        # proxy rows of every head: rows (h * L + proxy) of q_lr viewed as [H * L, r]
+        key = ("prows", str(q_lr.device))
+        if key not in self.__dict__:
+            rows = (torch.arange(H, device=q_lr.device, dtype=torch.int32)[:, None] * L
+                    + self.proxies[None, :]).reshape(-1)
+            self.__dict__[key] = rows
+        q2 = q_lr if q_lr.stride(0) == L * q_lr.stride(1) else q_lr.contiguous()
+        qp = ops.gather_rows(q2.reshape(H * L, r) if q2.is_contiguous() else
+                             torch.as_strided(q2, (H * L, r), (q2.stride(1), 1)),
+                             self.__dict__[key]).view(H, G, r)
+        return self._scores_topk(qp, k_lr, return_scores)
+
+    def _scores_topk(self, qp, k_lr, return_scores):
+        H, L, G = self.H, self.L, self.G
+        scores = ops.gemm_bf16(qp, k_lr, torch.float32)          # [H, G, L] fp32
+        idx, thr = ops.topk_rows(scores.view(H * G, L), self.kcount, G, self.k_max)
+        sel = SelectedKV(idx.view(H, G, self.k_max), self.kcount, thr.view(H, G), self.ks)
+        return (sel, scores) if return_scores else sel
+
+    # ------------------------------------------------------------- attention
+    def forward(self, q, k, v, sel: SelectedKV):
+        return ops.sparse_fwd(q, k, v, self.grp_rows, self.grp_size, sel.idx, sel.kcount,
+                              self.scale)
+
+    def backward(self, q, k, v, out, lse, dout, sel: SelectedKV, dk_acc=None, dv_acc=None):
+        if dk_acc is not None:
+            dk_acc.zero_()
+            dv_acc.zero_()
+        dq, dk32, dv32 = ops.sparse_bwd(q, k, v, out, dout, lse, self.grp_rows, self.grp_size,
+                                        sel.idx, sel.kcount, self.scale, dk_acc, dv_acc)
+        return dq, ops.f32_to_bf16(dk32), ops.f32_to_bf16(dv32)
+
+    def step(self, x, wt, q, k, v, dout, dk_acc=None, dv_acc=None):
+        """One fwd+bwd pass of the layer (the bench's unit of work)."""
+        sel = self.select(x, wt)
+        out, lse = self.forward(q, k, v, sel)
+        dq, dk, dv = self.backward(q, k, v, out, lse, dout, sel, dk_acc, dv_acc)
+        return out, dq, dk, dv
+
+    # ------------------------------------------------------------- accounting
+    def pairs(self) -> int:
+        """(query, key) pairs scored per pass: sum_h L * k_h."""
+        return sum(self.L * kh for kh in self.ks)
+
+    def work(self) -> dict:
+        """Algorithmic work per layer pass."""
+        H, r, L, G, D = self.H, self.r, self.L, self.G, self.D
+        pairs = self.pairs()
+        return {
+            "projection_flops": 2 * L * (H * D) * (2 * r * H),
+            "estimation_flops": 2 * H * G * L * r,
+            "topk_bytes": H * G * (L * 4 + 4) + sum(G * kh * 4 for kh in self.ks),
+            "fwd_flops": 4 * pairs * D,
+            "bwd_flops": 10 * pairs * D,
+        }

@@ -21,14 +21,14 @@ def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
-def _require_cuda(*ts: torch.Tensor) -> None:
+def _require_cuda(*ts) -> None:
     for t in ts:
-        if not t.is_cuda:
+        if t is not None and not t.is_cuda:
             raise _lib.DSVError("libdsv kernels need CUDA tensors (no CPU fallback exists)")
 
 
-def _ptr(t: torch.Tensor) -> int:
-    return t.data_ptr()
+def _ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
 
 
 # ------------------------------------------------------------------- K1 GEMM
@@ -108,11 +108,11 @@ def topk_rows(scores: torch.Tensor, k_per_head: torch.Tensor, rows_per_head: int
 
 
 # ------------------------------------------------------------------- K3 attention
-def sparse_fwd(q, k, v, grp_rows, grp_size, idx, kcount, scale=None, p_in_tmem=True):
+def sparse_fwd(q, k, v, grp_rows, grp_size, idx, kcount, scale=None, kcount_hg=None):
     """Group-tiled sparse attention forward. q: [H, Lq, D], k/v: [H, Lk, D] bf16.
 
-    grp_rows int32 [G, 128], grp_size int32 [G], idx int32 [H, G, ldk], kcount int32 [H].
-    Returns (out bf16 [H, Lq, D], lse2 fp32 [H, Lq]).
+    grp_rows int32 [G, 128], grp_size int32 [G], idx int32 [H, G, ldk], kcount int32 [H]
+    (or per-row counts kcount_hg int32 [H, G]). Returns (out bf16 [H, Lq, D], lse2 fp32 [H, Lq]).
     """
     _require_cuda(q, k, v, grp_rows, grp_size, idx, kcount)
     H, Lq, D = q.shape
@@ -123,13 +123,13 @@ def sparse_fwd(q, k, v, grp_rows, grp_size, idx, kcount, scale=None, p_in_tmem=T
     out = torch.empty_like(q)
     lse = torch.empty((H, Lq), device=q.device, dtype=torch.float32)
     _lib.call("dsv_sparse_fwd", _ptr(q), _ptr(k), _ptr(v), _ptr(grp_rows), _ptr(grp_size),
-              _ptr(idx), idx.stride(1), _ptr(kcount), H, G, Lq, Lk, D, float(scale), _ptr(out),
-              _ptr(lse), 0 if p_in_tmem else 1, _stream())
+              _ptr(idx), idx.stride(1), _ptr(kcount), _ptr(kcount_hg), H, G, Lq, Lk, D,
+              float(scale), _ptr(out), _ptr(lse), _stream())
     return out, lse
 
 
 def sparse_bwd(q, k, v, out, dout, lse, grp_rows, grp_size, idx, kcount, scale=None,
-               dk_acc=None, dv_acc=None):
+               dk_acc=None, dv_acc=None, kcount_hg=None):
     """Backward of sparse_fwd. Returns (dq bf16, dk_acc fp32, dv_acc fp32)."""
     _require_cuda(q, k, v, out, dout, lse)
     H, Lq, D = q.shape
@@ -143,13 +143,16 @@ def sparse_bwd(q, k, v, out, dout, lse, grp_rows, grp_size, idx, kcount, scale=N
     if dv_acc is None:
         dv_acc = torch.zeros((H, Lk, D), device=q.device, dtype=torch.float32)
     _lib.call("dsv_sparse_bwd", _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(dout), _ptr(lse),
-              _ptr(grp_rows), _ptr(grp_size), _ptr(idx), idx.stride(1), _ptr(kcount), H, G, Lq,
-              Lk, D, float(scale), _ptr(dq), _ptr(dk_acc), _ptr(dv_acc), _stream())
+              _ptr(grp_rows), _ptr(grp_size), _ptr(idx), idx.stride(1), _ptr(kcount),
+              _ptr(kcount_hg), H, G, Lq, Lk, D, float(scale), _ptr(dq), _ptr(dk_acc), _ptr(dv_acc),
+              _stream())
     return dq, dk_acc, dv_acc
 
 
 def rows_fwd(q, k, v, ptr, cols, scale=None):
-    """Ragged CSR sparse attention forward on CUDA cores. Returns (out fp32, lse fp32 natural)."""
+    """Ragged CSR sparse attention forward on CUDA cores (cols None = every key).
+
+    Returns (out fp32, lse fp32 natural)."""
     _require_cuda(q, k, v, ptr, cols)
     H, Lq, D = q.shape
     Lk = k.shape[1]
