@@ -10,7 +10,8 @@
  * Reference interfaces replaced (reference = /root/reference/pkg/src/dynsparse):
  *   dsv_project          predictor.py:94-100   project(x, w)            (X W, both sides, all heads)
  *   dsv_gemm_bf16        predictor.py:238-239  + selection.py:149 tile product (tcgen05 GEMM)
- *   dsv_scores_f32       selection.py:149/204/222 q_lr @ k_lr.T (fp32, small inner width)
+ *   dsv_proxy_scores     grouping.py:184-193 + selection.py:149 proxy-row scores (tcgen05)
+ *   dsv_scores_f32       selection.py:149/204/222 q_lr @ k_lr.T (fp32, CUDA cores)
  *   dsv_topk             selection.py:118-175  streaming_topk / :178-242 twopass_select
  *                        (exact top-k, ties -> lower index, ascending emit, k-th threshold)
  *   dsv_sparse_fwd       attention.py:153-187  sparse_attention (uniform/group-shared sets)
@@ -57,6 +58,13 @@ int dsv_gemm_bf16(const void* A, long long lda, long long a_bs, const void* B, l
  * Wt stacks the per-head W_q^T then W_k^T rows: row (side*H + h)*r + j. */
 int dsv_project(const void* X, const void* Wt, void* out, int L, int d_model, int n_out,
                 void* stream);
+
+/* K1b proxy scores on tcgen05: out[h][g][l] = sum_t q_prox[h][g][t] * k_lr[h][l][t] (fp32),
+ * bf16 inputs with rank r = 16; q_prox row stride ldq / head stride q_bs, k_lr row stride ldk /
+ * head stride k_bs (elements), out row stride ldo / head stride o_bs. Stores are coalesced. */
+int dsv_proxy_scores(const void* q_prox, long long ldq, long long q_bs, const void* k_lr,
+                     long long ldk, long long k_bs, float* out, long long ldo, long long o_bs,
+                     int H, int G, int L, int r, void* stream);
 
 /* fp32 scores C[b][i][j] = sum_t A[b][i][t] * B[b][j][t] (any r >= 1), deterministic
  * fmaf order t = 0..r-1. a_dtype: DSV_DTYPE_F32 or DSV_DTYPE_BF16 (for both A and B). */

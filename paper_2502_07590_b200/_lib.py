@@ -27,6 +27,8 @@ SIGNATURES = {
                       c_void_p, c_int, c_longlong, c_longlong, c_int, c_int, c_int, c_int,
                       c_void_p],
     "dsv_project": [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p],
+    "dsv_proxy_scores": [c_void_p, c_longlong, c_longlong, c_void_p, c_longlong, c_longlong,
+                         c_void_p, c_longlong, c_longlong, c_int, c_int, c_int, c_int, c_void_p],
     "dsv_scores_f32": [c_void_p, c_longlong, c_longlong, c_void_p, c_longlong, c_longlong,
                        c_void_p, c_longlong, c_longlong, c_int, c_int, c_int, c_int, c_int,
                        c_void_p],

@@ -33,6 +33,8 @@ int dsv_attn_bwd_tc_launch(const void*, const void*, const void*, const void*, c
                            const int*, const int*, int, int, int, int, int, float, float, void*,
                            float*, float*, cudaStream_t);
 int dsv_f32_to_bf16_launch(const float*, void*, long long, cudaStream_t);
+int dsv_proxy_scores_launch(const void*, long long, long long, const void*, long long, long long,
+                            float*, long long, long long, int, int, int, cudaStream_t);
 
 namespace {
 
@@ -147,6 +149,19 @@ int dsv_scores_f32(const void* A, long long lda, long long a_bs, const void* B, 
   return cuda_status(dsv_scores_f32_launch(A, lda, a_bs, B, ldb, b_bs, C, ldc, c_bs, nbatch, R,
                                            Lk, r, in_dtype == DSV_DTYPE_BF16, S(stream)),
                      "scores launch");
+}
+
+int dsv_proxy_scores(const void* q_prox, long long ldq, long long q_bs, const void* k_lr,
+                     long long ldk, long long k_bs, float* out, long long ldo, long long o_bs,
+                     int H, int G, int L, int r, void* stream) {
+  if (H <= 0 || G <= 0 || L <= 0) return fail(DSV_EINVAL, "proxy_scores: empty shape");
+  if (r != 16) return fail(DSV_EUNSUPPORTED, "proxy_scores: predictor rank %d (tcgen05 path: 16)", r);
+  if ((ldq * 2) % 16 || (q_bs * 2) % 16 || (ldk * 2) % 16 || (k_bs * 2) % 16 || !al16(q_prox) ||
+      !al16(k_lr))
+    return fail(DSV_EINVAL, "proxy_scores: rows must be 16-byte aligned");
+  return cuda_status(dsv_proxy_scores_launch(q_prox, ldq, q_bs, k_lr, ldk, k_bs, out, ldo, o_bs, H,
+                                             G, L, S(stream)),
+                     "proxy_scores launch");
 }
 
 int dsv_topk(const float* scores, long long ld, int rows, int L, const int* k_per_head,

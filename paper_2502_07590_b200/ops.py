@@ -85,6 +85,20 @@ def scores_f32(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None
     return out[0] if squeeze else out
 
 
+def proxy_scores(qp: torch.Tensor, k_lr: torch.Tensor, out: torch.Tensor | None = None):
+    """K1b on tcgen05: [H, G, r] . [H, L, r]^T -> fp32 [H, G, L] (r = 16, strided views ok)."""
+    _require_cuda(qp, k_lr)
+    H, G, r = qp.shape
+    L = k_lr.shape[1]
+    if qp.stride(2) != 1 or k_lr.stride(2) != 1:
+        raise ValueError("proxy_scores operands need unit stride along r")
+    if out is None:
+        out = torch.empty((H, G, L), device=qp.device, dtype=torch.float32)
+    _lib.call("dsv_proxy_scores", _ptr(qp), qp.stride(1), qp.stride(0), _ptr(k_lr), k_lr.stride(1),
+              k_lr.stride(0), _ptr(out), out.stride(1), out.stride(0), H, G, L, r, _stream())
+    return out
+
+
 # ------------------------------------------------------------------- K2 top-k
 def topk_rows(scores: torch.Tensor, k_per_head: torch.Tensor, rows_per_head: int,
               k_max: int | None = None):

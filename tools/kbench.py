@@ -49,6 +49,10 @@ def main():
     t = timeit(lambda: ops.gemm_bf16(qp, klr, torch.float32))
     by = H * G * L * 4
     print(f"scores_tc {t:8.3f} ms  {by / t / 1e6:8.1f} GB/s (write)")
+    t = timeit(lambda: ops.proxy_scores(qp, klr))
+    print(f"scores_t  {t:8.3f} ms  {by / t / 1e6:8.1f} GB/s (write)")
+    ref = ops.gemm_bf16(qp, klr, torch.float32)
+    print("proxy_scores max|diff| vs gemm:", float((ops.proxy_scores(qp, klr) - ref).abs().max()))
     t = timeit(lambda: ops.scores_f32(qp, klr))
     print(f"scores_f32{t:8.3f} ms  {by / t / 1e6:8.1f} GB/s (write)")
     sc = ops.gemm_bf16(qp, klr, torch.float32).reshape(H * G, L)
