@@ -47,16 +47,28 @@ class Ledger:
         self.received[phase] = self.received.get(phase, 0) + int(received)
 
 
-def _gather_rows(src2d: torch.Tensor, rows: torch.Tensor) -> torch.Tensor:
+def _gather_into(src2d: torch.Tensor, rows: torch.Tensor, out2d: torch.Tensor) -> None:
+    """out2d[j] = src2d[rows[j]] (row gather; dsv_gather_rows on CUDA tensors)."""
     if src2d.is_cuda:
         from . import ops
 
-        return ops.gather_rows(src2d, rows)
-    return src2d.index_select(0, rows.long())
+        ops.gather_rows(src2d, rows, out=out2d)
+    else:
+        out2d.copy_(src2d.index_select(0, rows.long()))
+
+
+def _gather_rows(src2d: torch.Tensor, rows: torch.Tensor) -> torch.Tensor:
+    out = torch.empty((rows.numel(), src2d.shape[1]), dtype=src2d.dtype, device=src2d.device)
+    _gather_into(src2d, rows, out)
+    return out
 
 
 class HeadParallelExchange:
-    """Head <-> sequence resharding for one process group (HCP, g_h = N)."""
+    """Head <-> sequence resharding for one process group (HCP, g_h = N).
+
+    Several tensors travel in one packed all-to-all: each contributes a column
+    range of the packed rows, gathered straight from its own layout.
+    """
 
     def __init__(self, n_heads: int, seq_len: int, assignment, group=None):
         self.group = group
@@ -73,22 +85,35 @@ class HeadParallelExchange:
         self.heads_of = [np.nonzero(self.assignment == r)[0] for r in range(self.world)]
         self.my_heads = self.heads_of[self.rank]
         self.ledger = Ledger()
-        self._perm_cache = {}
+        self._maps = {}
 
     # ---------------------------------------------------------------- index maps
-    def _send_rows(self, device) -> torch.Tensor:
-        """Rows of a head-major [H * chunk] local tensor, grouped by destination."""
-        key = ("send", str(device))
-        if key not in self._perm_cache:
-            rows = [h * self.chunk + t for r in range(self.world) for h in self.heads_of[r]
-                    for t in range(self.chunk)]
-            self._perm_cache[key] = torch.tensor(rows, dtype=torch.int32, device=device)
-        return self._perm_cache[key]
+    def _send_ht(self):
+        """(head, local token) of every packed send row, grouped by destination."""
+        if "send_ht" not in self._maps:
+            hh = np.concatenate([np.repeat(self.heads_of[r], self.chunk) for r in range(self.world)])
+            tt = np.tile(np.arange(self.chunk), self.H)
+            self._maps["send_ht"] = (hh, tt)
+        return self._maps["send_ht"]
 
-    def _recv_rows(self, device) -> torch.Tensor:
-        """Maps the received [src][my_heads][chunk] rows to [my_heads][L]."""
-        key = ("recv", str(device))
-        if key not in self._perm_cache:
+    def _rows(self, key, fn, device):
+        k = (key, str(device))
+        if k not in self._maps:
+            self._maps[k] = torch.from_numpy(np.ascontiguousarray(fn()).astype(np.int32)).to(device)
+        return self._maps[k]
+
+    def send_rows_headmajor(self, device):
+        hh, tt = self._send_ht()
+        return self._rows("hm", lambda: hh * self.chunk + tt, device)
+
+    def send_rows_lowrank(self, side: int, device):
+        """Rows of P [chunk, 2, H, r] viewed as [chunk * 2H, r]: (t, side, h)."""
+        hh, tt = self._send_ht()
+        return self._rows(("lr", side), lambda: tt * 2 * self.H + side * self.H + hh, device)
+
+    def _recv_rows(self, device):
+        """Received [src][my_heads][chunk] rows -> [my_heads][L]."""
+        def fn():
             nh = len(self.my_heads)
             out = np.empty(nh * self.L, dtype=np.int64)
             for hi in range(nh):
@@ -96,65 +121,103 @@ class HeadParallelExchange:
                     base = r * nh * self.chunk + hi * self.chunk
                     out[hi * self.L + r * self.chunk: hi * self.L + (r + 1) * self.chunk] = \
                         base + np.arange(self.chunk)
-            self._perm_cache[key] = torch.from_numpy(out.astype(np.int32)).to(device)
-        return self._perm_cache[key]
+            return out
+        return self._rows("recv", fn, device)
 
     def _inverse_rows(self, device):
         """[my_heads][L] rows grouped by destination rank (reverse exchange)."""
-        key = ("inv", str(device))
-        if key not in self._perm_cache:
-            nh = len(self.my_heads)
-            rows = [hi * self.L + r * self.chunk + t for r in range(self.world) for hi in range(nh)
-                    for t in range(self.chunk)]
-            self._perm_cache[key] = torch.tensor(rows, dtype=torch.int32, device=device)
-        return self._perm_cache[key]
+        nh = len(self.my_heads)
+        return self._rows("inv", lambda: np.array(
+            [hi * self.L + r * self.chunk + t for r in range(self.world) for hi in range(nh)
+             for t in range(self.chunk)], dtype=np.int64), device)
 
     def _back_rows(self, device):
         """Received [src][src_heads][chunk] rows -> head-major [H][chunk]."""
-        key = ("back", str(device))
-        if key not in self._perm_cache:
+        def fn():
             pos = np.empty(self.H * self.chunk, dtype=np.int64)
             off = 0
             for r in range(self.world):
                 for h in self.heads_of[r]:
                     pos[h * self.chunk: (h + 1) * self.chunk] = off + np.arange(self.chunk)
                     off += self.chunk
-            self._perm_cache[key] = torch.from_numpy(pos.astype(np.int32)).to(device)
-        return self._perm_cache[key]
+            return pos
+        return self._rows("back", fn, device)
 
     # ---------------------------------------------------------------- exchanges
+    def to_heads_packed(self, sources, phase: str = "hcp_fwd", async_op: bool = False):
+        """sources: list of (src2d, send_rows) whose send rows enumerate (dst, head, t).
+
+        Returns a handle; `finish(handle)` -> list of [my_heads, L, W_i] tensors.
+        """
+        dev = sources[0][0].device
+        dtype = sources[0][0].dtype
+        widths = [s.shape[1] for s, _ in sources]
+        W = sum(widths)
+        send = torch.empty((self.H * self.chunk, W), dtype=dtype, device=dev)
+        off = 0
+        for (src, rows), w in zip(sources, widths):
+            _gather_into(src, rows, send[:, off:off + w])
+            off += w
+        nh = len(self.my_heads)
+        recv = torch.empty((self.world * nh * self.chunk, W), dtype=dtype, device=dev)
+        in_split = [len(self.heads_of[r]) * self.chunk for r in range(self.world)]
+        out_split = [nh * self.chunk] * self.world
+        work = dist.all_to_all_single(recv, send, out_split, in_split, group=self.group,
+                                      async_op=async_op)
+        es = send.element_size() * W
+        self.ledger.add(phase, (sum(in_split) - in_split[self.rank]) * es,
+                        (sum(out_split) - out_split[self.rank]) * es)
+        return ("heads", work, recv, widths, send)
+
+    def to_tokens_packed(self, tensors, phase: str = "output_redistribute", async_op: bool = False):
+        """tensors: list of [my_heads, L, W_i] -> handle for list of [H, chunk, W_i]."""
+        nh = len(self.my_heads)
+        dev, dtype = tensors[0].device, tensors[0].dtype
+        widths = [t.shape[2] for t in tensors]
+        W = sum(widths)
+        send = torch.empty((nh * self.L, W), dtype=dtype, device=dev)
+        rows = self._inverse_rows(dev)
+        off = 0
+        for t, w in zip(tensors, widths):
+            if t.shape[0] != nh or t.shape[1] != self.L:
+                raise ValueError("shape does not match this rank's head plan")
+            _gather_into(t.reshape(nh * self.L, w), rows, send[:, off:off + w])
+            off += w
+        recv = torch.empty((self.H * self.chunk, W), dtype=dtype, device=dev)
+        in_split = [nh * self.chunk] * self.world
+        out_split = [len(self.heads_of[r]) * self.chunk for r in range(self.world)]
+        work = dist.all_to_all_single(recv, send, out_split, in_split, group=self.group,
+                                      async_op=async_op)
+        es = send.element_size() * W
+        self.ledger.add(phase, (sum(in_split) - in_split[self.rank]) * es,
+                        (sum(out_split) - out_split[self.rank]) * es)
+        return ("tokens", work, recv, widths, send)
+
+    def finish(self, handle):
+        kind, work, recv, widths, _send = handle
+        if work is not None:
+            work.wait()
+        dev = recv.device
+        rows = self._recv_rows(dev) if kind == "heads" else self._back_rows(dev)
+        lead = (len(self.my_heads), self.L) if kind == "heads" else (self.H, self.chunk)
+        outs, off = [], 0
+        for w in widths:
+            outs.append(_gather_rows(recv[:, off:off + w], rows).view(*lead, w))
+            off += w
+        return outs
+
+    # single-tensor conveniences (reference phase semantics)
     def to_heads(self, local: torch.Tensor, phase: str = "hcp_fwd") -> torch.Tensor:
         """[H, chunk, W] (all heads, my tokens) -> [my_heads, L, W] (my heads, all tokens)."""
         H, chunk, W = local.shape
         if H != self.H or chunk != self.chunk:
             raise ValueError(f"expected [{self.H}, {self.chunk}, *], got {tuple(local.shape)}")
-        flat = local.reshape(H * chunk, W)
-        send = _gather_rows(flat, self._send_rows(local.device))
-        nh = len(self.my_heads)
-        recv = torch.empty((self.world * nh * chunk, W), dtype=local.dtype, device=local.device)
-        in_split = [len(self.heads_of[r]) * chunk for r in range(self.world)]
-        out_split = [nh * chunk] * self.world
-        dist.all_to_all_single(recv, send, out_split, in_split, group=self.group)
-        es = local.element_size() * W
-        self.ledger.add(phase, (sum(in_split) - in_split[self.rank]) * es,
-                        (sum(out_split) - out_split[self.rank]) * es)
-        return _gather_rows(recv, self._recv_rows(local.device)).view(nh, self.L, W)
+        src = local.reshape(H * chunk, W)
+        return self.finish(self.to_heads_packed([(src, self.send_rows_headmajor(local.device))], phase))[0]
 
     def to_tokens(self, mine: torch.Tensor, phase: str = "output_redistribute") -> torch.Tensor:
         """[my_heads, L, W] -> [H, chunk, W] (inverse of to_heads)."""
-        nh, L, W = mine.shape
-        if nh != len(self.my_heads) or L != self.L:
-            raise ValueError("shape does not match this rank's head plan")
-        flat = mine.reshape(nh * L, W)
-        send = _gather_rows(flat, self._inverse_rows(mine.device))
-        recv = torch.empty((self.H * self.chunk, W), dtype=mine.dtype, device=mine.device)
-        in_split = [nh * self.chunk] * self.world
-        out_split = [len(self.heads_of[r]) * self.chunk for r in range(self.world)]
-        dist.all_to_all_single(recv, send, out_split, in_split, group=self.group)
-        es = mine.element_size() * W
-        self.ledger.add(phase, (sum(in_split) - in_split[self.rank]) * es,
-                        (sum(out_split) - out_split[self.rank]) * es)
-        return _gather_rows(recv, self._back_rows(mine.device)).view(self.H, self.chunk, W)
+        return self.finish(self.to_tokens_packed([mine], phase))[0]
 
     def expected_hcp_bytes(self, d: int, elem_width: int) -> float:
         """hcp_comm for this rank (Q, K, V in + O back), cpmodel.py:213-223."""
@@ -185,21 +248,30 @@ class HeadParallelDSV:
         self.local = DSVAttentionLayer(grid, len(mine), head_dim, d_lr, voxel, sp[mine], device)
 
     def step(self, x_local, wt, q, k, v, dout):
-        """x_local [L/N, H*D]; q, k, v, dout [H, L/N, D] -> (out, dq, dk, dv) [H, L/N, D]."""
+        """x_local [L/N, H*D]; q, k, v, dout [H, L/N, D] -> (out, dq, dk, dv) [H, L/N, D].
+
+        The dO exchange runs asynchronously during the forward, and O travels back
+        during the backward (NCCL streams overlap the attention kernels).
+        """
         from . import ops
 
-        H, r = self.H, self.r
+        H, r, D, ex = self.H, self.r, self.D, self.ex
+        dev = q.device
+        chunk = ex.chunk
         p = ops.project(x_local, wt)                                   # [L/N, 2 H r]
-        plr = p.view(-1, 2, H, r).permute(2, 0, 1, 3).reshape(H, -1, 2 * r)   # [H, L/N, 2r]
-        # one exchange for Q | K | V | Q_lr K_lr (same head plan)
-        packed = torch.cat([q, k, v, plr.contiguous()], dim=2)         # [H, L/N, 3D + 2r]
-        mine = self.ex.to_heads(packed, "hcp_fwd")                     # [h, L, 3D + 2r]
-        D = self.D
-        ql, kl, vl = (mine[:, :, i * D:(i + 1) * D].contiguous() for i in range(3))
-        lr = mine[:, :, 3 * D:]
-        sel = self.local.select_from_lowrank(lr[:, :, :r], lr[:, :, r:])
+        hm = ex.send_rows_headmajor(dev)
+        p_rows = p.view(chunk * 2 * H, r)
+        fwd = ex.to_heads_packed([(q.reshape(H * chunk, D), hm), (k.reshape(H * chunk, D), hm),
+                                  (v.reshape(H * chunk, D), hm),
+                                  (p_rows, ex.send_rows_lowrank(0, dev)),
+                                  (p_rows, ex.send_rows_lowrank(1, dev))], "hcp_fwd")
+        h_do = ex.to_heads_packed([(dout.reshape(H * chunk, D), hm)], "hcp_bwd_in", async_op=True)
+        ql, kl, vl, qlr, klr = ex.finish(fwd)
+        sel = self.local.select_from_lowrank(qlr, klr)
         out, lse = self.local.forward(ql, kl, vl, sel)
-        dout_m = self.ex.to_heads(dout, "hcp_bwd_in")
+        h_o = ex.to_tokens_packed([out], "output_redistribute", async_op=True)
+        (dout_m,) = ex.finish(h_do)
         dq, dk, dv = self.local.backward(ql, kl, vl, out, lse, dout_m, sel)
-        back = self.ex.to_tokens(torch.cat([out, dq, dk, dv], dim=2), "hcp_bwd_out")
-        return tuple(back[:, :, i * D:(i + 1) * D] for i in range(4))
+        grads = ex.finish(ex.to_tokens_packed([dq, dk, dv], "hcp_bwd_out"))
+        (out_local,) = ex.finish(h_o)
+        return (out_local, *grads)

@@ -236,14 +236,23 @@ int dsv_f32_to_bf16(const float* in, void* out, long long n, void* stream) {
 
 // ------------------------------------------------------------ gather rows
 namespace {
-__global__ void gather_rows_kernel(const uint8_t* __restrict__ src, long long sstride,
-                                   const int* __restrict__ rows, int n, int words,
-                                   uint8_t* __restrict__ out, long long ostride) {
-  const int i = blockIdx.x;
-  if (i >= n) return;
-  const uint32_t* s = reinterpret_cast<const uint32_t*>(src + (long long)rows[i] * sstride);
-  uint32_t* o = reinterpret_cast<uint32_t*>(out + (long long)i * ostride);
-  for (int w = threadIdx.x; w < words; w += blockDim.x) o[w] = s[w];
+// one warp per row; 16-byte vectors when every row start is 16-byte aligned
+template <bool kVec>
+__global__ void __launch_bounds__(256)
+gather_rows_kernel(const uint8_t* __restrict__ src, long long sstride, const int* __restrict__ rows,
+                   int n, int row_bytes, uint8_t* __restrict__ out, long long ostride) {
+  const int lane = threadIdx.x & 31;
+  for (long long r = (long long)blockIdx.x * 8 + (threadIdx.x >> 5); r < n; r += (long long)gridDim.x * 8) {
+    const uint8_t* s = src + (long long)rows[r] * sstride;
+    uint8_t* o = out + r * ostride;
+    if constexpr (kVec) {
+      for (int w = lane; w < row_bytes / 16; w += 32)
+        reinterpret_cast<uint4*>(o)[w] = __ldg(reinterpret_cast<const uint4*>(s) + w);
+    } else {
+      for (int w = lane; w < row_bytes / 4; w += 32)
+        reinterpret_cast<uint32_t*>(o)[w] = __ldg(reinterpret_cast<const uint32_t*>(s) + w);
+    }
+  }
 }
 }  // namespace
 
@@ -252,7 +261,14 @@ extern "C" int dsv_gather_rows(const void* src, long long src_stride, const int*
   if (n <= 0) return DSV_OK;
   if (row_bytes % 4 || src_stride % 4 || out_stride % 4)
     return fail(DSV_EINVAL, "gather_rows: byte sizes must be multiples of 4");
-  gather_rows_kernel<<<n, 128, 0, S(stream)>>>((const uint8_t*)src, src_stride, rows, n,
-                                               row_bytes / 4, (uint8_t*)out, out_stride);
+  const bool vec = row_bytes % 16 == 0 && src_stride % 16 == 0 && out_stride % 16 == 0 &&
+                   al16(src) && al16(out);
+  const int blocks = (int)((n + 7) / 8 < 148 * 16 ? (n + 7) / 8 : 148 * 16);
+  if (vec)
+    gather_rows_kernel<true><<<blocks, 256, 0, S(stream)>>>((const uint8_t*)src, src_stride, rows, n,
+                                                            row_bytes, (uint8_t*)out, out_stride);
+  else
+    gather_rows_kernel<false><<<blocks, 256, 0, S(stream)>>>((const uint8_t*)src, src_stride, rows, n,
+                                                             row_bytes, (uint8_t*)out, out_stride);
   return cuda_status((int)cudaGetLastError(), "gather_rows launch");
 }

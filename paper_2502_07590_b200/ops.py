@@ -202,6 +202,11 @@ def gather_rows(src: torch.Tensor, rows: torch.Tensor, out: torch.Tensor | None 
     _require_cuda(src, rows)
     rows = rows.to(torch.int32).contiguous()
     n = rows.numel()
+    if src.dim() != 2 or src.stride(1) != 1:
+        raise ValueError("gather_rows: src must be 2-D with unit column stride")
+    if out is not None and (out.dim() != 2 or out.stride(1) != 1 or out.shape[0] != n
+                            or out.shape[1] != src.shape[1] or out.dtype != src.dtype):
+        raise ValueError("gather_rows: out must be [len(rows), src.shape[1]] with unit column stride")
     if out is None:
         out = torch.empty((n, src.shape[1]), device=src.device, dtype=src.dtype)
     es = src.element_size()
