@@ -19,6 +19,8 @@
  *   dsv_sparse_bwd       trainer.py:110-117    autograd of the sparse attention (dQ, dK, dV)
  *   dsv_rows_fwd/_bwd    attention.py:176-183  ragged per-query index sets (CSR)
  *   dsv_gather_rows      cpsim.py:147-156/195-216 pack/unpack of head slices and KV rows
+ *   dsv_copy_jobs        cpsim.py:147-156/284-299 HCP head exchange written straight into
+ *                        the owners' buffers (peer pointers over NVLink)
  */
 #ifndef DSV_H_
 #define DSV_H_
@@ -114,6 +116,23 @@ int dsv_rows_bwd(const void* q, const void* k, const void* v, const float* out, 
 /* out[i] = src[rows[i]] for n rows of row_bytes bytes (row strides in bytes, multiples of 4). */
 int dsv_gather_rows(const void* src, long long src_stride, const int* rows, int n,
                     int row_bytes, void* out, long long out_stride, void* stream);
+
+/* One strided copy: `rows` rows of `row_bytes` bytes from src (+src_stride per row) to
+ * dst (+dst_stride per row). Six int64 fields, so a [njobs, 6] int64 device array is a
+ * job table. src/dst may be peer-mapped device pointers (CUDA IPC / symmetric memory). */
+typedef struct dsv_copy_job {
+  int64_t src;
+  int64_t dst;
+  int64_t src_stride;
+  int64_t dst_stride;
+  int64_t rows;
+  int64_t row_bytes;
+} dsv_copy_job;
+
+/* Run njobs copies from a DEVICE job table in one launch; every address, stride and
+ * row_bytes must be a multiple of 16 and rows * row_bytes / 16 < 2^31 per job.
+ * `splits` blocks cooperate on each job (1..1024). */
+int dsv_copy_jobs(const dsv_copy_job* jobs, int njobs, int splits, void* stream);
 
 /* fp32 -> bf16 conversion of n contiguous elements. */
 int dsv_f32_to_bf16(const float* in, void* out, long long n, void* stream);

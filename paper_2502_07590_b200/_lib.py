@@ -45,6 +45,7 @@ SIGNATURES = {
     "dsv_rows_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                      c_void_p, c_int, c_int, c_int, c_int, c_float, c_int, c_void_p, c_void_p,
                      c_void_p, c_void_p],
+    "dsv_copy_jobs": [c_void_p, c_int, c_int, c_void_p],
     "dsv_gather_rows": [c_void_p, c_longlong, c_void_p, c_int, c_int, c_void_p, c_longlong,
                         c_void_p],
     "dsv_f32_to_bf16": [c_void_p, c_void_p, c_longlong, c_void_p],

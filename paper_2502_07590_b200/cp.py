@@ -224,6 +224,170 @@ class HeadParallelExchange:
         return cpmodel.hcp_comm(self.H, len(self.my_heads), self.L, d, self.world, elem_width)
 
 
+class PeerExchange:
+    """HCP exchange over NVLink peer memory (one process per GPU, B200 NVSwitch).
+
+    Every rank owns one symmetric buffer holding the regions the DSV layer reads
+    and returns: Q, K, V, dO [heads, L, D] and Q_lr, K_lr [heads, L, r] for its
+    heads, and O, dQ, dK, dV [H, L/N, D] for its tokens. A sender writes its rows
+    straight into the owner's region (dsv_copy_jobs on peer pointers), so pack,
+    transfer and unpack are one kernel per direction; a device barrier on both
+    sides orders the writes (cpsim.py:125-161 and 284-299 phases, same bytes as
+    the all-to-all form, recorded in the same ledger).
+
+    The returned head-major/token-major tensors are views of the buffer and stay
+    valid until the next exchange.
+    """
+
+    def __init__(self, n_heads: int, seq_len: int, head_dim: int, d_lr: int, assignment,
+                 group=None, device=None, splits: int = 16):
+        import torch.distributed._symmetric_memory as symm
+
+        self.group = group if group is not None else dist.group.WORLD
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if seq_len % self.world:
+            raise ValueError("sequence length must divide the rank count")
+        self.H, self.L, self.D, self.r = int(n_heads), int(seq_len), int(head_dim), int(d_lr)
+        self.chunk = self.L // self.world
+        self.assignment = np.asarray(assignment, dtype=np.int64)
+        if self.assignment.shape != (self.H,) or self.assignment.min() < 0 or self.assignment.max() >= self.world:
+            raise ValueError("assignment must map every head to a rank")
+        if (self.D * 2) % 16 or (self.r * 2) % 16:
+            raise ValueError("peer exchange needs head_dim and d_lr multiples of 8")
+        self.heads_of = [np.nonzero(self.assignment == r)[0] for r in range(self.world)]
+        self.my_heads = self.heads_of[self.rank]
+        self.hi_of = np.zeros(self.H, dtype=np.int64)
+        for hs in self.heads_of:
+            self.hi_of[hs] = np.arange(len(hs))
+        self.splits = int(splits)
+        self.ledger = Ledger()
+        nh_max = max(len(h) for h in self.heads_of)
+        big, small, back = nh_max * self.L * self.D, nh_max * self.L * self.r, self.H * self.chunk * self.D
+        names = [("q", big), ("k", big), ("v", big), ("do", big), ("qlr", small), ("klr", small),
+                 ("o", back), ("dq", back), ("dk", back), ("dv", back)]
+        self.off, tot = {}, 0
+        for n, sz in names:
+            self.off[n] = tot
+            tot += -(-sz // 64) * 64                       # keep regions 128-byte aligned
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.buf = symm.empty(tot, dtype=torch.bfloat16, device=dev)
+        if hasattr(symm, "enable_symm_mem_for_group"):
+            try:
+                symm.enable_symm_mem_for_group(self.group.group_name)
+            except Exception:   # newer torch: implicit
+                pass
+        self.hdl = symm.rendezvous(self.buf, self.group)
+        self.ptrs = np.asarray([int(p) for p in self.hdl.buffer_ptrs], dtype=np.int64)
+        self._tables = {}
+
+    # ------------------------------------------------------------------ views
+    def region(self, name: str) -> torch.Tensor:
+        nh = len(self.my_heads)
+        o = self.off[name]
+        if name in ("q", "k", "v", "do"):
+            return self.buf[o: o + nh * self.L * self.D].view(nh, self.L, self.D)
+        if name in ("qlr", "klr"):
+            return self.buf[o: o + nh * self.L * self.r].view(nh, self.L, self.r)
+        return self.buf[o: o + self.H * self.chunk * self.D].view(self.H, self.chunk, self.D)
+
+    # ------------------------------------------------------------------ job tables
+    def _table(self, key, build):
+        t = self._tables.get(key)
+        if t is None:
+            if len(self._tables) >= 16:
+                self._tables.clear()
+            t = torch.from_numpy(build()).to(self.buf.device)
+            self._tables[key] = t
+        return t
+
+    def _fwd_jobs(self, q, k, v, do, p):
+        H, L, D, r, chunk, me = self.H, self.L, self.D, self.r, self.chunk, self.rank
+        h = np.arange(H, dtype=np.int64)
+        owner, hi = self.assignment, self.hi_of
+        dst_base = self.ptrs[owner]
+        jobs = []
+        for name, t in (("q", q), ("k", k), ("v", v), ("do", do)):
+            j = np.empty((H, 6), dtype=np.int64)
+            j[:, 0] = t.data_ptr() + h * chunk * D * 2
+            j[:, 1] = dst_base + 2 * (self.off[name] + (hi * L + me * chunk) * D)
+            j[:, 2] = j[:, 3] = chunk * D * 2
+            j[:, 4] = 1
+            j[:, 5] = chunk * D * 2
+            jobs.append(j)
+        for side, name in ((0, "qlr"), (1, "klr")):
+            j = np.empty((H, 6), dtype=np.int64)
+            j[:, 0] = p.data_ptr() + 2 * (side * H + h) * r
+            j[:, 1] = dst_base + 2 * (self.off[name] + (hi * L + me * chunk) * r)
+            j[:, 2] = 2 * H * r * 2
+            j[:, 3] = r * 2
+            j[:, 4] = chunk
+            j[:, 5] = r * 2
+            jobs.append(j)
+        return np.ascontiguousarray(np.concatenate(jobs))
+
+    def _back_jobs(self, tensors):
+        L, D, chunk = self.L, self.D, self.chunk
+        hs = self.my_heads
+        nh = len(hs)
+        hi = np.repeat(np.arange(nh, dtype=np.int64), self.world)
+        dst_r = np.tile(np.arange(self.world, dtype=np.int64), nh)
+        dst_h = np.repeat(hs.astype(np.int64), self.world)
+        jobs = []
+        for name, t in zip(("o", "dq", "dk", "dv"), tensors):
+            j = np.empty((nh * self.world, 6), dtype=np.int64)
+            j[:, 0] = t.data_ptr() + 2 * (hi * L + dst_r * chunk) * D
+            j[:, 1] = self.ptrs[dst_r] + 2 * (self.off[name] + dst_h * chunk * D)
+            j[:, 2] = j[:, 3] = chunk * D * 2
+            j[:, 4] = 1
+            j[:, 5] = chunk * D * 2
+            jobs.append(j)
+        return np.ascontiguousarray(np.concatenate(jobs))
+
+    def _run(self, table):
+        from . import ops
+
+        self.hdl.barrier(channel=0)          # owners are done reading the previous contents
+        ops.copy_jobs(table, self.splits)
+        self.hdl.barrier(channel=0)          # every writer is done: regions are complete
+
+    # ------------------------------------------------------------------ exchanges
+    def to_heads(self, q, k, v, do, p):
+        """q, k, v, do [H, L/N, D] and P [L/N, 2 H r] (this rank's tokens) ->
+        views Q, K, V, dO [my_heads, L, D], Q_lr, K_lr [my_heads, L, r]."""
+        for t in (q, k, v, do, p):
+            if not t.is_contiguous() or t.dtype != torch.bfloat16:
+                raise ValueError("peer exchange expects contiguous bf16 tensors")
+        if q.shape != (self.H, self.chunk, self.D) or p.shape != (self.chunk, 2 * self.H * self.r):
+            raise ValueError("shape does not match the exchange plan")
+        key = ("f",) + tuple(t.data_ptr() for t in (q, k, v, do, p))
+        self._run(self._table(key, lambda: self._fwd_jobs(q, k, v, do, p)))
+        self._account(("hcp_fwd", 3 * self.D + 2 * self.r), ("hcp_bwd_in", self.D), to_heads=True)
+        return tuple(self.region(n) for n in ("q", "k", "v", "do", "qlr", "klr"))
+
+    def to_tokens(self, o, dq, dk, dv):
+        """o, dq, dk, dv [my_heads, L, D] -> views [H, L/N, D] on the token owners."""
+        nh = len(self.my_heads)
+        for t in (o, dq, dk, dv):
+            if t.shape != (nh, self.L, self.D) or not t.is_contiguous() or t.dtype != torch.bfloat16:
+                raise ValueError("peer exchange expects contiguous bf16 [my_heads, L, D]")
+        key = ("b",) + tuple(t.data_ptr() for t in (o, dq, dk, dv))
+        self._run(self._table(key, lambda: self._back_jobs((o, dq, dk, dv))))
+        self._account(("output_redistribute", self.D), ("hcp_bwd_out", 3 * self.D), to_heads=False)
+        return tuple(self.region(n) for n in ("o", "dq", "dk", "dv"))
+
+    def _account(self, *phases, to_heads: bool):
+        nh = len(self.my_heads)
+        remote_heads_out = self.H - nh                 # my tokens of other ranks' heads
+        remote_in = nh * (self.world - 1)              # my heads' tokens held elsewhere
+        for phase, width in phases:
+            row = self.chunk * width * 2
+            if to_heads:
+                self.ledger.add(phase, remote_heads_out * row, remote_in * row)
+            else:
+                self.ledger.add(phase, remote_in * row, remote_heads_out * row)
+
+
 def plan_heads(sparsities, seq_len: int, head_dim: int, world: int, balanced: bool = True):
     """Head -> rank assignment: sparsity-aware `balance_heads` or the contiguous split."""
     if not balanced:
@@ -236,29 +400,58 @@ class HeadParallelDSV:
     """The DSV layer under HCP: sequence-sharded in, sequence-sharded out."""
 
     def __init__(self, grid, heads: int, head_dim: int, d_lr: int = 16, voxel=(8, 4, 4),
-                 sparsity=0.9, balanced: bool = True, group=None, device="cuda"):
+                 sparsity=0.9, balanced: bool = True, group=None, device="cuda",
+                 transport: str = "auto"):
         from .layer import DSVAttentionLayer
 
         self.world = dist.get_world_size(group)
         sp = np.broadcast_to(np.asarray(sparsity, dtype=np.float64), (heads,)).copy()
         self.assignment = plan_heads(sp, grid.size, head_dim, self.world, balanced)
-        self.ex = HeadParallelExchange(heads, grid.size, self.assignment, group)
+        if transport == "auto":
+            transport = "peer" if torch.device(device).type == "cuda" else "all_to_all"
+        if transport not in ("peer", "all_to_all"):
+            raise ValueError(f"unknown transport {transport!r}")
+        self.transport = transport
+        if transport == "peer":
+            self.ex = PeerExchange(heads, grid.size, head_dim, d_lr, self.assignment, group, device)
+        else:
+            self.ex = HeadParallelExchange(heads, grid.size, self.assignment, group)
         self.H, self.D, self.r = heads, head_dim, d_lr
         mine = self.ex.my_heads
         self.local = DSVAttentionLayer(grid, len(mine), head_dim, d_lr, voxel, sp[mine], device)
+        self.marks = None   # set to [] to record (name, cuda event) after each phase
+
+    def _mark(self, name):
+        if self.marks is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self.marks.append((name, ev))
+
+    def phase_ms(self):
+        """Per-phase device time of the last step recorded with marks=[]."""
+        torch.cuda.synchronize()
+        m = self.marks or []
+        return {b[0]: a[1].elapsed_time(b[1]) for a, b in zip(m, m[1:])}
 
     def step(self, x_local, wt, q, k, v, dout):
         """x_local [L/N, H*D]; q, k, v, dout [H, L/N, D] -> (out, dq, dk, dv) [H, L/N, D].
 
-        The dO exchange runs asynchronously during the forward, and O travels back
-        during the backward (NCCL streams overlap the attention kernels).
+        transport "peer": two peer-memory copy kernels per step (inputs to the head
+        owners, results back), outputs are views valid until the next step.
+        transport "all_to_all": packed torch.distributed all-to-alls (any backend);
+        the dO exchange runs asynchronously during the forward, and O travels back
+        during the backward.
         """
         from . import ops
 
+        if self.transport == "peer":
+            return self._step_peer(x_local, wt, q, k, v, dout)
         H, r, D, ex = self.H, self.r, self.D, self.ex
         dev = q.device
         chunk = ex.chunk
+        self._mark("start")
         p = ops.project(x_local, wt)                                   # [L/N, 2 H r]
+        self._mark("project")
         hm = ex.send_rows_headmajor(dev)
         p_rows = p.view(chunk * 2 * H, r)
         fwd = ex.to_heads_packed([(q.reshape(H * chunk, D), hm), (k.reshape(H * chunk, D), hm),
@@ -266,12 +459,38 @@ class HeadParallelDSV:
                                   (p_rows, ex.send_rows_lowrank(0, dev)),
                                   (p_rows, ex.send_rows_lowrank(1, dev))], "hcp_fwd")
         h_do = ex.to_heads_packed([(dout.reshape(H * chunk, D), hm)], "hcp_bwd_in", async_op=True)
+        self._mark("pack+send_fwd")
         ql, kl, vl, qlr, klr = ex.finish(fwd)
+        self._mark("recv_fwd+unpack")
         sel = self.local.select_from_lowrank(qlr, klr)
+        self._mark("select")
         out, lse = self.local.forward(ql, kl, vl, sel)
+        self._mark("fwd")
         h_o = ex.to_tokens_packed([out], "output_redistribute", async_op=True)
         (dout_m,) = ex.finish(h_do)
+        self._mark("send_o+recv_do")
         dq, dk, dv = self.local.backward(ql, kl, vl, out, lse, dout_m, sel)
+        self._mark("bwd")
         grads = ex.finish(ex.to_tokens_packed([dq, dk, dv], "hcp_bwd_out"))
+        self._mark("grads_back")
         (out_local,) = ex.finish(h_o)
+        self._mark("o_back")
         return (out_local, *grads)
+
+    def _step_peer(self, x_local, wt, q, k, v, dout):
+        from . import ops
+
+        self._mark("start")
+        p = ops.project(x_local, wt)                                   # [L/N, 2 H r]
+        self._mark("project")
+        ql, kl, vl, dout_m, qlr, klr = self.ex.to_heads(q, k, v, dout, p)
+        self._mark("exchange_in")
+        sel = self.local.select_from_lowrank(qlr, klr)
+        self._mark("select")
+        out, lse = self.local.forward(ql, kl, vl, sel)
+        self._mark("fwd")
+        dq, dk, dv = self.local.backward(ql, kl, vl, out, lse, dout_m, sel)
+        self._mark("bwd")
+        res = self.ex.to_tokens(out, dq, dk, dv)
+        self._mark("exchange_out")
+        return res

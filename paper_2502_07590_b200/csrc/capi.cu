@@ -115,7 +115,7 @@ int dsv_gemm_bf16(const void* A, long long lda, long long a_bs, const void* B, l
     return fail(DSV_EINVAL, "gemm: operand strides must be multiples of 16 bytes");
   if (c_dtype != DSV_DTYPE_F32 && c_dtype != DSV_DTYPE_BF16)
     return fail(DSV_EINVAL, "gemm: bad output dtype");
-  const int bn = N >= 256 ? 256 : 128;
+  const int bn = (N >= 256 && K > 64) ? 256 : 128;
   CUtensorMap ta, tb;
   {
     const uint64_t dims[3] = {(uint64_t)K, (uint64_t)M, (uint64_t)nbatch};
@@ -255,6 +255,43 @@ gather_rows_kernel(const uint8_t* __restrict__ src, long long sstride, const int
   }
 }
 }  // namespace
+
+// Job-table copy: blockIdx.x = job, blockIdx.y = split; each thread moves 16-byte
+// chunks, four in flight. HBM- or NVLink-bound; the stores may target peer memory.
+__global__ void __launch_bounds__(256) copy_jobs_kernel(const dsv_copy_job* __restrict__ jobs) {
+  const dsv_copy_job j = jobs[blockIdx.x];
+  const uint32_t cpr = (uint32_t)(j.row_bytes >> 4);
+  const uint32_t total = (uint32_t)j.rows * cpr;
+  const uint32_t step = gridDim.y * blockDim.x;
+  const uint8_t* src = reinterpret_cast<const uint8_t*>(j.src);
+  uint8_t* dst = reinterpret_cast<uint8_t*>(j.dst);
+  auto saddr = [&](uint32_t c) {
+    const uint32_t r = c / cpr, w = c - r * cpr;
+    return reinterpret_cast<const uint4*>(src + (long long)r * j.src_stride + (w << 4));
+  };
+  auto daddr = [&](uint32_t c) {
+    const uint32_t r = c / cpr, w = c - r * cpr;
+    return reinterpret_cast<uint4*>(dst + (long long)r * j.dst_stride + (w << 4));
+  };
+  uint32_t c = blockIdx.y * blockDim.x + threadIdx.x;
+  for (; c + 3 * step < total; c += 4 * step) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldcs(saddr(c + u * step));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) *daddr(c + u * step) = v[u];
+  }
+  for (; c < total; c += step) *daddr(c) = __ldcs(saddr(c));
+}
+
+extern "C" int dsv_copy_jobs(const dsv_copy_job* jobs, int njobs, int splits, void* stream) {
+  if (njobs <= 0) return DSV_OK;
+  if (!jobs || splits < 1 || splits > 1024)
+    return fail(DSV_EINVAL, "copy_jobs: bad job table or split count");
+  dim3 grid(njobs, splits);
+  copy_jobs_kernel<<<grid, 256, 0, S(stream)>>>(jobs);
+  return cuda_status((int)cudaGetLastError(), "copy_jobs launch");
+}
 
 extern "C" int dsv_gather_rows(const void* src, long long src_stride, const int* rows, int n,
                                int row_bytes, void* out, long long out_stride, void* stream) {

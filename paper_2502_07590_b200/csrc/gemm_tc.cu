@@ -31,7 +31,7 @@ struct SmemLayout {
 };
 
 template <int BN, int STAGES, bool kF32Out>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(128)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
             void* __restrict__ C, int M, int N, int K, long long ldc, long long c_bs) {
   using SL = SmemLayout<BN, STAGES>;
@@ -43,7 +43,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN, b = blockIdx.z;
+  // N tiles fastest: the CTAs sharing one A tile run together, so A streams from
+  // DRAM once (the projection's X is 196 MB at c2; B = Wt stays in L2)
+  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, b = blockIdx.z;
   const int nk = (K + BK - 1) / BK;
   constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
 
@@ -154,7 +156,7 @@ static int launch_gemm(const CUtensorMap* ta, const CUtensorMap* tb, void* C, in
   const int smem = SmemLayout<BN, STAGES>::kBytes;
   auto kern = gemm_kernel<BN, STAGES, F32>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  dim3 grid((M + BM - 1) / BM, (N + BN - 1) / BN, nbatch);
+  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, nbatch);
   kern<<<grid, 128, smem, st>>>(*ta, *tb, C, M, N, K, ldc, c_bs);
   return (int)cudaGetLastError();
 }
@@ -162,6 +164,10 @@ static int launch_gemm(const CUtensorMap* ta, const CUtensorMap* tb, void* C, in
 int dsv_gemm_launch(const CUtensorMap* ta, const CUtensorMap* tb, void* C, int M, int N, int K,
                     long long ldc, long long c_bs, int nbatch, int f32_out, int bn,
                     cudaStream_t st) {
+  if (K <= dsv::gemm::BK) {   // one k-block (proxy scores, K = r): small CTAs, several per SM
+    return f32_out ? launch_gemm<128, 1, true>(ta, tb, C, M, N, K, ldc, c_bs, nbatch, st)
+                   : launch_gemm<128, 1, false>(ta, tb, C, M, N, K, ldc, c_bs, nbatch, st);
+  }
   if (bn == 256) {
     return f32_out ? launch_gemm<256, 4, true>(ta, tb, C, M, N, K, ldc, c_bs, nbatch, st)
                    : launch_gemm<256, 4, false>(ta, tb, C, M, N, K, ldc, c_bs, nbatch, st);

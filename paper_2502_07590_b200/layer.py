@@ -140,3 +140,50 @@ class DSVAttentionLayer:
             "fwd_flops": 4 * pairs * D,
             "bwd_flops": 10 * pairs * D,
         }
+
+
+class HostPipeline:
+    """Runs a device step over host-resident batches, H2D of batch i+1 overlapping step i.
+
+    Two device buffer sets; the copies run on a side stream from pinned host memory
+    (the sequence of `step` calls on the current stream is unchanged). Each yielded
+    result is whatever `step(*device_inputs)` returned, already synchronised by the
+    caller's own D2H read.
+    """
+
+    def __init__(self, like, device):
+        dev = torch.device(device)
+        self.bufs = [[torch.empty(t.shape, dtype=t.dtype, device=dev) for t in like] for _ in range(2)]
+        self.copy = torch.cuda.Stream(dev)
+        self.ready = [torch.cuda.Event(), torch.cuda.Event()]
+        self.free = [None, None]
+        self.h2d_bytes = sum(t.numel() * t.element_size() for t in like)
+
+    def _stage(self, slot, host):
+        with torch.cuda.stream(self.copy):
+            if self.free[slot] is not None:
+                self.copy.wait_event(self.free[slot])
+            for src, dst in zip(host, self.bufs[slot]):
+                if not src.is_pinned():
+                    raise ValueError("HostPipeline expects pinned host tensors")
+                dst.copy_(src, non_blocking=True)
+            self.ready[slot].record(self.copy)
+
+    def run(self, step, batches):
+        it = iter(batches)
+        nxt = next(it, None)
+        slot = 0
+        if nxt is not None:
+            self._stage(slot, nxt)
+        while nxt is not None:
+            nxt = next(it, None)
+            if nxt is not None:
+                self._stage(slot ^ 1, nxt)
+            cur = torch.cuda.current_stream()
+            cur.wait_event(self.ready[slot])
+            res = step(*self.bufs[slot])
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            self.free[slot] = ev
+            yield res
+            slot ^= 1

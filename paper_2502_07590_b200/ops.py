@@ -215,6 +215,15 @@ def gather_rows(src: torch.Tensor, rows: torch.Tensor, out: torch.Tensor | None 
     return out
 
 
+def copy_jobs(jobs: torch.Tensor, splits: int = 16) -> None:
+    """Run a [njobs, 6] int64 device job table (src, dst, src_stride, dst_stride, rows,
+    row_bytes) in one launch (dsv_copy_jobs); addresses may be NVLink peer pointers."""
+    _require_cuda(jobs)
+    if jobs.dtype != torch.int64 or jobs.dim() != 2 or jobs.shape[1] != 6 or not jobs.is_contiguous():
+        raise ValueError("copy_jobs: expected a contiguous [njobs, 6] int64 table")
+    _lib.call("dsv_copy_jobs", _ptr(jobs), jobs.shape[0], int(splits), _stream())
+
+
 def f32_to_bf16(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     _require_cuda(x)
     x = x.contiguous()

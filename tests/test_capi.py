@@ -18,7 +18,7 @@ def _declared():
 def test_header_declares_the_boundary():
     names = _declared()
     for must in ("dsv_topk", "dsv_sparse_fwd", "dsv_sparse_bwd", "dsv_project", "dsv_gemm_bf16",
-                 "dsv_scores_f32", "dsv_rows_fwd", "dsv_rows_bwd", "dsv_gather_rows"):
+                 "dsv_scores_f32", "dsv_rows_fwd", "dsv_rows_bwd", "dsv_gather_rows", "dsv_copy_jobs"):
         assert must in names
 
 
