@@ -240,12 +240,16 @@ class PeerExchange:
     """
 
     def __init__(self, n_heads: int, seq_len: int, head_dim: int, d_lr: int, assignment,
-                 group=None, device=None, splits: int = 16):
-        import torch.distributed._symmetric_memory as symm
-
-        self.group = group if group is not None else dist.group.WORLD
-        self.rank = dist.get_rank(group)
-        self.world = dist.get_world_size(group)
+                 group=None, device=None, splits: int = 16, *, plan_only=None):
+        """plan_only=(rank, world, buffer_ptrs): index/job planning without a process
+        group or device memory (host tests drive the job tables through an emulator)."""
+        if plan_only is None:
+            self.group = group if group is not None else dist.group.WORLD
+            self.rank = dist.get_rank(group)
+            self.world = dist.get_world_size(group)
+        else:
+            self.group = None
+            self.rank, self.world = int(plan_only[0]), int(plan_only[1])
         if seq_len % self.world:
             raise ValueError("sequence length must divide the rank count")
         self.H, self.L, self.D, self.r = int(n_heads), int(seq_len), int(head_dim), int(d_lr)
@@ -270,6 +274,14 @@ class PeerExchange:
         for n, sz in names:
             self.off[n] = tot
             tot += -(-sz // 64) * 64                       # keep regions 128-byte aligned
+        self.total_elems = tot
+        self._tables = {}
+        if plan_only is not None:
+            self.buf, self.hdl = None, None
+            self.ptrs = np.asarray(plan_only[2], dtype=np.int64)
+            return
+        import torch.distributed._symmetric_memory as symm
+
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.buf = symm.empty(tot, dtype=torch.bfloat16, device=dev)
         if hasattr(symm, "enable_symm_mem_for_group"):
@@ -279,7 +291,6 @@ class PeerExchange:
                 pass
         self.hdl = symm.rendezvous(self.buf, self.group)
         self.ptrs = np.asarray([int(p) for p in self.hdl.buffer_ptrs], dtype=np.int64)
-        self._tables = {}
 
     # ------------------------------------------------------------------ views
     def region(self, name: str) -> torch.Tensor:
