@@ -134,6 +134,11 @@ typedef struct dsv_copy_job {
  * `splits` blocks cooperate on each job (1..1024). */
 int dsv_copy_jobs(const dsv_copy_job* jobs, int njobs, int splits, void* stream);
 
+/* Diagnostics: copy the backward kernel's phase timeline (clock64 stamps, filled only
+ * by builds with -DDSV_BWD_PROF; layout [8 CTAs][32 blocks][12 events] int64) into a
+ * host buffer. Returns the bytes copied or a negative value. */
+int dsv_debug_timeline(void* host_dst, int bytes);
+
 /* fp32 -> bf16 conversion of n contiguous elements. */
 int dsv_f32_to_bf16(const float* in, void* out, long long n, void* stream);
 

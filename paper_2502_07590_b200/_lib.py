@@ -13,7 +13,8 @@ from ctypes import c_float, c_int, c_longlong, c_void_p
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libdsv.so"
+# DSV_LIB: an alternate build of the same library (ablation / profiling variants)
+LIB_PATH = Path(os.environ["DSV_LIB"]) if os.environ.get("DSV_LIB") else _PKG / "libdsv.so"
 
 DSV_OK, DSV_EINVAL, DSV_EUNSUPPORTED, DSV_ECUDA = 0, 1, 2, 3
 DTYPE_F32, DTYPE_BF16 = 0, 1
@@ -45,6 +46,7 @@ SIGNATURES = {
     "dsv_rows_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                      c_void_p, c_int, c_int, c_int, c_int, c_float, c_int, c_void_p, c_void_p,
                      c_void_p, c_void_p],
+    "dsv_debug_timeline": [c_void_p, c_int],
     "dsv_copy_jobs": [c_void_p, c_int, c_int, c_void_p],
     "dsv_gather_rows": [c_void_p, c_longlong, c_void_p, c_int, c_int, c_void_p, c_longlong,
                         c_void_p],

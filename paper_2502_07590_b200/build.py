@@ -45,20 +45,23 @@ def up_to_date() -> bool:
     return LIB.exists() and LIB.stat().st_mtime >= _deps_mtime()
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, defines=(), out: Path | None = None) -> Path:
+    """defines: extra -D flags for a variant library written to `out` (tools only)."""
+    lib = Path(out) if out is not None else LIB
+    if not force and not defines and up_to_date():
         return LIB
     nvcc = _nvcc()
-    BUILD.mkdir(parents=True, exist_ok=True)
+    bdir = BUILD if not defines else BUILD.parent / ("dsv_" + "_".join(d.split("=")[0].lower() for d in defines))
+    bdir.mkdir(parents=True, exist_ok=True)
     objs = []
 
     def compile_one(src: Path):
-        obj = BUILD / (src.stem + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+        obj = bdir / (src.stem + ".o")
+        cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", str(src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src.name}:\n{res.stderr}")
-        (BUILD / (src.stem + ".ptxas.txt")).write_text(res.stderr)
+        (bdir / (src.stem + ".ptxas.txt")).write_text(res.stderr)
         return obj, res.stderr
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
@@ -66,14 +69,17 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             objs.append(obj)
             if verbose:
                 sys.stderr.write(log)
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python build.py [--force] [-v] [-DNAME=VAL ... --out path/libvariant.so]
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    out = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs, out=out))

@@ -14,22 +14,22 @@
 // domain of the scaled logits (lse2 = max + log2(sum)).
 //
 // Both kernels run one CTA per (head, group), head-major so the K/V of the two
-// or three heads in flight stay L2-resident, 416 threads:
-//   warps 0-3  : row workers (one TMEM lane = one row per thread)
-//   warp  4    : tcgen05.mma issuer (one elected lane) + TMEM owner
-//   warps 5-12 : gather producers — 256 threads issue 16-byte cp.async copies of
-//                the selected K/V rows straight into 128B-swizzled UMMA tiles
-//                (measured on B200: ~50 B/clk/SM for random 256 B rows, vs ~8 for
-//                TMA tile::gather4), a 3-deep (fwd) / 2-deep (bwd) ring.
+// or three heads in flight stay L2-resident. Gather producers issue 16-byte
+// cp.async copies of the selected K/V rows straight into 128B-swizzled UMMA tiles
+// (measured on B200: ~50 B/clk/SM for random 256 B rows, vs ~8 for TMA
+// tile::gather4). Forward, 544 threads: warps 0-7 two softmax warpgroups, warp 8
+// tcgen05.mma issuer + TMEM owner, warps 9-16 producers (3-deep K/V ring).
+// Backward, 864 threads: warps 0-15 row workers (4 per TMEM lane quarter), warp 16
+// MMA issuer, warps 17-18 producers, warps 19-26 dK/dV scatter.
 // Forward: S_j = Q K_j^T into one of two TMEM S buffers; softmax workers take
 // the row max in a first TMEM pass, write P (bf16) over S in a second, rescale
 // O in TMEM only when the max grows by > 2^8; O += P_{j-1} V_{j-1} reads P from
 // TMEM (A operand) and V from shared memory (MN-major B).
 // Backward (transposed, keys in TMEM lanes): S^T = K_j Q^T, dP^T = V_j dO^T;
 // workers (one key per thread) form P^T, dS^T in TMEM and dS in smem; then
-// dQ += dS K_j, dV_j = P^T dO, dK_j = dS^T Q; dV_j / dK_j rows are staged per
-// warp through shared memory and scatter-added with row-contiguous red.v4
-// (coalesced: 2x the L2 reduction rate of row-per-thread atomics).
+// dQ += dS K_j, dV_j = P^T dO, dK_j = dS^T Q; dV_j / dK_j rows are staged
+// through shared memory and scatter-added with row-contiguous red.v4 (coalesced:
+// 2x the L2 reduction rate of row-per-thread atomics) by dedicated warps.
 
 #include <cuda.h>
 #include "dsv_common.cuh"
@@ -39,27 +39,23 @@ namespace attn {
 
 constexpr int BQ = 128;   // queries per tile
 constexpr int BKV = 128;  // keys per block
-constexpr int kWorkWarps = 4;
-constexpr int kMmaWarp = 4;
-constexpr int kProdWarp0 = 5;
-constexpr int kProdWarps = 8;
+constexpr int kProdWarps = 8;                 // forward gather producers
 constexpr int kProdThreads = kProdWarps * 32;
-constexpr int kThreads = (kWorkWarps + 1 + kProdWarps) * 32;
 
-template <int D>
+template <int D, int NT = kProdThreads>
 struct Gather {
   static constexpr int kCPR = D / 8;                          // 16-byte chunks per row
-  static constexpr int kPer = 128 * kCPR / kProdThreads;      // chunks per thread per tile
-  static constexpr int kRowStep = kProdThreads / kCPR;        // rows between a thread's chunks
+  static constexpr int kPer = 128 * kCPR / NT;                // chunks per thread per tile
+  static constexpr int kRowStep = NT / kCPR;                  // rows between a thread's chunks
   static constexpr int kTile = 128 * D * 2;
 };
 
 // Issue the cp.async copies of one 128-row tile (rows[i] = absolute row id of
 // this thread's i-th chunk) into a 128B-swizzled K-major tile (atom = 64 cols).
-template <int D>
+template <int D, int NT = kProdThreads>
 DSV_DEV void issue_tile(uint8_t* tile, const __nv_bfloat16* base,
-                        const int (&rows)[Gather<D>::kPer], int ptid) {
-  using G = Gather<D>;
+                        const int (&rows)[Gather<D, NT>::kPer], int ptid) {
+  using G = Gather<D, NT>;
   const int q = ptid % G::kCPR, r0 = ptid / G::kCPR;
   const uint32_t t0 = smem_u32(tile) + (q >> 3) * (128 * 128);
 #pragma unroll
@@ -331,15 +327,51 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
 }
 
 // ====================================================================== bwd
-// Per KV block j (keys in TMEM lanes):
-//   A_j  MMA   S^T = K_j Q^T -> tA, dP^T = V_j dO^T -> tB          (V_j free after)
-//   B_j  work  P^T, dS^T (bf16) over tA/tB, dS -> smem
-//   C_j  MMA   dQ += dS K_j -> tDq (K_j free), dV_j -> tC, dK_j -> tA[64:] | tB[64:]
-//   C'_j work  dV_j, dK_j rows -> bf16 staging in smem; TMEM released
-//   D_j  prod  staging -> coalesced red.v4 into the fp32 dK/dV accumulators
-// D_j (bounded by the L2 reduction rate) overlaps A..C' of block j+1. Staging the
-// per-block contributions in bf16 rounds each contribution like P and dS already
-// are; the accumulation itself stays fp32.
+// Per KV block j (keys in TMEM lanes; TMEM columns: tA | tB | tC | tDq):
+//   A_j  MMA   S^T = K_j Q^T -> tA, dP^T = V_j dO^T -> tB            (V_j free after)
+//   B_j  work  P^T, dS^T (bf16) -> tC[0,64), tC[64,128); dS -> smem (MN-major)
+//   C_j  MMA   dQ += dS K_j -> tDq (K_j free), dV_j = P^T dO -> tA, dK_j = dS^T Q -> tB
+//   C'_j work  dV_j -> staging half 0, dK_j -> staging half 1 (bf16); TMEM is released
+//              as soon as both are in registers
+//   D_j  scat  staging -> coalesced red.global.add.v4.f32 into the fp32 accumulators
+// The fp32 adds into L2 (~5.5 TB/s on B200, measured for both red.v4 and TMA bulk
+// reductions) bound the backward on random selections: 128 KB of adds per block.
+// So the scatter warps only scatter — loads have their own warps — and each staging
+// half is freed on its own, which keeps the reduction stream busy while A..C' of
+// the next block run underneath it.
+// Staging rounds each per-block contribution to bf16 like P and dS already are;
+// the accumulation itself stays fp32.
+#ifndef DSV_BWD_WORK_WARPS
+#define DSV_BWD_WORK_WARPS 16
+#endif
+constexpr int kBwdWork = DSV_BWD_WORK_WARPS;        // multiple of 4 (TMEM lane quarters)
+constexpr int kBwdWPQ = kBwdWork / 4;              // worker warps per lane quarter
+constexpr int kBwdWorkThreads = kBwdWork * 32;
+constexpr int kBwdMmaWarp = kBwdWork;
+constexpr int kBwdLoadWarp0 = kBwdWork + 1;
+constexpr int kBwdLoadWarps = 2;
+constexpr int kBwdLoadThreads = kBwdLoadWarps * 32;
+constexpr int kBwdScatWarp0 = kBwdLoadWarp0 + kBwdLoadWarps;
+#ifndef DSV_BWD_SCAT_WARPS
+#define DSV_BWD_SCAT_WARPS 8
+#endif
+constexpr int kBwdScatWarps = DSV_BWD_SCAT_WARPS;
+constexpr int kBwdScatThreads = kBwdScatWarps * 32;
+constexpr int kBwdThreads = (kBwdScatWarp0 + kBwdScatWarps) * 32;   // 864 by default
+
+// Optional in-kernel timeline (variant builds with -DDSV_BWD_PROF): clock64 stamps of
+// each role's phase boundaries for the first kProfCtas CTAs, read by dsv_debug_timeline.
+constexpr int kProfCtas = 8, kProfBlocks = 32, kProfEv = 12;
+__device__ long long g_bwd_prof[kProfCtas][kProfBlocks][kProfEv];
+#ifdef DSV_BWD_PROF
+#define PROF(j, e) do { if (blockIdx.x < kProfCtas && (j) < kProfBlocks) g_bwd_prof[blockIdx.x][j][e] = clock64(); } while (0)
+#else
+#define PROF(j, e) do {} while (0)
+#endif
+#ifndef DSV_BWD_SCATTER
+#define DSV_BWD_SCATTER 0   // 1: ablation build only (no global adds)
+#endif
+
 template <int D>
 struct BwdSmem {
   static constexpr int kTile = 128 * D * 2;
@@ -348,16 +380,18 @@ struct BwdSmem {
   static constexpr int kdS = kdO + kTile;                 // [128 keys][128 q] bf16 (MN-major A)
   static constexpr int kK = kdS + 128 * 128 * 2;
   static constexpr int kV = kK + kTile;
-  static constexpr int kStg = kV + kTile;                 // [2 tensors][128 rows][D] bf16
+  static constexpr int kStg = kV + kTile;                 // [2 halves][128 rows][D] bf16
   static constexpr int kLse = kStg + 2 * 128 * D * 2;
   static constexpr int kDelta = kLse + 512;
   static constexpr int kBar = kDelta + 512;
   static constexpr int kBytes = kBar + 256 + 1024;
+  static_assert(kBytes <= 232448, "backward shared memory over 227 KB");
 };
 
 struct BwdBars {
   uint64_t q_full, k_full, v_full, k_empty, v_empty;
-  uint64_t sdp_full, pds_full, mma_done, tmem_free, stg_full, stg_free;
+  uint64_t sdp_full, pds_full, mma_done, tmem_free;
+  uint64_t stg_full[2], stg_free[2];                      // [0] = dV half, [1] = dK half
   uint32_t tmem;
 };
 
@@ -369,7 +403,7 @@ DSV_DEV uint32_t stg_off(int p, int q) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kBwdThreads, 1)
 sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __restrict__ dOg,
                   const __nv_bfloat16* __restrict__ Kg, const __nv_bfloat16* __restrict__ Vg,
                   const __nv_bfloat16* __restrict__ Og, const float* __restrict__ lse,
@@ -379,7 +413,7 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
                   float scale_log2,
                   __nv_bfloat16* __restrict__ dQ, float* __restrict__ dK, float* __restrict__ dV) {
   using SL = BwdSmem<D>;
-  using GT = Gather<D>;
+  using GT = Gather<D, kBwdLoadThreads>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = aligned_smem(smem_raw);
   BwdBars& B = *reinterpret_cast<BwdBars*>(smem + SL::kBar);
@@ -398,20 +432,23 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   const int nblk = (kh + BKV - 1) / BKV;
   const int* irow = idx + ((long long)h * G + g) * ldk;
   const int* mrow = grp_rows + (long long)g * BQ;
+  constexpr int kCh = D / 32;                              // 32-column chunks per tensor
 
-  if (warp == kMmaWarp) {
+  if (warp == kBwdMmaWarp) {
     if (lane == 0) {
-      mbar_init(&B.q_full, kProdThreads);
-      mbar_init(&B.k_full, kProdThreads);
-      mbar_init(&B.v_full, kProdThreads);
+      mbar_init(&B.q_full, kBwdLoadThreads);
+      mbar_init(&B.k_full, kBwdLoadThreads);
+      mbar_init(&B.v_full, kBwdLoadThreads);
       mbar_init(&B.k_empty, 1);
       mbar_init(&B.v_empty, 1);
       mbar_init(&B.sdp_full, 1);
-      mbar_init(&B.pds_full, 128);
+      mbar_init(&B.pds_full, kBwdWorkThreads);
       mbar_init(&B.mma_done, 1);
-      mbar_init(&B.tmem_free, 128);
-      mbar_init(&B.stg_full, 128);
-      mbar_init(&B.stg_free, kProdThreads);
+      mbar_init(&B.tmem_free, kBwdWorkThreads);
+      for (int t = 0; t < 2; ++t) {
+        mbar_init(&B.stg_full[t], kBwdWorkThreads);   // every worker, once per half
+        mbar_init(&B.stg_free[t], kBwdScatThreads);
+      }
       fence_barrier_init();
     }
     __syncwarp();
@@ -424,78 +461,82 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   const uint32_t tA = tmem, tB = tmem + 128, tC = tmem + 256, tDq = tmem + 384;
   const long long hoff = (long long)h * Lk * D;
 
-  if (warp >= kProdWarp0) {
-    // ------------------------------------------------------------ producers + scatter
-    const int ptid = threadIdx.x - kProdWarp0 * 32;
-    const int pw = ptid >> 5;
+  if (warp >= kBwdScatWarp0) {
+    // ------------------------------------------------------------ scatter
+    constexpr int RPW = 128 / kBwdScatWarps;        // staging rows per scatter warp
+    const int pw = warp - kBwdScatWarp0;            // rows [RPW pw, RPW pw + RPW)
+    const int stid = threadIdx.x - kBwdScatWarp0 * 32;
+    for (int jb = 0; jb < nblk; ++jb) {
+      const int kv = min(BKV, kh - jb * BKV);
+      const int myrow = pw * RPW + (lane % RPW);
+      const int mykey = myrow < kv ? __ldg(irow + jb * BKV + myrow) : 0;
+#pragma unroll 1
+      for (int t = 0; t < 2; ++t) {
+        mbar_wait(&B.stg_full[t], jb & 1);
+        if (stid == 0) PROF(jb, 8 + t);
+        float* acc = (t == 0 ? dV : dK) + hoff;
+        const uint8_t* stg = sStg + t * (128 * D * 2);
+        if constexpr (D == 128) {
+#pragma unroll 4
+          for (int rr = 0; rr < RPW; ++rr) {
+            const int p = pw * RPW + rr;
+            const int key = __shfl_sync(0xffffffffu, mykey, rr);
+            if (p < kv) {
+              const uint2 v = *reinterpret_cast<const uint2*>(stg + stg_off<D>(p, lane >> 1) + (lane & 1) * 8);
+#if DSV_BWD_SCATTER == 1
+              if (v.x == 0x7fc17fc1u) acc[0] = 0.f;   // ablation: no global traffic
+#else
+              red_add_v4(acc + (long long)key * D + lane * 4, bf16lo(v.x), bf16hi(v.x),
+                         bf16lo(v.y), bf16hi(v.y));
+#endif
+            }
+          }
+        } else {
+#pragma unroll 4
+          for (int rr = 0; rr < RPW; rr += 2) {
+            const int p = pw * RPW + rr + (lane >> 4);
+            const int key = __shfl_sync(0xffffffffu, mykey, rr + (lane >> 4));
+            if (p < kv) {
+              const int e = (lane & 15) * 4;
+              const uint2 v = *reinterpret_cast<const uint2*>(stg + stg_off<D>(p, e >> 3) + ((e >> 2) & 1) * 8);
+              red_add_v4(acc + (long long)key * D + e, bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y));
+            }
+          }
+        }
+        mbar_arrive(&B.stg_free[t]);
+      }
+      if (stid == 0) PROF(jb, 10);
+    }
+  } else if (warp >= kBwdLoadWarp0) {
+    // ------------------------------------------------------------ gather producers
+    const int ptid = threadIdx.x - kBwdLoadWarp0 * 32;
     const int r0 = ptid / GT::kCPR;
     int rows[GT::kPer];
     const int qbase = h * Lq;
 #pragma unroll
     for (int i = 0; i < GT::kPer; ++i) rows[i] = qbase + __ldg(mrow + r0 + i * GT::kRowStep);
-    issue_tile<D>(sQ, Qg, rows, ptid);
-    issue_tile<D>(sdO, dOg, rows, ptid);
+    issue_tile<D, kBwdLoadThreads>(sQ, Qg, rows, ptid);
+    issue_tile<D, kBwdLoadThreads>(sdO, dOg, rows, ptid);
     cp_async_arrive_noinc(&B.q_full);
     const int kbase = h * Lk;
-    // scatter of block jb: warp pw owns rows [16 pw, 16 pw + 16) of both tensors
-    auto scatter = [&](int jb) {
-      const int kv = min(BKV, kh - jb * BKV);
-      const int myrow = pw * 16 + (lane & 15);
-      const int mykey = myrow < kv ? __ldg(irow + jb * BKV + myrow) : 0;
-      mbar_wait(&B.stg_full, jb & 1);
-      if constexpr (D == 128) {
-#pragma unroll 4
-        for (int rr = 0; rr < 16; ++rr) {
-          const int p = pw * 16 + rr;
-          const int key = __shfl_sync(0xffffffffu, mykey, rr);
-          if (p < kv) {
-#pragma unroll
-            for (int t = 0; t < 2; ++t) {
-              const uint2 v = *reinterpret_cast<const uint2*>(
-                  sStg + t * (128 * D * 2) + stg_off<D>(p, lane >> 1) + (lane & 1) * 8);
-              red_add_v4((t == 0 ? dV : dK) + hoff + (long long)key * D + lane * 4,
-                         bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y));
-            }
-          }
-        }
-      } else {
-#pragma unroll 4
-        for (int rr = 0; rr < 16; rr += 2) {
-          const int p = pw * 16 + rr + (lane >> 4);
-          const int key = __shfl_sync(0xffffffffu, mykey, rr + (lane >> 4));
-          if (p < kv) {
-            const int e = (lane & 15) * 4;
-#pragma unroll
-            for (int t = 0; t < 2; ++t) {
-              const uint2 v = *reinterpret_cast<const uint2*>(
-                  sStg + t * (128 * D * 2) + stg_off<D>(p, e >> 3) + ((e >> 2) & 1) * 8);
-              red_add_v4((t == 0 ? dV : dK) + hoff + (long long)key * D + e,
-                         bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y));
-            }
-          }
-        }
-      }
-      mbar_arrive(&B.stg_free);
-    };
     for (int j = 0; j < nblk; ++j) {
 #pragma unroll
       for (int i = 0; i < GT::kPer; ++i)
         rows[i] = kbase + __ldg(irow + min(j * BKV + r0 + i * GT::kRowStep, kh - 1));
       if (j > 0) mbar_wait(&B.v_empty, (j - 1) & 1);
-      issue_tile<D>(sV, Vg, rows, ptid);
+      if (ptid == 0) PROF(j, 0);
+      issue_tile<D, kBwdLoadThreads>(sV, Vg, rows, ptid);
       cp_async_arrive_noinc(&B.v_full);
       if (j > 0) mbar_wait(&B.k_empty, (j - 1) & 1);
-      issue_tile<D>(sK, Kg, rows, ptid);
+      if (ptid == 0) PROF(j, 1);
+      issue_tile<D, kBwdLoadThreads>(sK, Kg, rows, ptid);
       cp_async_arrive_noinc(&B.k_full);
-      if (j > 0) scatter(j - 1);
     }
-    scatter(nblk - 1);
     cp_async_wait<0>();
-  } else if (warp == kMmaWarp) {
+  } else if (warp == kBwdMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idST = idesc_bf16_f32(128, 128, 0, 0);   // K_j . Q^T, V_j . dO^T
-    constexpr uint32_t idDV = idesc_bf16_f32(128, D, 0, 1);     // P^T(tmem) . dO(MN)
-    constexpr uint32_t idDK = idesc_bf16_f32(128, 64, 0, 1);    // dS^T(tmem) . Q(MN), 64 cols
+    constexpr uint32_t idTS = idesc_bf16_f32(128, D, 0, 1);     // P^T|dS^T (tmem) . dO|Q (MN)
     constexpr uint32_t idDQ = idesc_bf16_f32(128, D, 1, 1);     // dS(MN smem) . K_j(MN)
     const uint32_t aQ = smem_u32(sQ), adO = smem_u32(sdO), adS = smem_u32(sdS);
     const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
@@ -505,6 +546,7 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
       mbar_wait(&B.v_full, j & 1);
       if (j > 0) mbar_wait(&B.tmem_free, (j - 1) & 1);
       tc_fence_after();
+      if (lane == 0) PROF(j, 2);
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -522,6 +564,7 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
       __syncwarp();
       mbar_wait(&B.pds_full, j & 1);
       tc_fence_after();
+      if (lane == 0) PROF(j, 3);
       if (elect_one()) {
         // dQ += dS K_j    (A = dS MN-major in smem, B = K_j MN-major)
 #pragma unroll
@@ -529,29 +572,25 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
           mma_ss(tDq, sdesc_sw128(adS + kk * 2048, 128 * 128, 1024),
                  sdesc_sw128(aK + kk * 2048, 128 * 128, 1024), idDQ, (j | kk) != 0);
         mma_commit(&B.k_empty);
-        // dV_j = P^T dO   (A = P^T in TMEM cols tA[0,64), K = 128 queries)
+        // dV_j = P^T dO -> tA, dK_j = dS^T Q -> tB  (A from TMEM, K = 128 queries)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          mma_ts(tC, tA + kk * 8, sdesc_sw128(adO + kk * 2048, 128 * 128, 1024), idDV, kk > 0);
-        // dK_j = dS^T Q   (A = dS^T in TMEM cols tB[0,64)); N split in 64-column halves
+          mma_ts(tA, tC + kk * 8, sdesc_sw128(adO + kk * 2048, 128 * 128, 1024), idTS, kk > 0);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          mma_ts(tA + 64, tB + kk * 8, sdesc_sw128(aQ + kk * 2048, 128 * 128, 1024), idDK, kk > 0);
-          if constexpr (D == 128)
-            mma_ts(tB + 64, tB + kk * 8, sdesc_sw128(aQ + 128 * 128 + kk * 2048, 128 * 128, 1024),
-                   idDK, kk > 0);
-        }
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts(tB, tC + 64 + kk * 8, sdesc_sw128(aQ + kk * 2048, 128 * 128, 1024), idTS, kk > 0);
         mma_commit(&B.mma_done);
       }
       __syncwarp();
     }
   } else {
     // ------------------------------------------------------------ workers
-    const int row = warp * 32 + lane;   // query row in prologue/epilogue; key row per block
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const int quarter = warp & 3, cg = warp >> 2;   // TMEM lane quarter, 32-column slice
+    const int row = quarter * 32 + lane;            // query row (prologue/epilogue), key row (blocks)
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const int gsz = grp_size[g];
     const int tok = mrow[row];
-    {
+    if (cg == 0) {
       // prologue: lse2 and Delta = rowsum(dO * O) for this query row
       float dlt = 0.f, l2 = INFINITY;
       if (row < gsz) {
@@ -568,73 +607,102 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
         l2 = lse[(long long)h * Lq + tok];
       }
       sLse[row] = l2;
-      sDelta[row] = dlt;
-      named_bar_sync(1, 128);
+      sDelta[row] = dlt * scale;                    // dS = P (dP scale - Delta scale)
     }
+    named_bar_sync(1, kBwdWorkThreads);
+    // staging of one 32-column chunk (fp32 registers -> bf16 staging row)
+    auto stage = [&](const uint32_t (&r)[32], int t, int c) {
+      uint8_t* srow = sStg + t * (128 * D * 2);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<uint4*>(srow + stg_off<D>(row, c * 4 + q)) = make_uint4(
+            pack_bf16(__uint_as_float(r[8 * q + 0]), __uint_as_float(r[8 * q + 1])),
+            pack_bf16(__uint_as_float(r[8 * q + 2]), __uint_as_float(r[8 * q + 3])),
+            pack_bf16(__uint_as_float(r[8 * q + 4]), __uint_as_float(r[8 * q + 5])),
+            pack_bf16(__uint_as_float(r[8 * q + 6]), __uint_as_float(r[8 * q + 7])));
+    };
     for (int j = 0; j < nblk; ++j) {
       const int kv = min(BKV, kh - j * BKV);
       const bool kvalid = row < kv;
       mbar_wait(&B.sdp_full, j & 1);
       tc_fence_after();
+      if (threadIdx.x == 0) PROF(j, 4);
+      // ---- B: 16-query halves of this warp's 32-query slices, for its 32 keys
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t rs[32], rd[32];
-        tmem_ld32(tA + lane_off + c * 32, rs);
-        tmem_ld32(tB + lane_off + c * 32, rd);
+      for (int hs = cg * 2; hs < 8; hs += 2 * kBwdWPQ) {
+#pragma unroll 1
+      for (int hf = 0; hf < 2; ++hf) {
+        const int q0 = (hs + hf) * 16;
+        uint32_t rs[16], rd[16];
+        tmem_ld16(tA + lane_off + q0, rs);
+        tmem_ld16(tB + lane_off + q0, rd);
         tmem_ld_wait();
-        uint32_t pp[16], dd[16];
+        uint32_t pp[8], dd[8];
+        if (kvalid) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int q0 = c * 32 + 2 * i;
-          float p0 = fast_exp2(fmaf(__uint_as_float(rs[2 * i]), scale_log2, -sLse[q0]));
-          float p1 = fast_exp2(fmaf(__uint_as_float(rs[2 * i + 1]), scale_log2, -sLse[q0 + 1]));
-          float d0 = p0 * (__uint_as_float(rd[2 * i]) - sDelta[q0]) * scale;
-          float d1 = p1 * (__uint_as_float(rd[2 * i + 1]) - sDelta[q0 + 1]) * scale;
-          if (!kvalid) { p0 = p1 = d0 = d1 = 0.f; }
-          pp[i] = pack_bf16(p0, p1);
-          dd[i] = pack_bf16(d0, d1);
-        }
-        tmem_st16(tA + lane_off + c * 16, pp);
-        tmem_st16(tB + lane_off + c * 16, dd);
-        // dS row (this key) into the MN-major dS tile: atom c/2, chunks (c%2)*4..+3
+          for (int i = 0; i < 8; i += 2) {
+            const float4 l = *reinterpret_cast<const float4*>(sLse + q0 + 2 * i);
+            const float4 dl = *reinterpret_cast<const float4*>(sDelta + q0 + 2 * i);
+            const float p0 = fast_exp2(fmaf(__uint_as_float(rs[2 * i]), scale_log2, -l.x));
+            const float p1 = fast_exp2(fmaf(__uint_as_float(rs[2 * i + 1]), scale_log2, -l.y));
+            const float p2 = fast_exp2(fmaf(__uint_as_float(rs[2 * i + 2]), scale_log2, -l.z));
+            const float p3 = fast_exp2(fmaf(__uint_as_float(rs[2 * i + 3]), scale_log2, -l.w));
+            pp[i] = pack_bf16(p0, p1);
+            pp[i + 1] = pack_bf16(p2, p3);
+            dd[i] = pack_bf16(p0 * fmaf(__uint_as_float(rd[2 * i]), scale, -dl.x),
+                              p1 * fmaf(__uint_as_float(rd[2 * i + 1]), scale, -dl.y));
+            dd[i + 1] = pack_bf16(p2 * fmaf(__uint_as_float(rd[2 * i + 2]), scale, -dl.z),
+                                  p3 * fmaf(__uint_as_float(rd[2 * i + 3]), scale, -dl.w));
+          }
+        } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint8_t* dst = sdS + (c >> 1) * (128 * 128) + sw128_off(row, (c & 1) * 4 + q);
-          *reinterpret_cast<uint4*>(dst) = make_uint4(dd[4 * q], dd[4 * q + 1], dd[4 * q + 2], dd[4 * q + 3]);
+          for (int i = 0; i < 8; ++i) pp[i] = dd[i] = 0u;
         }
+        tmem_st8(tC + lane_off + (q0 >> 1), pp);
+        tmem_st8(tC + 64 + lane_off + (q0 >> 1), dd);
+        // dS row (this key) into the MN-major dS tile: atom q0/64, 16-byte chunks
+        uint8_t* base = sdS + (q0 >> 6) * (128 * 128);
+        const int ch = (q0 & 63) >> 3;
+        *reinterpret_cast<uint4*>(base + sw128_off(row, ch)) = make_uint4(dd[0], dd[1], dd[2], dd[3]);
+        *reinterpret_cast<uint4*>(base + sw128_off(row, ch + 1)) = make_uint4(dd[4], dd[5], dd[6], dd[7]);
+      }
       }
       tmem_st_wait();
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&B.pds_full);
-      // ---- C': dV_j / dK_j rows -> bf16 staging (after the previous scatter drained it)
+      if (threadIdx.x == 0) PROF(j, 5);
+      // ---- C': dV_j | dK_j 32-column chunks -> bf16 staging halves. Tasks n = cg,
+      // cg + WPQ, ... of the 2 * kCh per quarter (t = n / kCh, chunk n % kCh); TMEM is
+      // released after the last TMEM read, before that chunk is staged.
       mbar_wait(&B.mma_done, j & 1);
       tc_fence_after();
-      if (j > 0) mbar_wait(&B.stg_free, (j - 1) & 1);
+      if (threadIdx.x == 0) PROF(j, 6);
+      int cur_t = 0;
 #pragma unroll 1
-      for (int n = 0; n < 2 * (D / 32); ++n) {
-        const int t = n / (D / 32), c = n % (D / 32);
-        const uint32_t taddr = t == 0 ? tC + c * 32 : (c < 2 ? tA : tB) + 64 + (c & 1) * 32;
+      for (int n = cg; n < 2 * kCh; n += kBwdWPQ) {
+        const int t = n / kCh, c = n % kCh;
         uint32_t r[32];
-        tmem_ld32(taddr + lane_off, r);
+        tmem_ld32((t == 0 ? tA : tB) + lane_off + c * 32, r);
         tmem_ld_wait();
-        uint8_t* srow = sStg + t * (128 * D * 2);
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          *reinterpret_cast<uint4*>(srow + stg_off<D>(row, c * 4 + q)) = make_uint4(
-              pack_bf16(__uint_as_float(r[8 * q + 0]), __uint_as_float(r[8 * q + 1])),
-              pack_bf16(__uint_as_float(r[8 * q + 2]), __uint_as_float(r[8 * q + 3])),
-              pack_bf16(__uint_as_float(r[8 * q + 4]), __uint_as_float(r[8 * q + 5])),
-              pack_bf16(__uint_as_float(r[8 * q + 6]), __uint_as_float(r[8 * q + 7])));
+        if (n + kBwdWPQ >= 2 * kCh) {
+          tc_fence_before();
+          mbar_arrive(&B.tmem_free);                // last TMEM read of this block
+          if (threadIdx.x == 0) PROF(j, 7);
+        }
+        if (t != cur_t) { mbar_arrive(&B.stg_full[0]); cur_t = 1; }
+        if (n - kBwdWPQ < 0 || (n - kBwdWPQ) / kCh != t) {
+          if (j > 0) mbar_wait(&B.stg_free[t], (j - 1) & 1);   // first chunk of half t
+        }
+        stage(r, t, c);
       }
-      tc_fence_before();
-      mbar_arrive(&B.tmem_free);
-      mbar_arrive(&B.stg_full);
+      if (cur_t == 0) mbar_arrive(&B.stg_full[0]);
+      mbar_arrive(&B.stg_full[1]);
     }
     // ---------------- dQ epilogue (query rows); the last mma_done covered dQ
     __nv_bfloat16* qrow = dQ + ((long long)h * Lq + tok) * D;
 #pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = cg; c < D / 32; c += 4) {
       uint32_t r[32];
       tmem_ld32(tDq + lane_off + c * 32, r);
       tmem_ld_wait();
@@ -651,7 +719,7 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == kMmaWarp) tmem_dealloc(tmem, 512);
+  if (warp == kBwdMmaWarp) tmem_dealloc(tmem, 512);
 }
 
 __global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
@@ -705,7 +773,7 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* O
   auto kern = sparse_bwd_kernel<D>;
   const int smem = BwdSmem<D>::kBytes;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  kern<<<H * G, kThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)dO,
+  kern<<<H * G, kBwdThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)dO,
                                       (const __nv_bfloat16*)k, (const __nv_bfloat16*)v,
                                       (const __nv_bfloat16*)O, lse, grp_rows, grp_size, idx, ldk,
                                       kcount, kcount_hg, G, Lq, Lk, scale, scale_log2,
@@ -725,6 +793,12 @@ int dsv_attn_bwd_tc_launch(const void* q, const void* k, const void* v, const vo
     return bwd_launch<64>(q, k, v, O, dO, lse, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H,
                           G, Lq, Lk, scale, scale_log2, dQ, dK, dV, st);
   return 1;
+}
+
+int dsv_debug_timeline_copy(void* dst, int bytes) {
+  const int n = (int)sizeof(g_bwd_prof) < bytes ? (int)sizeof(g_bwd_prof) : bytes;
+  if (cudaMemcpyFromSymbol(dst, g_bwd_prof, n) != cudaSuccess) return -1;
+  return n;
 }
 
 int dsv_f32_to_bf16_launch(const float* in, void* out, long long n, cudaStream_t st) {

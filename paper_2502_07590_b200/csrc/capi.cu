@@ -284,6 +284,12 @@ __global__ void __launch_bounds__(256) copy_jobs_kernel(const dsv_copy_job* __re
   for (; c < total; c += step) *daddr(c) = __ldcs(saddr(c));
 }
 
+int dsv_debug_timeline_copy(void* dst, int bytes);
+extern "C" int dsv_debug_timeline(void* host_dst, int bytes) {
+  if (!host_dst || bytes <= 0) return fail(DSV_EINVAL, "debug_timeline: bad buffer");
+  return dsv_debug_timeline_copy(host_dst, bytes);
+}
+
 extern "C" int dsv_copy_jobs(const dsv_copy_job* jobs, int njobs, int splits, void* stream) {
   if (njobs <= 0) return DSV_OK;
   if (!jobs || splits < 1 || splits > 1024)
