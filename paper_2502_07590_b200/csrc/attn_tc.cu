@@ -17,8 +17,9 @@
 // or three heads in flight stay L2-resident. Gather producers issue 16-byte
 // cp.async copies of the selected K/V rows straight into 128B-swizzled UMMA tiles
 // (measured on B200: ~50 B/clk/SM for random 256 B rows, vs ~8 for TMA
-// tile::gather4). Forward, 544 threads: warps 0-7 two softmax warpgroups, warp 8
-// tcgen05.mma issuer + TMEM owner, warps 9-16 producers (3-deep K/V ring).
+// tile::gather4). Forward, 800 threads: warps 0-15 softmax (4 warps per TMEM lane
+// quarter, one 32-key slice each), warp 16 tcgen05.mma issuer + TMEM owner, warps
+// 17-24 producers (K ring 2-deep, V ring 3-deep, three S/P buffers in TMEM).
 // Backward, 864 threads: warps 0-15 row workers (4 per TMEM lane quarter), warp 16
 // MMA issuer, warps 17-18 producers, warps 19-26 dK/dV scatter.
 // Forward: S_j = Q K_j^T into one of two TMEM S buffers; softmax workers take
@@ -64,63 +65,150 @@ DSV_DEV void issue_tile(uint8_t* tile, const __nv_bfloat16* base,
 }
 
 // ====================================================================== fwd
-constexpr int kFwdStages = 3;
-constexpr int kFwdSoftWGs = 2;                                   // warps 0-7
-constexpr int kFwdMmaWarp = 8;
-constexpr int kFwdProdWarp0 = 9;
-constexpr int kFwdThreads = (kFwdSoftWGs * 4 + 1 + kProdWarps) * 32;   // 544
+constexpr int kFwdKStages = 2;                                   // K_j frees after S_j
+constexpr int kFwdStages = 3;                                    // V ring (frees after PV_j)
+constexpr int kFwdSBufs = 3;                                     // S/P buffers in TMEM
+constexpr int kFwdSoftWGs = 4;                                   // warps 0-15
+constexpr int kFwdSoftThreads = kFwdSoftWGs * 128;
+constexpr int kFwdMmaWarp = kFwdSoftWGs * 4;
+constexpr int kFwdProdWarp0 = kFwdMmaWarp + 1;
+constexpr int kFwdThreads = (kFwdProdWarp0 + kProdWarps) * 32;   // 800
 
 template <int D>
 struct FwdSmem {
   static constexpr int kTile = 128 * D * 2;
   static constexpr int kQ = 0;
   static constexpr int kK = kQ + kTile;
-  static constexpr int kV = kK + kFwdStages * kTile;
-  static constexpr int kML = kQ;   // [2 WG][2][128] floats, reuses Q once all MMAs are done
-  static constexpr int kBar = kV + kFwdStages * kTile;
+  static constexpr int kV = kK + kFwdKStages * kTile;
+  static constexpr int kMax = kV + kFwdStages * kTile;   // [2 parity][4 slices][128] fp32
+  static constexpr int kBar = kMax + 2 * kFwdSoftWGs * 128 * 4;
   static constexpr int kBytes = kBar + 256 + 1024;
 };
 
 struct FwdBars {
   uint64_t q_full;
-  uint64_t kv_full[kFwdStages], kv_empty[kFwdStages];
-  uint64_t s_full[2], p_full[2];
+  uint64_t k_full[kFwdKStages], k_empty[kFwdKStages];     // K_j is free once S_j is done,
+  uint64_t v_full[kFwdStages], v_empty[kFwdStages];       // V_j only after PV_j
+  // per S/P buffer, so no barrier can run two phases ahead of its waiter
+  uint64_t s_full[kFwdSBufs], p_full[kFwdSBufs], pv_done[kFwdSBufs];
   uint64_t o_final;
   uint32_t tmem;
 };
+
+// Optional in-kernel timeline (variant builds with -DDSV_BWD_PROF / -DDSV_FWD_PROF):
+// clock64 stamps of each role's phase boundaries for the first kProfCtas CTAs of the
+// backward (or forward) kernel, read back by dsv_debug_timeline.
+constexpr int kProfCtas = 8, kProfBlocks = 32, kProfEv = 12;
+__device__ long long g_bwd_prof[kProfCtas][kProfBlocks][kProfEv];
+#define PROF_STAMP(j, e) do { if (blockIdx.x < kProfCtas && (j) < kProfBlocks) g_bwd_prof[blockIdx.x][j][e] = clock64(); } while (0)
+#ifdef DSV_BWD_PROF
+#define PROF(j, e) PROF_STAMP(j, e)
+#else
+#define PROF(j, e) do {} while (0)
+#endif
+#ifdef DSV_FWD_PROF
+#define FPROF(j, e) PROF_STAMP(j, e)
+#else
+#define FPROF(j, e) do {} while (0)
+#endif
 
 // Shared-memory base aligned to 1024 B without leaving the shared address space.
 DSV_DEV uint8_t* aligned_smem(uint8_t* raw) {
   return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
 }
 
-// Softmax pass 2 over one S buffer: P = 2^(s*scale_log2 - m) (bf16) written over
-// the S columns already read; returns the row sum of P.
+// Softmax pass 1: row max of the raw scores of one S buffer (two TMEM loads in flight,
+// 3-input max).
 template <bool kMasked>
-DSV_DEV float softmax_p_pass(uint32_t tS, float scale_log2, float m, int kv) {
-  float lsum = 0.f;
+DSV_DEV float softmax_max_pass(uint32_t tS, int kv) {
+  float mx = -INFINITY;
 #pragma unroll 1
-  for (int c = 0; c < BKV / 32; ++c) {
-    uint32_t r[32];
-    tmem_ld32(tS + c * 32, r);
+  for (int c = 0; c < BKV / 32; c += 2) {
+    uint32_t r0[32], r1[32];
+    tmem_ld32(tS + c * 32, r0);
+    tmem_ld32(tS + (c + 1) * 32, r1);
     tmem_ld_wait();
-    uint32_t pk[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      float p0 = fast_exp2(fmaf(__uint_as_float(r[2 * i]), scale_log2, -m));
-      float p1 = fast_exp2(fmaf(__uint_as_float(r[2 * i + 1]), scale_log2, -m));
+    for (int i = 0; i < 32; i += 2) {
+      float a0 = __uint_as_float(r0[i]), a1 = __uint_as_float(r0[i + 1]);
+      float b0 = __uint_as_float(r1[i]), b1 = __uint_as_float(r1[i + 1]);
       if constexpr (kMasked) {
-        if (c * 32 + 2 * i >= kv) p0 = 0.f;
-        if (c * 32 + 2 * i + 1 >= kv) p1 = 0.f;
+        if (c * 32 + i >= kv) a0 = -INFINITY;
+        if (c * 32 + i + 1 >= kv) a1 = -INFINITY;
+        if ((c + 1) * 32 + i >= kv) b0 = -INFINITY;
+        if ((c + 1) * 32 + i + 1 >= kv) b1 = -INFINITY;
       }
-      lsum += p0 + p1;
-      pk[i] = pack_bf16(p0, p1);
+      mx = fmax3f(mx, a0, a1);
+      mx = fmax3f(mx, b0, b1);
     }
-    tmem_st16(tS + c * 16, pk);
   }
-  return lsum;
+  return mx;
 }
 
+#ifndef DSV_POLY_EVERY
+#define DSV_POLY_EVERY 4      // one pair in DSV_POLY_EVERY takes the polynomial (0: none)
+#endif
+#ifndef DSV_P_CHUNKS
+#define DSV_P_CHUNKS 2        // 32-column chunks loaded per TMEM wait in pass 2
+#endif
+// P for one 32-column chunk of raw scores: 2^(s*scale_log2 - m) with packed FMAs; one
+// pair in four takes the polynomial exp2 on the FMA pipe, the rest the MUFU.
+template <bool kMasked>
+DSV_DEV void softmax_p_chunk(const uint32_t (&r)[32], uint32_t tdst, f32x2 sc2, f32x2 nm2, int c,
+                             int kv, f32x2& lsum2) {
+  uint32_t pk[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const f32x2 x = ffma2(f2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), sc2, nm2);
+    float2 p;
+    if (DSV_POLY_EVERY > 0 && (i % (DSV_POLY_EVERY > 0 ? DSV_POLY_EVERY : 1)) == DSV_POLY_EVERY - 1) {
+      p = f2u(exp2_poly2(x));
+    } else {
+      const float2 xv = f2u(x);
+      p = make_float2(fast_exp2(xv.x), fast_exp2(xv.y));
+    }
+    if constexpr (kMasked) {
+      if (c * 32 + 2 * i >= kv) p.x = 0.f;
+      if (c * 32 + 2 * i + 1 >= kv) p.y = 0.f;
+    }
+    lsum2 = fadd2(lsum2, f2(p.x, p.y));
+    pk[i] = pack_bf16(p.x, p.y);
+  }
+  tmem_st16(tdst, pk);
+}
+
+// Softmax pass 2 over one S buffer: P = 2^(s*scale_log2 - m) (bf16) written over
+// the S columns already read (chunk c -> columns [16c, 16c+16)); returns the row sum.
+template <bool kMasked>
+DSV_DEV float softmax_p_pass(uint32_t tS, float scale_log2, float m, int kv) {
+  const f32x2 sc2 = f2(scale_log2, scale_log2), nm2 = f2(-m, -m);
+  f32x2 lsum2 = f2(0.f, 0.f);
+#pragma unroll 1
+  for (int c = 0; c < BKV / 32; c += DSV_P_CHUNKS) {
+    uint32_t r0[32];
+    tmem_ld32(tS + c * 32, r0);
+    if constexpr (DSV_P_CHUNKS == 2) {
+      uint32_t r1[32];
+      tmem_ld32(tS + (c + 1) * 32, r1);
+      tmem_ld_wait();
+      softmax_p_chunk<kMasked>(r0, tS + c * 16, sc2, nm2, c, kv, lsum2);
+      softmax_p_chunk<kMasked>(r1, tS + (c + 1) * 16, sc2, nm2, c + 1, kv, lsum2);
+    } else {
+      tmem_ld_wait();
+      softmax_p_chunk<kMasked>(r0, tS + c * 16, sc2, nm2, c, kv, lsum2);
+    }
+  }
+  const float2 l = f2u(lsum2);
+  return l.x + l.y;
+}
+
+// Forward structure. All four softmax warpgroups work on every key block: warp w
+// owns TMEM lanes 32 (w % 4).. (query rows) and key columns [32 (w / 4), +32), so a
+// block's softmax is spread over 16 warps and the row max is exchanged through
+// shared memory once per block. With one O accumulator the
+// TMEM holds three S/P buffers, and the MMA issues S_{j+3} right after PV_j: the
+// softmax of block j+1 never waits for PV_j to drain. O is rescaled (lazily, when
+// the running max grows by > 2^8) only after PV_{j-1} has completed.
 template <int D>
 __global__ void __launch_bounds__(kFwdThreads, 1)
 sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __restrict__ Kg,
@@ -131,14 +219,14 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
                   float* __restrict__ lse) {
   using SL = FwdSmem<D>;
   using GT = Gather<D>;
-  constexpr int ST = kFwdStages;
+  constexpr int ST = kFwdStages, KST = kFwdKStages, NS = kFwdSBufs;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = aligned_smem(smem_raw);
   FwdBars& B = *reinterpret_cast<FwdBars*>(smem + SL::kBar);
   uint8_t* sQ = smem + SL::kQ;
   uint8_t* sK = smem + SL::kK;
   uint8_t* sV = smem + SL::kV;
-  float* sML = reinterpret_cast<float*>(smem + SL::kML);
+  float* sMax = reinterpret_cast<float*>(smem + SL::kMax);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = blockIdx.x / G, g = blockIdx.x - h * G;
@@ -150,8 +238,13 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   if (warp == kFwdMmaWarp) {
     if (lane == 0) {
       mbar_init(&B.q_full, kProdThreads);
-      for (int s = 0; s < ST; ++s) { mbar_init(&B.kv_full[s], kProdThreads); mbar_init(&B.kv_empty[s], 1); }
-      for (int s = 0; s < 2; ++s) { mbar_init(&B.s_full[s], 1); mbar_init(&B.p_full[s], 128); }
+      for (int s = 0; s < KST; ++s) { mbar_init(&B.k_full[s], kProdThreads / 2); mbar_init(&B.k_empty[s], 1); }
+      for (int s = 0; s < ST; ++s) { mbar_init(&B.v_full[s], kProdThreads / 2); mbar_init(&B.v_empty[s], 1); }
+      for (int s = 0; s < NS; ++s) {
+        mbar_init(&B.s_full[s], 1);
+        mbar_init(&B.p_full[s], kFwdSoftThreads);
+        mbar_init(&B.pv_done[s], 1);
+      }
       mbar_init(&B.o_final, 1);
       fence_barrier_init();
     }
@@ -162,164 +255,186 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = B.tmem;
-  const uint32_t tS0 = tmem, tO0 = tmem + 256;   // S_b at tS0 + 128 b, O_w at tO0 + 128 w
+  const uint32_t tS0 = tmem, tO = tmem + NS * 128;   // S/P buffer b at tS0 + 128 b
 
   if (warp >= kFwdProdWarp0) {
     // ------------------------------------------------------------ producers
-    // cp.async copies arrive on the stage's "full" barrier asynchronously
-    // (cp.async.mbarrier.arrive.noinc: one arrival per producer thread).
+    // Two groups of 4 warps: one streams K tiles, the other V tiles, each through its
+    // own 3-deep ring (K_j frees as soon as S_j is computed, so K runs ahead while V
+    // waits for the PV products). cp.async copies arrive on the stage's "full"
+    // barrier asynchronously (cp.async.mbarrier.arrive.noinc, one per thread).
+    using GH = Gather<D, kProdThreads / 2>;
     const int ptid = threadIdx.x - kFwdProdWarp0 * 32;
-    const int r0 = ptid / GT::kCPR;
-    int rows[GT::kPer];
-    const int qbase = h * Lq;
+    {
+      const int r0 = ptid / GT::kCPR;
+      int qrows[GT::kPer];
 #pragma unroll
-    for (int i = 0; i < GT::kPer; ++i) rows[i] = qbase + __ldg(mrow + r0 + i * GT::kRowStep);
-    issue_tile<D>(sQ, Qg, rows, ptid);
-    cp_async_arrive_noinc(&B.q_full);
+      for (int i = 0; i < GT::kPer; ++i) qrows[i] = h * Lq + __ldg(mrow + r0 + i * GT::kRowStep);
+      issue_tile<D>(sQ, Qg, qrows, ptid);
+      cp_async_arrive_noinc(&B.q_full);
+    }
+    const bool is_v = ptid >= kProdThreads / 2;
+    const int gtid = is_v ? ptid - kProdThreads / 2 : ptid;
+    const int r0 = gtid / GH::kCPR;
+    const __nv_bfloat16* src = is_v ? Vg : Kg;
+    uint8_t* ring = is_v ? sV : sK;
+    uint64_t* full = is_v ? B.v_full : B.k_full;
+    uint64_t* empty = is_v ? B.v_empty : B.k_empty;
+    const int nst = is_v ? ST : KST;
     const int kbase = h * Lk;
+    int rows[GH::kPer];
     for (int j = 0; j < nblk; ++j) {
-      const int st = j % ST;
+      const int st = j % nst;
 #pragma unroll
-      for (int i = 0; i < GT::kPer; ++i)
-        rows[i] = kbase + __ldg(irow + min(j * BKV + r0 + i * GT::kRowStep, kh - 1));
-      if (j >= ST) mbar_wait(&B.kv_empty[st], ((j / ST) - 1) & 1);
-      issue_tile<D>(sK + st * SL::kTile, Kg, rows, ptid);
-      issue_tile<D>(sV + st * SL::kTile, Vg, rows, ptid);
-      cp_async_arrive_noinc(&B.kv_full[st]);
+      for (int i = 0; i < GH::kPer; ++i)
+        rows[i] = kbase + __ldg(irow + min(j * BKV + r0 + i * GH::kRowStep, kh - 1));
+      if (j >= nst) mbar_wait(&empty[st], ((j / nst) - 1) & 1);
+      if (gtid == 0) FPROF(j, is_v ? 6 : 5);
+      issue_tile<D, kProdThreads / 2>(ring + st * SL::kTile, src, rows, gtid);
+      cp_async_arrive_noinc(&full[st]);
     }
     cp_async_wait<0>();
   } else if (warp == kFwdMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
+    // order: S_0 S_1 S_2 PV_0 S_3 PV_1 S_4 ... (S_{j+3} reuses the buffer PV_j just read)
     constexpr uint32_t idS = idesc_bf16_f32(128, BKV, 0, 0);
     constexpr uint32_t idO = idesc_bf16_f32(128, D, 0, 1);
     const uint32_t aQ = smem_u32(sQ);
+    auto issue_s = [&](int s) {
+      const int st = s % KST;
+      mbar_wait(&B.k_full[st], (s / KST) & 1);
+      tc_fence_after();
+      if (lane == 0) FPROF(s, 0);
+      if (elect_one()) {
+        const uint32_t aK = smem_u32(sK + st * SL::kTile);
+        const uint32_t dS = tS0 + (s % NS) * 128;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+          mma_ss(dS, sdesc_sw128(aQ + off, 16, 1024), sdesc_sw128(aK + off, 16, 1024), idS, kk > 0);
+        }
+        mma_commit(&B.s_full[s % NS]);
+        mma_commit(&B.k_empty[st]);
+      }
+      __syncwarp();
+    };
     mbar_wait(&B.q_full, 0);
-    for (int j = 0; j <= nblk; ++j) {
-      if (j < nblk) {
-        const int st = j % ST;
-        mbar_wait(&B.kv_full[st], (j / ST) & 1);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t aK = smem_u32(sK + st * SL::kTile);
-          const uint32_t dS = tS0 + (j & 1) * 128;
+    for (int s = 0; s < NS && s < nblk; ++s) issue_s(s);
+    for (int j = 0; j < nblk; ++j) {
+      const int st = j % ST;
+      mbar_wait(&B.p_full[j % NS], (j / NS) & 1);
+      mbar_wait(&B.v_full[st], (j / ST) & 1);
+      tc_fence_after();
+      if (lane == 0) FPROF(j, 1);
+      if (elect_one()) {
+        const uint32_t aV = smem_u32(sV + st * SL::kTile);
+        const uint32_t tP = tS0 + (j % NS) * 128;
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-            mma_ss(dS, sdesc_sw128(aQ + off, 16, 1024), sdesc_sw128(aK + off, 16, 1024), idS,
-                   kk > 0);
-          }
-          mma_commit(&B.s_full[j & 1]);
-        }
-        __syncwarp();
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          mma_ts(tO, tP + kk * 8, sdesc_sw128(aV + kk * 2048, 128 * 128, 1024), idO, (j > 0 || kk > 0));
+        mma_commit(&B.v_empty[st]);
+        mma_commit(&B.pv_done[j % NS]);
+        if (j == nblk - 1) mma_commit(&B.o_final);
       }
-      if (j >= 1) {
-        const int jp = j - 1, st = jp % ST, w = jp & 1;
-        mbar_wait(&B.p_full[w], (jp >> 1) & 1);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t aV = smem_u32(sV + st * SL::kTile);
-#pragma unroll
-          for (int kk = 0; kk < BKV / 16; ++kk)
-            mma_ts(tO0 + w * 128, tS0 + w * 128 + kk * 8,
-                   sdesc_sw128(aV + kk * 2048, 128 * 128, 1024), idO, (jp >= 2 || kk > 0));
-          mma_commit(&B.kv_empty[st]);
-          if (jp == nblk - 1) mma_commit(&B.o_final);
-        }
-        __syncwarp();
-      }
+      __syncwarp();
+      if (j + NS < nblk) issue_s(j + NS);
     }
   } else {
-    // ------------------------------------------------------------ softmax WGs
-    // WG w takes blocks j = w, w+2, ... with its own (m, l) and O_w accumulator.
-    // When it sees S_j, PV_{j-2} (the last writer of O_w) has completed: the
-    // MMA issued S_j after PV_{j-2}, and S_j's commit covers all prior MMAs.
-    const int wg = warp >> 2, wq = warp & 3;
+    // ------------------------------------------------------------ softmax warps
+    // warp w: TMEM lanes 32 (w % 4).. (query rows), key columns [32 (w / 4), +32)
+    const int cq = warp >> 2, wq = warp & 3;
     const int row = wq * 32 + lane;
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    const uint32_t tS = tS0 + wg * 128 + lane_off;
-    const uint32_t tO = tO0 + wg * 128 + lane_off;
+    constexpr int kOc = D / kFwdSoftWGs;              // O columns per warp (rescale, store)
     float m_run = -INFINITY, l_run = 0.f;
-    for (int j = wg; j < nblk; j += 2) {
+    for (int j = 0; j < nblk; ++j) {
       const int kv = min(BKV, kh - j * BKV);
-      mbar_wait(&B.s_full[wg], (j >> 1) & 1);
+      const uint32_t tS = tS0 + (j % NS) * 128 + lane_off;
+      mbar_wait(&B.s_full[j % NS], (j / NS) & 1);
       tc_fence_after();
+      if (warp == 0 && lane == 0) FPROF(j, 2);
+      // the 32 raw scores stay in registers across the max exchange, so the in-place
+      // P writes below cannot race with another warp's reads
+      uint32_t r[32];
+      tmem_ld32(tS + cq * 32, r);
+      tmem_ld_wait();
+      if (warp == 0 && lane == 0) FPROF(j, 7);
       float mx = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < BKV / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tS + c * 32, r);
-        tmem_ld_wait();
-        if (kv == BKV) {
+      if (kv == BKV) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));
-        } else {
+        for (int i = 0; i < 32; i += 2) mx = fmax3f(mx, __uint_as_float(r[i]), __uint_as_float(r[i + 1]));
+      } else {
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (c * 32 + i < kv) mx = fmaxf(mx, __uint_as_float(r[i]));
-        }
+        for (int i = 0; i < 32; ++i)
+          if (cq * 32 + i < kv) mx = fmaxf(mx, __uint_as_float(r[i]));
       }
-      mx *= scale_log2;
-      if (j == wg) {
+      // row max over the four column slices, through a parity double buffer
+      float* xch = sMax + (j & 1) * (kFwdSoftWGs * 128);
+      xch[cq * 128 + row] = mx;
+      if (warp == 0 && lane == 0) FPROF(j, 8);
+      named_bar_sync(1, kFwdSoftThreads);
+      mx = fmax3f(fmaxf(xch[row], xch[128 + row]), xch[256 + row], xch[384 + row]) * scale_log2;
+      if (warp == 0 && lane == 0) FPROF(j, 3);
+      if (j == 0) {
         m_run = mx;
       } else if (mx > m_run + 8.f) {
+        // rescale O (this warp's D/4 columns) once PV_{j-1} has landed
+        mbar_wait(&B.pv_done[(j - 1) % NS], ((j - 1) / NS) & 1);
+        tc_fence_after();
         const float alpha = fast_exp2(m_run - mx);
         l_run *= alpha;
 #pragma unroll 1
-        for (int c = 0; c < D / 16; ++c) {
-          uint32_t r[16];
-          tmem_ld16(tO + c * 16, r);
+        for (int c = cq * kOc; c < (cq + 1) * kOc; c += 16) {
+          uint32_t o[16];
+          tmem_ld16(tO + lane_off + c, o);
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-          tmem_st16(tO + c * 16, r);
+          for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st16(tO + lane_off + c, o);
         }
-        tmem_st_wait();
         m_run = mx;
       }
-      l_run += (kv == BKV) ? softmax_p_pass<false>(tS, scale_log2, m_run, kv)
-                           : softmax_p_pass<true>(tS, scale_log2, m_run, kv);
+      // P = 2^(s scale_log2 - m) for keys [32 cq, +32): bf16 into columns [16 cq, +16)
+      const f32x2 sc2 = f2(scale_log2, scale_log2), nm2 = f2(-m_run, -m_run);
+      f32x2 lsum2 = f2(0.f, 0.f);
+      if (kv == BKV) softmax_p_chunk<false>(r, tS + cq * 16, sc2, nm2, cq, kv, lsum2);
+      else softmax_p_chunk<true>(r, tS + cq * 16, sc2, nm2, cq, kv, lsum2);
+      const float2 ls = f2u(lsum2);
+      l_run += ls.x + ls.y;
+      if (warp == 0 && lane == 0) FPROF(j, 9);
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&B.p_full[wg]);
+      mbar_arrive(&B.p_full[j % NS]);
+      if (warp == 0 && lane == 0) FPROF(j, 4);
     }
-    // ---------------- epilogue: merge the two WGs' partial softmax states
+    // ---------------- epilogue: combine the slices' row sums, normalise, store
     mbar_wait(&B.o_final, 0);
     tc_fence_after();
-    sML[(wg * 2 + 0) * 128 + row] = m_run;
-    sML[(wg * 2 + 1) * 128 + row] = l_run;
-    named_bar_sync(1, 256);
-    const float m0 = sML[0 * 128 + row], l0 = sML[1 * 128 + row];
-    const float m1 = sML[2 * 128 + row], l1 = sML[3 * 128 + row];
-    const float m = fmaxf(m0, m1);
-    const float a0 = l0 > 0.f ? fast_exp2(m0 - m) : 0.f;
-    const float a1 = l1 > 0.f ? fast_exp2(m1 - m) : 0.f;
-    const float denom = l0 * a0 + l1 * a1;
-    const float inv = 1.f / denom;
-    const float c0 = a0 * inv, c1 = a1 * inv;
+    float* lx = sMax + (nblk & 1) * (kFwdSoftWGs * 128);   // the buffer block nblk-2 used
+    named_bar_sync(1, kFwdSoftThreads);
+    lx[cq * 128 + row] = l_run;
+    named_bar_sync(1, kFwdSoftThreads);
+    const float denom = (lx[row] + lx[128 + row]) + (lx[256 + row] + lx[384 + row]);
+    const float inv = denom > 0.f ? 1.f / denom : 0.f;
     const int gsz = grp_size[g];
     const int tok = mrow[row];
     __nv_bfloat16* orow = O + ((long long)h * Lq + tok) * D;
-    constexpr int kChunks = D / 32;
 #pragma unroll 1
-    for (int c = wg * (kChunks / 2); c < (wg + 1) * (kChunks / 2); ++c) {
-      uint32_t r0[32], r1[32];
-      tmem_ld32(tO0 + lane_off + c * 32, r0);
-      tmem_ld32(tO0 + 128 + lane_off + c * 32, r1);
+    for (int c = cq * kOc; c < (cq + 1) * kOc; c += 16) {
+      uint32_t o[16];
+      tmem_ld16(tO + lane_off + c, o);
       tmem_ld_wait();
       if (row < gsz) {
-        float o[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          o[i] = (a0 > 0.f ? __uint_as_float(r0[i]) * c0 : 0.f) +
-                 (a1 > 0.f ? __uint_as_float(r1[i]) * c1 : 0.f);
-#pragma unroll
-        for (int i = 0; i < 32; i += 8)
-          *reinterpret_cast<uint4*>(orow + c * 32 + i) =
-              make_uint4(pack_bf16(o[i], o[i + 1]), pack_bf16(o[i + 2], o[i + 3]),
-                         pack_bf16(o[i + 4], o[i + 5]), pack_bf16(o[i + 6], o[i + 7]));
+        for (int i = 0; i < 16; i += 8)
+          *reinterpret_cast<uint4*>(orow + c + i) =
+              make_uint4(pack_bf16(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv),
+                         pack_bf16(__uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv),
+                         pack_bf16(__uint_as_float(o[i + 4]) * inv, __uint_as_float(o[i + 5]) * inv),
+                         pack_bf16(__uint_as_float(o[i + 6]) * inv, __uint_as_float(o[i + 7]) * inv));
       }
     }
-    if (wg == 0 && row < gsz) lse[(long long)h * Lq + tok] = m + __log2f(denom);
+    if (cq == 0 && row < gsz) lse[(long long)h * Lq + tok] = m_run + __log2f(denom);
   }
   tc_fence_before();
   __syncthreads();
@@ -359,15 +474,6 @@ constexpr int kBwdScatWarps = DSV_BWD_SCAT_WARPS;
 constexpr int kBwdScatThreads = kBwdScatWarps * 32;
 constexpr int kBwdThreads = (kBwdScatWarp0 + kBwdScatWarps) * 32;   // 864 by default
 
-// Optional in-kernel timeline (variant builds with -DDSV_BWD_PROF): clock64 stamps of
-// each role's phase boundaries for the first kProfCtas CTAs, read by dsv_debug_timeline.
-constexpr int kProfCtas = 8, kProfBlocks = 32, kProfEv = 12;
-__device__ long long g_bwd_prof[kProfCtas][kProfBlocks][kProfEv];
-#ifdef DSV_BWD_PROF
-#define PROF(j, e) do { if (blockIdx.x < kProfCtas && (j) < kProfBlocks) g_bwd_prof[blockIdx.x][j][e] = clock64(); } while (0)
-#else
-#define PROF(j, e) do {} while (0)
-#endif
 #ifndef DSV_BWD_SCATTER
 #define DSV_BWD_SCATTER 0   // 1: ablation build only (no global adds)
 #endif

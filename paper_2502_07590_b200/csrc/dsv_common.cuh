@@ -49,6 +49,59 @@ DSV_DEV void bulk_reduce_add_f32(float* gdst, const void* ssrc, uint32_t bytes) 
 DSV_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 DSV_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 DSV_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// ---- packed fp32x2 arithmetic (FFMA2 / FADD2 / FMUL2 on sm_100) and 3-input max
+typedef unsigned long long f32x2;
+DSV_DEV f32x2 f2(float lo, float hi) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+DSV_DEV float2 f2u(f32x2 v) {
+  float2 r;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+DSV_DEV f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+DSV_DEV f32x2 fadd2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+DSV_DEV f32x2 fmul2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+DSV_DEV float fmax3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+// 2^x on the FMA/ALU pipes for a pair (x <= 0 in the softmax): round-to-nearest split
+// through the 1.5*2^23 magic add (no FRND/F2I, which share the quarter-rate unit with
+// MUFU), degree-3 minimax for 2^f on [-1/2, 1/2] (max rel. error 7.5e-5, far below
+// bf16's 3.9e-3), exponent added as integer bits. Offloads part of the exponentials
+// from the 16/clk/SM MUFU unit.
+DSV_DEV f32x2 exp2_poly2(f32x2 x) {
+  float2 v = f2u(x);
+  v.x = fmaxf(v.x, -125.f);
+  v.y = fmaxf(v.y, -125.f);
+  const f32x2 magic = f2(12582912.f, 12582912.f);
+  const f32x2 xc = f2(v.x, v.y);
+  const f32x2 t = fadd2(xc, magic);
+  const f32x2 jf = fadd2(t, f2(-12582912.f, -12582912.f));
+  const f32x2 fr = ffma2(jf, f2(-1.f, -1.f), xc);
+  f32x2 p = ffma2(fr, f2(0.05517044f, 0.05517044f), f2(0.2426081f, 0.2426081f));
+  p = ffma2(fr, p, f2(0.69326096f, 0.69326096f));
+  p = ffma2(fr, p, f2(0.99992834f, 0.99992834f));
+  const float2 q = f2u(p), tt = f2u(t);
+  return f2(__int_as_float(__float_as_int(q.x) + (__float_as_int(tt.x) << 23)),
+            __int_as_float(__float_as_int(q.y) + (__float_as_int(tt.y) << 23)));
+}
 DSV_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
 }

@@ -110,7 +110,7 @@ int main() {
         cudaEventRecord(b); cudaEventSynchronize(b);
         float ms; cudaEventElapsedTime(&ms, a, b);
         if (it == 2) printf("grid %3d %-22s: %.3f ms  %7.1f GB/s  per-block %.0f ns  err=%s\n", grid, names[v], ms,
-                            (v>=4? (v==4?2:4):1) * bytes / ms / 1e6, ms * 1e6 / NT / grid_mult, cudaGetErrorString(cudaGetLastError()));
+                            (v == 4 ? 2 : (v == 5 || v == 6) ? 4 : 1) * bytes / ms / 1e6, ms * 1e6 / NT / grid_mult, cudaGetErrorString(cudaGetLastError()));
       }
     }
   }
