@@ -23,7 +23,7 @@ int dsv_rows_fwd_launch(const void*, const void*, const void*, const long long*,
 int dsv_rows_bwd_launch(const void*, const void*, const void*, const float*, const float*,
                         const void*, const long long*, const int*, int, int, int, int, float, int,
                         float*, float*, float*, cudaStream_t);
-int dsv_gemm_launch(const CUtensorMap*, const CUtensorMap*, void*, int, int, int, long long,
+int dsv_gemm_launch(const CUtensorMap*, const CUtensorMap*, const CUtensorMap*, void*, int, int, int, long long,
                     long long, int, int, int, cudaStream_t);
 int dsv_attn_fwd_tc_launch(const void*, const void*, const void*, const int*, const int*,
                            const int*, long long, const int*, const int*, int, int, int, int, int,
@@ -75,7 +75,8 @@ EncodeTiledFn encode_fn() {
 // bf16 tensor map with up to 3 dims: dims[0] innermost (elements), strides in bytes for
 // dims 1..rank-1, 128B swizzle.
 bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
-              const uint64_t* strides_bytes, const uint32_t* box) {
+              const uint64_t* strides_bytes, const uint32_t* box,
+              CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t gd[5];
@@ -83,7 +84,7 @@ bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
   cuuint32_t bx[5], es[5];
   for (int i = 0; i < rank; ++i) { gd[i] = dims[i]; bx[i] = box[i]; es[i] = 1; }
   for (int i = 0; i + 1 < rank; ++i) gs[i] = strides_bytes[i];
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), gd, gs, bx,
+  CUresult r = fn(m, dt, rank, const_cast<void*>(base), gd, gs, bx,
                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -129,7 +130,18 @@ int dsv_gemm_bf16(const void* A, long long lda, long long a_bs, const void* B, l
     const uint32_t box[3] = {64, (uint32_t)bn, 1};
     if (!make_map(&tb, B, 3, dims, st, box)) return fail(DSV_EINVAL, "gemm: tensor map B");
   }
-  return cuda_status(dsv_gemm_launch(&ta, &tb, C, M, N, K, ldc, c_bs, nbatch,
+  // fp32 output of a one-k-block GEMM (the proxy scores): TMA tensor stores of
+  // 32-column swizzled slices instead of row-per-thread stores
+  CUtensorMap tc;
+  const CUtensorMap* tcp = nullptr;
+  if (c_dtype == DSV_DTYPE_F32 && K <= 64 && al16(C) && (ldc * 4) % 16 == 0 &&
+      (nbatch == 1 || (c_bs * 4) % 16 == 0)) {
+    const uint64_t dims[3] = {(uint64_t)N, (uint64_t)M, (uint64_t)nbatch};
+    const uint64_t st[2] = {(uint64_t)ldc * 4, (uint64_t)(nbatch > 1 ? c_bs : (long long)M * ldc) * 4};
+    const uint32_t box[3] = {32, 128, 1};
+    if (make_map(&tc, C, 3, dims, st, box, CU_TENSOR_MAP_DATA_TYPE_FLOAT32)) tcp = &tc;
+  }
+  return cuda_status(dsv_gemm_launch(&ta, &tb, tcp, C, M, N, K, ldc, c_bs, nbatch,
                                      c_dtype == DSV_DTYPE_F32, bn, S(stream)),
                      "gemm launch");
 }

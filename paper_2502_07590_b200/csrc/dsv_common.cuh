@@ -47,6 +47,7 @@ DSV_DEV void bulk_reduce_add_f32(float* gdst, const void* ssrc, uint32_t bytes) 
                :: "l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes) : "memory");
 }
 DSV_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+DSV_DEV void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 DSV_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 DSV_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 // ---- packed fp32x2 arithmetic (FFMA2 / FADD2 / FMUL2 on sm_100) and 3-input max
@@ -147,6 +148,11 @@ DSV_DEV void tma_load_2d(void* dst, const void* tmap, uint64_t* bar, int c0, int
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4}], [%2];"
       :: "r"(smem_u32(dst)), "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1) : "memory");
+}
+// TMA tensor store from shared memory (bulk-group completion).
+DSV_DEV void tma_store_3d(const void* tmap, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
+               :: "l"(tmap), "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2) : "memory");
 }
 DSV_DEV void tma_load_3d(void* dst, const void* tmap, uint64_t* bar, int c0, int c1, int c2) {
   asm volatile(

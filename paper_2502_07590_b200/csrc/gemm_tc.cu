@@ -22,22 +22,25 @@ namespace gemm {
 
 constexpr int BM = 128, BK = 64;
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool kTmaStore = false>
 struct SmemLayout {
   static constexpr int kA = BM * BK * 2;
   static constexpr int kB = BN * BK * 2;
   static constexpr int kStage = kA + kB;
-  static constexpr int kBytes = STAGES * kStage + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kOut = kTmaStore ? 2 * BM * 32 * 4 : 0;   // two 128 x 32 fp32 slices
+  static constexpr int kBytes = STAGES * kStage + kOut + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-template <int BN, int STAGES, bool kF32Out>
+template <int BN, int STAGES, bool kF32Out, bool kTmaStore = false>
 __global__ void __launch_bounds__(128)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+            const __grid_constant__ CUtensorMap tmC,
             void* __restrict__ C, int M, int N, int K, long long ldc, long long c_bs) {
-  using SL = SmemLayout<BN, STAGES>;
+  using SL = SmemLayout<BN, STAGES, kTmaStore>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SL::kStage);
+  uint8_t* sOut = smem + STAGES * SL::kStage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SL::kStage + SL::kOut);
   uint64_t* empty = full + STAGES;
   uint64_t* accum = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
@@ -104,6 +107,37 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   tc_fence_after();
   const int row = m0 + warp * 32 + lane;
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  if constexpr (kTmaStore) {
+    // 32-column slices: TMEM -> 128B-swizzled smem (conflict-free 16-byte stores) ->
+    // one TMA tensor store per slice, two slices in flight; TMA clips the edges.
+    const int r = warp * 32 + lane;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld32(trow + c * 32, v);
+      tmem_ld_wait();
+      uint8_t* buf = sOut + (c & 1) * (BM * 32 * 4);
+      if (c >= 2) {
+        if (threadIdx.x == 0) bulk_wait_read1();
+        __syncthreads();
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<uint4*>(buf + r * 128 + ((q ^ (r & 7)) << 4)) =
+            make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        tma_store_3d(&tmC, buf, n0 + c * 32, m0, b);
+        bulk_commit();
+      }
+    }
+    if (threadIdx.x == 0) bulk_wait_all();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, kTmemCols);
+    return;
+  }
   const bool vec_ok = kF32Out ? ((ldc & 3) == 0) : ((ldc & 7) == 0);
 #pragma unroll 1
   for (int c = 0; c < BN; c += 32) {
@@ -149,29 +183,31 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 }  // namespace gemm
 }  // namespace dsv
 
-template <int BN, int STAGES, bool F32>
-static int launch_gemm(const CUtensorMap* ta, const CUtensorMap* tb, void* C, int M, int N, int K,
-                       long long ldc, long long c_bs, int nbatch, cudaStream_t st) {
+template <int BN, int STAGES, bool F32, bool TMA_ST = false>
+static int launch_gemm(const CUtensorMap* ta, const CUtensorMap* tb, const CUtensorMap* tc, void* C,
+                       int M, int N, int K, long long ldc, long long c_bs, int nbatch,
+                       cudaStream_t st) {
   using namespace dsv::gemm;
-  const int smem = SmemLayout<BN, STAGES>::kBytes;
-  auto kern = gemm_kernel<BN, STAGES, F32>;
+  const int smem = SmemLayout<BN, STAGES, TMA_ST>::kBytes;
+  auto kern = gemm_kernel<BN, STAGES, F32, TMA_ST>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, nbatch);
-  kern<<<grid, 128, smem, st>>>(*ta, *tb, C, M, N, K, ldc, c_bs);
+  kern<<<grid, 128, smem, st>>>(*ta, *tb, tc ? *tc : *ta, C, M, N, K, ldc, c_bs);
   return (int)cudaGetLastError();
 }
 
-int dsv_gemm_launch(const CUtensorMap* ta, const CUtensorMap* tb, void* C, int M, int N, int K,
-                    long long ldc, long long c_bs, int nbatch, int f32_out, int bn,
-                    cudaStream_t st) {
+int dsv_gemm_launch(const CUtensorMap* ta, const CUtensorMap* tb, const CUtensorMap* tc, void* C,
+                    int M, int N, int K, long long ldc, long long c_bs, int nbatch, int f32_out,
+                    int bn, cudaStream_t st) {
   if (K <= dsv::gemm::BK) {   // one k-block (proxy scores, K = r): small CTAs, several per SM
-    return f32_out ? launch_gemm<128, 1, true>(ta, tb, C, M, N, K, ldc, c_bs, nbatch, st)
-                   : launch_gemm<128, 1, false>(ta, tb, C, M, N, K, ldc, c_bs, nbatch, st);
+    if (f32_out && tc) return launch_gemm<128, 1, true, true>(ta, tb, tc, C, M, N, K, ldc, c_bs, nbatch, st);
+    return f32_out ? launch_gemm<128, 1, true>(ta, tb, nullptr, C, M, N, K, ldc, c_bs, nbatch, st)
+                   : launch_gemm<128, 1, false>(ta, tb, nullptr, C, M, N, K, ldc, c_bs, nbatch, st);
   }
   if (bn == 256) {
-    return f32_out ? launch_gemm<256, 4, true>(ta, tb, C, M, N, K, ldc, c_bs, nbatch, st)
-                   : launch_gemm<256, 4, false>(ta, tb, C, M, N, K, ldc, c_bs, nbatch, st);
+    return f32_out ? launch_gemm<256, 4, true>(ta, tb, nullptr, C, M, N, K, ldc, c_bs, nbatch, st)
+                   : launch_gemm<256, 4, false>(ta, tb, nullptr, C, M, N, K, ldc, c_bs, nbatch, st);
   }
-  return f32_out ? launch_gemm<128, 4, true>(ta, tb, C, M, N, K, ldc, c_bs, nbatch, st)
-                 : launch_gemm<128, 4, false>(ta, tb, C, M, N, K, ldc, c_bs, nbatch, st);
+  return f32_out ? launch_gemm<128, 4, true>(ta, tb, nullptr, C, M, N, K, ldc, c_bs, nbatch, st)
+                 : launch_gemm<128, 4, false>(ta, tb, nullptr, C, M, N, K, ldc, c_bs, nbatch, st);
 }
