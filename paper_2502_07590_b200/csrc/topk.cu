@@ -8,30 +8,31 @@
 //   * the threshold is the k-th largest score (= min of the kept scores);
 //   * -0.0 compares equal to +0.0 (numpy semantics).
 //
-// B200 design: the row is streamed from HBM exactly once, by small CTAs (256
-// threads, several per SM, persistent over rows) so that one CTA's barriers and
-// scans overlap other CTAs' streaming:
-//   1. a 2048-entry strided sample gives a value band [lo, hi] expected to hold
-//      the k-th value T (value-linear 1024-bucket histogram, +- 4 sigma of the
-//      binomial sample count);
-//   2. one vectorised pass (float4 loads, evict-first): entries > hi set their bit
-//      in a shared-memory keep-mask (plain bit order, built from per-lane nibbles
-//      with three shuffles per 128 columns), entries in the band are appended
-//      (order key, column) to a candidate list;
-//   3. if #above < k <= #above + #candidates, T is found exactly by an 8-bit radix
-//      select over the candidate keys, candidates > T join the mask, and the first
-//      ties in column order fill the remaining budget;
-//   4. the mask is emitted in ascending column order by a block scan of popcounts.
-// Rows where the band misses (massive ties, non-finite samples, candidate overflow)
-// take a whole-row radix select and an ordered two-pass compaction (same output).
-// HBM traffic per row: one read of the row + k * 4 bytes of indices.
+// B200 design: persistent CTAs (1024 threads, one row at a time, grid = #SMs).
+// A row is brought into shared memory with one cp.async.bulk copy (the next
+// row of the CTA is prefetched into L2 while the current one is processed).
+// Three passes over the row in shared memory:
+//   1. histogram: 2048 buckets linear in the score value over a range taken
+//      from a strided sample (bucket = clamp(int(fma(v, a, b)))): monotone in
+//      v, so the bucket b* holding the k-th value T follows from a suffix scan;
+//      bell-shaped rows spread over many buckets, so smem atomics rarely collide;
+//   2. per contiguous warp segment: count the entries in buckets > b* (all kept)
+//      and compact the bucket-b* entries (value, index) into a candidate list;
+//      T is then found exactly among the candidates by key-space bucket
+//      refinement (<= 3 levels for 32-bit order keys), and the candidates give
+//      each warp segment its (> T, == T) counts;
+//   3. ordered compaction with warp ballots: keep v > T, and v == T while the
+//      tie budget k - #(> T) lasts in index order (twopass_select's emit) —
+//      ascending output, no sort. Float compares give -0.0 == +0.0.
+// Rows whose T-bucket is too large (massive ties, non-finite ranges) fall back
+// to key-space refinement over the whole row and a counting pass.
+// HBM traffic per row = one read of the row + k*4 bytes of indices.
 
 #include "dsv_common.cuh"
 
 // Optional phase profiling (tools/topk_phase.cu): cycles per phase, CTA 0 thread 0.
 #ifdef DSV_TOPK_PROF
 __device__ unsigned long long g_topk_prof[16];
-__device__ unsigned int g_topk_slow;
 #define TOPK_MARK(n) do { if (threadIdx.x == 0 && blockIdx.x == 0) { const long long _t = clock64(); \
     g_topk_prof[n] += _t - _prof_t; _prof_t = _t; } } while (0)
 #else
@@ -41,13 +42,12 @@ __device__ unsigned int g_topk_slow;
 namespace dsv {
 namespace topk {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 1024;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMinBlocks = 4;                 // CTAs per SM the kernel is built for
-constexpr int kBuckets = 1024;                // sample histogram
-constexpr int kSample = 2048;
+constexpr int kBuckets = 2048;
 constexpr int kCandCap = 4096;
-constexpr int kCandW = kCandCap / kWarps;     // per-warp candidate region
+constexpr int kSample = 8192;
+constexpr int kCandW = kCandCap / kWarps;   // per-warp candidate staging (pass 1)
 
 DSV_DEV uint32_t f2key(float f) {
   uint32_t u = __float_as_uint(f);
@@ -61,124 +61,132 @@ DSV_DEV float key2f(uint32_t k) {
 
 struct alignas(16) Smem {
   uint32_t hist[kBuckets];
-  uint32_t cand[kCandCap];        // candidate order keys
-  uint32_t cidx[kCandCap];        // candidate columns
-  uint32_t wsum[kWarps];
-  uint32_t wcnt[kWarps];          // candidates per warp region
-  uint32_t ncand, nabove;
-  uint32_t b_hi, b_lo;
-  uint32_t prefix, need, neq;     // radix-select state
+  uint32_t cand[kCandCap];       // candidate order keys
+  uint32_t cidx[kCandCap];       // candidate column ids
+  uint32_t wa[kWarps], wb[kWarps], wc[kWarps], wd[kWarps];
+  uint32_t s_lo, s_hi, s_need, s_ncand, s_mode, s_gt_total, s_cmin, s_cmax, s_kband;
+  float s_vmin, s_vmax;
+  uint64_t bar;
 };
 
+template <bool kSmem>
+struct Src {
+  const float* vals;   // smem row (kSmem) or global row
+  DSV_DEV float val(int i) const {
+    if constexpr (kSmem) return vals[i];
+    else return __ldg(vals + i);
+  }
+  DSV_DEV uint32_t key(int i) const { return f2key(val(i)); }
+};
+
+DSV_DEV uint32_t warp_min(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+DSV_DEV uint32_t warp_max(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
 // Value-space bucket: correctly rounded fma and saturating conversion keep it
-// monotone non-decreasing in v.
+// monotone non-decreasing in v (also for +-inf outside the sampled range).
 DSV_DEV int vbucket(float v, float a, float b) {
   return min(max(__float2int_rz(__fmaf_rn(v, a, b)), 0), kBuckets - 1);
 }
 
-// Block-wide exclusive scan of one value per thread; returns the exclusive prefix
-// and the total through *total.
-DSV_DEV uint32_t block_excl_scan(Smem& S, uint32_t v, uint32_t* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t inc = v;
+// Keep-mask addressing: plain (bit i&31 of word i>>5) or the pass-1 vec4 layout
+// (chunk of 128 columns = 4 words; column 128c + 4l + j -> word 4c + j, bit l).
+DSV_DEV uint32_t mword(uint32_t i, bool vec4) {
+  return vec4 ? ((i >> 7) << 2) + (i & 3) : (i >> 5);
+}
+DSV_DEV uint32_t mbit(uint32_t i, bool vec4) {
+  return vec4 ? 1u << ((i & 127) >> 2) : 1u << (i & 31);
+}
+
+// Locate bucket b* with sum_{b>b*} hist < need <= sum_{b>=b*} hist. Each thread owns
+// buckets 2t, 2t+1. Returns through smem: wa[0] = b*, wb[0] = count above, wc[0]=count at.
+DSV_DEV void find_bucket(Smem& S, uint32_t need, int tid, int lane, int warp) {
+  const uint32_t h0 = S.hist[2 * tid], h1 = S.hist[2 * tid + 1];
+  const uint32_t tot = h0 + h1;
+  uint32_t v = tot;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += x;
+    const uint32_t t = __shfl_down_sync(0xffffffffu, v, o);
+    if (lane + o < 32) v += t;
   }
+  if (lane == 0) S.wc[warp] = v;       // warp totals
   __syncthreads();
-  if (lane == 31) S.wsum[warp] = inc;
-  __syncthreads();
-  uint32_t base = 0, tot = 0;
+  // exclusive suffix over warps: sum of totals of warps > warp
+  uint32_t wt = S.wc[lane];
+  uint32_t suf = wt;
 #pragma unroll
-  for (int w = 0; w < kWarps; ++w) {
-    const uint32_t s = S.wsum[w];
-    base += w < warp ? s : 0u;
-    tot += s;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_down_sync(0xffffffffu, suf, o);
+    if (lane + o < 32) suf += t;
   }
-  *total = tot;
-  return base + inc - v;
+  const uint32_t after = __shfl_sync(0xffffffffu, suf - wt, warp);
+  const uint32_t incl = v + after;     // sum of buckets >= 2 tid
+  const uint32_t excl = incl - tot;    // sum of buckets > 2 tid + 1
+  __syncthreads();
+  if (excl < need && need <= excl + h1) { S.wa[0] = 2 * tid + 1; S.wb[0] = excl; S.wc[0] = h1; }
+  else if (excl + h1 < need && need <= incl) { S.wa[0] = 2 * tid; S.wb[0] = excl + h1; S.wc[0] = h0; }
+  __syncthreads();
 }
 
-// Key-space bucketing of [lo, lo + span): bucket(x) = ((x - lo) * M) >> 32 with
-// M = floor(nb 2^32 / span) — monotone, < nb, exact (one key per bucket) when
-// span <= nb, and a multiply instead of a 64-bit division per key.
-struct KMap {
-  uint32_t lo;
-  uint64_t m;
-  DSV_DEV uint32_t bucket(uint32_t key) const { return (uint32_t)(((uint64_t)(key - lo) * m) >> 32); }
-  // offset (from lo) of the first key that maps to bucket b: ceil(b 2^32 / m)
-  DSV_DEV uint64_t first(uint64_t b) const { return ((b << 32) + m - 1) / m; }
-};
-DSV_DEV uint32_t nbuckets(uint64_t span) {
-  return span < (uint64_t)kBuckets ? (uint32_t)span : (uint32_t)kBuckets;
-}
-DSV_DEV KMap kmap(uint32_t lo, uint32_t hi) {
-  const uint64_t span = (uint64_t)(hi - lo) + 1ull;
-  return KMap{lo, ((uint64_t)nbuckets(span) << 32) / span};
-}
-
-// Exact selection in key space: the need-th largest key among the keys fed by
-// `feed` (called with a per-key visitor), all of which lie in [lo, hi]. Each level
-// histograms [lo, hi] linearly into <= kBuckets buckets (keys of a narrow value
-// band spread evenly, so the shared-memory atomics rarely collide) and keeps the
-// bucket holding the need-th key; a level whose buckets are single keys ends it.
-// With `prefilled`, S.hist already holds the first level's histogram. Leaves
-// S.prefix = T, S.need = how many keys equal to T are kept, S.neq = how many keys
-// equal T in total.
-template <typename Feed>
-DSV_DEV void key_select(Smem& S, uint32_t need, uint32_t lo, uint32_t hi, bool prefilled, Feed feed) {
-  const int tid = threadIdx.x;
-#pragma unroll 1
-  for (int level = 0; level < 8; ++level) {
-    const KMap km = kmap(lo, hi);
-    if (level > 0 || !prefilled) {
-      for (int b = tid; b < kBuckets; b += kThreads) S.hist[b] = 0;
-      __syncthreads();
-      feed([&](uint32_t key) {
-        if (key >= lo && key <= hi) atomicAdd(&S.hist[km.bucket(key)], 1u);
-      });
-      __syncthreads();
-    }
-    // C(b) = keys in buckets >= b; thread owns buckets 4 tid .. 4 tid + 3
-    uint32_t h[4], own = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) { h[i] = S.hist[4 * tid + i]; own += h[i]; }
-    uint32_t total;
-    const uint32_t before = block_excl_scan(S, own, &total);
-    uint32_t c = total - before;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t cn = c - h[i];
-      if (cn < need && need <= c) {
-        const uint64_t bb = 4 * tid + i;
-        S.prefix = lo + (uint32_t)km.first(bb);                                // new lo
-        S.b_hi = lo + (uint32_t)min((unsigned long long)(km.first(bb + 1) - 1ull), (unsigned long long)(hi - lo));   // new hi
-        S.need = need - cn;
-        S.neq = h[i];
-      }
-      c = cn;
+// Key-space refinement: [s_lo, s_hi] holds T, s_need-th largest inside; source is
+// the candidate buffer (s_mode == 1) or the whole row.
+template <bool kSmem>
+DSV_DEV void refine(Smem& S, const Src<kSmem>& src, int L, int tid, int lane, int warp) {
+  for (int level = 0; level < 40; ++level) {
+    const uint32_t lo = S.s_lo, hi = S.s_hi, need = S.s_need, mode = S.s_mode;
+    if (lo == hi) return;
+    const uint64_t span = (uint64_t)(hi - lo) + 1ull;
+    const uint32_t nb = span < (uint64_t)kBuckets ? (uint32_t)span : (uint32_t)kBuckets;
+    for (int b = tid; b < kBuckets; b += kThreads) S.hist[b] = 0;
+    __syncthreads();
+    const int n = mode ? (int)S.s_ncand : L;
+    for (int i = tid; i < n; i += kThreads) {
+      const uint32_t key = mode ? S.cand[i] : src.key(i);
+      if (key >= lo && key <= hi)
+        atomicAdd(&S.hist[(uint32_t)(((uint64_t)(key - lo) * nb) / span)], 1u);
     }
     __syncthreads();
-    lo = S.prefix;
-    hi = S.b_hi;
-    need = S.need;
-    if (lo == hi) return;          // single key: S.prefix = T, S.neq = its count
+    find_bucket(S, need, tid, lane, warp);
+    const uint64_t b = S.wa[0];
+    const uint32_t nlo = lo + (uint32_t)((b * span + nb - 1) / nb);
+    const uint32_t nhi = lo + (uint32_t)(((b + 1) * span + nb - 1) / nb) - 1u;
+    const uint32_t above = S.wb[0];
+    __syncthreads();
+    if (tid == 0) { S.s_lo = nlo; S.s_hi = nhi; S.s_need = need - above; }
+    __syncthreads();
   }
 }
 
-template <bool kVec>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
+template <bool kSmem>
+__global__ void __launch_bounds__(kThreads, 1)
 topk_rows_kernel(const float* __restrict__ scores, long long ld, int rows, int L,
                  const int* __restrict__ k_per_head, int rows_per_head,
                  int* __restrict__ out_idx, long long out_ld, float* __restrict__ out_thr) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
-  uint32_t* mask = reinterpret_cast<uint32_t*>(smem_raw + sizeof(Smem));
+  float* buf = reinterpret_cast<float*>(smem_raw + sizeof(Smem));
+  const int nw = (L + 31) >> 5;                        // 32-column mask words
+  uint32_t* mask = reinterpret_cast<uint32_t*>(smem_raw + sizeof(Smem) + (kSmem ? (size_t)L * 4 : 0));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nw = (L + 31) >> 5;                  // 32-column mask words
-  const int n4 = kVec ? (L >> 2) : 0;            // full float4 chunks
+  const bool bulk = kSmem && (((ld * 4) & 15) == 0) &&
+                    ((reinterpret_cast<uintptr_t>(scores) & 15) == 0) && L >= 4;
+  const int n4 = L >> 2;
+  const int seg = (((L + kWarps - 1) / kWarps) + 31) & ~31;   // contiguous warp segments
+  const int s0 = warp * seg, s1 = min(L, s0 + seg);
   const uint32_t lt = (1u << lane) - 1u;
+  const int sstride = max(1, L / kSample) | 1;             // odd: conflict-free sample reads
+  const bool vec4 = false;   // plain keep-mask layout (see mword / mbit)
+  if (tid == 0) { mbar_init(&S.bar, 1); fence_barrier_init(); }
+  __syncthreads();
+  uint32_t phase = 0;
+  bool inflight = false;   // this row's bulk copy was issued during the previous row
 #ifdef DSV_TOPK_PROF
   long long _prof_t = clock64();
 #endif
@@ -186,294 +194,351 @@ topk_rows_kernel(const float* __restrict__ scores, long long ld, int rows, int L
   for (int row = blockIdx.x; row < rows; row += gridDim.x) {
     const int k = k_per_head[row / rows_per_head];
     const float* grow = scores + (long long)row * ld;
-    int* orow = out_idx + (long long)row * out_ld;
-    if (kVec && tid == 0 && row + (int)gridDim.x < rows)   // next row of this CTA into L2
-      prefetch_l2(scores + (long long)(row + gridDim.x) * ld, (uint32_t)(n4 * 16));
-    if (k >= L) {
-      // keep everything; threshold = row minimum
-      float mn = INFINITY;
-      for (int i = tid; i < L; i += kThreads) { orow[i] = i; mn = fminf(mn, __ldg(grow + i)); }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      if (lane == 0) S.wsum[warp] = __float_as_uint(mn);
-      __syncthreads();
-      if (tid == 0) {
-        float m = INFINITY;
-        for (int w = 0; w < kWarps; ++w) m = fminf(m, __uint_as_float(S.wsum[w]));
-        out_thr[row] = m == 0.f ? 0.f : m;
+    if (tid == 0 && row + 2 * (int)gridDim.x < rows && n4 > 0)
+      prefetch_l2(scores + (long long)(row + 2 * gridDim.x) * ld, (uint32_t)n4 * 16u);
+
+    // ---- stage the row (raw fp32) in shared memory
+    if constexpr (kSmem) {
+      if (bulk) {
+        if (tid == 0 && !inflight) {
+          fence_proxy_async_smem();   // previous row's generic reads before the async write
+          mbar_arrive_expect_tx(&S.bar, (uint32_t)n4 * 16u);
+          bulk_load(buf, grow, (uint32_t)n4 * 16u, &S.bar);
+        }
+        inflight = false;
+        for (int i = (n4 << 2) + tid; i < L; i += kThreads) buf[i] = __ldg(grow + i);
+        mbar_wait(&S.bar, phase);
+        phase ^= 1;
+      } else {
+        for (int i = tid; i < L; i += kThreads) buf[i] = __ldg(grow + i);
       }
       __syncthreads();
-      continue;
     }
-    if (k <= 0) {
-      if (tid == 0) out_thr[row] = INFINITY;
-      continue;
-    }
-
-    // ---- 1. strided sample: range, histogram, band [b_lo, b_hi]
-    float sv[kSample / kThreads];
-    float mn = INFINITY, mx = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < kSample / kThreads; ++j) {
-      const int i = (int)(((long long)(tid + j * kThreads) * L) / kSample);
-      sv[j] = __ldg(grow + min(i, L - 1));
-      mn = fminf(mn, sv[j]);
-      mx = fmaxf(mx, sv[j]);
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    }
-    for (int b = tid; b < kBuckets; b += kThreads) S.hist[b] = 0;
-    for (int w = tid; w < nw; w += kThreads) mask[w] = 0;
-    if (tid == 0) { S.ncand = 0; S.nabove = 0; }
-    __syncthreads();
-    if (lane == 0) S.wsum[warp] = __float_as_uint(mn);
-    __syncthreads();
-    float bmn = INFINITY;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) bmn = fminf(bmn, __uint_as_float(S.wsum[w]));
-    __syncthreads();
-    if (lane == 0) S.wsum[warp] = __float_as_uint(mx);
-    __syncthreads();
-    float bmx = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) bmx = fmaxf(bmx, __uint_as_float(S.wsum[w]));
-    bool fast = isfinite(bmn) && isfinite(bmx) && bmx > bmn;
+    Src<kSmem> src{kSmem ? buf : grow};
     TOPK_MARK(0);
-    float hi_v = INFINITY, lo_v = -INFINITY;
-    if (fast) {
-      const float ba = (float)kBuckets / (bmx - bmn), bb = -bmn * ba;
-#pragma unroll
-      for (int j = 0; j < kSample / kThreads; ++j) atomicAdd(&S.hist[vbucket(sv[j], ba, bb)], 1u);
-      __syncthreads();
-      // suffix counts C(b) = samples in buckets >= b; thread owns buckets 4t..4t+3
-      const float t = (float)k * (float)kSample / (float)L;
-      const float m = 4.f * sqrtf(fmaxf(t * (1.f - t / kSample), 1.f)) + 2.f;
-      const float tm = t - m, tp = t + m;
-      uint32_t h[4], own = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) { h[i] = S.hist[4 * tid + i]; own += h[i]; }
-      uint32_t total;
-      const uint32_t before = block_excl_scan(S, own, &total);   // buckets < 4 tid
-      // C(4t + i) = total - before - sum(h[0..i-1])
-      if (tid == 0) { S.b_hi = kBuckets - 1; S.b_lo = 0; }
-      __syncthreads();
-      float c = (float)(total - before);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float cn = c - (float)h[i];   // C(b + 1)
-        const uint32_t b = 4 * tid + i;
-        if (tm > 0.f && cn <= tm && c > tm) S.b_hi = b;
-        if (tp < (float)kSample && c >= tp && cn < tp) S.b_lo = b;
-        c = cn;
-      }
-      __syncthreads();
-      const int b_hi = (int)S.b_hi, b_lo = min((int)S.b_lo, b_hi);
-      hi_v = b_hi >= kBuckets - 1 ? INFINITY : bmn + (float)(b_hi + 1) / ba;
-      lo_v = b_lo <= 0 ? -INFINITY : bmn + (float)b_lo / ba;
-    }
-    __syncthreads();
-    for (int b = tid; b < kBuckets; b += kThreads) S.hist[b] = 0;   // first selection level
-    __syncthreads();
-    TOPK_MARK(1);
 
-    uint32_t T = 0;
-    if (fast) {
-      // ---- 2. one pass: above-mask bits (plain order: word (4 q0)/32 + m holds lanes
-      //      8m..8m+7 of a warp's 128-column chunk, 4 bits each) and band candidates,
-      //      appended with ballots (no serial scan) and histogrammed for the first
-      //      key-selection level on the way
-      const uint32_t klo = f2key(lo_v), khi = f2key(hi_v);
-      const KMap km0 = kmap(klo, khi);
-      uint32_t nab = 0, wc = 0;                  // wc: this warp's candidates (uniform)
-      uint32_t* wcand = S.cand + warp * kCandW;
-      uint32_t* wcidx = S.cidx + warp * kCandW;
-      auto put = [&](uint32_t slot, float v, int i) {
-        const uint32_t key = f2key(v);
-        if (slot < (uint32_t)kCandW) { wcand[slot] = key; wcidx[slot] = (uint32_t)i; }
-        atomicAdd(&S.hist[km0.bucket(key)], 1u);
-      };
-      if constexpr (kVec) {
-        // kU float4 loads per lane in flight before any is consumed
-        constexpr int kU = 4;
-        const float4* g4 = reinterpret_cast<const float4*>(grow);
-        const float4 ninf = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-        for (int qb = warp * 32; qb < n4; qb += kU * kThreads) {
-          float4 vb[kU];
+    // ---- value range from a strided sample (any range is correct; a good one is fast)
+    {
+      const int i = (int)(((long long)tid * L) / kThreads);
+      const float v = i < L ? src.val(i) : src.val(0);
+      float mn = v, mx = v;
 #pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const int q = qb + u * kThreads + lane;
-            vb[u] = q < n4 ? __ldcs(g4 + q) : ninf;
-          }
+      for (int o = 16; o; o >>= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      }
+      if (lane == 0) { S.wa[warp] = __float_as_uint(mn); S.wb[warp] = __float_as_uint(mx); }
+      for (int b = tid; b < kBuckets; b += kThreads) S.hist[b] = 0;
+      __syncthreads();
+      if (warp == 0) {
+        mn = __uint_as_float(S.wa[lane]);
+        mx = __uint_as_float(S.wb[lane]);
 #pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const int q0 = qb + u * kThreads, q = q0 + lane;
-            if (q0 >= n4) break;
-            const float4 v = vb[u];
-            const bool g0 = v.x > hi_v, g1 = v.y > hi_v, g2 = v.z > hi_v, g3 = v.w > hi_v;
-            const uint32_t gt = (uint32_t)g0 | ((uint32_t)g1 << 1) | ((uint32_t)g2 << 2) | ((uint32_t)g3 << 3);
-            nab += __popc(gt);
-            uint32_t wv = gt << (4 * (lane & 7));
-            wv |= __shfl_xor_sync(0xffffffffu, wv, 1);
-            wv |= __shfl_xor_sync(0xffffffffu, wv, 2);
-            wv |= __shfl_xor_sync(0xffffffffu, wv, 4);
-            if ((lane & 7) == 0 && q < n4) mask[(q0 >> 3) + (lane >> 3)] = wv;
-            const bool i0 = !g0 && v.x >= lo_v, i1 = !g1 && v.y >= lo_v;
-            const bool i2 = !g2 && v.z >= lo_v, i3 = !g3 && v.w >= lo_v;
-            const uint32_t b0 = __ballot_sync(0xffffffffu, i0), b1 = __ballot_sync(0xffffffffu, i1);
-            const uint32_t b2 = __ballot_sync(0xffffffffu, i2), b3 = __ballot_sync(0xffffffffu, i3);
-            const uint32_t c0 = __popc(b0), c01 = c0 + __popc(b1), c012 = c01 + __popc(b2);
-            const uint32_t wtot = c012 + __popc(b3);
-            if (i0) put(wc + __popc(b0 & lt), v.x, 4 * q);
-            if (i1) put(wc + c0 + __popc(b1 & lt), v.y, 4 * q + 1);
-            if (i2) put(wc + c01 + __popc(b2 & lt), v.z, 4 * q + 2);
-            if (i3) put(wc + c012 + __popc(b3 & lt), v.w, 4 * q + 3);
-            wc += wtot;
-          }
+        for (int o = 16; o; o >>= 1) {
+          mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (lane == 0) {
+          S.s_vmin = mn; S.s_vmax = mx; S.s_ncand = 0; S.s_mode = 0;
+          S.s_cmin = 0xffffffffu; S.s_cmax = 0u;
         }
       }
-      __syncthreads();   // plain mask-word stores above before the tail's atomicOr
-      // scalar part: the tail (or the whole row without 16-byte alignment)
-      for (int i0 = 4 * n4 + warp * 32; i0 < L; i0 += kThreads) {
-        const int i = i0 + lane;
-        const float v = i < L ? __ldcs(grow + i) : -INFINITY;
-        const bool g = v > hi_v, in = !g && v >= lo_v && i < L;
-        if (g) { atomicOr(&mask[i >> 5], 1u << (i & 31)); ++nab; }
-        const uint32_t bi = __ballot_sync(0xffffffffu, in);
-        if (in) put(wc + __popc(bi & lt), v, i);
-        wc += __popc(bi);
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) nab += __shfl_xor_sync(0xffffffffu, nab, o);
-      if (lane == 0) { atomicAdd(&S.nabove, nab); S.wcnt[warp] = wc; }
       __syncthreads();
-      TOPK_MARK(2);
-      const uint32_t nabove = S.nabove;
-      uint32_t nc = 0, wmax = 0;
+    }
+    const float vmin = S.s_vmin, vmax = S.s_vmax;
+    bool fast = isfinite(vmin) && isfinite(vmax) && vmax > vmin;
+    const float ba = fast ? (float)kBuckets / (vmax - vmin) : 0.f;
+    const float bb = -vmin * ba;
+    uint32_t n_above = 0;   // this warp's entries in buckets > B_hi
+    if (fast) {
+      // ---- sample histogram (kSample strided entries) -> bucket band [B_lo, B_hi]
+      //      expected to hold T: ~k*kSample/L sample entries lie above T, +- 4 sigma.
 #pragma unroll
-      for (int w = 0; w < kWarps; ++w) { nc += S.wcnt[w]; wmax = max(wmax, S.wcnt[w]); }
-      fast = wmax <= (uint32_t)kCandW && nabove < (uint32_t)k && (uint32_t)k <= nabove + nc;
-      TOPK_MARK(3);
-      if (fast) {
-        // ---- 3. exact T among the candidates
-        // candidate slot c lives in warp region c / kCandW, valid below that warp's count
-        auto valid = [&](int c) { return (uint32_t)(c % kCandW) < S.wcnt[c / kCandW]; };
-        key_select(S, (uint32_t)k - nabove, klo, khi, true, [&](auto visit) {
-          for (int c = tid; c < kCandCap; c += kThreads)
-            if (valid(c)) visit(S.cand[c]);
-        });
-        T = S.prefix;
-        TOPK_MARK(4);
-        const uint32_t keep_eq = S.need, n_eq = S.neq;
-        for (int c = tid; c < kCandCap; c += kThreads) {
-          if (!valid(c)) continue;
-          const uint32_t key = S.cand[c];
-          bool keep = key > T;
-          if (key == T) {
-            if (n_eq <= keep_eq) {
-              keep = true;
-            } else {
-              const uint32_t i = S.cidx[c];
-              uint32_t rank = 0;
-              for (int c2 = 0; c2 < kCandCap; ++c2)
-                rank += (valid(c2) && S.cand[c2] == T && S.cidx[c2] < i);
-              keep = rank < keep_eq;
-            }
-          }
-          if (keep) { const uint32_t i = S.cidx[c]; atomicOr(&mask[i >> 5], 1u << (i & 31)); }
+      for (int j = 0; j < kSample / kThreads; ++j) {
+        const int i = min((tid + j * kThreads) * sstride, L - 1);
+        atomicAdd(&S.hist[vbucket(src.val(i), ba, bb)], 1u);
+      }
+      __syncthreads();
+      {
+        const float t = (float)k * (float)kSample / (float)L;
+        const float m = 4.f * sqrtf(fmaxf(t * (1.f - t / kSample), 1.f)) + 2.f;
+        const float tm = t - m, tp = t + m;
+        const uint32_t h0 = S.hist[2 * tid], h1 = S.hist[2 * tid + 1];
+        uint32_t v = h0 + h1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t x = __shfl_down_sync(0xffffffffu, v, o);
+          if (lane + o < 32) v += x;
+        }
+        if (lane == 0) S.wc[warp] = v;
+        if (tid == 0) { S.wa[0] = kBuckets - 1; S.wb[0] = 0; }   // defaults: B_hi = top, B_lo = 0
+        __syncthreads();
+        const uint32_t wt = S.wc[lane];
+        uint32_t suf = wt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t x = __shfl_down_sync(0xffffffffu, suf, o);
+          if (lane + o < 32) suf += x;
+        }
+        const uint32_t after = __shfl_sync(0xffffffffu, suf - wt, warp);
+        // C(b) = samples in buckets >= b, for b = 2 tid, 2 tid + 1, 2 tid + 2
+        const float c0 = (float)(v + after), c1 = c0 - (float)h0, c2 = c1 - (float)h1;
+        __syncthreads();
+        if (tm > 0.f) {
+          if (c1 <= tm && c0 > tm) S.wa[0] = 2 * tid;
+          if (c2 <= tm && c1 > tm) S.wa[0] = 2 * tid + 1;
+        }
+        if (tp < (float)kSample) {
+          if (c0 >= tp && c1 < tp) S.wb[0] = 2 * tid;
+          if (c1 >= tp && c2 < tp) S.wb[0] = 2 * tid + 1;
         }
         __syncthreads();
-        TOPK_MARK(5);
-        // ---- 4. ordered emit: warp w owns a contiguous range of mask words, lane j
-        //      the j-th word of each 32-word group (warp scan of the popcounts)
-        const int wpw = (nw + kWarps - 1) / kWarps;
-        const int a0 = min(nw, warp * wpw), a1 = min(nw, a0 + wpw);
-        uint32_t wcnt = 0;
-        for (int w = a0 + lane; w < a1; w += 32) wcnt += __popc(mask[w]);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) wcnt += __shfl_xor_sync(0xffffffffu, wcnt, o);
-        uint32_t tot;
-        uint32_t base = block_excl_scan(S, lane == 0 ? wcnt : 0u, &tot);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        for (int g0 = a0; g0 < a1; g0 += 32) {
-          const int w = g0 + lane;
-          uint32_t m = w < a1 ? mask[w] : 0u;
-          const uint32_t c = __popc(m);
-          uint32_t inc = c;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += x;
+      }
+      const int b_hi = (int)S.wa[0], b_lo = min((int)S.wb[0], b_hi);
+      // value band: above <=> v > hi_v, candidate <=> lo_v <= v <= hi_v (any choice is
+      // exact after the band check below; bucket edges make it tight)
+      const float hi_v = b_hi >= kBuckets - 1 ? INFINITY : vmin + (float)(b_hi + 1) / ba;
+      const float lo_v = b_lo <= 0 ? -INFINITY : vmin + (float)b_lo / ba;
+      TOPK_MARK(1);
+      // ---- pass 1: per contiguous warp segment, above-mask words and band candidates
+      //      (staged per warp: no shared counter, so no cross-warp atomic contention)
+      uint32_t cmin = 0xffffffffu, cmax = 0u, wcnt = 0;
+      uint32_t* wcand = S.cand + warp * kCandW;
+      uint32_t* wcidx = S.cidx + warp * kCandW;
+      for (int base = s0; base < s1; base += 32) {
+        const int i = base + lane;
+        const bool valid = i < s1;
+        const float v = valid ? src.val(i) : -INFINITY;
+        const uint32_t mab = __ballot_sync(0xffffffffu, v > hi_v);
+        if (lane == 0) mask[base >> 5] = mab;
+        n_above += __popc(mab);
+        const bool in = valid && v >= lo_v && v <= hi_v;
+        const uint32_t msk = __ballot_sync(0xffffffffu, in);
+        if (msk) {
+          if (in) {
+            const uint32_t slot = wcnt + __popc(msk & lt);
+            const uint32_t key = f2key(v);
+            if (slot < (uint32_t)kCandW) { wcand[slot] = key; wcidx[slot] = (uint32_t)i; }
+            cmin = min(cmin, key);
+            cmax = max(cmax, key);
           }
-          uint32_t pos = base + inc - c;
-          while (m) {
-            orow[pos++] = w * 32 + __ffs(m) - 1;
-            m &= m - 1;
-          }
-          base += __shfl_sync(0xffffffffu, inc, 31);
+          wcnt += __popc(msk);
         }
       }
+      TOPK_MARK(8);
+      cmin = warp_min(cmin);
+      cmax = warp_max(cmax);
+      if (lane == 0) {
+        atomicMin(&S.s_cmin, cmin);
+        atomicMax(&S.s_cmax, cmax);
+        S.wc[warp] = n_above;
+        S.wd[warp] = wcnt;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        uint32_t tot = S.wc[lane];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        const uint32_t c = S.wd[lane];
+        uint32_t ci = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t x = __shfl_up_sync(0xffffffffu, ci, o);
+          if (lane >= o) ci += x;
+        }
+        const bool over = __any_sync(0xffffffffu, c > (uint32_t)kCandW);
+        S.wb[lane] = ci - c;                   // compacted base of this warp's candidates
+        const uint32_t nc = __shfl_sync(0xffffffffu, ci, 31);
+        if (lane == 0) {
+          const bool ok = !over && tot < (uint32_t)k && (uint32_t)k <= tot + nc;
+          S.s_mode = ok ? 1u : 2u;
+          S.s_ncand = nc;
+          S.s_lo = S.s_cmin; S.s_hi = S.s_cmax;
+          S.s_need = (uint32_t)k - tot; S.s_kband = (uint32_t)k - tot;
+        }
+      }
+      __syncthreads();
+      fast = S.s_mode == 1;
+      if (fast) {
+        // compact the per-warp staging into one list (destinations never overlap a
+        // later warp's source region: each warp holds <= kCandW entries)
+        uint32_t kk[kCandW / 32], ii[kCandW / 32];
+        const uint32_t cb = S.wb[warp];
+#pragma unroll
+        for (int j = 0; j < kCandW / 32; ++j) {
+          const uint32_t q = j * 32 + lane;
+          kk[j] = q < wcnt ? wcand[q] : 0u;
+          ii[j] = q < wcnt ? wcidx[q] : 0u;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kCandW / 32; ++j) {
+          const uint32_t q = j * 32 + lane;
+          if (q < wcnt) { S.cand[cb + q] = kk[j]; S.cidx[cb + q] = ii[j]; }
+        }
+        TOPK_MARK(9);
+        // the row buffer is no longer needed on the fast path: start the next row's load
+        if constexpr (kSmem) {
+          if (bulk && tid == 0 && row + (int)gridDim.x < rows) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&S.bar, (uint32_t)n4 * 16u);
+            bulk_load(buf, scores + (long long)(row + gridDim.x) * ld, (uint32_t)n4 * 16u, &S.bar);
+          }
+          inflight = bulk && row + (int)gridDim.x < rows;
+        }
+      }
+      __syncthreads();
+      TOPK_MARK(2);
     }
     if (!fast) {
-#ifdef DSV_TOPK_PROF
-      if (tid == 0) atomicAdd(&g_topk_slow, 1u);
-#endif
-      // ---- slow path: whole-row radix select, then ordered two-pass compaction over
-      //      contiguous warp segments
-      uint32_t kmn = 0xffffffffu, kmx = 0u;
+      // whole-row key-space refinement (ties-heavy or non-finite rows)
+      uint32_t kmin = 0xffffffffu, kmax = 0u;
       for (int i = tid; i < L; i += kThreads) {
-        const uint32_t key = f2key(__ldg(grow + i));
-        kmn = min(kmn, key);
-        kmx = max(kmx, key);
+        const uint32_t q = src.key(i);
+        kmin = min(kmin, q);
+        kmax = max(kmax, q);
+      }
+      kmin = warp_min(kmin);
+      kmax = warp_max(kmax);
+      __syncthreads();
+      if (lane == 0) { S.wa[warp] = kmin; S.wb[warp] = kmax; }
+      __syncthreads();
+      if (warp == 0) {
+        const uint32_t a = warp_min(S.wa[lane]), b = warp_max(S.wb[lane]);
+        if (lane == 0) { S.s_lo = a; S.s_hi = b; S.s_need = (uint32_t)k; S.s_mode = 0; }
+      }
+      __syncthreads();
+    }
+    TOPK_MARK(3);
+    refine<kSmem>(S, src, L, tid, lane, warp);
+    TOPK_MARK(4);
+    const uint32_t T = S.s_lo;
+    const float Tf = key2f(T);
+
+    int* orow = out_idx + (long long)row * out_ld;
+    if (fast) {
+      // ---- kept candidates join the above-mask: key > T, then the first ties in index order
+      if (tid == 0) { S.s_gt_total = 0; S.s_cmin = 0; }      // reused: #cand > T, #ties
+      __syncthreads();
+      const int nc = (int)min(S.s_ncand, (uint32_t)kCandCap);
+      uint32_t cgt = 0, ceq = 0;
+      for (int c = tid; c < nc; c += kThreads) {
+        const uint32_t key = S.cand[c];
+        if (key > T) { const uint32_t i = S.cidx[c]; atomicOr(&mask[mword(i, vec4)], mbit(i, vec4)); ++cgt; }
+        else if (key == T) ++ceq;
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
-        kmn = min(kmn, __shfl_xor_sync(0xffffffffu, kmn, o));
-        kmx = max(kmx, __shfl_xor_sync(0xffffffffu, kmx, o));
+        cgt += __shfl_xor_sync(0xffffffffu, cgt, o);
+        ceq += __shfl_xor_sync(0xffffffffu, ceq, o);
+      }
+      if (lane == 0 && (cgt | ceq)) { atomicAdd(&S.s_gt_total, cgt); atomicAdd(&S.s_cmin, ceq); }
+      __syncthreads();
+      const uint32_t need_eq = S.s_kband - S.s_gt_total;   // k - #above - #(cand > T)
+      const uint32_t nties = S.s_cmin;
+      for (int c = tid; c < nc; c += kThreads) {
+        if (S.cand[c] != T) continue;
+        const uint32_t i = S.cidx[c];
+        uint32_t rank = 0;
+        if (nties > need_eq)
+          for (int c2 = 0; c2 < nc; ++c2) rank += (S.cand[c2] == T && S.cidx[c2] < i);
+        if (rank < need_eq) atomicOr(&mask[mword(i, vec4)], mbit(i, vec4));
       }
       __syncthreads();
-      if (tid == 0) { S.b_lo = 0xffffffffu; S.b_hi = 0u; }
+      TOPK_MARK(5);
+      // ---- ordered emit from the keep-mask: block scan of per-thread popcounts
+      //      (vec4 layout: one thread per 128-column chunk = 4 words)
+      const int gw = vec4 ? 4 : 1;                      // words per unit
+      const int nu = vec4 ? (L + 127) / 128 : nw;       // units
+      const int upt = (nu + kThreads - 1) / kThreads;
+      const int u0 = tid * upt, u1 = min(nu, u0 + upt);
+      uint32_t cnt = 0;
+      for (int u = u0; u < u1; ++u)
+        for (int j = 0; j < gw; ++j) cnt += __popc(mask[u * gw + j]);
+      uint32_t inc = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += x;
+      }
+      if (lane == 31) S.wc[warp] = inc;
       __syncthreads();
-      if (lane == 0) { atomicMin(&S.b_lo, kmn); atomicMax(&S.b_hi, kmx); }
-      __syncthreads();
-      key_select(S, (uint32_t)k, S.b_lo, S.b_hi, false, [&](auto visit) {
-        for (int i = tid; i < L; i += kThreads) visit(f2key(__ldg(grow + i)));
-      });
-      T = S.prefix;
-      const uint32_t keep_eq = S.need;
-      const int seg = (((L + kWarps - 1) / kWarps) + 31) & ~31;
-      const int s0 = warp * seg, s1 = min(L, s0 + seg);
+      uint32_t wbase = 0;
+      if (lane < warp) wbase = S.wc[lane];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) wbase += __shfl_xor_sync(0xffffffffu, wbase, o);
+      uint32_t pos = wbase + inc - cnt;
+      for (int u = u0; u < u1; ++u) {
+        if (vec4) {
+          const uint32_t m0 = mask[4 * u], m1 = mask[4 * u + 1], m2 = mask[4 * u + 2], m3 = mask[4 * u + 3];
+          uint32_t any = m0 | m1 | m2 | m3;
+          while (any) {
+            const int l = __ffs(any) - 1;
+            any &= any - 1;
+            const int c0 = u * 128 + 4 * l;
+            if ((m0 >> l) & 1u) orow[pos++] = c0;
+            if ((m1 >> l) & 1u) orow[pos++] = c0 + 1;
+            if ((m2 >> l) & 1u) orow[pos++] = c0 + 2;
+            if ((m3 >> l) & 1u) orow[pos++] = c0 + 3;
+          }
+        } else {
+          uint32_t m = mask[u];
+          while (m) {
+            const int bit = __ffs(m) - 1;
+            orow[pos++] = u * 32 + bit;
+            m &= m - 1;
+          }
+        }
+      }
+    } else {
+      // ---- slow path: per-warp (> T, == T) counts by a scan, then ordered compaction
       uint32_t ngt = 0, neq = 0;
       for (int base = s0; base < s1; base += 32) {
         const int i = base + lane;
-        const uint32_t key = i < s1 ? f2key(__ldg(grow + i)) : 0u;
-        ngt += __popc(__ballot_sync(0xffffffffu, i < s1 && key > T));
-        neq += __popc(__ballot_sync(0xffffffffu, i < s1 && key == T));
+        const bool valid = i < s1;
+        const float v = valid ? src.val(i) : 0.f;
+        ngt += __popc(__ballot_sync(0xffffffffu, valid && v > Tf));
+        neq += __popc(__ballot_sync(0xffffffffu, valid && v == Tf));
       }
-      // exclusive prefixes over warps of (gt, eq)
-      uint32_t tot_gt, tot_eq;
-      const uint32_t gbase = block_excl_scan(S, lane == 0 ? ngt : 0u, &tot_gt);
-      const uint32_t ebase = block_excl_scan(S, lane == 0 ? neq : 0u, &tot_eq);
-      uint32_t gb = __shfl_sync(0xffffffffu, gbase, 0), eb = __shfl_sync(0xffffffffu, ebase, 0);
-      uint32_t kept = gb + min(eb, keep_eq);
-      uint32_t eqs = eb;
+      __syncthreads();
+      if (lane == 0) { S.wa[warp] = ngt; S.wb[warp] = neq; }
+      __syncthreads();
+      if (warp == 0) {
+        const uint32_t g = S.wa[lane], e = S.wb[lane];
+        uint32_t gi = g, ei = e;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t1 = __shfl_up_sync(0xffffffffu, gi, o);
+          const uint32_t t2 = __shfl_up_sync(0xffffffffu, ei, o);
+          if (lane >= o) { gi += t1; ei += t2; }
+        }
+        const uint32_t gtot = __shfl_sync(0xffffffffu, gi, 31);
+        const uint32_t need_eq = (uint32_t)k - gtot;
+        const uint32_t gex = gi - g, eex = ei - e;
+        S.wa[lane] = gex + min(eex, need_eq);  // kept entries before this warp
+        S.wb[lane] = eex;                       // ties before this warp
+        if (lane == 0) S.s_gt_total = gtot;
+      }
+      __syncthreads();
+      const uint32_t need_eq = (uint32_t)k - S.s_gt_total;
+      uint32_t kept = S.wa[warp];
+      uint32_t eqs = S.wb[warp];
       for (int base = s0; base < s1; base += 32) {
         const int i = base + lane;
-        const uint32_t key = i < s1 ? f2key(__ldg(grow + i)) : 0u;
-        const uint32_t mgt = __ballot_sync(0xffffffffu, i < s1 && key > T);
-        const uint32_t meq = __ballot_sync(0xffffffffu, i < s1 && key == T);
-        const bool keq = ((meq >> lane) & 1u) && (eqs + __popc(meq & lt)) < keep_eq;
-        const uint32_t mkeep = mgt | __ballot_sync(0xffffffffu, keq);
+        const bool valid = i < s1;
+        const float v = valid ? src.val(i) : 0.f;
+        const uint32_t mgt = __ballot_sync(0xffffffffu, valid && v > Tf);
+        const uint32_t meq = __ballot_sync(0xffffffffu, valid && v == Tf);
+        const bool keep_eq = ((meq >> lane) & 1u) && (eqs + __popc(meq & lt)) < need_eq;
+        const uint32_t mkeep = mgt | __ballot_sync(0xffffffffu, keep_eq);
         if ((mkeep >> lane) & 1u) orow[kept + __popc(mkeep & lt)] = i;
         kept += __popc(mkeep);
         eqs += __popc(meq);
       }
     }
+    if (tid == 0) out_thr[row] = Tf;
     TOPK_MARK(6);
-    if (tid == 0) out_thr[row] = key2f(T);
-    __syncthreads();   // shared state reused by the next row
+    __syncthreads();   // buffers reused by the next row
     TOPK_MARK(7);
   }
 }
@@ -482,7 +547,10 @@ topk_rows_kernel(const float* __restrict__ scores, long long ld, int rows, int L
 }  // namespace dsv
 
 size_t dsv_topk_smem_bytes(int L) {
-  return sizeof(dsv::topk::Smem) + (((size_t)L + 31) / 32) * 4;   // keep-mask
+  const size_t mask = (((size_t)L + 127) / 128 * 4 + 4) * 4;
+  const size_t base = sizeof(dsv::topk::Smem) + mask;
+  const size_t need = base + (size_t)L * 4;
+  return need <= 227 * 1024 ? need : base;
 }
 
 int dsv_topk_launch(const float* scores, long long ld, int rows, int L, const int* k_per_head,
@@ -490,20 +558,24 @@ int dsv_topk_launch(const float* scores, long long ld, int rows, int L, const in
                     cudaStream_t stream) {
   using namespace dsv::topk;
   if (rows <= 0) return 0;
-  const size_t smem = dsv_topk_smem_bytes(L);
-  if (smem > 227 * 1024) return (int)cudaErrorInvalidValue;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const bool vec = ((ld * 4) % 16 == 0) && ((reinterpret_cast<uintptr_t>(scores) & 15) == 0);
-  auto kern = vec ? topk_rows_kernel<true> : topk_rows_kernel<false>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
-  per_sm = per_sm < 1 ? 1 : per_sm;
-  const long long want = (long long)sms * per_sm;
-  const int grid = (int)(rows < want ? rows : want);
-  kern<<<grid, kThreads, smem, stream>>>(scores, ld, rows, L, k_per_head, rows_per_head, out_idx,
-                                         out_ld, out_thr);
+  const int grid = rows < sms ? rows : sms;
+  const size_t mask = (((size_t)L + 127) / 128 * 4 + 4) * 4;
+  const size_t base = sizeof(Smem) + mask;
+  const size_t need = base + (size_t)L * 4;
+  if (base > 227 * 1024) return (int)cudaErrorInvalidValue;
+  if (need <= 227 * 1024) {
+    cudaFuncSetAttribute(topk_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)need);
+    topk_rows_kernel<true><<<grid, kThreads, need, stream>>>(
+        scores, ld, rows, L, k_per_head, rows_per_head, out_idx, out_ld, out_thr);
+  } else {
+    cudaFuncSetAttribute(topk_rows_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)base);
+    topk_rows_kernel<false><<<grid, kThreads, base, stream>>>(
+        scores, ld, rows, L, k_per_head, rows_per_head, out_idx, out_ld, out_thr);
+  }
   return (int)cudaGetLastError();
 }
