@@ -134,6 +134,17 @@ typedef struct dsv_copy_job {
  * `splits` blocks cooperate on each job (1..1024). */
 int dsv_copy_jobs(const dsv_copy_job* jobs, int njobs, int splits, void* stream);
 
+/* The same job semantics from a HOST job table, executed by the copy engines (one
+ * cudaMemcpyAsync per flat job, cudaMemcpy2DAsync per strided job) on `stream`: no SM
+ * time, so an exchange can run underneath the attention kernels. */
+int dsv_copy_jobs_ce(const dsv_copy_job* jobs, int njobs, void* stream);
+
+/* Stream memory operations for cross-GPU signalling without SM time: write `value` to
+ * a 4-byte device (or peer-mapped) word after all prior work of `stream`, and make
+ * `stream` wait until a word is >= value (monotone step counters). */
+int dsv_stream_write_u32(void* addr, unsigned int value, void* stream);
+int dsv_stream_wait_u32_geq(const void* addr, unsigned int value, void* stream);
+
 /* Diagnostics: copy the backward kernel's phase timeline (clock64 stamps, filled only
  * by builds with -DDSV_BWD_PROF; layout [8 CTAs][32 blocks][12 events] int64) into a
  * host buffer. Returns the bytes copied or a negative value. */

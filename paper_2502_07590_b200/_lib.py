@@ -48,6 +48,9 @@ SIGNATURES = {
                      c_void_p, c_void_p],
     "dsv_debug_timeline": [c_void_p, c_int],
     "dsv_copy_jobs": [c_void_p, c_int, c_int, c_void_p],
+    "dsv_copy_jobs_ce": [c_void_p, c_int, c_void_p],
+    "dsv_stream_write_u32": [c_void_p, ctypes.c_uint, c_void_p],
+    "dsv_stream_wait_u32_geq": [c_void_p, ctypes.c_uint, c_void_p],
     "dsv_gather_rows": [c_void_p, c_longlong, c_void_p, c_int, c_int, c_void_p, c_longlong,
                         c_void_p],
     "dsv_f32_to_bf16": [c_void_p, c_void_p, c_longlong, c_void_p],

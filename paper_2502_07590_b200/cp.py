@@ -269,7 +269,8 @@ class PeerExchange:
         nh_max = max(len(h) for h in self.heads_of)
         big, small, back = nh_max * self.L * self.D, nh_max * self.L * self.r, self.H * self.chunk * self.D
         names = [("q", big), ("k", big), ("v", big), ("do", big), ("qlr", small), ("klr", small),
-                 ("o", back), ("dq", back), ("dk", back), ("dv", back)]
+                 ("o", back), ("dq", back), ("dk", back), ("dv", back),
+                 ("flags", 2 * 3 * self.world)]          # int32 [3 kinds][world] arrival flags
         self.off, tot = {}, 0
         for n, sz in names:
             self.off[n] = tot
@@ -291,6 +292,10 @@ class PeerExchange:
                 pass
         self.hdl = symm.rendezvous(self.buf, self.group)
         self.ptrs = np.asarray([int(p) for p in self.hdl.buffer_ptrs], dtype=np.int64)
+        self.buf[self.off["flags"]: self.off["flags"] + 2 * 3 * self.world].zero_()
+        torch.cuda.synchronize(dev)
+        dist.barrier(self.group)
+        self._step = 0
 
     # ------------------------------------------------------------------ views
     def region(self, name: str) -> torch.Tensor:
@@ -312,24 +317,33 @@ class PeerExchange:
             self._tables[key] = t
         return t
 
-    def _fwd_jobs(self, q, k, v, do, p):
-        H, L, D, r, chunk, me = self.H, self.L, self.D, self.r, self.chunk, self.rank
+    def _head_jobs(self, named):
+        """Flat per-head jobs: this rank's token chunk of head h of each tensor [H, L/N, D]
+        -> the owner's region rows [hi, rank * L/N, :)."""
+        H, L, D, chunk, me = self.H, self.L, self.D, self.chunk, self.rank
         h = np.arange(H, dtype=np.int64)
-        owner, hi = self.assignment, self.hi_of
-        dst_base = self.ptrs[owner]
+        dst_base = self.ptrs[self.assignment]
         jobs = []
-        for name, t in (("q", q), ("k", k), ("v", v), ("do", do)):
+        for name, t in named:
             j = np.empty((H, 6), dtype=np.int64)
             j[:, 0] = t.data_ptr() + h * chunk * D * 2
-            j[:, 1] = dst_base + 2 * (self.off[name] + (hi * L + me * chunk) * D)
+            j[:, 1] = dst_base + 2 * (self.off[name] + (self.hi_of * L + me * chunk) * D)
             j[:, 2] = j[:, 3] = chunk * D * 2
             j[:, 4] = 1
             j[:, 5] = chunk * D * 2
             jobs.append(j)
+        return np.ascontiguousarray(np.concatenate(jobs))
+
+    def _lowrank_jobs(self, p):
+        """Rows of P [L/N, 2, H, r] -> the owners' Q_lr / K_lr regions (32-byte rows)."""
+        H, L, r, chunk, me = self.H, self.L, self.r, self.chunk, self.rank
+        h = np.arange(H, dtype=np.int64)
+        dst_base = self.ptrs[self.assignment]
+        jobs = []
         for side, name in ((0, "qlr"), (1, "klr")):
             j = np.empty((H, 6), dtype=np.int64)
             j[:, 0] = p.data_ptr() + 2 * (side * H + h) * r
-            j[:, 1] = dst_base + 2 * (self.off[name] + (hi * L + me * chunk) * r)
+            j[:, 1] = dst_base + 2 * (self.off[name] + (self.hi_of * L + me * chunk) * r)
             j[:, 2] = 2 * H * r * 2
             j[:, 3] = r * 2
             j[:, 4] = chunk
@@ -337,7 +351,11 @@ class PeerExchange:
             jobs.append(j)
         return np.ascontiguousarray(np.concatenate(jobs))
 
-    def _back_jobs(self, tensors):
+    def _fwd_jobs(self, q, k, v, do, p):
+        return np.ascontiguousarray(np.concatenate([
+            self._head_jobs((("q", q), ("k", k), ("v", v), ("do", do))), self._lowrank_jobs(p)]))
+
+    def _back_jobs(self, tensors, names=("o", "dq", "dk", "dv")):
         L, D, chunk = self.L, self.D, self.chunk
         hs = self.my_heads
         nh = len(hs)
@@ -345,7 +363,7 @@ class PeerExchange:
         dst_r = np.tile(np.arange(self.world, dtype=np.int64), nh)
         dst_h = np.repeat(hs.astype(np.int64), self.world)
         jobs = []
-        for name, t in zip(("o", "dq", "dk", "dv"), tensors):
+        for name, t in zip(names, tensors):
             j = np.empty((nh * self.world, 6), dtype=np.int64)
             j[:, 0] = t.data_ptr() + 2 * (hi * L + dst_r * chunk) * D
             j[:, 1] = self.ptrs[dst_r] + 2 * (self.off[name] + dst_h * chunk * D)
@@ -354,6 +372,15 @@ class PeerExchange:
             j[:, 5] = chunk * D * 2
             jobs.append(j)
         return np.ascontiguousarray(np.concatenate(jobs))
+
+    def _host_table(self, key, build):
+        t = self._tables.get(key)
+        if t is None:
+            if len(self._tables) >= 16:
+                self._tables.clear()
+            t = build()
+            self._tables[key] = t
+        return t
 
     def _run(self, table):
         from . import ops
@@ -366,15 +393,18 @@ class PeerExchange:
     def to_heads(self, q, k, v, do, p):
         """q, k, v, do [H, L/N, D] and P [L/N, 2 H r] (this rank's tokens) ->
         views Q, K, V, dO [my_heads, L, D], Q_lr, K_lr [my_heads, L, r]."""
+        self._check_in(q, k, v, do, p)
+        key = ("f",) + tuple(t.data_ptr() for t in (q, k, v, do, p))
+        self._run(self._table(key, lambda: self._fwd_jobs(q, k, v, do, p)))
+        self._account(("hcp_fwd", 3 * self.D + 2 * self.r), ("hcp_bwd_in", self.D), to_heads=True)
+        return tuple(self.region(n) for n in ("q", "k", "v", "do", "qlr", "klr"))
+
+    def _check_in(self, q, k, v, do, p):
         for t in (q, k, v, do, p):
             if not t.is_contiguous() or t.dtype != torch.bfloat16:
                 raise ValueError("peer exchange expects contiguous bf16 tensors")
         if q.shape != (self.H, self.chunk, self.D) or p.shape != (self.chunk, 2 * self.H * self.r):
             raise ValueError("shape does not match the exchange plan")
-        key = ("f",) + tuple(t.data_ptr() for t in (q, k, v, do, p))
-        self._run(self._table(key, lambda: self._fwd_jobs(q, k, v, do, p)))
-        self._account(("hcp_fwd", 3 * self.D + 2 * self.r), ("hcp_bwd_in", self.D), to_heads=True)
-        return tuple(self.region(n) for n in ("q", "k", "v", "do", "qlr", "klr"))
 
     def to_tokens(self, o, dq, dk, dv):
         """o, dq, dk, dv [my_heads, L, D] -> views [H, L/N, D] on the token owners."""
@@ -385,6 +415,93 @@ class PeerExchange:
         key = ("b",) + tuple(t.data_ptr() for t in (o, dq, dk, dv))
         self._run(self._table(key, lambda: self._back_jobs((o, dq, dk, dv))))
         self._account(("output_redistribute", self.D), ("hcp_bwd_out", 3 * self.D), to_heads=False)
+        return tuple(self.region(n) for n in ("o", "dq", "dk", "dv"))
+
+    # ------------------------------------------------------------------ overlapped step
+    def _flag(self, rank: int, kind: int, src: int) -> int:
+        """Address of rank's arrival flag for data of `kind` (0 Q/K/V, 1 dO, 2 O) from src."""
+        return int(self.ptrs[rank]) + 2 * self.off["flags"] + 4 * (kind * self.world + src)
+
+    def _signal(self, kind: int, step: int, stream) -> None:
+        from . import _lib
+
+        for r in range(self.world):
+            if r != self.rank:
+                _lib.call("dsv_stream_write_u32", self._flag(r, kind, self.rank), step, stream.cuda_stream)
+
+    def _await(self, kind: int, step: int, stream) -> None:
+        from . import _lib
+
+        for r in range(self.world):
+            if r != self.rank:
+                _lib.call("dsv_stream_wait_u32_geq", self._flag(self.rank, kind, r), step, stream.cuda_stream)
+
+    def overlapped(self, q, k, v, do, p, select, forward, backward):
+        """One HCP step with the bulk of the exchange on the copy engines:
+
+        compute stream: barrier | Q_lr/K_lr rows (copy kernel) | barrier | select |
+                        wait Q,K,V | forward | wait dO | backward | dQ,dK,dV (copy kernel) |
+                        barrier | wait O
+        side stream:    Q,K,V (copy engines) | signal | dO | signal | wait fwd | O | signal
+
+        Arrival is signalled with stream memory operations (a value write into each
+        owner's flag word, a wait-until->= on the consumer's stream): no kernel spins on
+        an SM while the attention kernels run.
+
+        select/forward/backward are callables on the compute stream (the local layer).
+        Returns (O, dQ, dK, dV) views [H, L/N, D] of this rank's tokens.
+        """
+        from . import ops
+
+        self._check_in(q, k, v, do, p)
+        cur = torch.cuda.current_stream()
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(device=self.buf.device)
+        side = self._side
+        ptrs = tuple(t.data_ptr() for t in (q, k, v, do, p))
+        qkv = self._host_table(("qkv",) + ptrs, lambda: self._head_jobs((("q", q), ("k", k), ("v", v))))
+        dj = self._host_table(("do",) + ptrs, lambda: self._head_jobs((("do", do),)))
+        lr = self._table(("lr",) + ptrs, lambda: self._lowrank_jobs(p))
+        # host issue order keeps the GPU busy: the select kernels are queued before the
+        # (slow to issue) copy-engine jobs, the forward before the dO / O jobs
+        self.hdl.barrier(channel=0)                   # everyone is done with the last step
+        ev0 = torch.cuda.Event()
+        ev0.record(cur)
+        ev_qkv, ev_do, ev_f, ev_o = (torch.cuda.Event() for _ in range(4))
+        self._step += 1
+        step = self._step
+        ops.copy_jobs(lr, self.splits)
+        self.hdl.barrier(channel=0)
+        ql, kl, vl, dom, qlr, klr = (self.region(n) for n in ("q", "k", "v", "do", "qlr", "klr"))
+        sel = select(qlr, klr)
+        side.wait_event(ev0)
+        ops.copy_jobs_ce(qkv, side)
+        self._signal(0, step, side)
+        ev_qkv.record(side)
+        cur.wait_event(ev_qkv)                        # this rank's own (local) copies
+        self._await(0, step, cur)
+        out, lse = forward(ql, kl, vl, sel)
+        ev_f.record(cur)
+        ops.copy_jobs_ce(dj, side)
+        self._signal(1, step, side)
+        ev_do.record(side)
+        side.wait_event(ev_f)
+        oj = self._host_table(("o", out.data_ptr()), lambda: self._back_jobs((out,), ("o",)))
+        ops.copy_jobs_ce(oj, side)
+        self._signal(2, step, side)
+        ev_o.record(side)
+        cur.wait_event(ev_do)
+        self._await(1, step, cur)
+        dq, dk, dv = backward(ql, kl, vl, out, lse, dom, sel)
+        gj = self._table(("g",) + tuple(t.data_ptr() for t in (dq, dk, dv)),
+                         lambda: self._back_jobs((dq, dk, dv), ("dq", "dk", "dv")))
+        ops.copy_jobs(gj, self.splits)
+        self.hdl.barrier(channel=0)
+        cur.wait_event(ev_o)
+        self._await(2, step, cur)
+        self._account(("hcp_fwd", 3 * self.D + 2 * self.r), ("hcp_bwd_in", self.D), to_heads=True)
+        self._account(("output_redistribute", self.D), ("hcp_bwd_out", 3 * self.D), to_heads=False)
+        self._keep = (out, dq, dk, dv)                # alive until the side stream has read them
         return tuple(self.region(n) for n in ("o", "dq", "dk", "dv"))
 
     def _account(self, *phases, to_heads: bool):
@@ -412,7 +529,7 @@ class HeadParallelDSV:
 
     def __init__(self, grid, heads: int, head_dim: int, d_lr: int = 16, voxel=(8, 4, 4),
                  sparsity=0.9, balanced: bool = True, group=None, device="cuda",
-                 transport: str = "auto"):
+                 transport: str = "auto", overlap: bool = False):
         from .layer import DSVAttentionLayer
 
         self.world = dist.get_world_size(group)
@@ -423,6 +540,7 @@ class HeadParallelDSV:
         if transport not in ("peer", "all_to_all"):
             raise ValueError(f"unknown transport {transport!r}")
         self.transport = transport
+        self.overlap = bool(overlap) and transport == "peer"
         if transport == "peer":
             self.ex = PeerExchange(heads, grid.size, head_dim, d_lr, self.assignment, group, device)
         else:
@@ -491,16 +609,38 @@ class HeadParallelDSV:
     def _step_peer(self, x_local, wt, q, k, v, dout):
         from . import ops
 
+        loc = self.local
         self._mark("start")
         p = ops.project(x_local, wt)                                   # [L/N, 2 H r]
         self._mark("project")
+        if self.overlap:
+            # copy-engine exchange under the compute (measured slower on B200 at 2-4 GPUs:
+            # the copy engines move ~200 GB/s here vs ~570 GB/s for the copy kernel)
+            def select(qlr, klr):
+                r = loc.select_from_lowrank(qlr, klr)
+                self._mark("select")   # includes the Q_lr/K_lr exchange
+                return r
+
+            def forward(ql, kl, vl, sel):
+                r = loc.forward(ql, kl, vl, sel)
+                self._mark("fwd")
+                return r
+
+            def backward(*a):
+                r = loc.backward(*a)
+                self._mark("bwd")
+                return r
+
+            res = self.ex.overlapped(q, k, v, dout, p, select, forward, backward)
+            self._mark("grads_exchange")
+            return res
         ql, kl, vl, dout_m, qlr, klr = self.ex.to_heads(q, k, v, dout, p)
         self._mark("exchange_in")
-        sel = self.local.select_from_lowrank(qlr, klr)
+        sel = loc.select_from_lowrank(qlr, klr)
         self._mark("select")
-        out, lse = self.local.forward(ql, kl, vl, sel)
+        out, lse = loc.forward(ql, kl, vl, sel)
         self._mark("fwd")
-        dq, dk, dv = self.local.backward(ql, kl, vl, out, lse, dout_m, sel)
+        dq, dk, dv = loc.backward(ql, kl, vl, out, lse, dout_m, sel)
         self._mark("bwd")
         res = self.ex.to_tokens(out, dq, dk, dv)
         self._mark("exchange_out")

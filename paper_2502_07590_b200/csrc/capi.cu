@@ -72,6 +72,20 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
+// Stream memory operations (executed by the GPU front end, no SM time): a peer's copy
+// engines signal data arrival with a value write, the consumer's stream waits on it.
+using WriteValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+template <typename Fn>
+Fn driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess)
+    return reinterpret_cast<Fn>(p);
+  return nullptr;
+}
+
 // bf16 tensor map with up to 3 dims: dims[0] innermost (elements), strides in bytes for
 // dims 1..rank-1, 128B swizzle.
 bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
@@ -116,7 +130,10 @@ int dsv_gemm_bf16(const void* A, long long lda, long long a_bs, const void* B, l
     return fail(DSV_EINVAL, "gemm: operand strides must be multiples of 16 bytes");
   if (c_dtype != DSV_DTYPE_F32 && c_dtype != DSV_DTYPE_BF16)
     return fail(DSV_EINVAL, "gemm: bad output dtype");
-  const int bn = (N >= 256 && K > 64) ? 256 : 128;
+  int bn = (N >= 256 && K > 64) ? 256 : 128;
+  if (bn == 256 && (long long)((M + 127) / 128) * ((N + 255) / 256) * nbatch < 2LL * dsv_device_sm_count())
+    bn = 128;   // too few 128 x 256 tiles to fill the GPU twice
+
   CUtensorMap ta, tb;
   {
     const uint64_t dims[3] = {(uint64_t)K, (uint64_t)M, (uint64_t)nbatch};
@@ -300,6 +317,44 @@ int dsv_debug_timeline_copy(void* dst, int bytes);
 extern "C" int dsv_debug_timeline(void* host_dst, int bytes) {
   if (!host_dst || bytes <= 0) return fail(DSV_EINVAL, "debug_timeline: bad buffer");
   return dsv_debug_timeline_copy(host_dst, bytes);
+}
+
+extern "C" int dsv_stream_write_u32(void* addr, unsigned int value, void* stream) {
+  static WriteValueFn fn = driver_fn<WriteValueFn>("cuStreamWriteValue32");
+  if (!fn) return fail(DSV_EUNSUPPORTED, "stream_write_u32: driver entry point missing");
+  if (!addr || (reinterpret_cast<uintptr_t>(addr) & 3)) return fail(DSV_EINVAL, "stream_write_u32: bad address");
+  const CUresult r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(addr), value,
+                        CU_STREAM_WRITE_VALUE_DEFAULT);
+  return r == CUDA_SUCCESS ? DSV_OK : fail(DSV_ECUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+}
+
+extern "C" int dsv_stream_wait_u32_geq(const void* addr, unsigned int value, void* stream) {
+  static WaitValueFn fn = driver_fn<WaitValueFn>("cuStreamWaitValue32");
+  if (!fn) return fail(DSV_EUNSUPPORTED, "stream_wait_u32: driver entry point missing");
+  if (!addr || (reinterpret_cast<uintptr_t>(addr) & 3)) return fail(DSV_EINVAL, "stream_wait_u32: bad address");
+  const CUresult r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(addr), value,
+                        CU_STREAM_WAIT_VALUE_GEQ);
+  return r == CUDA_SUCCESS ? DSV_OK : fail(DSV_ECUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+}
+
+extern "C" int dsv_copy_jobs_ce(const dsv_copy_job* jobs, int njobs, void* stream) {
+  if (njobs <= 0) return DSV_OK;
+  if (!jobs) return fail(DSV_EINVAL, "copy_jobs_ce: null job table");
+  for (int i = 0; i < njobs; ++i) {
+    const dsv_copy_job& j = jobs[i];
+    if (j.rows <= 0 || j.row_bytes <= 0) continue;
+    cudaError_t e;
+    if (j.rows == 1 || (j.src_stride == j.row_bytes && j.dst_stride == j.row_bytes)) {
+      e = cudaMemcpyAsync(reinterpret_cast<void*>(j.dst), reinterpret_cast<const void*>(j.src),
+                          (size_t)(j.rows * j.row_bytes), cudaMemcpyDeviceToDevice, S(stream));
+    } else {
+      e = cudaMemcpy2DAsync(reinterpret_cast<void*>(j.dst), (size_t)j.dst_stride,
+                            reinterpret_cast<const void*>(j.src), (size_t)j.src_stride,
+                            (size_t)j.row_bytes, (size_t)j.rows, cudaMemcpyDeviceToDevice, S(stream));
+    }
+    if (e != cudaSuccess) return cuda_status((int)e, "copy_jobs_ce");
+  }
+  return DSV_OK;
 }
 
 extern "C" int dsv_copy_jobs(const dsv_copy_job* jobs, int njobs, int splits, void* stream) {

@@ -208,6 +208,8 @@ int dsv_gemm_launch(const CUtensorMap* ta, const CUtensorMap* tb, const CUtensor
     return f32_out ? launch_gemm<256, 4, true>(ta, tb, nullptr, C, M, N, K, ldc, c_bs, nbatch, st)
                    : launch_gemm<256, 4, false>(ta, tb, nullptr, C, M, N, K, ldc, c_bs, nbatch, st);
   }
-  return f32_out ? launch_gemm<128, 4, true>(ta, tb, nullptr, C, M, N, K, ldc, c_bs, nbatch, st)
-                 : launch_gemm<128, 4, false>(ta, tb, nullptr, C, M, N, K, ldc, c_bs, nbatch, st);
+  // 128-wide tiles (narrow N, or few output tiles such as the projection of one rank's
+  // L/N tokens): 3 stages, two CTAs per SM
+  return f32_out ? launch_gemm<128, 3, true>(ta, tb, nullptr, C, M, N, K, ldc, c_bs, nbatch, st)
+                 : launch_gemm<128, 3, false>(ta, tb, nullptr, C, M, N, K, ldc, c_bs, nbatch, st);
 }
