@@ -22,7 +22,7 @@ def main(which):
     qlr = P[:, : r * H].reshape(L, H, r)
     klr = P[:, r * H:].reshape(L, H, r).permute(1, 0, 2).contiguous()
     qp = qlr[plan.proxies_tensor(dev).long()].permute(1, 0, 2).contiguous()
-    sc = ops.proxy_scores(qp, klr).reshape(H * G, L)
+    sc = ops.gemm_bf16(qp, klr, torch.float32).reshape(H * G, L)   # the layer's K1b path
     kp = torch.full((H,), k, dtype=torch.int32, device=dev)
     idx, _ = ops.topk_rows(sc, kp, G)
     idx = idx.reshape(H, G, k)
