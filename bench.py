@@ -35,6 +35,27 @@ GRID = (16, 40, 50)
 HEADS, HEAD_DIM, D_LR, VOXEL, SPARSITY = 24, 128, 16, (8, 4, 4), 0.9
 WORKLOAD = ("c2: one video-DiT attention block, L=32000 (16x40x50 latent), 24 heads, d=128, "
             "r=16 predictor, sparsity 0.9 (k=3200), voxel groups (8,4,4) -> 260 query tiles")
+# --workload: c2 is the headline (BASELINE.json configs[1]); c3 / c4 are the >= 128k-token
+# configurations the north_star's scaling target is quoted on
+WORKLOADS = {
+    "c2": {"grid": GRID, "heads": HEADS, "sparsity": SPARSITY, "desc": WORKLOAD},
+    "c3": {"grid": (32, 64, 64), "heads": 16, "sparsity": 0.9,
+           "desc": ("c3: 3B-scale video-DiT layer, L=131072 (32x64x64), 16 heads, d=128, r=16, "
+                    "sparsity 0.9 (k=13108), voxel groups (8,4,4) -> 1024 query tiles")},
+    "c4": {"grid": (32, 64, 64), "heads": 24, "sparsity": "sweep",
+           "desc": ("c4: L=131072 (32x64x64), 24 heads, d=128, r=16, per-head sparsity "
+                    "0.50..0.95 (shuffled, seed 0), sparsity-aware head re-balancing")},
+}
+
+
+def _sparsities(wl: dict, heads: int):
+    import numpy as np
+
+    if wl["sparsity"] == "sweep":   # s_h = 0.50 + 0.45 h / (H - 1), shuffled
+        s = 0.50 + 0.45 * np.arange(heads) / (heads - 1)
+        np.random.default_rng(0).shuffle(s)
+        return s
+    return wl["sparsity"]
 
 
 def _args():
@@ -46,6 +67,7 @@ def _args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=float(os.environ.get("DSV_CPU_BUDGET", 12)))
     ap.add_argument("--unbalanced", action="store_true", help="contiguous head split (no rebalance)")
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     return ap.parse_args()
 
 
@@ -166,15 +188,17 @@ def run_gpu(args) -> None:
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    grid = TokenGrid(*GRID)
-    L, H, D = grid.size, HEADS, HEAD_DIM
+    wl = WORKLOADS[args.workload]
+    grid = TokenGrid(*wl["grid"])
+    L, H, D = grid.size, wl["heads"], HEAD_DIM
+    sparsity = _sparsities(wl, H)
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
 
     def rnd(*shape):
         return torch.randn(shape, device=dev, generator=gen).to(torch.bfloat16)
 
     if world == 1:
-        layer = DSVAttentionLayer(grid, H, D, D_LR, VOXEL, SPARSITY, dev)
+        layer = DSVAttentionLayer(grid, H, D, D_LR, VOXEL, sparsity, dev)
         wt = layer.predictor_weights(seed=0)
         x, q, k, v, do = rnd(L, H * D), rnd(H, L, D), rnd(H, L, D), rnd(H, L, D), rnd(H, L, D)
         dk_acc = torch.zeros((H, L, D), device=dev, dtype=torch.float32)
@@ -197,7 +221,7 @@ def run_gpu(args) -> None:
     else:
         from paper_2502_07590_b200.cp import HeadParallelDSV
 
-        cp = HeadParallelDSV(grid, H, D, D_LR, VOXEL, SPARSITY, balanced=not args.unbalanced,
+        cp = HeadParallelDSV(grid, H, D, D_LR, VOXEL, sparsity, balanced=not args.unbalanced,
                              device=dev)
         layer = cp.local
         chunk = L // world
@@ -300,20 +324,27 @@ def run_gpu(args) -> None:
 
     peaks = _peaks()
     value = L / (ms / 1e3)
-    tot_flops = work["projection_flops"] + work["estimation_flops"] + work["fwd_flops"] + work["bwd_flops"]
-    if world > 1:
-        tot_flops *= H / layer.H
+    from paper_2502_07590_b200.selection import k_from_sparsity
+
+    all_ks = [k_from_sparsity(float(s_h), L) for s_h in np.broadcast_to(sparsity, (H,))]
+    G_all = layer.G
+    # whole-layer algorithmic work (all heads), whatever this rank holds
+    tot_flops = (2 * L * (H * D) * (2 * D_LR * H) + 2 * H * G_all * L * D_LR
+                 + 14 * L * sum(all_ks) * D)
     dense_eq = 4 * L * L * D * H * 3.5
     res = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic: N(0,1) X, Q, K, V, dO in bf16; random-init predictor W (N(0,1/sqrt(d)))",
-        "config": {"workload": WORKLOAD, "tokens": L, "heads": H, "head_dim": D, "d_lr": D_LR,
-                   "sparsity": SPARSITY, "k_per_group": layer.ks[0], "voxel": list(VOXEL),
+        "config": {"workload": wl["desc"], "tokens": L, "heads": H, "head_dim": D, "d_lr": D_LR,
+                   "sparsity": (SPARSITY if args.workload == "c2" else
+                                [round(float(x), 4) for x in np.broadcast_to(sparsity, (H,))]),
+                   "k_per_group": all_ks[0] if args.workload == "c2" else all_ks,
+                   "voxel": list(VOXEL),
                    "groups": layer.G, "parallelism": f"hcp{world}" if world > 1 else "single",
                    "head_plan": "balance_heads" if not args.unbalanced else "contiguous",
-                   "l2_note": "inputs (X, Q, K, V, dO: 0.98 GB) exceed the 126 MB L2"},
+                   "l2_note": f"inputs (X, Q, K, V, dO: {5 * L * H * D * 2 / 1e9:.2f} GB) exceed the 126 MB L2"},
         "effective_tflops": {"algorithmic": tot_flops / (ms / 1e3) / 1e12,
                              "dense_equivalent": dense_eq / (ms / 1e3) / 1e12},
         "gpu_launches": launches_per_step * args.steps,
@@ -338,7 +369,7 @@ def run_gpu(args) -> None:
         }
     if e2e is not None:
         res["e2e"] = e2e
-    if world == 1 and os.environ.get("DSV_CPU_BASELINE", "1") != "0":
+    if world == 1 and args.workload == "c2" and os.environ.get("DSV_CPU_BASELINE", "1") != "0":
         cb = cpu_oracle(args.cpu_budget)
         res["cpu_baseline"] = {"value": cb["tokens_per_s"], "unit": "tokens/s", "cores": _cores(),
                                "kind": "port", "sample": cb["sample"],

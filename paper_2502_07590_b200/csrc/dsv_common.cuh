@@ -119,6 +119,9 @@ DSV_DEV bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
   return ok != 0;
 }
+#ifndef DSV_SLEEP_NS
+#define DSV_SLEEP_NS 128
+#endif
 // Blocking wait. With DSV_WATCHDOG a wait that has not completed after ~4 s
 // (a pipeline bug) traps instead of hanging the GPU.
 DSV_DEV uint64_t globaltimer_ns() {
@@ -139,6 +142,23 @@ DSV_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(addr, parity)) {
   }
 #endif
+}
+// Wait with nanosleep back-off, for warps whose waits are not latency-critical (the
+// gather producers and scatter warps): a parked warp does not compete for issue slots
+// with the softmax / row-worker warps, which a spinning try_wait loop does.
+DSV_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  if (mbar_try_wait(addr, parity)) return;
+#ifdef DSV_WATCHDOG
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t n = 0;
+#endif
+  while (!mbar_try_wait(addr, parity)) {
+    __nanosleep(DSV_SLEEP_NS);
+#ifdef DSV_WATCHDOG
+    if ((++n & 255u) == 0 && globaltimer_ns() - t0 > 4000000000ull) __trap();
+#endif
+  }
 }
 
 // ----------------------------------------------------------------- TMA
