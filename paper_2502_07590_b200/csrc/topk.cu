@@ -25,7 +25,8 @@
 //      tie budget k - #(> T) lasts in index order (twopass_select's emit) —
 //      ascending output, no sort. Float compares give -0.0 == +0.0.
 // Rows whose T-bucket is too large (massive ties, non-finite ranges) fall back
-// to key-space refinement over the whole row and a counting pass.
+// to key-space refinement over the whole row and a counting pass. Rows too long for
+// shared memory go to the streaming kernel in topk_stream.cu.
 // HBM traffic per row = one read of the row + k*4 bytes of indices.
 
 #include "dsv_common.cuh"
@@ -553,6 +554,9 @@ size_t dsv_topk_smem_bytes(int L) {
   return need <= 227 * 1024 ? need : base;
 }
 
+int dsv_topk_stream_launch(const float*, long long, int, int, const int*, int, int*, long long,
+                           float*, cudaStream_t);
+
 int dsv_topk_launch(const float* scores, long long ld, int rows, int L, const int* k_per_head,
                     int rows_per_head, int* out_idx, long long out_ld, float* out_thr,
                     cudaStream_t stream) {
@@ -566,16 +570,12 @@ int dsv_topk_launch(const float* scores, long long ld, int rows, int L, const in
   const size_t base = sizeof(Smem) + mask;
   const size_t need = base + (size_t)L * 4;
   if (base > 227 * 1024) return (int)cudaErrorInvalidValue;
-  if (need <= 227 * 1024) {
-    cudaFuncSetAttribute(topk_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)need);
-    topk_rows_kernel<true><<<grid, kThreads, need, stream>>>(
-        scores, ld, rows, L, k_per_head, rows_per_head, out_idx, out_ld, out_thr);
-  } else {
-    cudaFuncSetAttribute(topk_rows_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)base);
-    topk_rows_kernel<false><<<grid, kThreads, base, stream>>>(
-        scores, ld, rows, L, k_per_head, rows_per_head, out_idx, out_ld, out_thr);
-  }
+  if (need > 227 * 1024)   // the row does not fit in shared memory: streaming kernel
+    return dsv_topk_stream_launch(scores, ld, rows, L, k_per_head, rows_per_head, out_idx, out_ld,
+                                  out_thr, stream);
+  cudaFuncSetAttribute(topk_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)need);
+  topk_rows_kernel<true><<<grid, kThreads, need, stream>>>(
+      scores, ld, rows, L, k_per_head, rows_per_head, out_idx, out_ld, out_thr);
   return (int)cudaGetLastError();
 }

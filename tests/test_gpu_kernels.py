@@ -61,6 +61,23 @@ def test_topk_global_path(cuda):
     _check_topk(scores, [7000, 1], 2, cuda)
 
 
+@pytest.mark.parametrize("L,ks", [(131072, [13108, 65536, 1, 131071]), (100003, [10001, 3])])
+def test_topk_streaming_long_rows(cuda, L, ks):
+    # rows beyond the shared-memory budget: two-pass streaming kernel (topk_stream.cu)
+    rng = np.random.default_rng(L)
+    scores = (rng.standard_normal((2 * len(ks), L)) * rng.uniform(0.1, 10, size=(2 * len(ks), 1))).astype(np.float32)
+    _check_topk(scores, ks, 2, cuda)
+
+
+def test_topk_streaming_ties_zero_inf(cuda):
+    rng = np.random.default_rng(9)
+    L = 90000
+    ints = rng.integers(-3, 4, size=(4, L)).astype(np.float32)
+    vals = np.array([-0.0, 0.0, 1.0, -1.0, np.inf, -np.inf, 0.5], dtype=np.float32)
+    special = vals[rng.integers(0, vals.size, size=(4, L))]
+    _check_topk(np.concatenate([ints, special]), [1, 9000, 45000, 89999], 2, cuda)
+
+
 def test_topk_ties_integer_scores(cuda):
     rng = np.random.default_rng(1)
     L = 5000
