@@ -30,7 +30,8 @@ import torch.distributed as dist
 from . import cpmodel
 
 PHASES = ("hcp_fwd", "scp_index_exchange", "scp_kv", "output_redistribute", "hcp_bwd_in",
-          "hcp_bwd_out")
+          "hcp_bwd_out", "scp_grad")   # scp_grad: dK/dV of gathered rows back to their owners
+                                       # (the reference simulator is forward-only)
 
 
 @dataclass
@@ -522,6 +523,178 @@ def plan_heads(sparsities, seq_len: int, head_dim: int, world: int, balanced: bo
         return cpmodel.contiguous_heads(len(sparsities), world).assignment
     loads = cpmodel.head_loads(sparsities, seq_len, head_dim)
     return cpmodel.balance_heads(loads, world).assignment
+
+
+class HybridExchange:
+    """Hybrid head x selective-sequence CP: g_h-way HCP inside each of g_s SCP groups
+    (cpsim.py:125-161), then selective KV gathering between the g_s ranks that hold the
+    same heads (cpsim.py:164-216), and the output redistribution (cpsim.py:284-299).
+
+    Rank layout and placements follow `cpmodel.rank_layout` ("hcp-first": the g_h ranks
+    of a group are consecutive, "scp-first": strided). Every rank calls the constructor
+    (it creates the sub-groups collectively). Requests are per head: a rank asks the
+    peer holding span(g') for the union of the key rows its span's queries selected
+    inside span(g'), and the peer serves exactly those rows; the ledger records the
+    reference's byte model (8 B per head list + 4 B per index, 2 x D x width per row).
+    """
+
+    def __init__(self, n_heads: int, seq_len: int, assignment, g_h: int, g_s: int,
+                 placement: str = "hcp-first", group=None):
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if g_h * g_s != self.world:
+            raise ValueError("g_h * g_s must equal the number of ranks")
+        if seq_len % self.world:
+            raise ValueError("sequence length must divide the rank count")
+        self.H, self.L, self.g_h, self.g_s = int(n_heads), int(seq_len), int(g_h), int(g_s)
+        self.chunk = self.L // self.world
+        self.layout = cpmodel.rank_layout(self.world, g_h, g_s, placement)
+        self.pos, self.grp = self.layout[self.rank]
+        self.assignment = np.asarray(assignment, dtype=np.int64)
+        if self.assignment.shape != (self.H,) or self.assignment.min() < 0 or self.assignment.max() >= g_h:
+            raise ValueError("assignment must map every head to a position in [0, g_h)")
+        self.heads = np.nonzero(self.assignment == self.pos)[0]
+        ranks_of_group = [sorted(r for r in range(self.world) if self.layout[r][1] == g) for g in range(g_s)]
+        ranks_at_pos = [sorted(r for r in range(self.world) if self.layout[r][0] == p) for p in range(g_h)]
+        glob = (lambda rs: rs) if group is None else (lambda rs: [dist.get_global_rank(group, r) for r in rs])
+        hcp_groups = [dist.new_group(glob(rs)) for rs in ranks_of_group]
+        scp_groups = [dist.new_group(glob(rs)) for rs in ranks_at_pos]
+        self.hcp_group, self.scp_group = hcp_groups[self.grp], scp_groups[self.pos]
+        self.spans = [np.sort(np.concatenate([np.arange(r * self.chunk, (r + 1) * self.chunk)
+                                              for r in rs])) for rs in ranks_of_group]
+        self.span = self.spans[self.grp]
+        self.span_len = self.span.size
+        self.span_of = np.empty(self.L, dtype=np.int64)       # global row -> SCP group
+        self.local_at = np.empty(self.L, dtype=np.int64)      # global row -> index in its span
+        for g, sp in enumerate(self.spans):
+            self.span_of[sp] = g
+            self.local_at[sp] = np.arange(sp.size)
+        self.hcp = HeadParallelExchange(self.H, self.span_len, self.assignment, self.hcp_group)
+        self.ledger = self.hcp.ledger                           # one ledger for all phases
+
+    # ------------------------------------------------------------------ requests
+    def requests_from_sets(self, sets):
+        """sets: per head (global id) a list over the global queries of index arrays.
+        Returns {peer group: [sorted unique int64 rows of span(peer), per local head]}."""
+        req = {}
+        for g in range(self.g_s):
+            if g == self.grp:
+                continue
+            per_head = []
+            for h in self.heads:
+                need = np.unique(np.concatenate([np.asarray(sets[h][q], dtype=np.int64)
+                                                 for q in self.span] or [np.zeros(0, np.int64)]))
+                per_head.append(need[self.span_of[need] == g])
+            req[g] = per_head
+        return req
+
+    def requests_from_idx(self, idx, counts):
+        """GPU form: idx int32 [heads, groups, k_max] of global key rows (group r of head h
+        valid up to counts[h, r]); same result as requests_from_sets."""
+        hp = idx.shape[0]
+        mark = torch.zeros((hp, self.L), dtype=torch.bool, device=idx.device)
+        kmax = idx.shape[2]
+        valid = torch.arange(kmax, device=idx.device)[None, None, :] < counts[:, :, None]
+        for h in range(hp):
+            rows = idx[h][valid[h]].long()
+            mark[h, rows] = True
+        span_of = torch.from_numpy(self.span_of).to(idx.device)
+        req = {}
+        for g in range(self.g_s):
+            if g == self.grp:
+                continue
+            sel = mark & (span_of == g)[None, :]
+            req[g] = [torch.nonzero(sel[h]).flatten().cpu().numpy() for h in range(hp)]
+        return req
+
+    # ------------------------------------------------------------------ exchanges
+    def _a2a(self, send_parts, dtype, device, width):
+        """all-to-all over the SCP group: send_parts[g] = tensor [n_g, width] to group g."""
+        g_s = self.g_s
+        cnt = torch.tensor([p.shape[0] for p in send_parts], dtype=torch.int64, device=device)
+        rcnt = torch.empty_like(cnt)
+        dist.all_to_all_single(rcnt, cnt, group=self.scp_group)
+        rc = [int(x) for x in rcnt.cpu()]
+        send = torch.cat([p.reshape(-1, width).to(dtype) for p in send_parts]) if sum(
+            p.shape[0] for p in send_parts) else torch.zeros((0, width), dtype=dtype, device=device)
+        recv = torch.empty((sum(rc), width), dtype=dtype, device=device)
+        dist.all_to_all_single(recv, send, rc, [p.shape[0] for p in send_parts], group=self.scp_group)
+        return list(torch.split(recv, rc)), rc
+
+    def fetch_kv(self, k_span, v_span, req):
+        """k_span, v_span [heads, span_len, D] (this rank's heads over its span).
+        req: {peer group: [rows per head]} -> {peer group: (K rows, V rows) per head}."""
+        dev, D = k_span.device, k_span.shape[2]
+        hp = len(self.heads)
+        # 1. requested row lists (per head counts + ids) -> owners
+        ids_parts, cnt_parts = [], []
+        for g in range(self.g_s):
+            per_head = req.get(g, [np.zeros(0, np.int64)] * hp)
+            cnt_parts.append(torch.tensor([len(r) for r in per_head], dtype=torch.int64, device=dev)[:, None])
+            ids_parts.append(torch.from_numpy(np.concatenate(per_head).astype(np.int64)
+                                              if hp else np.zeros(0, np.int64)).to(dev)[:, None])
+            if g != self.grp:
+                n_idx = sum(len(r) for r in per_head)
+                self.ledger.add("scp_index_exchange", 8 * hp + 4 * n_idx, 0)
+        got_cnt, _ = self._a2a(cnt_parts, torch.int64, dev, 1)
+        got_ids, _ = self._a2a(ids_parts, torch.int64, dev, 1)
+        for g in range(self.g_s):
+            if g != self.grp:
+                self.ledger.add("scp_index_exchange", 0, 8 * hp + 4 * got_ids[g].shape[0])
+        # 2. owners serve the rows: [K | V] per requested row, in request order
+        local_at = torch.from_numpy(self.local_at).to(dev)
+        serve, self._served = [], []
+        for g in range(self.g_s):
+            counts = [int(c) for c in got_cnt[g].flatten().cpu()]
+            ids = got_ids[g].flatten()
+            parts, o = [], 0
+            for hi, c in enumerate(counts):
+                at = local_at[ids[o:o + c]]
+                parts.append(torch.cat([k_span[hi, at], v_span[hi, at]], dim=1))
+                o += c
+            self._served.append((counts, ids))
+            rows = torch.cat(parts) if parts else torch.zeros((0, 2 * D), dtype=k_span.dtype, device=dev)
+            serve.append(rows)
+            if g != self.grp:
+                self.ledger.add("scp_kv", rows.shape[0] * 2 * D * k_span.element_size(), 0)
+        got_rows, _ = self._a2a(serve, k_span.dtype, dev, 2 * D)
+        out = {}
+        for g in range(self.g_s):
+            if g == self.grp:
+                continue
+            per_head = req.get(g, [np.zeros(0, np.int64)] * hp)
+            splits = [len(r) for r in per_head]
+            rows = got_rows[g]
+            self.ledger.add("scp_kv", 0, rows.shape[0] * 2 * D * k_span.element_size())
+            out[g] = [(r[:, :D], r[:, D:]) for r in torch.split(rows, splits)]
+        return out
+
+    def return_grads(self, dk_rows, dv_rows, dk_span, dv_span):
+        """Backward of fetch_kv: dk_rows/dv_rows {peer group: [rows grads per head]} (fp32)
+        are sent to the owners, which add them into dk_span/dv_span [heads, span_len, D]."""
+        dev, D = dk_span.device, dk_span.shape[2]
+        hp = len(self.heads)
+        parts = []
+        for g in range(self.g_s):
+            if g == self.grp or g not in dk_rows:
+                parts.append(torch.zeros((0, 2 * D), dtype=dk_span.dtype, device=dev))
+                continue
+            parts.append(torch.cat([torch.cat([a, b], dim=1) for a, b in zip(dk_rows[g], dv_rows[g])])
+                         if hp else torch.zeros((0, 2 * D), dtype=dk_span.dtype, device=dev))
+            self.ledger.add("scp_grad", parts[-1].shape[0] * 2 * D * dk_span.element_size(), 0)
+        got, _ = self._a2a(parts, dk_span.dtype, dev, 2 * D)
+        local_at = torch.from_numpy(self.local_at).to(dev)
+        for g in range(self.g_s):
+            if g == self.grp:
+                continue
+            counts, ids = self._served[g]
+            rows, o = got[g], 0
+            self.ledger.add("scp_grad", 0, rows.shape[0] * 2 * D * dk_span.element_size())
+            for hi, c in enumerate(counts):
+                at = local_at[ids[o:o + c]]
+                dk_span[hi].index_add_(0, at, rows[o:o + c, :D])
+                dv_span[hi].index_add_(0, at, rows[o:o + c, D:])
+                o += c
 
 
 class HeadParallelDSV:
