@@ -68,6 +68,8 @@ def _args():
     ap.add_argument("--cpu-budget", type=float, default=float(os.environ.get("DSV_CPU_BUDGET", 12)))
     ap.add_argument("--unbalanced", action="store_true", help="contiguous head split (no rebalance)")
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--scp", type=int, default=1,
+                    help="g_s > 1: hybrid CP, N/g_s head groups x g_s selective-sequence groups")
     return ap.parse_args()
 
 
@@ -179,6 +181,7 @@ def run_gpu(args) -> None:
 
     from paper_2502_07590_b200 import ops
     from paper_2502_07590_b200.grid import TokenGrid
+    from paper_2502_07590_b200.grouping import build_groups
     from paper_2502_07590_b200.layer import DSVAttentionLayer
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -219,10 +222,14 @@ def run_gpu(args) -> None:
         launches_per_step = 8   # project, gather, scores gemm, topk, fwd, bwd, 2x f32->bf16
         work = layer.work()
     else:
-        from paper_2502_07590_b200.cp import HeadParallelDSV
+        from paper_2502_07590_b200.cp import HeadParallelDSV, HybridDSV
 
-        cp = HeadParallelDSV(grid, H, D, D_LR, VOXEL, sparsity, balanced=not args.unbalanced,
-                             device=dev)
+        if args.scp > 1:
+            cp = HybridDSV(grid, H, D, D_LR, VOXEL, sparsity, world // args.scp, args.scp,
+                           balanced=not args.unbalanced, device=dev)
+        else:
+            cp = HeadParallelDSV(grid, H, D, D_LR, VOXEL, sparsity, balanced=not args.unbalanced,
+                                 device=dev)
         layer = cp.local
         chunk = L // world
         g0 = torch.Generator(device="cpu").manual_seed(0)
@@ -327,7 +334,7 @@ def run_gpu(args) -> None:
     from paper_2502_07590_b200.selection import k_from_sparsity
 
     all_ks = [k_from_sparsity(float(s_h), L) for s_h in np.broadcast_to(sparsity, (H,))]
-    G_all = layer.G
+    G_all = len(build_groups(grid, VOXEL).members)
     # whole-layer algorithmic work (all heads), whatever this rank holds
     tot_flops = (2 * L * (H * D) * (2 * D_LR * H) + 2 * H * G_all * L * D_LR
                  + 14 * L * sum(all_ks) * D)
@@ -342,7 +349,9 @@ def run_gpu(args) -> None:
                                 [round(float(x), 4) for x in np.broadcast_to(sparsity, (H,))]),
                    "k_per_group": all_ks[0] if args.workload == "c2" else all_ks,
                    "voxel": list(VOXEL),
-                   "groups": layer.G, "parallelism": f"hcp{world}" if world > 1 else "single",
+                   "groups": layer.G if world == 1 else len(build_groups(grid, VOXEL).members),
+                   "parallelism": ("single" if world == 1 else f"hcp{world}" if args.scp == 1
+                                   else f"hcp{world // args.scp}xscp{args.scp}"),
                    "head_plan": "balance_heads" if not args.unbalanced else "contiguous",
                    "l2_note": f"inputs (X, Q, K, V, dO: {5 * L * H * D * 2 / 1e9:.2f} GB) exceed the 126 MB L2"},
         "effective_tflops": {"algorithmic": tot_flops / (ms / 1e3) / 1e12,

@@ -697,7 +697,25 @@ class HybridExchange:
                 o += c
 
 
-class HeadParallelDSV:
+class _PhaseMarks:
+    """Optional per-phase CUDA events on the compute stream (bench.py stage_ms)."""
+
+    marks = None   # set to [] to record (name, cuda event) after each phase
+
+    def _mark(self, name):
+        if self.marks is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self.marks.append((name, ev))
+
+    def phase_ms(self):
+        """Per-phase device time of the last step recorded with marks=[]."""
+        torch.cuda.synchronize()
+        m = self.marks or []
+        return {b[0]: a[1].elapsed_time(b[1]) for a, b in zip(m, m[1:])}
+
+
+class HeadParallelDSV(_PhaseMarks):
     """The DSV layer under HCP: sequence-sharded in, sequence-sharded out."""
 
     def __init__(self, grid, heads: int, head_dim: int, d_lr: int = 16, voxel=(8, 4, 4),
@@ -721,19 +739,6 @@ class HeadParallelDSV:
         self.H, self.D, self.r = heads, head_dim, d_lr
         mine = self.ex.my_heads
         self.local = DSVAttentionLayer(grid, len(mine), head_dim, d_lr, voxel, sp[mine], device)
-        self.marks = None   # set to [] to record (name, cuda event) after each phase
-
-    def _mark(self, name):
-        if self.marks is not None:
-            ev = torch.cuda.Event(enable_timing=True)
-            ev.record()
-            self.marks.append((name, ev))
-
-    def phase_ms(self):
-        """Per-phase device time of the last step recorded with marks=[]."""
-        torch.cuda.synchronize()
-        m = self.marks or []
-        return {b[0]: a[1].elapsed_time(b[1]) for a, b in zip(m, m[1:])}
 
     def step(self, x_local, wt, q, k, v, dout):
         """x_local [L/N, H*D]; q, k, v, dout [H, L/N, D] -> (out, dq, dk, dv) [H, L/N, D].
@@ -816,5 +821,107 @@ class HeadParallelDSV:
         dq, dk, dv = loc.backward(ql, kl, vl, out, lse, dout_m, sel)
         self._mark("bwd")
         res = self.ex.to_tokens(out, dq, dk, dv)
+        self._mark("exchange_out")
+        return res
+
+
+class HybridDSV(_PhaseMarks):
+    """The DSV layer under hybrid CP (g_h x g_s, "hcp-first" placement).
+
+    Each rank holds L/N tokens of all heads. Inside its SCP group (g_h consecutive
+    ranks spanning L/g_s contiguous tokens) the inputs are resharded to the heads its
+    position owns (packed all-to-all); K_lr is all-gathered between the g_s ranks with
+    the same heads (r = 16 columns: the selection sees every key, as on one GPU); the
+    voxel groups of the span are selected and their remote critical K/V rows gathered
+    selectively (HybridExchange.fetch_kv); the attention runs on full-length buffers
+    addressed by global token; the gradients of gathered rows go back to their owners
+    and the outputs back to the token owners. The span must align with the voxel
+    groups (L/g_s tokens = whole frames, a multiple of the voxel depth).
+    """
+
+    def __init__(self, grid, heads: int, head_dim: int, d_lr: int, voxel, sparsity, g_h: int,
+                 g_s: int, balanced: bool = True, group=None, device="cuda"):
+        from .grouping import build_groups
+        from .layer import DSVAttentionLayer
+
+        self.H, self.D, self.r, self.L = heads, head_dim, d_lr, grid.size
+        sp = np.broadcast_to(np.asarray(sparsity, dtype=np.float64), (heads,)).copy()
+        self.assignment = plan_heads(sp, self.L, head_dim, g_h, balanced)
+        self.ex = HybridExchange(heads, self.L, self.assignment, g_h, g_s, "hcp-first", group)
+        span = self.ex.span
+        self.s0, self.span_len = int(span[0]), int(span.size)
+        if not np.array_equal(span, np.arange(self.s0, self.s0 + self.span_len)):
+            raise ValueError("hybrid layer needs contiguous spans (hcp-first placement)")
+        plan = build_groups(grid, voxel)
+        inside = [i for i, m in enumerate(plan.members)
+                  if m.min() >= self.s0 and m.max() < self.s0 + self.span_len]
+        n_in = sum(plan.members[i].size for i in inside)
+        if n_in != self.span_len:
+            raise ValueError("the sequence span of an SCP group must hold whole voxel groups "
+                             "(L / g_s tokens = a multiple of the voxel depth in frames)")
+        self.heads = self.ex.heads
+        self.local = DSVAttentionLayer(grid, len(self.heads), head_dim, d_lr, voxel,
+                                       sp[self.heads], device, groups=inside)
+        self.device = torch.device(device)
+
+    def step(self, x_local, wt, q, k, v, dout):
+        """x_local [L/N, H*D]; q, k, v, dout [H, L/N, D] -> (out, dq, dk, dv) [H, L/N, D]."""
+        from . import ops
+
+        ex, hx = self.ex, self.ex.hcp
+        H, r, D, L = self.H, self.r, self.D, self.L
+        hp, dev = len(self.heads), q.device
+        chunk = hx.chunk
+        sl = slice(self.s0, self.s0 + self.span_len)
+        self._mark("start")
+        p = ops.project(x_local, wt)                                    # [L/N, 2 H r]
+        self._mark("project")
+        hm = hx.send_rows_headmajor(dev)
+        p_rows = p.view(chunk * 2 * H, r)
+        h = hx.finish(hx.to_heads_packed(
+            [(t.reshape(H * chunk, D), hm) for t in (q, k, v, dout)]
+            + [(p_rows, hx.send_rows_lowrank(0, dev)), (p_rows, hx.send_rows_lowrank(1, dev))],
+            "hcp_fwd"))
+        ql, kl, vl, dol, qlr, klr = h
+        full = lambda t: torch.empty((hp, L, t.shape[2]), dtype=t.dtype, device=dev)
+        Qf, Kf, Vf, dOf, Qlr = full(ql), full(kl), full(vl), full(dol), full(qlr)
+        for dst, src in ((Qf, ql), (Kf, kl), (Vf, vl), (dOf, dol), (Qlr, qlr)):
+            dst[:, sl] = src
+        # every key's K_lr for the selection: all-gather over the ranks holding these heads
+        parts = [torch.empty_like(klr) for _ in range(ex.g_s)]
+        dist.all_gather(parts, klr.contiguous(), group=ex.scp_group)
+        Klr = torch.cat([pp[:, None] for pp in parts], dim=1).reshape(hp, L, r)
+        self._mark("exchange_in")
+        sel = self.local.select_from_lowrank(Qlr, Klr)
+        self._mark("select")
+        counts = sel.kcount[:, None].expand(hp, self.local.G)
+        req = ex.requests_from_idx(sel.idx, counts)
+        remote = ex.fetch_kv(kl, vl, req)
+        for g, per_head in remote.items():
+            for hi, (kr, vr) in enumerate(per_head):
+                rows = torch.from_numpy(req[g][hi]).to(dev)
+                Kf[hi, rows] = kr
+                Vf[hi, rows] = vr
+        self._mark("scp_fetch")
+        out, lse = self.local.forward(Qf, Kf, Vf, sel)
+        self._mark("fwd")
+        dk32 = torch.zeros((hp, L, D), dtype=torch.float32, device=dev)
+        dv32 = torch.zeros_like(dk32)
+        dq, dk32, dv32 = ops.sparse_bwd(Qf, Kf, Vf, out, dOf, lse, self.local.grp_rows,
+                                        self.local.grp_size, sel.idx, sel.kcount,
+                                        self.local.scale, dk32, dv32)
+        self._mark("bwd")
+        dk_rows = {g: [dk32[hi, torch.from_numpy(r).to(dev)] for hi, r in enumerate(per)]
+                   for g, per in req.items()}
+        dv_rows = {g: [dv32[hi, torch.from_numpy(r).to(dev)] for hi, r in enumerate(per)]
+                   for g, per in req.items()}
+        dk_span, dv_span = dk32[:, sl], dv32[:, sl]
+        ex.return_grads(dk_rows, dv_rows, dk_span, dv_span)
+        dk = ops.f32_to_bf16(dk_span.contiguous())
+        dv = ops.f32_to_bf16(dv_span.contiguous())
+        self._mark("scp_grad")
+        h_o = hx.to_tokens_packed([out[:, sl].contiguous()], "output_redistribute")
+        grads = hx.finish(hx.to_tokens_packed([dq[:, sl].contiguous(), dk, dv], "hcp_bwd_out"))
+        res = (hx.finish(h_o)[0], *grads)
         self._mark("exchange_out")
         return res

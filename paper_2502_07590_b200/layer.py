@@ -43,7 +43,9 @@ class DSVAttentionLayer:
     """Predictor + selection + sparse attention for one layer, device resident."""
 
     def __init__(self, grid: TokenGrid, heads: int, head_dim: int, d_lr: int = 16,
-                 voxel=(8, 4, 4), sparsity=0.9, device="cuda"):
+                 voxel=(8, 4, 4), sparsity=0.9, device="cuda", groups=None):
+        """groups: optional subset of the plan's voxel groups this layer serves (a
+        sequence shard under hybrid CP); queries/keys stay addressed by global token."""
         self.grid = grid
         self.H = int(heads)
         self.D = int(head_dim)
@@ -57,11 +59,18 @@ class DSVAttentionLayer:
         self.k_max = max(self.ks)
         self.grp_rows, self.grp_size = self.plan.tables(self.device)
         self.proxies = self.plan.proxies_tensor(self.device)
+        self._G = self.plan.n_groups
+        if groups is not None:
+            sel = torch.as_tensor(np.asarray(groups, dtype=np.int64), device=self.device)
+            self.grp_rows = self.grp_rows[sel].contiguous()
+            self.grp_size = self.grp_size[sel].contiguous()
+            self.proxies = self.proxies[sel].contiguous()
+            self._G = int(sel.numel())
         self.scale = 1.0 / math.sqrt(self.D)
 
     @property
     def G(self) -> int:
-        return self.plan.n_groups
+        return self._G
 
     # ------------------------------------------------------------- predictor
     def predictor_weights(self, seed: int = 0) -> torch.Tensor:
@@ -126,8 +135,9 @@ class DSVAttentionLayer:
 
     # ------------------------------------------------------------- accounting
     def pairs(self) -> int:
-        """(query, key) pairs scored per pass: sum_h L * k_h."""
-        return sum(self.L * kh for kh in self.ks)
+        """(query, key) pairs scored per pass: sum over this layer's query groups and heads."""
+        nq = int(self.grp_size.sum().item()) if self._G != self.plan.n_groups else self.L
+        return sum(nq * kh for kh in self.ks)
 
     def work(self) -> dict:
         """Algorithmic work per layer pass."""

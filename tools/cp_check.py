@@ -1,6 +1,7 @@
 """HCP on N GPUs vs the single-GPU layer on the same inputs (torchrun, NCCL).
 
-usage: torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/cp_check.py [--skewed]
+usage: torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/cp_check.py [--skewed] [--hybrid]
+(--hybrid: g_h = N/2 head groups x g_s = 2 selective-sequence groups, HybridDSV)
 Every rank builds the same global inputs (seeded), keeps its L/N token chunk, runs
 HeadParallelDSV.step; the chunks of O, dQ, dK, dV are gathered and compared with
 DSVAttentionLayer.step on rank 0, and the exchange ledger with hcp_comm.
@@ -16,7 +17,7 @@ import torch.distributed as dist
 
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
 from paper_2502_07590_b200 import cpmodel  # noqa: E402
-from paper_2502_07590_b200.cp import HeadParallelDSV  # noqa: E402
+from paper_2502_07590_b200.cp import HeadParallelDSV, HybridDSV  # noqa: E402
 from paper_2502_07590_b200.grid import TokenGrid  # noqa: E402
 from paper_2502_07590_b200.layer import DSVAttentionLayer  # noqa: E402
 
@@ -26,7 +27,8 @@ def main():
     dev = torch.device("cuda", int(os.environ["LOCAL_RANK"]))
     torch.cuda.set_device(dev)
     dist.init_process_group("nccl", device_id=dev)
-    grid = TokenGrid(8, 16, 16)
+    hybrid = "--hybrid" in sys.argv
+    grid = TokenGrid(16, 16, 16) if hybrid else TokenGrid(8, 16, 16)
     H, D, r = 8, 128, 16
     L = grid.size
     sp = np.linspace(0.5, 0.95, H) if "--skewed" in sys.argv else np.full(H, 0.9)
@@ -36,7 +38,10 @@ def main():
     wt = (torch.randn((2 * H * r, H * D), generator=g) / math.sqrt(H * D)).to(torch.bfloat16).to(dev)
     chunk = L // world
     sl = slice(rank * chunk, (rank + 1) * chunk)
-    cp = HeadParallelDSV(grid, H, D, r, (8, 4, 4), sp, balanced=True, device=dev)
+    if hybrid:
+        cp = HybridDSV(grid, H, D, r, (8, 4, 4), sp, world // 2, 2, balanced=True, device=dev)
+    else:
+        cp = HeadParallelDSV(grid, H, D, r, (8, 4, 4), sp, balanced=True, device=dev)
     outs = cp.step(x[sl].contiguous(), wt, *(t[:, sl].contiguous() for t in (q, k, v, do)))
     gathered = []
     for t in outs:
@@ -53,10 +58,13 @@ def main():
             ok &= rel < 1e-2
         print("assignment", cp.assignment.tolist())
     led = cp.ex.ledger
-    got = max(led.sent["hcp_fwd"], led.received["hcp_fwd"])
-    # one packed exchange of Q|K|V|Q_lr|K_lr: 3 D + 2 r columns per token
-    expect_qkv = cpmodel.hcp_comm(H, len(cp.ex.my_heads), L, D, world, 2) * 3 / 4 * (3 * D + 2 * r) / (3 * D)
-    print(f"rank {rank}: hcp_fwd bytes {got} (closed form for the packed payload {expect_qkv:.0f})")
+    if hybrid:
+        print(f"rank {rank}: ledger sent {led.sent} received {led.received}")
+    else:
+        got = max(led.sent["hcp_fwd"], led.received["hcp_fwd"])
+        # one packed exchange of Q|K|V|Q_lr|K_lr: 3 D + 2 r columns per token
+        expect_qkv = cpmodel.hcp_comm(H, len(cp.ex.my_heads), L, D, world, 2) * 3 / 4 * (3 * D + 2 * r) / (3 * D)
+        print(f"rank {rank}: hcp_fwd bytes {got} (closed form for the packed payload {expect_qkv:.0f})")
     ok_t = torch.tensor([int(ok)], device=dev)
     dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
     dist.destroy_process_group()
