@@ -19,6 +19,8 @@
  *   dsv_sparse_bwd       trainer.py:110-117    autograd of the sparse attention (dQ, dK, dV)
  *   dsv_rows_fwd/_bwd    attention.py:176-183  ragged per-query index sets (CSR)
  *   dsv_gather_rows      cpsim.py:147-156/195-216 pack/unpack of head slices and KV rows
+ *   dsv_critical_counts  profiler.py:48-79 + attention.py:118-140 (sampled sparsity profiler:
+ *                        critical-KV prefix length per scored row)
  *   dsv_copy_jobs        cpsim.py:147-156/284-299 HCP head exchange written straight into
  *                        the owners' buffers (peer pointers over NVLink)
  */
@@ -116,6 +118,13 @@ int dsv_rows_bwd(const void* q, const void* k, const void* v, const float* out, 
 /* out[i] = src[rows[i]] for n rows of row_bytes bytes (row strides in bytes, multiples of 4). */
 int dsv_gather_rows(const void* src, long long src_stride, const int* rows, int n,
                     int row_bytes, void* out, long long out_stride, void* stream);
+
+/* Critical-KV mass counts (profiler.py:48-79, attention.py:118-140): for each row of fp32
+ * raw scores x (q . k, unscaled), p = softmax(x / sqrt_d) in fp64, and out[row] = the
+ * length of the shortest descending-p prefix (ties toward the lower index) whose mass
+ * reaches min(theta, sum p) - 1e-9. theta in (0, 1]. */
+int dsv_critical_counts(const float* scores, long long ld, int rows, int L, double sqrt_d,
+                        double theta, int* out, void* stream);
 
 /* One strided copy: `rows` rows of `row_bytes` bytes from src (+src_stride per row) to
  * dst (+dst_stride per row). Six int64 fields, so a [njobs, 6] int64 device array is a

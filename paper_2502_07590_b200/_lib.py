@@ -48,6 +48,8 @@ SIGNATURES = {
                      c_void_p, c_void_p],
     "dsv_debug_timeline": [c_void_p, c_int],
     "dsv_copy_jobs": [c_void_p, c_int, c_int, c_void_p],
+    "dsv_critical_counts": [c_void_p, c_longlong, c_int, c_int, ctypes.c_double, ctypes.c_double,
+                            c_void_p, c_void_p],
     "dsv_copy_jobs_ce": [c_void_p, c_int, c_void_p],
     "dsv_stream_write_u32": [c_void_p, ctypes.c_uint, c_void_p],
     "dsv_stream_wait_u32_geq": [c_void_p, ctypes.c_uint, c_void_p],

@@ -23,6 +23,7 @@ int dsv_rows_fwd_launch(const void*, const void*, const void*, const long long*,
 int dsv_rows_bwd_launch(const void*, const void*, const void*, const float*, const float*,
                         const void*, const long long*, const int*, int, int, int, int, float, int,
                         float*, float*, float*, cudaStream_t);
+int dsv_critical_counts_launch(const float*, long long, int, int, double, double, int*, cudaStream_t);
 int dsv_gemm_launch(const CUtensorMap*, const CUtensorMap*, const CUtensorMap*, void*, int, int, int, long long,
                     long long, int, int, int, cudaStream_t);
 int dsv_attn_fwd_tc_launch(const void*, const void*, const void*, const int*, const int*,
@@ -317,6 +318,15 @@ int dsv_debug_timeline_copy(void* dst, int bytes);
 extern "C" int dsv_debug_timeline(void* host_dst, int bytes) {
   if (!host_dst || bytes <= 0) return fail(DSV_EINVAL, "debug_timeline: bad buffer");
   return dsv_debug_timeline_copy(host_dst, bytes);
+}
+
+extern "C" int dsv_critical_counts(const float* scores, long long ld, int rows, int L,
+                                   double sqrt_d, double theta, int* out, void* stream) {
+  if (rows < 0 || L < 1 || ld < L) return fail(DSV_EINVAL, "critical_counts: bad shape");
+  if (!(theta > 0.0 && theta <= 1.0)) return fail(DSV_EINVAL, "critical_counts: theta must lie in (0, 1]");
+  if (!(sqrt_d > 0.0)) return fail(DSV_EINVAL, "critical_counts: sqrt_d must be positive");
+  return cuda_status(dsv_critical_counts_launch(scores, ld, rows, L, sqrt_d, theta, out, S(stream)),
+                     "critical_counts launch");
 }
 
 extern "C" int dsv_stream_write_u32(void* addr, unsigned int value, void* stream) {

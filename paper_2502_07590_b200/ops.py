@@ -215,6 +215,17 @@ def gather_rows(src: torch.Tensor, rows: torch.Tensor, out: torch.Tensor | None 
     return out
 
 
+def critical_counts(scores: torch.Tensor, sqrt_d: float, theta: float) -> torch.Tensor:
+    """Critical-KV prefix length per row of raw fp32 scores [R, L] (dsv_critical_counts)."""
+    _require_cuda(scores)
+    if scores.dtype != torch.float32 or scores.dim() != 2 or scores.stride(1) != 1:
+        raise ValueError("critical_counts: scores must be a row-major fp32 matrix")
+    out = torch.empty((scores.shape[0],), dtype=torch.int32, device=scores.device)
+    _lib.call("dsv_critical_counts", _ptr(scores), scores.stride(0), scores.shape[0], scores.shape[1],
+              float(sqrt_d), float(theta), _ptr(out), _stream())
+    return out
+
+
 def copy_jobs(jobs: torch.Tensor, splits: int = 16) -> None:
     """Run a [njobs, 6] int64 device job table (src, dst, src_stride, dst_stride, rows,
     row_bytes) in one launch (dsv_copy_jobs); addresses may be NVLink peer pointers."""

@@ -72,6 +72,11 @@ def main():
     dv = torch.zeros_like(dk)
     t = timeit(lambda: ops.sparse_bwd(q, kk, v, o, do, lse, rows, size, idx, kp, dk_acc=dk, dv_acc=dv))
     print(f"bwd       {t:8.3f} ms  {2.5 * fl_f / t / 1e9:8.1f} TFLOP/s")
+    # sampled sparsity profiler (factor 16: 2000 rows per head scored against all keys)
+    from paper_2502_07590_b200 import profiler as PF
+    cfg = PF.SampleConfig(factor=16)
+    t = timeit(lambda: PF.measure_block_sparsity(list(q), list(kk), 0.9, cfg), iters=3, warm=1)
+    print(f"profiler  {t:8.3f} ms  (24 heads x 2000 sampled rows x {L} keys, theta 0.9)")
 
 
 if __name__ == "__main__":
