@@ -19,6 +19,8 @@
  *   dsv_sparse_bwd       trainer.py:110-117    autograd of the sparse attention (dQ, dK, dV)
  *   dsv_rows_fwd/_bwd    attention.py:176-183  ragged per-query index sets (CSR)
  *   dsv_gather_rows      cpsim.py:147-156/195-216 pack/unpack of head slices and KV rows
+ *   dsv_pred_pass        predictor.py:103-194 (predictor training step: row statistics and the
+ *                        two gradient contractions, streaming the target matrix)
  *   dsv_critical_counts  profiler.py:48-79 + attention.py:118-140 (sampled sparsity profiler:
  *                        critical-KV prefix length per scored row)
  *   dsv_copy_jobs        cpsim.py:147-156/284-299 HCP head exchange written straight into
@@ -41,6 +43,7 @@ extern "C" {
 
 #define DSV_DTYPE_F32 0
 #define DSV_DTYPE_BF16 1
+#define DSV_DTYPE_F64 2
 
 /* Library version (major*10000 + minor*100 + patch) and last error text (thread-local). */
 int dsv_version(void);
@@ -118,6 +121,16 @@ int dsv_rows_bwd(const void* q, const void* k, const void* v, const float* out, 
 /* out[i] = src[rows[i]] for n rows of row_bytes bytes (row strides in bytes, multiples of 4). */
 int dsv_gather_rows(const void* src, long long src_stride, const int* rows, int n,
                     int row_bytes, void* out, long long out_stride, void* stream);
+
+/* Predictor training passes over the target T [R, S] (row stride ldt elements, dtype
+ * DSV_DTYPE_F32 or DSV_DTYPE_F64) with A_hat = Q_lr K_lr^T recomputed in fp64
+ * (Q_lr [R, r], K_lr [S, r] fp64 row-major, r <= 64):
+ *   stage 0: out [R, 4] = per row (|a|^2, |t|^2, a.t, |a - t|^2)
+ *   stage 1: out [R, r] = G K_lr      with G[i, :] = uw[i, 0] T[i, :] + uw[i, 1] A_hat[i, :]
+ *   stage 2: out [S, r] = G^T Q_lr    (uw [R, 2] fp64; unused by stage 0) */
+int dsv_pred_pass(int stage, const double* q_lr, const double* k_lr, const void* target,
+                  int target_dtype, long long ldt, int R, int S, int r, const double* uw,
+                  double* out, void* stream);
 
 /* Critical-KV mass counts (profiler.py:48-79, attention.py:118-140): for each row of fp32
  * raw scores x (q . k, unscaled), p = softmax(x / sqrt_d) in fp64, and out[row] = the

@@ -17,7 +17,7 @@ _PKG = Path(__file__).resolve().parent
 LIB_PATH = Path(os.environ["DSV_LIB"]) if os.environ.get("DSV_LIB") else _PKG / "libdsv.so"
 
 DSV_OK, DSV_EINVAL, DSV_EUNSUPPORTED, DSV_ECUDA = 0, 1, 2, 3
-DTYPE_F32, DTYPE_BF16 = 0, 1
+DTYPE_F32, DTYPE_BF16, DTYPE_F64 = 0, 1, 2
 
 # name -> argtypes (restype is int unless listed in _RESTYPES)
 SIGNATURES = {
@@ -48,6 +48,8 @@ SIGNATURES = {
                      c_void_p, c_void_p],
     "dsv_debug_timeline": [c_void_p, c_int],
     "dsv_copy_jobs": [c_void_p, c_int, c_int, c_void_p],
+    "dsv_pred_pass": [c_int, c_void_p, c_void_p, c_void_p, c_int, c_longlong, c_int, c_int, c_int,
+                      c_void_p, c_void_p, c_void_p],
     "dsv_critical_counts": [c_void_p, c_longlong, c_int, c_int, ctypes.c_double, ctypes.c_double,
                             c_void_p, c_void_p],
     "dsv_copy_jobs_ce": [c_void_p, c_int, c_void_p],

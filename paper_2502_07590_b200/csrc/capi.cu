@@ -24,6 +24,8 @@ int dsv_rows_bwd_launch(const void*, const void*, const void*, const float*, con
                         const void*, const long long*, const int*, int, int, int, int, float, int,
                         float*, float*, float*, cudaStream_t);
 int dsv_critical_counts_launch(const float*, long long, int, int, double, double, int*, cudaStream_t);
+int dsv_pred_pass_launch(int, const double*, const double*, const void*, int, long long, int, int,
+                         int, const double*, double*, cudaStream_t);
 int dsv_gemm_launch(const CUtensorMap*, const CUtensorMap*, const CUtensorMap*, void*, int, int, int, long long,
                     long long, int, int, int, cudaStream_t);
 int dsv_attn_fwd_tc_launch(const void*, const void*, const void*, const int*, const int*,
@@ -318,6 +320,19 @@ int dsv_debug_timeline_copy(void* dst, int bytes);
 extern "C" int dsv_debug_timeline(void* host_dst, int bytes) {
   if (!host_dst || bytes <= 0) return fail(DSV_EINVAL, "debug_timeline: bad buffer");
   return dsv_debug_timeline_copy(host_dst, bytes);
+}
+
+extern "C" int dsv_pred_pass(int stage, const double* q_lr, const double* k_lr, const void* target,
+                             int target_dtype, long long ldt, int R, int n_keys, int r, const double* uw,
+                             double* out, void* stream) {
+  if (stage < 0 || stage > 2) return fail(DSV_EINVAL, "pred_pass: stage must be 0, 1 or 2");
+  if (R < 1 || n_keys < 1 || r < 1 || r > 64 || ldt < n_keys) return fail(DSV_EINVAL, "pred_pass: bad shape");
+  if (target_dtype != DSV_DTYPE_F32 && target_dtype != DSV_DTYPE_F64)
+    return fail(DSV_EINVAL, "pred_pass: target must be fp32 or fp64");
+  if (stage > 0 && !uw) return fail(DSV_EINVAL, "pred_pass: stages 1-2 need the row coefficients");
+  return cuda_status(dsv_pred_pass_launch(stage, q_lr, k_lr, target, target_dtype == DSV_DTYPE_F64,
+                                          ldt, R, n_keys, r, uw, out, S(stream)),
+                     "pred_pass launch");
 }
 
 extern "C" int dsv_critical_counts(const float* scores, long long ld, int rows, int L,

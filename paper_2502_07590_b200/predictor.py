@@ -9,8 +9,13 @@ and its top-k keys are the critical KV estimate. Here:
                           the device (same result as the reference's
                           top-k_max + re-rank, predictor.py:246-259, because the
                           top-k set of a row is nested in its top-k_max set).
-The predictor training step (loss_and_grads / train_step, predictor.py:139-214)
-is SURVEY §8(f) "next" work and is not part of this path yet.
+  * loss_and_grads /   -> the training step (predictor.py:103-214) on
+    train_step            device in fp64: Q_lr, K_lr and the final dW contractions are
+                          cuBLAS DGEMMs (plain library GEMMs); the [R, S] part — row
+                          statistics, G K_lr and G^T Q_lr with G = u_i T + w_i A_hat — are
+                          three passes of dsv_pred_pass streaming the target, never
+                          materialising A_hat or G. Adam runs on the host copies exactly
+                          as the reference (params stay numpy, mutated in place).
 """
 
 from __future__ import annotations
@@ -21,12 +26,13 @@ import numpy as np
 import torch
 
 from . import _convert as cv
-from . import ops
+from . import _lib, ops
 from .attention import CriticalIndexSet
 from .selection import k_from_sparsity, topk_scores_device
 
 COS_WEIGHT = 0.95
 NORM_WEIGHT = 0.05
+_NORM_FLOOR = 1e-12
 
 
 @dataclass
@@ -130,3 +136,122 @@ def estimate_critical(params: PredictorParams, x, k=None, sparsity=None, *, flop
     idx = res[0].cpu().numpy()
     sets = CriticalIndexSet([idx[i, : sizes[i]] for i in range(s_total)], theta=None)
     return (sets, res[2]) if return_scores else sets
+
+
+@dataclass
+class PredictorLossReport:
+    """predictor.py:86-91."""
+
+    cos_loss: float
+    norm_loss: float
+    total: float
+    step_skipped: bool = False
+
+
+def predictor_loss(a_hat, a_target) -> PredictorLossReport:
+    """Composite loss between given predicted and true score rows (predictor.py:139-148)."""
+    a_hat = np.asarray(cv.as_matrix("A_hat", a_hat), dtype=np.float64)
+    a_target = np.asarray(cv.as_matrix("A_target", a_target), dtype=np.float64)
+    if a_hat.shape != a_target.shape:
+        raise ValueError(f"shape mismatch: {a_hat.shape} vs {a_target.shape}")
+    n = a_hat.shape[0]
+    an, tn = np.linalg.norm(a_hat, axis=1), np.linalg.norm(a_target, axis=1)
+    live = tn > _NORM_FLOOR
+    nz = live & (an > _NORM_FLOOR)
+    cos = np.zeros(n)
+    cos[nz] = np.sum(a_hat[nz] * a_target[nz], axis=1) / (an[nz] * tn[nz])
+    cos_loss = float(np.sum(np.where(live, 1.0 - cos, 0.0)) / n)
+    norm_loss = float(np.linalg.norm(a_hat - a_target)) / max(float(np.linalg.norm(a_target)), _NORM_FLOOR)
+    return PredictorLossReport(cos_loss, norm_loss, COS_WEIGHT * cos_loss + NORM_WEIGHT * norm_loss)
+
+
+def _dev_f64(t, dev):
+    if isinstance(t, torch.Tensor):
+        return t.to(device=dev, dtype=torch.float64)
+    return torch.as_tensor(np.asarray(t, dtype=np.float64), device=dev)
+
+
+def loss_and_grads(params: PredictorParams, x, a_target, rows=None, device="cuda"):
+    """Loss report plus analytic gradients w.r.t. W_q and W_k (predictor.py:151-194).
+
+    x [S, d]; a_target [R, S] (R = len(rows) or S), numpy or device tensor (fp32 / fp64).
+    Returns (PredictorLossReport, grad_wq, grad_wk) with numpy fp64 gradients.
+    """
+    dev = torch.device(device)
+    xm = cv.as_matrix("X", x)
+    if xm.shape[1] != params.d:
+        raise ValueError(f"X has {xm.shape[1]} cols but W_q has {params.d} rows")
+    X = _dev_f64(xm, dev)
+    Xr = X if rows is None else X.index_select(0, torch.as_tensor(np.asarray(rows, dtype=np.int64), device=dev))
+    R, S = Xr.shape[0], X.shape[0]
+    if isinstance(a_target, torch.Tensor):
+        T = a_target.to(dev)
+        if T.dtype not in (torch.float32, torch.float64):
+            T = T.double()
+    else:
+        T = torch.as_tensor(np.asarray(a_target, dtype=np.float64), device=dev)
+    if T.dim() != 2 or tuple(T.shape) != (R, S):
+        raise ValueError(f"A_target must be ({R}, {S}), got {tuple(T.shape)}")
+    T = T.contiguous()
+    wq, wk = _dev_f64(params.w_q, dev), _dev_f64(params.w_k, dev)
+    q_lr = (Xr @ wq).contiguous()                       # [R, r]
+    k_lr = (X @ wk).contiguous()                        # [S, r]
+    r = q_lr.shape[1]
+    tdt = _lib.DTYPE_F64 if T.dtype == torch.float64 else _lib.DTYPE_F32
+    stats = torch.empty((R, 4), dtype=torch.float64, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.call("dsv_pred_pass", 0, q_lr.data_ptr(), k_lr.data_ptr(), T.data_ptr(), tdt, T.stride(0),
+              R, S, r, 0, stats.data_ptr(), st)
+    a2, t2, at, d2 = stats.unbind(1)
+    an, tn = a2.sqrt(), t2.sqrt()
+    live = tn > _NORM_FLOOR
+    nz = live & (an > _NORM_FLOOR)
+    one = torch.ones_like(an)
+    cos = torch.where(nz, at / torch.where(nz, an * tn, one), torch.zeros_like(an))
+    cos_loss = float(torch.where(live, 1.0 - cos, torch.zeros_like(cos)).sum().item()) / R
+    denom = max(float(t2.sum().sqrt().item()), _NORM_FLOOR)
+    dist = float(d2.sum().sqrt().item())
+    # G[i, :] = u_i T[i, :] + w_i A_hat[i, :]
+    u = torch.where(nz, -1.0 / (torch.where(nz, an * tn, one) * R), torch.zeros_like(an)) * COS_WEIGHT
+    w = torch.where(nz, cos / (torch.where(nz, an * an, one) * R), torch.zeros_like(an)) * COS_WEIGHT
+    if dist > _NORM_FLOOR:
+        u = u - NORM_WEIGHT / (denom * dist)
+        w = w + NORM_WEIGHT / (denom * dist)
+    uw = torch.stack([u, w], dim=1).contiguous()
+    g1 = torch.empty((R, r), dtype=torch.float64, device=dev)
+    g2 = torch.empty((S, r), dtype=torch.float64, device=dev)
+    _lib.call("dsv_pred_pass", 1, q_lr.data_ptr(), k_lr.data_ptr(), T.data_ptr(), tdt, T.stride(0),
+              R, S, r, uw.data_ptr(), g1.data_ptr(), st)
+    _lib.call("dsv_pred_pass", 2, q_lr.data_ptr(), k_lr.data_ptr(), T.data_ptr(), tdt, T.stride(0),
+              R, S, r, uw.data_ptr(), g2.data_ptr(), st)
+    grad_wq = (Xr.t() @ g1).cpu().numpy()
+    grad_wk = (X.t() @ g2).cpu().numpy()
+    norm_loss = dist / denom
+    report = PredictorLossReport(cos_loss, norm_loss, COS_WEIGHT * cos_loss + NORM_WEIGHT * norm_loss)
+    return report, grad_wq, grad_wk
+
+
+def _adam_update(w, grad, m, v, lr, beta1, beta2, eps, step):
+    """predictor.py:197-204 (host, in place)."""
+    m *= beta1
+    m += (1.0 - beta1) * grad
+    v *= beta2
+    v += (1.0 - beta2) * grad**2
+    w -= lr * (m / (1.0 - beta1**step)) / (np.sqrt(v / (1.0 - beta2**step)) + eps)
+
+
+def train_step(params: PredictorParams, x, a_target, rows=None, device="cuda") -> PredictorLossReport:
+    """One Adam step on the device gradients; mutates `params` (predictor.py:207-214).
+    A non-finite gradient skips the update and flags the report."""
+    report, gq, gk = loss_and_grads(params, x, a_target, rows=rows, device=device)
+    if not (np.all(np.isfinite(gq)) and np.all(np.isfinite(gk))):
+        report.step_skipped = True
+        params.loss_history.append(report.total)
+        return report
+    params.step += 1
+    _adam_update(params.w_q, gq, params.m_q, params.v_q, params.lr, params.beta1, params.beta2,
+                 params.eps, params.step)
+    _adam_update(params.w_k, gk, params.m_k, params.v_k, params.lr, params.beta1, params.beta2,
+                 params.eps, params.step)
+    params.loss_history.append(report.total)
+    return report

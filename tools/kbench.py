@@ -77,6 +77,14 @@ def main():
     cfg = PF.SampleConfig(factor=16)
     t = timeit(lambda: PF.measure_block_sparsity(list(q), list(kk), 0.9, cfg), iters=3, warm=1)
     print(f"profiler  {t:8.3f} ms  (24 heads x 2000 sampled rows x {L} keys, theta 0.9)")
+    # predictor training step for one head: X [L, H*D], 2000 sampled rows, fp32 target [2000, L]
+    from paper_2502_07590_b200 import predictor as PR
+    prm = PR.PredictorParams.initialize(H * D, r, seed=0)
+    xs = X.double()
+    rws = PF.sample_queries(L, cfg)
+    tgt = torch.randn((rws.size, L), device=dev, generator=g)
+    t = timeit(lambda: PR.train_step(prm, xs, tgt, rows=rws), iters=3, warm=1)
+    print(f"predictor {t:8.3f} ms  (one head: train_step, R=2000 rows x {L} keys, d={H * D}, r={r})")
 
 
 if __name__ == "__main__":
