@@ -371,9 +371,20 @@ def run_gpu(args) -> None:
                            "peak_source": f"{peaks['source']} bf16 sustained",
                            "traffic": traffic, "algorithmic_flops": work["bwd_flops"]}
         fwd_ach = work["fwd_flops"] / (stage_ms["fwd"] / 1e3) / 1e12
+        # the L2-side bounds of the attention kernels (measured caps on this B200:
+        # random 256 B row gathers ~14 TB/s, tools/gather_bench.cu; fp32 reductions into
+        # L2-resident rows ~5.5 TB/s, tools/scatter_bench.cu)
+        pair_rows = work["fwd_flops"] / (4 * D)              # sum over (head, query) of k
+        gather_b = 2 * (pair_rows / 128) * D * 2             # K and V rows per 128-query tile
+        red_b = 2 * (pair_rows / 128) * D * 4                # dK and dV fp32 adds per tile
         res["kernels_roofline"] = {
             "sparse_fwd": {"ms": stage_ms["fwd"], "achieved_tflops": fwd_ach,
-                           "frac": fwd_ach / peaks["bf16_sustained"]},
+                           "frac": fwd_ach / peaks["bf16_sustained"],
+                           "l2_gather_tbs": gather_b / (stage_ms["fwd"] / 1e3) / 1e12,
+                           "l2_gather_frac_of_14tbs": gather_b / (stage_ms["fwd"] / 1e3) / 14e12},
+            "sparse_bwd_l2": {"fp32_reduction_tbs": red_b / (bwd_ms / 1e3) / 1e12,
+                              "frac_of_5.5tbs": red_b / (bwd_ms / 1e3) / 5.5e12,
+                              "gather_tbs": gather_b / (bwd_ms / 1e3) / 1e12},
             "select(project+scores+topk)": {"ms": stage_ms["select"]},
         }
     if e2e is not None:

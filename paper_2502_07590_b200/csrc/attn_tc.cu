@@ -95,6 +95,9 @@ struct FwdBars {
   uint32_t tmem;
 };
 
+#ifndef DSV_FWD_ABLATE
+#define DSV_FWD_ABLATE 0   // 1: ablation build only (forward without the softmax math)
+#endif
 // Optional in-kernel timeline (variant builds with -DDSV_BWD_PROF / -DDSV_FWD_PROF):
 // clock64 stamps of each role's phase boundaries for the first kProfCtas CTAs of the
 // backward (or forward) kernel, read back by dsv_debug_timeline.
@@ -397,8 +400,17 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
       // P = 2^(s scale_log2 - m) for keys [32 cq, +32): bf16 into columns [16 cq, +16)
       const f32x2 sc2 = f2(scale_log2, scale_log2), nm2 = f2(-m_run, -m_run);
       f32x2 lsum2 = f2(0.f, 0.f);
+#if DSV_FWD_ABLATE == 1
+      {   // ablation build: no exponentials (P = raw bits), measures the MMA/load pipeline
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pk[i] = r[2 * i] ^ r[2 * i + 1];
+        tmem_st16(tS + cq * 16, pk);
+      }
+#else
       if (kv == BKV) softmax_p_chunk<false>(r, tS + cq * 16, sc2, nm2, cq, kv, lsum2);
       else softmax_p_chunk<true>(r, tS + cq * 16, sc2, nm2, cq, kv, lsum2);
+#endif
       const float2 ls = f2u(lsum2);
       l_run += ls.x + ls.y;
       if (warp == 0 && lane == 0) FPROF(j, 9);
