@@ -21,6 +21,7 @@
  *   dsv_gather_rows      cpsim.py:147-156/195-216 pack/unpack of head slices and KV rows
  *   dsv_pred_pass        predictor.py:103-194 (predictor training step: row statistics and the
  *                        two gradient contractions, streaming the target matrix)
+ *   dsv_varint_*         serialize.py:119-151 encode_index_sets (varint-delta wire format)
  *   dsv_critical_counts  profiler.py:48-79 + attention.py:118-140 (sampled sparsity profiler:
  *                        critical-KV prefix length per scored row)
  *   dsv_copy_jobs        cpsim.py:147-156/284-299 HCP head exchange written straight into
@@ -131,6 +132,17 @@ int dsv_gather_rows(const void* src, long long src_stride, const int* rows, int 
 int dsv_pred_pass(int stage, const double* q_lr, const double* k_lr, const void* target,
                   int target_dtype, long long ldt, int R, int S, int r, const double* uw,
                   double* out, void* stream);
+
+/* Varint-delta index-set encoding (serialize.py:119-151). Rows r of idx (row stride ld
+ * elements) hold counts[r] (or k_uniform when counts == NULL) strictly increasing indices.
+ * dsv_varint_index_bytes: out_len[r] = encoded bytes of row r (count varint + deltas).
+ * dsv_varint_encode: writes row r's bytes at out + row_off[r] (the caller places the
+ * varint(n_rows) header and the scan of out_len). *err |= 1 for a negative first index,
+ * |= 2 for a non-increasing row (the reference raises ValueError). */
+int dsv_varint_index_bytes(const int* idx, long long ld, const int* counts, int k_uniform, int rows,
+                           long long* out_len, int* err, void* stream);
+int dsv_varint_encode(const int* idx, long long ld, const int* counts, int k_uniform, int rows,
+                      const long long* row_off, unsigned char* out, int* err, void* stream);
 
 /* Critical-KV mass counts (profiler.py:48-79, attention.py:118-140): for each row of fp32
  * raw scores x (q . k, unscaled), p = softmax(x / sqrt_d) in fp64, and out[row] = the

@@ -50,6 +50,9 @@ SIGNATURES = {
     "dsv_copy_jobs": [c_void_p, c_int, c_int, c_void_p],
     "dsv_pred_pass": [c_int, c_void_p, c_void_p, c_void_p, c_int, c_longlong, c_int, c_int, c_int,
                       c_void_p, c_void_p, c_void_p],
+    "dsv_varint_index_bytes": [c_void_p, c_longlong, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p],
+    "dsv_varint_encode": [c_void_p, c_longlong, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p,
+                          c_void_p],
     "dsv_critical_counts": [c_void_p, c_longlong, c_int, c_int, ctypes.c_double, ctypes.c_double,
                             c_void_p, c_void_p],
     "dsv_copy_jobs_ce": [c_void_p, c_int, c_void_p],

@@ -24,6 +24,8 @@ int dsv_rows_bwd_launch(const void*, const void*, const void*, const float*, con
                         const void*, const long long*, const int*, int, int, int, int, float, int,
                         float*, float*, float*, cudaStream_t);
 int dsv_critical_counts_launch(const float*, long long, int, int, double, double, int*, cudaStream_t);
+int dsv_varint_launch(int, const int*, long long, const int*, int, int, long long*, unsigned char*, int*,
+                      cudaStream_t);
 int dsv_pred_pass_launch(int, const double*, const double*, const void*, int, long long, int, int,
                          int, const double*, double*, cudaStream_t);
 int dsv_gemm_launch(const CUtensorMap*, const CUtensorMap*, const CUtensorMap*, void*, int, int, int, long long,
@@ -333,6 +335,21 @@ extern "C" int dsv_pred_pass(int stage, const double* q_lr, const double* k_lr, 
   return cuda_status(dsv_pred_pass_launch(stage, q_lr, k_lr, target, target_dtype == DSV_DTYPE_F64,
                                           ldt, R, n_keys, r, uw, out, S(stream)),
                      "pred_pass launch");
+}
+
+extern "C" int dsv_varint_index_bytes(const int* idx, long long ld, const int* counts, int k_uniform,
+                                      int rows, long long* out_len, int* err, void* stream) {
+  if (rows < 0 || ld < 0 || (!counts && k_uniform < 0) || !err) return fail(DSV_EINVAL, "varint_index_bytes: bad arguments");
+  return cuda_status(dsv_varint_launch(0, idx, ld, counts, k_uniform, rows, out_len, nullptr, err, S(stream)),
+                     "varint_index_bytes launch");
+}
+
+extern "C" int dsv_varint_encode(const int* idx, long long ld, const int* counts, int k_uniform, int rows,
+                                 const long long* row_off, unsigned char* out, int* err, void* stream) {
+  if (rows < 0 || ld < 0 || (!counts && k_uniform < 0) || !err || !out) return fail(DSV_EINVAL, "varint_encode: bad arguments");
+  return cuda_status(dsv_varint_launch(1, idx, ld, counts, k_uniform, rows,
+                                       const_cast<long long*>(row_off), out, err, S(stream)),
+                     "varint_encode launch");
 }
 
 extern "C" int dsv_critical_counts(const float* scores, long long ld, int rows, int L,

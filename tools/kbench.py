@@ -72,6 +72,12 @@ def main():
     dv = torch.zeros_like(dk)
     t = timeit(lambda: ops.sparse_bwd(q, kk, v, o, do, lse, rows, size, idx, kp, dk_acc=dk, dv_acc=dv))
     print(f"bwd       {t:8.3f} ms  {2.5 * fl_f / t / 1e9:8.1f} TFLOP/s")
+    # index-set wire format: varint-delta encoding of the layer's critical sets on device
+    from paper_2502_07590_b200 import serialize as SZ
+    flat = idx.reshape(H * G, k)
+    enc = SZ.encode_device(flat)
+    t = timeit(lambda: SZ.encode_device(flat), iters=5, warm=1)
+    print(f"varint    {t:8.3f} ms  {flat.numel() * 4 / 1e6:.0f} MB int32 -> {enc.numel() / 1e6:.0f} MB encoded")
     # sampled sparsity profiler (factor 16: 2000 rows per head scored against all keys)
     from paper_2502_07590_b200 import profiler as PF
     cfg = PF.SampleConfig(factor=16)
