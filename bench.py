@@ -68,6 +68,8 @@ def _args():
     ap.add_argument("--cpu-budget", type=float, default=float(os.environ.get("DSV_CPU_BUDGET", 12)))
     ap.add_argument("--unbalanced", action="store_true", help="contiguous head split (no rebalance)")
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--overlap", default=os.environ.get("DSV_OVERLAP", "none"), choices=["none", "sm", "ce"],
+                    help="HCP exchange under the compute on a side stream (copy kernel / copy engines)")
     ap.add_argument("--scp", type=int, default=1,
                     help="g_s > 1: hybrid CP, N/g_s head groups x g_s selective-sequence groups")
     return ap.parse_args()
@@ -229,7 +231,8 @@ def run_gpu(args) -> None:
                            balanced=not args.unbalanced, device=dev)
         else:
             cp = HeadParallelDSV(grid, H, D, D_LR, VOXEL, sparsity, balanced=not args.unbalanced,
-                                 device=dev)
+                                 device=dev,
+                                 overlap=False if args.overlap == "none" else args.overlap)
         layer = cp.local
         chunk = L // world
         g0 = torch.Generator(device="cpu").manual_seed(0)

@@ -437,13 +437,14 @@ class PeerExchange:
             if r != self.rank:
                 _lib.call("dsv_stream_wait_u32_geq", self._flag(self.rank, kind, r), step, stream.cuda_stream)
 
-    def overlapped(self, q, k, v, do, p, select, forward, backward):
-        """One HCP step with the bulk of the exchange on the copy engines:
+    def overlapped(self, q, k, v, do, p, select, forward, backward, engine: str = "sm"):
+        """One HCP step with the bulk of the exchange under the compute, moved either by the
+        copy kernel on a side stream (engine "sm") or by the copy engines ("ce"):
 
         compute stream: barrier | Q_lr/K_lr rows (copy kernel) | barrier | select |
                         wait Q,K,V | forward | wait dO | backward | dQ,dK,dV (copy kernel) |
                         barrier | wait O
-        side stream:    Q,K,V (copy engines) | signal | dO | signal | wait fwd | O | signal
+        side stream:    Q,K,V | signal | dO | signal | wait fwd | O | signal
 
         Arrival is signalled with stream memory operations (a value write into each
         owner's flag word, a wait-until->= on the consumer's stream): no kernel spins on
@@ -460,8 +461,16 @@ class PeerExchange:
             self._side = torch.cuda.Stream(device=self.buf.device)
         side = self._side
         ptrs = tuple(t.data_ptr() for t in (q, k, v, do, p))
-        qkv = self._host_table(("qkv",) + ptrs, lambda: self._head_jobs((("q", q), ("k", k), ("v", v))))
-        dj = self._host_table(("do",) + ptrs, lambda: self._head_jobs((("do", do),)))
+        table = self._host_table if engine == "ce" else self._table
+        qkv = table(("qkv", engine) + ptrs, lambda: self._head_jobs((("q", q), ("k", k), ("v", v))))
+        dj = table(("do", engine) + ptrs, lambda: self._head_jobs((("do", do),)))
+
+        def send(jobs):
+            if engine == "ce":
+                ops.copy_jobs_ce(jobs, side)
+            else:
+                with torch.cuda.stream(side):
+                    ops.copy_jobs(jobs, self.splits)
         lr = self._table(("lr",) + ptrs, lambda: self._lowrank_jobs(p))
         # host issue order keeps the GPU busy: the select kernels are queued before the
         # (slow to issue) copy-engine jobs, the forward before the dO / O jobs
@@ -476,19 +485,19 @@ class PeerExchange:
         ql, kl, vl, dom, qlr, klr = (self.region(n) for n in ("q", "k", "v", "do", "qlr", "klr"))
         sel = select(qlr, klr)
         side.wait_event(ev0)
-        ops.copy_jobs_ce(qkv, side)
+        send(qkv)
         self._signal(0, step, side)
         ev_qkv.record(side)
         cur.wait_event(ev_qkv)                        # this rank's own (local) copies
         self._await(0, step, cur)
         out, lse = forward(ql, kl, vl, sel)
         ev_f.record(cur)
-        ops.copy_jobs_ce(dj, side)
+        send(dj)
         self._signal(1, step, side)
         ev_do.record(side)
         side.wait_event(ev_f)
-        oj = self._host_table(("o", out.data_ptr()), lambda: self._back_jobs((out,), ("o",)))
-        ops.copy_jobs_ce(oj, side)
+        oj = table(("o", engine, out.data_ptr()), lambda: self._back_jobs((out,), ("o",)))
+        send(oj)
         self._signal(2, step, side)
         ev_o.record(side)
         cur.wait_event(ev_do)
@@ -731,7 +740,9 @@ class HeadParallelDSV(_PhaseMarks):
         if transport not in ("peer", "all_to_all"):
             raise ValueError(f"unknown transport {transport!r}")
         self.transport = transport
+        # overlap: False, True / "sm" (copy kernel on a side stream) or "ce" (copy engines)
         self.overlap = bool(overlap) and transport == "peer"
+        self.overlap_engine = overlap if isinstance(overlap, str) else "sm"
         if transport == "peer":
             self.ex = PeerExchange(heads, grid.size, head_dim, d_lr, self.assignment, group, device)
         else:
@@ -809,7 +820,8 @@ class HeadParallelDSV(_PhaseMarks):
                 self._mark("bwd")
                 return r
 
-            res = self.ex.overlapped(q, k, v, dout, p, select, forward, backward)
+            res = self.ex.overlapped(q, k, v, dout, p, select, forward, backward,
+                                     engine=self.overlap_engine)
             self._mark("grads_exchange")
             return res
         ql, kl, vl, dout_m, qlr, klr = self.ex.to_heads(q, k, v, dout, p)

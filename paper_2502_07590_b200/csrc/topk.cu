@@ -175,11 +175,12 @@ topk_rows_kernel(const float* __restrict__ scores, long long ld, int rows, int L
   float* buf = reinterpret_cast<float*>(smem_raw + sizeof(Smem));
   const int nw = (L + 31) >> 5;                        // 32-column mask words
   uint32_t* mask = reinterpret_cast<uint32_t*>(smem_raw + sizeof(Smem) + (kSmem ? (size_t)L * 4 : 0));
+  uint32_t* bmask = mask + ((L + 127) / 128 * 4 + 4);   // band-candidate bits (pass 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool bulk = kSmem && (((ld * 4) & 15) == 0) &&
                     ((reinterpret_cast<uintptr_t>(scores) & 15) == 0) && L >= 4;
   const int n4 = L >> 2;
-  const int seg = (((L + kWarps - 1) / kWarps) + 31) & ~31;   // contiguous warp segments
+  const int seg = (((L + kWarps - 1) / kWarps) + 127) & ~127;  // contiguous warp segments (x128)
   const int s0 = warp * seg, s1 = min(L, s0 + seg);
   const uint32_t lt = (1u << lane) - 1u;
   const int sstride = max(1, L / kSample) | 1;             // odd: conflict-free sample reads
@@ -306,27 +307,65 @@ topk_rows_kernel(const float* __restrict__ scores, long long ld, int rows, int L
       uint32_t cmin = 0xffffffffu, cmax = 0u, wcnt = 0;
       uint32_t* wcand = S.cand + warp * kCandW;
       uint32_t* wcidx = S.cidx + warp * kCandW;
-      for (int base = s0; base < s1; base += 32) {
-        const int i = base + lane;
-        const bool valid = i < s1;
-        const float v = valid ? src.val(i) : -INFINITY;
-        const uint32_t mab = __ballot_sync(0xffffffffu, v > hi_v);
-        if (lane == 0) mask[base >> 5] = mab;
-        n_above += __popc(mab);
-        const bool in = valid && v >= lo_v && v <= hi_v;
-        const uint32_t msk = __ballot_sync(0xffffffffu, in);
-        if (msk) {
-          if (in) {
-            const uint32_t slot = wcnt + __popc(msk & lt);
-            const uint32_t key = f2key(v);
-            if (slot < (uint32_t)kCandW) { wcand[slot] = key; wcidx[slot] = (uint32_t)i; }
-            cmin = min(cmin, key);
-            cmax = max(cmax, key);
-          }
-          wcnt += __popc(msk);
+      // 128 columns per warp step: one 16-byte shared load per lane; the above-mask words
+      // (plain bit order) are assembled from per-lane nibbles with three shuffles
+      for (int base = s0; base < s1; base += 128) {
+        const int i0 = base + 4 * lane;
+        float4 v;
+        if (kSmem && i0 + 3 < s1) {
+          v = reinterpret_cast<const float4*>(src.vals)[i0 >> 2];
+        } else {
+          v.x = i0 < s1 ? src.val(i0) : 0.f;
+          v.y = i0 + 1 < s1 ? src.val(i0 + 1) : 0.f;
+          v.z = i0 + 2 < s1 ? src.val(i0 + 2) : 0.f;
+          v.w = i0 + 3 < s1 ? src.val(i0 + 3) : 0.f;
         }
+        const bool ok0 = i0 < s1, ok1 = i0 + 1 < s1, ok2 = i0 + 2 < s1, ok3 = i0 + 3 < s1;
+        const bool g0 = ok0 && v.x > hi_v, g1 = ok1 && v.y > hi_v, g2 = ok2 && v.z > hi_v, g3 = ok3 && v.w > hi_v;
+        const uint32_t gt = (uint32_t)g0 | ((uint32_t)g1 << 1) | ((uint32_t)g2 << 2) | ((uint32_t)g3 << 3);
+        n_above += __popc(gt);
+        uint32_t wv = gt << (4 * (lane & 7));
+        wv |= __shfl_xor_sync(0xffffffffu, wv, 1);
+        wv |= __shfl_xor_sync(0xffffffffu, wv, 2);
+        wv |= __shfl_xor_sync(0xffffffffu, wv, 4);
+        if ((lane & 7) == 0 && base + 32 * (lane >> 3) < s1) mask[(base >> 5) + (lane >> 3)] = wv;
+        const bool n0 = ok0 && !g0 && v.x >= lo_v, n1 = ok1 && !g1 && v.y >= lo_v;
+        const bool n2 = ok2 && !g2 && v.z >= lo_v, n3 = ok3 && !g3 && v.w >= lo_v;
+        uint32_t bw = ((uint32_t)n0 | ((uint32_t)n1 << 1) | ((uint32_t)n2 << 2) | ((uint32_t)n3 << 3))
+                      << (4 * (lane & 7));
+        bw |= __shfl_xor_sync(0xffffffffu, bw, 1);
+        bw |= __shfl_xor_sync(0xffffffffu, bw, 2);
+        bw |= __shfl_xor_sync(0xffffffffu, bw, 4);
+        if ((lane & 7) == 0 && base + 32 * (lane >> 3) < s1) bmask[(base >> 5) + (lane >> 3)] = bw;
+      }
+      __syncwarp();
+      // band candidates from this warp's band-mask words: lane j takes word j of each
+      // 32-word group, a warp scan of the popcounts gives the slots
+      for (int w0 = s0 >> 5; w0 < ((s1 + 31) >> 5); w0 += 32) {
+        const int w = w0 + lane;
+        uint32_t m = w < ((s1 + 31) >> 5) ? bmask[w] : 0u;
+        const uint32_t c = __popc(m);
+        uint32_t inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += x;
+        }
+        uint32_t slot = wcnt + inc - c;
+        while (m) {
+          const int i = w * 32 + __ffs(m) - 1;
+          m &= m - 1;
+          const uint32_t key = f2key(src.val(i));
+          if (slot < (uint32_t)kCandW) { wcand[slot] = key; wcidx[slot] = (uint32_t)i; }
+          ++slot;
+          cmin = min(cmin, key);
+          cmax = max(cmax, key);
+        }
+        wcnt += __shfl_sync(0xffffffffu, inc, 31);
       }
       TOPK_MARK(8);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) n_above += __shfl_xor_sync(0xffffffffu, n_above, o);   // per-lane counts
       cmin = warp_min(cmin);
       cmax = warp_max(cmax);
       if (lane == 0) {
@@ -548,7 +587,7 @@ topk_rows_kernel(const float* __restrict__ scores, long long ld, int rows, int L
 }  // namespace dsv
 
 size_t dsv_topk_smem_bytes(int L) {
-  const size_t mask = (((size_t)L + 127) / 128 * 4 + 4) * 4;
+  const size_t mask = 2 * (((size_t)L + 127) / 128 * 4 + 4) * 4;   // keep + band masks
   const size_t base = sizeof(dsv::topk::Smem) + mask;
   const size_t need = base + (size_t)L * 4;
   return need <= 227 * 1024 ? need : base;
@@ -566,7 +605,7 @@ int dsv_topk_launch(const float* scores, long long ld, int rows, int L, const in
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = rows < sms ? rows : sms;
-  const size_t mask = (((size_t)L + 127) / 128 * 4 + 4) * 4;
+  const size_t mask = 2 * (((size_t)L + 127) / 128 * 4 + 4) * 4;   // keep + band masks
   const size_t base = sizeof(Smem) + mask;
   const size_t need = base + (size_t)L * 4;
   if (base > 227 * 1024) return (int)cudaErrorInvalidValue;

@@ -41,7 +41,8 @@ def main():
     if hybrid:
         cp = HybridDSV(grid, H, D, r, (8, 4, 4), sp, world // 2, 2, balanced=True, device=dev)
     else:
-        cp = HeadParallelDSV(grid, H, D, r, (8, 4, 4), sp, balanced=True, device=dev)
+        ov = next((a.split("=")[1] for a in sys.argv if a.startswith("--overlap=")), False)
+        cp = HeadParallelDSV(grid, H, D, r, (8, 4, 4), sp, balanced=True, device=dev, overlap=ov)
     outs = cp.step(x[sl].contiguous(), wt, *(t[:, sl].contiguous() for t in (q, k, v, do)))
     gathered = []
     for t in outs:

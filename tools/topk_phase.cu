@@ -1,5 +1,8 @@
 // Phase breakdown of the K2 top-k kernel at the c2 shape (6240 rows x 32000, k = 3200).
 #define DSV_TOPK_PROF 1
+#ifdef ABL
+#define DSV_TOPK_ABLATE 1
+#endif
 #include "../paper_2502_07590_b200/csrc/topk.cu"
 #include "../paper_2502_07590_b200/csrc/topk_stream.cu"
 #include <cstdio>
