@@ -40,7 +40,10 @@ namespace attn {
 
 constexpr int BQ = 128;   // queries per tile
 constexpr int BKV = 128;  // keys per block
-constexpr int kProdWarps = 8;                 // forward gather producers
+#ifndef DSV_PROD_WARPS
+#define DSV_PROD_WARPS 8
+#endif
+constexpr int kProdWarps = DSV_PROD_WARPS;    // forward gather producers
 constexpr int kProdThreads = kProdWarps * 32;
 
 template <int D, int NT = kProdThreads>
@@ -68,7 +71,10 @@ DSV_DEV void issue_tile(uint8_t* tile, const __nv_bfloat16* base,
 constexpr int kFwdKStages = 2;                                   // K_j frees after S_j
 constexpr int kFwdStages = 3;                                    // V ring (frees after PV_j)
 constexpr int kFwdSBufs = 3;                                     // S/P buffers in TMEM
-constexpr int kFwdSoftWGs = 4;                                   // warps 0-15
+#ifndef DSV_FWD_SOFT_WGS
+#define DSV_FWD_SOFT_WGS 4
+#endif
+constexpr int kFwdSoftWGs = DSV_FWD_SOFT_WGS;                    // warps 0-15
 constexpr int kFwdSoftThreads = kFwdSoftWGs * 128;
 constexpr int kFwdMmaWarp = kFwdSoftWGs * 4;
 constexpr int kFwdProdWarp0 = kFwdMmaWarp + 1;
