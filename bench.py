@@ -70,6 +70,8 @@ def _args():
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--overlap", default=os.environ.get("DSV_OVERLAP", "none"), choices=["none", "sm", "ce"],
                     help="HCP exchange under the compute on a side stream (copy kernel / copy engines)")
+    ap.add_argument("--graph", action="store_true", default=os.environ.get("DSV_GRAPH", "0") == "1",
+                    help="replay the step as one captured CUDA graph")
     ap.add_argument("--scp", type=int, default=1,
                     help="g_s > 1: hybrid CP, N/g_s head groups x g_s selective-sequence groups")
     return ap.parse_args()
@@ -250,6 +252,32 @@ def run_gpu(args) -> None:
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    eager_step = step
+    if args.graph:
+        # one CUDA graph per step: the host issues one launch instead of ~20 kernels
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            step()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        with torch.cuda.graph(graph):
+            step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+        def step(ev=None):
+            graph.replay()
+        eager_stage_names, stage_names = stage_names, ()
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
 
     clocks = ClockSampler(local_rank)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(stage_names))]
@@ -281,10 +309,19 @@ def run_gpu(args) -> None:
             vals = [(starts[i] if si == 0 else evs[i][si - 1]).elapsed_time(evs[i][si])
                     for i in range(args.steps)]
             stage_ms[name] = sum(vals) / len(vals)
+    if args.graph and world == 1:
+        # per-stage times from one extra eager (untimed) step with events
+        ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        st0 = torch.cuda.Event(enable_timing=True)
+        st0.record()
+        eager_step(ev1)
+        torch.cuda.synchronize()
+        stage_ms = {name: (st0 if i == 0 else ev1[i - 1]).elapsed_time(ev1[i])
+                    for i, name in enumerate(eager_stage_names)}
     if world > 1:
         # one extra (untimed) step with per-phase events on the compute stream
         cp.marks = []
-        step()
+        eager_step()
         stage_ms = cp.phase_ms()
         cp.marks = None
 
@@ -360,6 +397,7 @@ def run_gpu(args) -> None:
         "effective_tflops": {"algorithmic": tot_flops / (ms / 1e3) / 1e12,
                              "dense_equivalent": dense_eq / (ms / 1e3) / 1e12},
         "gpu_launches": launches_per_step * args.steps,
+        "cuda_graph": bool(args.graph),
         "clocks": clk,
     }
     if stage_ms:

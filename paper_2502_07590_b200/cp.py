@@ -310,13 +310,16 @@ class PeerExchange:
 
     # ------------------------------------------------------------------ job tables
     def _table(self, key, build):
+        """Device job table cached by the pointers it encodes. Uploaded from pinned host
+        memory (kept alive with the table), so a step can be captured in a CUDA graph."""
         t = self._tables.get(key)
         if t is None:
             if len(self._tables) >= 16:
                 self._tables.clear()
-            t = torch.from_numpy(build()).to(self.buf.device)
+            host = torch.from_numpy(build()).pin_memory()
+            t = (host.to(self.buf.device, non_blocking=True), host)
             self._tables[key] = t
-        return t
+        return t[0]
 
     def _head_jobs(self, named):
         """Flat per-head jobs: this rank's token chunk of head h of each tensor [H, L/N, D]
