@@ -45,6 +45,9 @@ WORKLOADS = {
     "c4": {"grid": (32, 64, 64), "heads": 24, "sparsity": "sweep",
            "desc": ("c4: L=131072 (32x64x64), 24 heads, d=128, r=16, per-head sparsity "
                     "0.50..0.95 (shuffled, seed 0), sparsity-aware head re-balancing")},
+    "c5": {"grid": (32, 128, 128), "heads": 24, "sparsity": 0.9,
+           "desc": ("c5: large video-DiT layer, L=524288 (32x128x128), 24 heads, d=128, r=16, "
+                    "sparsity 0.9 (k=52429), voxel groups (8,4,4) -> 4096 query tiles")},
 }
 
 

@@ -386,10 +386,13 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
       if (warp == 0 && lane == 0) FPROF(j, 3);
       if (j == 0) {
         m_run = mx;
-      } else if (mx > m_run + 8.f) {
-        // rescale O (this warp's D/4 columns) once PV_{j-1} has landed
+      } else if (__any_sync(0xffffffffu, mx > m_run + 8.f)) {
+        // rescale O (this warp's D/4 columns) once PV_{j-1} has landed. The decision is
+        // warp-uniform: tcgen05.ld/st are warp-collective, so every lane takes the branch
+        // and a row whose max did not grow rescales by alpha = 1.
         mbar_wait(&B.pv_done[(j - 1) % NS], ((j - 1) / NS) & 1);
         tc_fence_after();
+        mx = fmaxf(mx, m_run);
         const float alpha = fast_exp2(m_run - mx);
         l_run *= alpha;
 #pragma unroll 1

@@ -119,6 +119,9 @@ DSV_DEV bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
   return ok != 0;
 }
+#ifdef DSV_NO_WATCHDOG   // diagnostic builds: a stuck wait hangs instead of trapping
+#undef DSV_WATCHDOG
+#endif
 #ifndef DSV_SLEEP_NS
 #define DSV_SLEEP_NS 128
 #endif

@@ -18,6 +18,7 @@ grouping.py:196-216 grouped_sparse_attention and its autograd
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -108,10 +109,31 @@ class DSVAttentionLayer:
 
     def _scores_topk(self, qp, k_lr, return_scores):
         H, L, G = self.H, self.L, self.G
-        scores = ops.gemm_bf16(qp, k_lr, torch.float32)          # [H, G, L] fp32
-        idx, thr = ops.topk_rows(scores.view(H * G, L), self.kcount, G, self.k_max)
+        hc = H if return_scores else self.score_heads_per_chunk()
+        if hc >= H:
+            scores = ops.gemm_bf16(qp, k_lr, torch.float32)          # [H, G, L] fp32
+            idx, thr = ops.topk_rows(scores.view(H * G, L), self.kcount, G, self.k_max)
+        else:
+            # long sequences (c5: 8.6 GB of scores per head): score and select hc heads at a
+            # time through one reused buffer; the index lists land in place
+            dev = qp.device
+            idx = torch.empty((H * G, self.k_max), device=dev, dtype=torch.int32)
+            thr = torch.empty((H * G,), device=dev, dtype=torch.float32)
+            buf = torch.empty((hc, G, L), device=dev, dtype=torch.float32)
+            for h0 in range(0, H, hc):
+                h1 = min(H, h0 + hc)
+                sc = ops.gemm_bf16(qp[h0:h1], k_lr[h0:h1], torch.float32, out=buf[: h1 - h0])
+                ops.topk_rows(sc.view(-1, L), self.kcount[h0:h1], G, self.k_max,
+                              out=(idx[h0 * G:h1 * G], thr[h0 * G:h1 * G]))
+            scores = None
         sel = SelectedKV(idx.view(H, G, self.k_max), self.kcount, thr.view(H, G), self.ks)
         return (sel, scores) if return_scores else sel
+
+    def score_heads_per_chunk(self) -> int:
+        """Heads scored per pass: the fp32 score matrices stay under DSV_SCORE_BYTES (16 GiB)."""
+        per_head = self.G * self.L * 4
+        budget = int(os.environ.get("DSV_SCORE_BYTES", str(16 << 30)))
+        return max(1, min(self.H, budget // per_head))
 
     # ------------------------------------------------------------- attention
     def forward(self, q, k, v, sel: SelectedKV):

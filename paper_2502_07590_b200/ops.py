@@ -32,8 +32,11 @@ def _ptr(t) -> int:
 
 
 # ------------------------------------------------------------------- K1 GEMM
-def gemm_bf16(a: torch.Tensor, b: torch.Tensor, out_dtype=torch.float32) -> torch.Tensor:
-    """Batched C = A . B^T on tcgen05. a: [nb, M, K] or [M, K] bf16, b: [nb, N, K] or [N, K]."""
+def gemm_bf16(a: torch.Tensor, b: torch.Tensor, out_dtype=torch.float32, out=None) -> torch.Tensor:
+    """Batched C = A . B^T on tcgen05. a: [nb, M, K] or [M, K] bf16, b: [nb, N, K] or [N, K].
+
+    out: optional preallocated C (unit stride along N) of the result's shape and dtype.
+    """
     _require_cuda(a, b)
     squeeze = a.dim() == 2
     if squeeze:
@@ -46,7 +49,12 @@ def gemm_bf16(a: torch.Tensor, b: torch.Tensor, out_dtype=torch.float32) -> torc
         raise ValueError(f"gemm shape mismatch {tuple(a.shape)} x {tuple(b.shape)}")
     if a.stride(2) != 1 or b.stride(2) != 1:
         raise ValueError("gemm operands need unit stride along K")
-    c = torch.empty((nb, M, N), device=a.device, dtype=out_dtype)
+    if out is None:
+        c = torch.empty((nb, M, N), device=a.device, dtype=out_dtype)
+    else:
+        c = out.unsqueeze(0) if squeeze else out
+        if tuple(c.shape) != (nb, M, N) or c.dtype != out_dtype or c.stride(2) != 1:
+            raise ValueError("gemm out has the wrong shape, dtype or layout")
     _lib.call("dsv_gemm_bf16", _ptr(a), a.stride(1), a.stride(0), _ptr(b), b.stride(1), b.stride(0),
               _ptr(c), _F32 if out_dtype == torch.float32 else _BF16, c.stride(1), c.stride(0),
               M, N, K, nb, _stream())
@@ -101,11 +109,11 @@ def proxy_scores(qp: torch.Tensor, k_lr: torch.Tensor, out: torch.Tensor | None 
 
 # ------------------------------------------------------------------- K2 top-k
 def topk_rows(scores: torch.Tensor, k_per_head: torch.Tensor, rows_per_head: int,
-              k_max: int | None = None):
+              k_max: int | None = None, out=None):
     """Exact top-k per row of fp32 scores [R, L] (row r uses k_per_head[r // rows_per_head]).
 
     Returns (idx int32 [R, k_max] ascending — entries past a row's k are
-    undefined, thresholds fp32 [R]).
+    undefined, thresholds fp32 [R]). out: optional preallocated (idx, thr) pair.
     """
     _require_cuda(scores, k_per_head)
     if scores.dtype != torch.float32 or scores.dim() != 2 or scores.stride(1) != 1:
@@ -114,8 +122,14 @@ def topk_rows(scores: torch.Tensor, k_per_head: torch.Tensor, rows_per_head: int
     kp = k_per_head.to(device=scores.device, dtype=torch.int32).contiguous()
     if k_max is None:
         k_max = int(kp.max().item())
-    idx = torch.empty((R, k_max), device=scores.device, dtype=torch.int32)
-    thr = torch.empty((R,), device=scores.device, dtype=torch.float32)
+    if out is None:
+        idx = torch.empty((R, k_max), device=scores.device, dtype=torch.int32)
+        thr = torch.empty((R,), device=scores.device, dtype=torch.float32)
+    else:
+        idx, thr = out
+        if (idx.dtype != torch.int32 or idx.shape[0] != R or idx.shape[1] < k_max or idx.stride(1) != 1
+                or thr.dtype != torch.float32 or thr.shape != (R,) or not thr.is_contiguous()):
+            raise ValueError("topk out must be (int32 [R, >=k_max] rows, fp32 [R])")
     _lib.call("dsv_topk", _ptr(scores), scores.stride(0), R, L, _ptr(kp), rows_per_head, _ptr(idx),
               idx.stride(0), _ptr(thr), _stream())
     return idx, thr

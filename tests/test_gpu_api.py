@@ -189,3 +189,22 @@ def test_layer_select_heterogeneous_sparsity(cuda):
         ref, thr = oracle.topk_from_scores(sc[h], layer.ks[h])
         np.testing.assert_array_equal(sel.idx[h, :, : layer.ks[h]].cpu().numpy(), ref)
         np.testing.assert_array_equal(sel.thresholds[h].cpu().numpy(), thr.astype(np.float32))
+
+
+def test_layer_select_head_chunked_matches_whole(cuda, monkeypatch):
+    # long-sequence mode: heads scored through a reused buffer (DSV_SCORE_BYTES) give the
+    # same index lists and thresholds as scoring all heads at once
+    grid = TokenGrid(8, 16, 16)
+    sp = [0.5, 0.7, 0.9, 0.95, 0.8]
+    layer = DSVAttentionLayer(grid, 5, 128, 16, voxel=(8, 4, 4), sparsity=sp, device=cuda)
+    g = torch.Generator(device="cpu").manual_seed(4)
+    x = torch.randn((grid.size, 5 * 128), generator=g).to(torch.bfloat16).to(cuda)
+    wt = layer.predictor_weights(2)
+    whole, _ = layer.select(x, wt, return_scores=True)
+    monkeypatch.setenv("DSV_SCORE_BYTES", str(2 * layer.G * layer.L * 4))
+    assert layer.score_heads_per_chunk() == 2
+    chunked = layer.select(x, wt)
+    for h in range(5):
+        kh = layer.ks[h]
+        assert torch.equal(chunked.idx[h, :, :kh], whole.idx[h, :, :kh])
+    assert torch.equal(chunked.thresholds, whole.thresholds)

@@ -69,6 +69,15 @@ def test_topk_streaming_long_rows(cuda, L, ks):
     _check_topk(scores, ks, 2, cuda)
 
 
+def test_topk_streaming_c5_rows(cuda):
+    # c5 row length (L = 524288, 32x128x128) at k = 52429 (90% sparsity) and the extremes
+    rng = np.random.default_rng(524288)
+    L = 524288
+    scores = rng.standard_normal((6, L)).astype(np.float32)
+    scores[4] = np.round(scores[4] * 4)        # heavy ties
+    _check_topk(scores, [52429, 1, L - 1], 2, cuda)
+
+
 def test_topk_streaming_ties_zero_inf(cuda):
     rng = np.random.default_rng(9)
     L = 90000
@@ -208,6 +217,37 @@ def test_sparse_fwd_full_set_equals_dense(cuda):
                             torch.tensor([L], dtype=torch.int32, device=cuda))
     ref = oracle.full_attention(*(_bf(t).double().numpy()[0] for t in (q, k, v)))
     assert np.max(np.abs(out.float().cpu().numpy()[0] - ref)) < 3e-2
+
+
+def test_sparse_fwd_late_max_jump_on_some_rows(cuda):
+    # a few query rows meet a key in the last key block whose logit is far above the rows'
+    # running max (online-softmax rescale), the other rows of the same warp do not: the
+    # rescale must stay warp-uniform (tcgen05.ld/st are warp-collective)
+    D, H = 128, 1
+    plan = build_groups(TokenGrid(4, 8, 16), (2, 8, 8))
+    L = plan.grid.size
+    rng = np.random.default_rng(11)
+    q, k, v, do = (rng.standard_normal((H, L, D)).astype(np.float32) for _ in range(4))
+    hot = rng.choice(L, size=20, replace=False)
+    for i, r in enumerate(hot):
+        k[0, L - 1 - i] = q[0, r]
+    idx = np.tile(np.arange(L, dtype=np.int32), (H, plan.n_groups, 1))
+    rows, size = plan.tables(cuda)
+    kc = torch.tensor([L], dtype=torch.int32, device=cuda)
+    qb, kb, vb, dob = (_bf(t).to(cuda) for t in (q, k, v, do))
+    idx_t = torch.from_numpy(idx).to(cuda)
+    out, lse = ops.sparse_fwd(qb, kb, vb, rows, size, idx_t, kc)
+    dq, dk, dv = ops.sparse_bwd(qb, kb, vb, out, dob, lse, rows, size, idx_t, kc)
+    torch.cuda.synchronize()
+    qd, kd, vd, dod = (_bf(t).double().numpy()[0] for t in (q, k, v, do))
+    sets = [np.arange(L)] * plan.n_groups
+    ref, ref_lse = oracle.grouped_attention_fwd(qd, kd, vd, plan.members, sets)
+    assert np.max(np.abs(out.float().cpu().numpy()[0] - ref)) < 3e-2
+    assert np.max(np.abs(lse.cpu().numpy()[0] * math.log(2.0) - ref_lse)) < 2e-2
+    rdq, rdk, rdv = oracle.grouped_attention_bwd(qd, kd, vd, plan.members, sets, dod)
+    assert _rel_l2(dq.float().cpu().numpy()[0], rdq) < 3e-2
+    assert _rel_l2(dk.cpu().numpy()[0], rdk) < 3e-2
+    assert _rel_l2(dv.cpu().numpy()[0], rdv) < 3e-2
 
 
 # ---------------------------------------------------------------- CSR path
