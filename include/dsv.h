@@ -80,6 +80,16 @@ int dsv_scores_f32(const void* A, long long lda, long long a_bs, const void* B, 
                    long long b_bs, float* C, long long ldc, long long c_bs, int nbatch, int R,
                    int Lk, int r, int in_dtype, void* stream);
 
+/* K1b + K2 fused: exact top-k of the proxy scores q_prox[h][g] . k_lr[h][l] (bf16, rank
+ * r <= 64) without materialising them. Same scores (same tcgen05 sequence) and the same
+ * selection semantics as dsv_gemm_bf16 (fp32 out) followed by dsv_topk with
+ * rows_per_head = G: out_idx[h*G + g][0..k_h) ascending, out_thr[h*G + g].
+ * split: CTAs per 128-row tile splitting the key range (cluster), 0 = automatic. */
+int dsv_select_fused(const void* q_prox, long long ldq, long long q_bs, const void* k_lr,
+                     long long ldk, long long k_bs, int H, int G, int L, int r,
+                     const int* k_per_head, int* out_idx, long long out_ld, float* out_thr,
+                     int split, void* stream);
+
 /* Exact top-k per row of an fp32 score matrix (K2).
  * scores: [rows][ld] fp32; row r uses k = k_per_head[r / rows_per_head] (1 <= k <= L).
  * out_idx: [rows][out_ld] int32 ascending column ids (first k entries written);
@@ -183,6 +193,9 @@ int dsv_stream_wait_u32_geq(const void* addr, unsigned int value, void* stream);
  * by builds with -DDSV_BWD_PROF; layout [8 CTAs][32 blocks][12 events] int64) into a
  * host buffer. Returns the bytes copied or a negative value. */
 int dsv_debug_timeline(void* host_dst, int bytes);
+/* Diagnostics: the fused selection's pass timeline (globaltimer ns stamps of CTA 0, filled
+ * only by builds with -DDSV_FSEL_PROF; layout [64 passes][8 events] uint64). */
+int dsv_debug_select_timeline(void* host_dst, int bytes);
 
 /* fp32 -> bf16 conversion of n contiguous elements. */
 int dsv_f32_to_bf16(const float* in, void* out, long long n, void* stream);

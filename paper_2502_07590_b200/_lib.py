@@ -33,6 +33,9 @@ SIGNATURES = {
     "dsv_scores_f32": [c_void_p, c_longlong, c_longlong, c_void_p, c_longlong, c_longlong,
                        c_void_p, c_longlong, c_longlong, c_int, c_int, c_int, c_int, c_int,
                        c_void_p],
+    "dsv_select_fused": [c_void_p, c_longlong, c_longlong, c_void_p, c_longlong, c_longlong, c_int,
+                         c_int, c_int, c_int, c_void_p, c_void_p, c_longlong, c_void_p, c_int,
+                         c_void_p],
     "dsv_topk": [c_void_p, c_longlong, c_int, c_int, c_void_p, c_int, c_void_p, c_longlong,
                  c_void_p, c_void_p],
     "dsv_sparse_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_longlong,
@@ -47,6 +50,7 @@ SIGNATURES = {
                      c_void_p, c_int, c_int, c_int, c_int, c_float, c_int, c_void_p, c_void_p,
                      c_void_p, c_void_p],
     "dsv_debug_timeline": [c_void_p, c_int],
+    "dsv_debug_select_timeline": [c_void_p, c_int],
     "dsv_copy_jobs": [c_void_p, c_int, c_int, c_void_p],
     "dsv_pred_pass": [c_int, c_void_p, c_void_p, c_void_p, c_int, c_longlong, c_int, c_int, c_int,
                       c_void_p, c_void_p, c_void_p],

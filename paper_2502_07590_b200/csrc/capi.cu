@@ -38,6 +38,8 @@ int dsv_attn_bwd_tc_launch(const void*, const void*, const void*, const void*, c
                            const int*, const int*, int, int, int, int, int, float, float, void*,
                            float*, float*, cudaStream_t);
 int dsv_f32_to_bf16_launch(const float*, void*, long long, cudaStream_t);
+int dsv_select_fused_launch(const CUtensorMap*, const CUtensorMap*, int, int, int, const int*, int*,
+                            long long, float*, int, cudaStream_t);
 int dsv_proxy_scores_launch(const void*, long long, long long, const void*, long long, long long,
                             float*, long long, long long, int, int, int, cudaStream_t);
 
@@ -95,7 +97,8 @@ Fn driver_fn(const char* name) {
 // dims 1..rank-1, 128B swizzle.
 bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
               const uint64_t* strides_bytes, const uint32_t* box,
-              CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
+              CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t gd[5];
@@ -104,7 +107,7 @@ bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
   for (int i = 0; i < rank; ++i) { gd[i] = dims[i]; bx[i] = box[i]; es[i] = 1; }
   for (int i = 0; i + 1 < rank; ++i) gs[i] = strides_bytes[i];
   CUresult r = fn(m, dt, rank, const_cast<void*>(base), gd, gs, bx,
-                  es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -196,6 +199,48 @@ int dsv_proxy_scores(const void* q_prox, long long ldq, long long q_bs, const vo
   return cuda_status(dsv_proxy_scores_launch(q_prox, ldq, q_bs, k_lr, ldk, k_bs, out, ldo, o_bs, H,
                                              G, L, S(stream)),
                      "proxy_scores launch");
+}
+
+int dsv_select_fused(const void* q_prox, long long ldq, long long q_bs, const void* k_lr,
+                     long long ldk, long long k_bs, int H, int G, int L, int r,
+                     const int* k_per_head, int* out_idx, long long out_ld, float* out_thr,
+                     int split, void* stream) {
+  if (H <= 0 || G <= 0 || L <= 0) return fail(DSV_EINVAL, "select_fused: empty shape");
+  if (r < 1 || r > 16) return fail(DSV_EUNSUPPORTED, "select_fused: predictor rank %d (1..16)", r);
+  if (!al16(q_prox) || !al16(k_lr) || (ldq * 2) % 16 || (ldk * 2) % 16 || (q_bs * 2) % 16 ||
+      (k_bs * 2) % 16)
+    return fail(DSV_EINVAL, "select_fused: rows must be 16-byte aligned");
+  CUtensorMap ta, tb;
+  {
+    const uint64_t dims[3] = {(uint64_t)r, (uint64_t)G, (uint64_t)H};
+    const uint64_t st[2] = {(uint64_t)ldq * 2, (uint64_t)(H > 1 ? q_bs : (long long)G * ldq) * 2};
+    const uint32_t box[3] = {16, 128, 1};
+    if (!make_map(&ta, q_prox, 3, dims, st, box, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, CU_TENSOR_MAP_SWIZZLE_32B))
+      return fail(DSV_EINVAL, "select_fused: tensor map Q");
+  }
+  {
+    const uint64_t dims[3] = {(uint64_t)r, (uint64_t)L, (uint64_t)H};
+    const uint64_t st[2] = {(uint64_t)ldk * 2, (uint64_t)(H > 1 ? k_bs : (long long)L * ldk) * 2};
+    const uint32_t box[3] = {16, 128, 1};
+    if (!make_map(&tb, k_lr, 3, dims, st, box, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, CU_TENSOR_MAP_SWIZZLE_32B))
+      return fail(DSV_EINVAL, "select_fused: tensor map K");
+  }
+  // key-range split per 128-row tile (a cluster of `split` CTAs): fewest waves per unit
+  // of per-CTA work, at least one 128-key tile per CTA
+  const int n_mt = H * ((G + 127) / 128), nt = (L + 127) / 128;
+  int ns = split;
+  if (ns <= 0) {
+    const int sms = dsv_device_sm_count();
+    double best = 1e30;
+    for (int s = 1; s <= 4 && s <= nt; ++s) {
+      const double cost = (double)((n_mt * s + sms - 1) / sms) / s;
+      if (cost < best - 1e-9) { best = cost; ns = s; }
+    }
+  }
+  if (ns < 1 || ns > 8 || ns > nt) return fail(DSV_EINVAL, "select_fused: split %d", ns);
+  return cuda_status(dsv_select_fused_launch(&ta, &tb, H, G, L, k_per_head, out_idx, out_ld,
+                                             out_thr, ns, S(stream)),
+                     "select_fused launch");
 }
 
 int dsv_topk(const float* scores, long long ld, int rows, int L, const int* k_per_head,
@@ -319,6 +364,11 @@ __global__ void __launch_bounds__(256) copy_jobs_kernel(const dsv_copy_job* __re
 }
 
 int dsv_debug_timeline_copy(void* dst, int bytes);
+int dsv_debug_select_timeline_copy(void* dst, int bytes);
+extern "C" int dsv_debug_select_timeline(void* host_dst, int bytes) {
+  if (!host_dst || bytes <= 0) return fail(DSV_EINVAL, "debug_select_timeline: bad buffer");
+  return dsv_debug_select_timeline_copy(host_dst, bytes);
+}
 extern "C" int dsv_debug_timeline(void* host_dst, int bytes) {
   if (!host_dst || bytes <= 0) return fail(DSV_EINVAL, "debug_timeline: bad buffer");
   return dsv_debug_timeline_copy(host_dst, bytes);

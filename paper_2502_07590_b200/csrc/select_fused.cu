@@ -1,0 +1,797 @@
+// select_fused.cu — K1b + K2 fused: proxy scores recomputed on tcgen05, exact top-k per
+// row, no [H, G, L] fp32 score matrix in HBM.
+//
+// Semantics: those of K2 (topk.cu; reference pkg/src/dynsparse/selection.py:82-115
+// `_merge_block`, :166-174 emit, :178-242 `twopass_select`) applied to the scores of K1b
+// (reference selection.py:149, Q_lr[proxies] . K_lr^T per head). The score of (row, key)
+// is one tcgen05 kind::f16 M=128 N=128 K=16 MMA on the same bf16 operands as the unfused
+// K1b GEMM (gemm_tc.cu), whose first MMA of the k-block is this instruction and whose
+// other three add products of the zero padding (exact zeros); the values are identical —
+// at most the sign of an exactly-zero score differs, which the selection does not see
+// (-0.0 == +0.0) — so the fused selection equals the unfused one bit for bit.
+//
+// Why: the unfused path writes H G L fp32 scores and K2 reads them twice (c2: 0.8 GB
+// written + 1.6 GB read; c5: 206 GB + 412 GB). Here the scores are recomputed per pass —
+// one MMA per 128 x 128 tile (r <= 16) from TMA-fed shared memory (32B-swizzled 4 KB
+// tiles, 16 in flight), B (K_lr) tiles L2
+// resident — and each pass touches only TMEM, registers and shared memory.
+//
+// CTA = one 128-row tile of one head's proxy rows x a contiguous key range; a cluster
+// of S CTAs splits the key range of one row tile (S chosen so the grid fills the SMs;
+// per-pass partials are combined through distributed shared memory). Warp 0: TMA
+// producer (B ring), warp 1: MMA issuer (4 TMEM accumulators x 128 columns), warps 2..:
+// epilogue, each TMEM lane quadrant covered by kEpiWarps/4 warps that split a tile's
+// 128 columns. Per row, passes over the key range (all rows advance together):
+//   MINMAX / SHIST (a 16-tile strided sample): value-linear 128-bucket histogram of the
+//       sample -> a key band [klo, khi] expected to hold the k-th value T;
+//   FULL (repeat): count keys > khi and histogram the band key-linearly (128 buckets),
+//       or, once the bucket holding T has <= kCap entries, collect them; T is exact when
+//       the bucket is one key value or after the candidate pass;
+//   EMIT: bit masks (s > T) and (s == T) per 32 columns staged in shared memory, then a
+//       warp per row emits ascending column indices, ties at T in column order up to the
+//       row's quota (ties resolve toward lower indices), coalesced per row.
+// Scores are compared as floats: with the order key f2key (-0.0 == +0.0, monotone) every
+// band edge is converted to the float with that key (the one key without a float, the
+// image of -0.0, is handled explicitly). Columns past L are NaN (no comparison holds).
+
+#include <cuda.h>
+#include <stdint.h>
+#include "dsv_common.cuh"
+
+__device__ unsigned long long g_fsel_prof[64][8];
+#ifdef DSV_FSEL_PROF
+#define FPROF_AT(p, e) do { if (blockIdx.x == 0 && (p) < 64) g_fsel_prof[(p)][(e)] = dsv::globaltimer_ns(); } while (0)
+#else
+#define FPROF_AT(p, e) do { } while (0)
+#endif
+
+namespace dsv {
+namespace fsel {
+
+constexpr int BM = 128, BN = 128, BK = 16;   // one K=16 MMA per tile (rank r <= 16)
+constexpr int kStages = 8;                    // B (K_lr) tiles in flight (4 KB each)
+constexpr int kScratch = 36;                  // words per epilogue thread: one 32-column chunk (padded)
+constexpr int kAcc = 4;                       // TMEM accumulators (4 x 128 columns)
+#ifndef DSV_FSEL_EPI_WARPS
+#define DSV_FSEL_EPI_WARPS 16
+#endif
+constexpr int kEpiWarps = DSV_FSEL_EPI_WARPS;
+constexpr int kParts = kEpiWarps / 4;         // threads per row
+constexpr int kCols = BN / kParts;            // columns per thread per tile
+constexpr int kEpiThreads = 32 * kEpiWarps;
+constexpr int kThreads = 64 + kEpiThreads;
+constexpr int kBuckets = 128;
+constexpr int kCap = 128;                     // candidates per row (cluster-wide) = bucket words
+constexpr int kSampleTiles = 48;
+constexpr int kFlushTiles = 8;                // tiles per emission flush (1024 columns)
+constexpr int kStageStride = kFlushTiles * 8 + 1;   // words per row (padded)
+constexpr uint32_t KEY_LO = 0x007FFFFFu;      // key of -inf
+constexpr uint32_t KEY_HI = 0xFF800000u;      // key of +inf
+constexpr uint32_t KEY_NEG0 = 0x7FFFFFFFu;    // the key no float maps to (-0.0 -> +0.0)
+
+#ifndef DSV_FSEL_SLEEP
+#define DSV_FSEL_SLEEP 0
+#endif
+#if DSV_FSEL_SLEEP
+#define FSEL_WAIT mbar_wait_sleep
+#else
+#define FSEL_WAIT mbar_wait
+#endif
+#ifndef DSV_FSEL_ABLATE
+#define DSV_FSEL_ABLATE 0          // 1: epilogue skips the per-element work (pipeline only)
+#endif
+
+enum : uint32_t { ST_REFINE = 0, ST_CAND = 1, ST_DONE = 2 };
+enum : uint32_t { P_MINMAX = 0, P_SHIST = 1, P_FULL = 2, P_EMIT = 3, P_EXIT = 4 };
+
+struct SL {
+  static constexpr int kA = 0;
+  static constexpr int kB = kA + BM * BK * 2;
+  static constexpr int kU = kB + kStages * BN * BK * 2;              // hist / candidates
+  static constexpr int kStage = kU + BM * kBuckets * 4;              // emission masks
+  static constexpr int kRows = kStage + ((BM * kStageStride * 4 + 15) / 16) * 16;
+  static constexpr int kRowArrays = 20;                              // see Rows
+  static constexpr int kScr = kRows + kRowArrays * BM * 4;          // band-element scratch
+  static constexpr int kBar = kScr + kEpiThreads * kScratch * 4;
+  static constexpr int kBytes = kBar + 512 + 1024;
+};
+
+struct Bars {
+  uint64_t full[kStages], empty[kStages], acc_full[kAcc], acc_empty[kAcc], a_full;
+  uint32_t tmem;
+  uint32_t pass, ntiles, flag, nfull;
+};
+
+// per-row state, structure of arrays (BM entries each)
+struct Rows {
+  uint32_t* k; uint32_t* klo; uint32_t* khi; uint32_t* above; uint32_t* state;
+  uint32_t* T; uint32_t* pos; uint32_t* quota; uint32_t* taken; uint32_t* ncand;
+  float* smin; float* smax;
+  uint32_t* cta_above;             // this CTA's count > khi (sum over parts)
+  float* cta_min; float* cta_max;
+  uint32_t* part_above;            // [kParts][BM] (kParts <= 4)
+};
+
+DSV_DEV Rows rows_of(uint8_t* base) {
+  uint32_t* u = reinterpret_cast<uint32_t*>(base);
+  Rows r;
+  r.k = u; r.klo = u + BM; r.khi = u + 2 * BM; r.above = u + 3 * BM; r.state = u + 4 * BM;
+  r.T = u + 5 * BM; r.pos = u + 6 * BM; r.quota = u + 7 * BM; r.taken = u + 8 * BM;
+  r.ncand = u + 9 * BM;
+  r.smin = reinterpret_cast<float*>(u + 10 * BM); r.smax = reinterpret_cast<float*>(u + 11 * BM);
+  r.cta_above = u + 12 * BM;
+  r.cta_min = reinterpret_cast<float*>(u + 13 * BM); r.cta_max = reinterpret_cast<float*>(u + 14 * BM);
+  r.part_above = u + 15 * BM;      // 4 x BM
+  return r;
+}
+
+DSV_DEV uint32_t f2key(float f) {
+  uint32_t u = __float_as_uint(f);
+  if (u == 0x80000000u) u = 0u;
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+DSV_DEV float key2f(uint32_t k) {
+  const uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+  return __uint_as_float(u);
+}
+// float h with (s > h) <=> key(s) > k, for every non-NaN s
+DSV_DEV float upper_f(uint32_t k) { return k == KEY_NEG0 ? __uint_as_float(0x80000001u) : key2f(k); }
+
+// K-major operand, 32-byte rows (16 bf16 along K), 32B-swizzled (TMA SWIZZLE_32B), 8-row
+// groups 256 B apart
+DSV_DEV uint64_t sdesc_sw32(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                 // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(256 >> 4) << 32;        // SBO
+  d |= (uint64_t)1 << 46;                 // descriptor version (Blackwell)
+  d |= (uint64_t)6 << 61;                 // SWIZZLE_32B
+  return d;
+}
+
+// ------------------------------------------------------------------ cluster helpers
+DSV_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+DSV_DEV void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+DSV_DEV uint32_t dsmem_addr(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+DSV_DEV uint32_t ld_dsmem(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+DSV_DEV uint32_t ld_peer(const uint32_t* p, uint32_t rank, uint32_t me) {
+  return rank == me ? *reinterpret_cast<const volatile uint32_t*>(p) : ld_dsmem(dsmem_addr(p, rank));
+}
+
+// key range of cluster rank s: tiles [s nt / S, (s + 1) nt / S)
+DSV_DEV int range_lo(int nt, int S, int s) { return (int)(((long long)nt * s) / S); }
+// i-th sample tile of a range [t0, t1)
+// 1/8 of the range, at least 8 and at most kSampleTiles tiles
+DSV_DEV int sample_count(int n) { return min(n, max(8, min(kSampleTiles, n / 8))); }
+DSV_DEV int sample_tile(int t0, int n, int ns, int i) { return t0 + (int)(((long long)i * n) / ns); }
+
+// tile processed at step i of the current pass
+DSV_DEV int pass_tile(uint32_t pass, int t0, int n, int i) {
+  if (pass == P_MINMAX || pass == P_SHIST) return sample_tile(t0, n, sample_count(n), i);
+  return t0 + i;
+}
+
+template <int N>
+DSV_DEV void tmem_ld_cols(uint32_t taddr, uint32_t (&v)[N]) {
+  static_assert(N % 32 == 0, "columns per thread must be a multiple of 32");
+#pragma unroll
+  for (int c = 0; c < N / 32; ++c) {
+    uint32_t r[32];
+    tmem_ld32(taddr + c * 32, r);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[c * 32 + i] = r[i];
+  }
+}
+
+// ------------------------------------------------------------------ pass finalize
+// One warp per row, after the pass's partials are complete cluster-wide. Lane l owns
+// histogram buckets 4l .. 4l+3 (summed over the cluster's CTAs); "cum(b)" = entries in
+// buckets >= b.
+DSV_DEV uint32_t warp_sum(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+// inclusive suffix sum over lanes (lane l: sum of lanes l..31)
+DSV_DEV uint32_t warp_suffix(uint32_t v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_down_sync(0xffffffffu, v, o);
+    if (lane + o < 32) v += y;
+  }
+  return v;
+}
+
+DSV_DEV void finalize_row(Rows& R, uint32_t* U, int r, int lane, uint32_t pass, uint32_t S,
+                          uint32_t me, uint32_t ns, int L) {
+  const uint32_t st = R.state[r];
+  if (pass == P_MINMAX) {
+    if (lane == 0) {
+      float a = __int_as_float(0x7f800000), b = __int_as_float(0xff800000);
+      for (uint32_t s = 0; s < S; ++s) {
+        a = fminf(a, __uint_as_float(ld_peer(reinterpret_cast<uint32_t*>(R.cta_min) + r, s, me)));
+        b = fmaxf(b, __uint_as_float(ld_peer(reinterpret_cast<uint32_t*>(R.cta_max) + r, s, me)));
+      }
+      R.smin[r] = a;
+      R.smax[r] = b;
+    }
+    return;
+  }
+  if (st == ST_DONE) return;
+  const uint32_t* hrow = U + r * kBuckets + 4 * lane;
+  uint32_t c[4] = {0u, 0u, 0u, 0u};
+  if (pass == P_SHIST || st == ST_REFINE) {
+    for (uint32_t s = 0; s < S; ++s) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) c[q] += ld_peer(hrow + q, s, me);
+    }
+  }
+  const uint32_t lsum = c[0] + c[1] + c[2] + c[3];
+  const uint32_t excl = warp_suffix(lsum, lane) - lsum;     // entries in higher lanes' buckets
+  if (pass == P_SHIST) {
+    const float lo = R.smin[r], hi = R.smax[r];
+    const double tgt = (double)R.k[r] * ns / L;
+    const double marg = 4.0 * sqrt(fmax(tgt * (1.0 - tgt / ns), 0.0)) + 4.0;
+    const double hi_rank = tgt - marg, lo_rank = tgt + marg;
+    // highest bucket with cum > hi_rank / cum >= lo_rank
+    int bh = -1, bl = -1;
+    uint32_t cum = excl;
+#pragma unroll
+    for (int q = 3; q >= 0; --q) {
+      cum += c[q];
+      if (bh < 0 && cum > hi_rank) bh = 4 * lane + q;
+      if (bl < 0 && cum >= lo_rank) bl = 4 * lane + q;
+    }
+    int b_hi = bh, b_lo = bl;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      b_hi = max(b_hi, __shfl_xor_sync(0xffffffffu, b_hi, o));
+      b_lo = max(b_lo, __shfl_xor_sync(0xffffffffu, b_lo, o));
+    }
+    if (lane == 0) {
+      uint32_t klo = KEY_LO, khi = KEY_HI;
+      if (hi > lo) {
+        const float va = (float)kBuckets / (hi - lo);
+        if (b_hi >= 0 && b_hi < kBuckets - 1) khi = f2key(lo + (float)(b_hi + 1) / va);
+        if (b_lo > 0) klo = f2key(lo + (float)b_lo / va);
+        if (klo > khi) { klo = KEY_LO; khi = KEY_HI; }
+        klo = max(klo, KEY_LO);
+        khi = min(khi, KEY_HI);
+      } else if (hi == lo) {
+        klo = khi = f2key(lo);
+      }
+      R.klo[r] = klo;
+      R.khi[r] = khi;
+    }
+    return;
+  }
+  // ---- P_FULL
+  const uint32_t k = R.k[r];
+  uint32_t above = 0;
+  for (uint32_t s = 0; s < S; ++s) above += ld_peer(R.cta_above + r, s, me);
+  const uint32_t klo = R.klo[r], khi = R.khi[r];
+  if (st == ST_REFINE) {
+    const uint32_t band = __shfl_sync(0xffffffffu, excl + lsum, 0);
+    if (above >= k) {                                   // T above the band
+      if (lane == 0) { R.klo[r] = khi + 1; R.khi[r] = KEY_HI; }
+      return;
+    }
+    if (above + band < k) {                             // T below the band
+      if (lane == 0) { R.khi[r] = klo - 1; R.klo[r] = KEY_LO; }
+      return;
+    }
+    // the bucket holding T: entries above it < k <= entries above it + its count
+    int pick = -1;
+    uint32_t pick_above = 0, pick_cnt = 0;
+    uint32_t cum = above + excl;
+#pragma unroll
+    for (int q = 3; q >= 0; --q) {
+      if (pick < 0 && c[q] > 0 && cum < k && cum + c[q] >= k) { pick = 4 * lane + q; pick_above = cum; pick_cnt = c[q]; }
+      cum += c[q];
+    }
+    const uint32_t who = __ballot_sync(0xffffffffu, pick >= 0);
+    const int src = __ffs(who) - 1;
+    pick = __shfl_sync(0xffffffffu, pick, src);
+    pick_above = __shfl_sync(0xffffffffu, pick_above, src);
+    pick_cnt = __shfl_sync(0xffffffffu, pick_cnt, src);
+    const uint64_t span = (uint64_t)(khi - klo) + 1ull;
+    const uint64_t nb = span < (uint64_t)kBuckets ? span : (uint64_t)kBuckets;
+    const uint64_t mult = (nb << 32) / span;
+    const uint64_t bb = (uint64_t)pick;
+    const uint64_t f0 = ((bb << 32) + mult - 1) / mult;
+    const uint64_t f1 = (((bb + 1) << 32) + mult - 1) / mult;
+    const uint32_t nlo = klo + (uint32_t)f0;
+    const uint64_t top = f1 - 1 < (uint64_t)(khi - klo) ? f1 - 1 : (uint64_t)(khi - klo);
+    const uint32_t nhi = klo + (uint32_t)top;
+    uint32_t nst = ST_REFINE;
+    if (nlo == nhi) {
+      // T is this single key: per-CTA counts > T (its count above the old band top plus
+      // its entries in buckets above `pick`) and == T (its entries in `pick`)
+      const uint32_t need = k - pick_above;
+      uint32_t pos = 0, eq_before = 0, my_quota = 0;
+      for (uint32_t s = 0; s <= me; ++s) {
+        uint32_t part = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (4 * lane + q > pick) part += ld_peer(hrow + q, s, me);
+        const uint32_t gt = warp_sum(part) + ld_peer(R.cta_above + r, s, me);
+        const uint32_t eq = ld_peer(U + r * kBuckets + pick, s, me);
+        const uint32_t qv = eq_before >= need ? 0u : min(eq, need - eq_before);
+        if (s < me) pos += gt + qv; else my_quota = qv;
+        eq_before += eq;
+      }
+      nst = ST_DONE;
+      if (lane == 0) { R.T[r] = nlo; R.pos[r] = pos; R.quota[r] = my_quota; }
+    } else if (pick_cnt <= (uint32_t)kCap) {
+      nst = ST_CAND;
+    }
+    if (lane == 0) { R.klo[r] = nlo; R.khi[r] = nhi; R.state[r] = nst; }
+    return;
+  }
+  // ---- ST_CAND: T = the (k - above)-th largest of the band's candidates (all CTAs)
+  // lane holds candidates lane + 32 q of the concatenated per-CTA lists
+  uint32_t cv[4], cs[4];
+  uint32_t n = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) { cv[q] = 0u; cs[q] = 0xffffffffu; }
+  for (uint32_t s = 0; s < S; ++s) {
+    const uint32_t ns = min(ld_peer(R.ncand + r, s, me), (uint32_t)kCap);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t i = (uint32_t)(lane + 32 * q);
+      if (i >= n && i < n + ns && i < (uint32_t)kCap) { cv[q] = ld_peer(U + r * kBuckets + (i - n), s, me); cs[q] = s; }
+    }
+    n += ns;
+  }
+  if (n > (uint32_t)kCap) n = kCap;
+  const uint32_t m = k - above;                         // rank of T among the candidates
+  uint32_t gt[4] = {0u, 0u, 0u, 0u}, eq[4] = {0u, 0u, 0u, 0u};
+  for (uint32_t j = 0; j < n; ++j) {
+    const uint32_t y = __shfl_sync(0xffffffffu, cv[j >> 5], j & 31);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { gt[q] += y > cv[q]; eq[q] += y == cv[q]; }
+  }
+  uint32_t T = 0;
+  bool mine = false;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t i = (uint32_t)(lane + 32 * q);
+    if (i < n && gt[q] < m && m <= gt[q] + eq[q]) { T = cv[q]; mine = true; }
+  }
+  const uint32_t who = __ballot_sync(0xffffffffu, mine);
+  T = __shfl_sync(0xffffffffu, T, __ffs(who) - 1);
+  uint32_t gl = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) gl += (lane + 32 * q < (int)n && cv[q] > T) ? 1u : 0u;
+  const uint32_t need = m - warp_sum(gl);                // ties at T kept, in column order
+  uint32_t pos = 0, eq_before = 0, my_quota = 0;
+  for (uint32_t s = 0; s <= me; ++s) {
+    uint32_t g = 0, e = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (cs[q] == s) { g += cv[q] > T; e += cv[q] == T; }
+    }
+    g = warp_sum(g) + ld_peer(R.cta_above + r, s, me);
+    e = warp_sum(e);
+    const uint32_t qv = eq_before >= need ? 0u : min(e, need - eq_before);
+    if (s < me) pos += g + qv; else my_quota = qv;
+    eq_before += e;
+  }
+  if (lane == 0) { R.T[r] = T; R.pos[r] = pos; R.quota[r] = my_quota; R.state[r] = ST_DONE; }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    int G, int L, int n_mt, const int* __restrict__ kcount,
+                    int* __restrict__ out_idx, long long ldo, float* __restrict__ out_thr) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Bars& B = *reinterpret_cast<Bars*>(smem + SL::kBar);
+  uint32_t* U = reinterpret_cast<uint32_t*>(smem + SL::kU);
+  uint32_t* stage = reinterpret_cast<uint32_t*>(smem + SL::kStage);
+  Rows R = rows_of(smem + SL::kRows);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t S = gridDim.x / (uint32_t)(n_mt);   // cluster size (grid = n_mt x S)
+  const uint32_t me = S > 1 ? cluster_rank() : 0u;
+  const int tile_id = blockIdx.x / S;
+  const int h = tile_id / ((G + BM - 1) / BM);
+  const int m0 = (tile_id - h * ((G + BM - 1) / BM)) * BM;
+  const int nt = (L + BN - 1) / BN;
+  const int t0 = range_lo(nt, S, me), t1 = range_lo(nt, S, me + 1);
+  const int nrange = t1 - t0;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      prefetch_tmap(&tmA);
+      prefetch_tmap(&tmB);
+      for (int s = 0; s < kStages; ++s) { mbar_init(&B.full[s], 1); mbar_init(&B.empty[s], 1); }
+      for (int a = 0; a < kAcc; ++a) { mbar_init(&B.acc_full[a], 1); mbar_init(&B.acc_empty[a], kEpiWarps); }
+      mbar_init(&B.a_full, 1);
+      B.pass = P_MINMAX;
+      B.nfull = 0;
+      B.ntiles = sample_count(nrange);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    tmem_alloc(&B.tmem, 512);
+  }
+  // row state
+  for (int r = threadIdx.x; r < BM; r += kThreads) {
+    const bool live = m0 + r < G;
+    const int kh = kcount[h];
+    R.k[r] = (uint32_t)(kh < 1 ? 1 : (kh > L ? L : kh));
+    R.klo[r] = KEY_LO; R.khi[r] = KEY_HI; R.above[r] = 0;
+    R.state[r] = live ? ST_REFINE : ST_DONE;
+    R.T[r] = 0; R.pos[r] = 0; R.quota[r] = 0; R.taken[r] = 0; R.ncand[r] = 0;
+  }
+  for (int i = threadIdx.x; i < BM * kBuckets; i += kThreads) U[i] = 0;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = B.tmem;
+
+  // cluster-wide sample size (valid columns of every CTA's sample tiles)
+  uint32_t ns_total = 0;
+  for (uint32_t s = 0; s < S; ++s) {
+    const int a0 = range_lo(nt, S, s), n = range_lo(nt, S, s + 1) - a0, cnt = sample_count(n);
+    for (int i = 0; i < cnt; ++i) ns_total += (uint32_t)min(BN, L - sample_tile(a0, n, cnt, i) * BN);
+  }
+  uint32_t seq = 0;    // tiles through the pipeline so far (same count in every role)
+  const bool prof = threadIdx.x == 64;
+  (void)prof;
+  for (int np = 0;; ++np) {
+    __syncthreads();
+    const uint32_t pass = B.pass;
+    const int ntl = (int)B.ntiles;
+    if (pass == P_EXIT) break;
+    if (prof) FPROF_AT(np, 0);
+
+    if (warp == 0) {
+      // ------------------------------------------------------------ TMA producer
+      if (lane == 0) {
+        if (seq == 0) {
+          mbar_arrive_expect_tx(&B.a_full, BM * BK * 2);
+          tma_load_3d(smem + SL::kA, &tmA, &B.a_full, 0, m0, h);
+        }
+        for (int i = 0; i < ntl; ++i, ++seq) {
+          const int t = pass_tile(pass, t0, nrange, i);
+          const int s = seq % kStages;
+          if (seq >= (uint32_t)kStages) FSEL_WAIT(&B.empty[s], ((seq / kStages) - 1) & 1);
+          mbar_arrive_expect_tx(&B.full[s], BN * BK * 2);
+          tma_load_3d(smem + SL::kB + s * (BN * BK * 2), &tmB, &B.full[s], 0, t * BN, h);
+        }
+      } else {
+        seq += ntl;
+      }
+      __syncwarp();
+    } else if (warp == 1) {
+      // ------------------------------------------------------------ MMA issuer
+      if (lane == 0) {
+        constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, 0, 0);
+        if (seq == 0) mbar_wait(&B.a_full, 0);
+        const uint32_t sa = smem_u32(smem + SL::kA);
+        for (int i = 0; i < ntl; ++i, ++seq) {
+          const int s = seq % kStages, a = seq % kAcc;
+          FSEL_WAIT(&B.full[s], (seq / kStages) & 1);
+          if (seq >= (uint32_t)kAcc) FSEL_WAIT(&B.acc_empty[a], ((seq / kAcc) - 1) & 1);
+          tc_fence_after();
+          const uint32_t sb = smem_u32(smem + SL::kB + s * (BN * BK * 2));
+          mma_ss(tmem + a * BN, sdesc_sw32(sa), sdesc_sw32(sb), idesc, 0u);
+          mma_commit(&B.empty[s]);
+          mma_commit(&B.acc_full[a]);
+        }
+      } else {
+        seq += ntl;
+      }
+      __syncwarp();
+    } else {
+      // ------------------------------------------------------------ epilogue
+      const int ew = warp - 2;
+      const int q = warp & 3;                 // TMEM lane quadrant of this warp
+      const int part = ew >> 2;               // column slice of each tile
+      const int row = q * 32 + lane;
+      const uint32_t st = R.state[row];
+      const uint32_t klo = R.klo[row], khi = R.khi[row];
+      const float hi_f = st == ST_DONE ? __int_as_float(0x7f800000) : upper_f(khi);
+      const float lo_f = st == ST_DONE ? __int_as_float(0x7fc00000) : key2f(klo);
+      const uint64_t span = (uint64_t)(khi - klo) + 1ull;
+      const uint64_t nb = span < (uint64_t)kBuckets ? span : (uint64_t)kBuckets;
+      const uint64_t mult = (nb << 32) / span;
+      const float T_f = key2f(R.T[row]);
+      const bool emit_live = st == ST_DONE && m0 + row < G;
+      float va = 0.f, vb = 0.f;               // SHIST mapping: bucket = va * s + vb
+      if (pass == P_SHIST) {
+        const float lo = R.smin[row], hi = R.smax[row];
+        va = (hi > lo) ? (float)kBuckets / (hi - lo) : 0.f;
+        vb = -lo * va;
+      }
+      uint32_t cnt = 0;
+      float mn = __int_as_float(0x7f800000), mx = __int_as_float(0xff800000);
+      uint32_t* hist = U + row * kBuckets;
+      uint32_t* cand = U + row * kBuckets;    // candidates reuse the row's histogram space
+      uint32_t* scr = reinterpret_cast<uint32_t*>(smem + SL::kScr) + (threadIdx.x - 64) * kScratch;
+      int ft = 0, flush_t0 = t0;
+      const bool warp_idle = __all_sync(0xffffffffu, st == ST_DONE);
+
+      for (int i = 0; i < ntl; ++i, ++seq) {
+        const int t = pass_tile(pass, t0, nrange, i);
+        const int a = seq % kAcc;
+        mbar_wait(&B.acc_full[a], (seq / kAcc) & 1);
+        tc_fence_after();
+        if (prof && i == 0) FPROF_AT(np, 1);
+        uint32_t v[kCols];
+        tmem_ld_cols<kCols>(tmem + ((uint32_t)(q * 32) << 16) + a * BN + part * kCols, v);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&B.acc_empty[a]);
+        const int col0 = t * BN + part * kCols;
+        if (col0 + kCols > L) {
+#pragma unroll
+          for (int j = 0; j < kCols; ++j) if (col0 + j >= L) v[j] = 0x7fc00000u;   // NaN
+        }
+        if (DSV_FSEL_ABLATE) {
+          if (v[0] == 0x12345678u && v[kCols - 1] == 0x9abcdef0u) cnt += 1;   // keep the loads
+        } else if (pass == P_FULL) {
+          if (!warp_idle) {
+            // per 32 columns: count above the band (predicated adds) and a band bit mask;
+            // the band entries (rare after the first refinement) are handled per set bit
+#pragma unroll
+            for (int c = 0; c < kCols / 32; ++c) {
+              // four independent partial masks: no serial dependency through one register
+              uint32_t gm[4] = {0u, 0u, 0u, 0u}, bm[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const float s = __uint_as_float(v[c * 32 + j]);
+                const bool gt = s > hi_f;
+                if (gt) gm[j & 3] |= 1u << j;
+                if (!gt && s >= lo_f) bm[j & 3] |= 1u << j;
+              }
+              cnt += __popc((gm[0] | gm[1]) | (gm[2] | gm[3]));
+              const uint32_t band = (bm[0] | bm[1]) | (bm[2] | bm[3]);
+              if (band) {
+                // the chunk goes to this thread's scratch row (conflict-free 16-byte
+                // stores), then only its band entries are visited
+#pragma unroll
+                for (int j = 0; j < 32; j += 4)
+                  *reinterpret_cast<uint4*>(scr + j) = make_uint4(v[c * 32 + j], v[c * 32 + j + 1],
+                                                                  v[c * 32 + j + 2], v[c * 32 + j + 3]);
+                uint32_t bb = band;
+                if (st == ST_REFINE) {
+                  do {
+                    const int j = __ffs(bb) - 1;
+                    bb &= bb - 1;
+                    const uint32_t key = f2key(__uint_as_float(scr[j]));
+                    atomicAdd(hist + (uint32_t)(((uint64_t)(key - klo) * mult) >> 32), 1u);
+                  } while (bb);
+                } else {
+                  const uint32_t slot0 = atomicAdd(R.ncand + row, (uint32_t)__popc(bb));
+                  uint32_t slot = slot0;
+                  do {
+                    const int j = __ffs(bb) - 1;
+                    bb &= bb - 1;
+                    if (slot < (uint32_t)kCap) cand[slot] = f2key(__uint_as_float(scr[j]));
+                    ++slot;
+                  } while (bb);
+                }
+              }
+            }
+          }
+        } else if (pass == P_EMIT) {
+          // masks (s > T) and (s == T), 32 columns per word
+#pragma unroll
+          for (int w = 0; w < kCols / 32; ++w) {
+            uint32_t gm[4] = {0u, 0u, 0u, 0u}, em[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float s = __uint_as_float(v[w * 32 + j]);
+              if (s > T_f) gm[j & 3] |= 1u << j;
+              if (s == T_f) em[j & 3] |= 1u << j;
+            }
+            const uint32_t gt = (gm[0] | gm[1]) | (gm[2] | gm[3]);
+            const uint32_t eq = (em[0] | em[1]) | (em[2] | em[3]);
+            const int wi = part * (kCols / 32) + w;
+            stage[row * kStageStride + ft * 8 + wi] = emit_live ? gt : 0u;
+            stage[row * kStageStride + ft * 8 + 4 + wi] = emit_live ? eq : 0u;
+          }
+          ++ft;
+          if (ft == kFlushTiles || i == ntl - 1) {
+            named_bar_sync(1, kEpiThreads);
+            // flush: warp per row, lane = one 32-column word
+            constexpr int kRowsPerWarp = BM / kEpiWarps;
+            for (int rr = 0; rr < kRowsPerWarp; ++rr) {
+              const int r = ew * kRowsPerWarp + rr;
+              if (m0 + r >= G) continue;
+              const int wt = lane >> 2, wi = lane & 3;
+              uint32_t gt = 0, eq = 0;
+              if (wt < ft) {
+                gt = stage[r * kStageStride + wt * 8 + wi];
+                eq = stage[r * kStageStride + wt * 8 + 4 + wi];
+              }
+              const uint32_t quota = R.quota[r], taken = R.taken[r];
+              const uint32_t ec = __popc(eq);
+              uint32_t ex = ec;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, ex, o);
+                if (lane >= o) ex += y;
+              }
+              const uint32_t eq_before = taken + ex - ec;
+              const uint32_t take = eq_before >= quota ? 0u : min(ec, quota - eq_before);
+              uint32_t keep = 0;
+              if (take == ec) {
+                keep = eq;
+              } else {
+                uint32_t x = eq;
+                for (uint32_t c = 0; c < take; ++c) { const uint32_t lb = x & (0u - x); keep |= lb; x ^= lb; }
+              }
+              uint32_t word = gt | keep;
+              const uint32_t c = __popc(word);
+              uint32_t cx = c;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, cx, o);
+                if (lane >= o) cx += y;
+              }
+              const uint32_t total = __shfl_sync(0xffffffffu, cx, 31);
+              uint32_t tk = take;
+#pragma unroll
+              for (int o = 16; o; o >>= 1) tk += __shfl_xor_sync(0xffffffffu, tk, o);
+              uint32_t p = R.pos[r] + cx - c;
+              int* orow = out_idx + ((long long)h * G + m0 + r) * ldo;
+              const int cbase = (flush_t0 + wt) * BN + wi * 32;
+              while (word) {
+                const int b = __ffs(word) - 1;
+                orow[p++] = cbase + b;
+                word &= word - 1;
+              }
+              __syncwarp();
+              if (lane == 0) { R.pos[r] += total; R.taken[r] = taken + tk; }
+              __syncwarp();
+            }
+            named_bar_sync(1, kEpiThreads);
+            flush_t0 = t0 + i + 1;
+            ft = 0;
+          }
+        } else if (pass == P_MINMAX) {
+#pragma unroll
+          for (int j = 0; j < kCols; ++j) {
+            const float s = __uint_as_float(v[j]);
+            mn = fminf(mn, s);
+            mx = fmaxf(mx, s);
+          }
+        } else {   // P_SHIST
+          if (m0 + row < G) {
+#pragma unroll
+            for (int j = 0; j < kCols; ++j) {
+              const float s = __uint_as_float(v[j]);
+              if (s == s) {
+                const int b = min(max(__float2int_rz(__fmaf_rn(s, va, vb)), 0), kBuckets - 1);
+                atomicAdd(hist + b, 1u);
+              }
+            }
+          }
+        }
+      }
+      // partials of this pass -> per-CTA totals
+      if (prof) FPROF_AT(np, 2);
+      if (pass == P_FULL) R.part_above[part * BM + row] = cnt;
+      if (pass == P_MINMAX) {
+        reinterpret_cast<float*>(R.part_above)[part * BM + row] = mn;
+        reinterpret_cast<float*>(stage)[part * BM + row] = mx;
+      }
+      named_bar_sync(1, kEpiThreads);
+      if (part == 0) {
+        if (pass == P_FULL) {
+          uint32_t c = 0;
+          for (int p = 0; p < kParts; ++p) c += R.part_above[p * BM + row];
+          R.cta_above[row] = c;
+        } else if (pass == P_MINMAX) {
+          float a = __int_as_float(0x7f800000), b = __int_as_float(0xff800000);
+          for (int p = 0; p < kParts; ++p) {
+            a = fminf(a, reinterpret_cast<float*>(R.part_above)[p * BM + row]);
+            b = fmaxf(b, reinterpret_cast<float*>(stage)[p * BM + row]);
+          }
+          R.cta_min[row] = a;
+          R.cta_max[row] = b;
+        }
+      }
+    }
+
+    // ---------------------------------------------------------------- pass end
+    if (prof) FPROF_AT(np, 3);
+    if (S > 1) cluster_sync(); else __syncthreads();
+    if (prof) FPROF_AT(np, 4);
+    if (warp >= 2 && pass != P_EMIT) {
+      for (int r = warp - 2; r < BM; r += kEpiWarps)
+        finalize_row(R, U, r, lane, pass, S, me, ns_total, L);
+    }
+    if (prof) FPROF_AT(np, 5);
+    if (S > 1) cluster_sync(); else __syncthreads();
+    if (prof) FPROF_AT(np, 6);
+    // clear this CTA's partials for the next pass; choose the next pass
+    if (warp >= 2) {
+      const int et = threadIdx.x - 64;
+      for (int i = et; i < BM * kBuckets; i += kEpiThreads) U[i] = 0;
+      for (int r = et; r < BM; r += kEpiThreads) R.ncand[r] = 0;
+      if (et == 0) B.flag = 0;
+      named_bar_sync(1, kEpiThreads);
+      if (et < BM && R.state[et] != ST_DONE) atomicOr(&B.flag, 1u);
+      named_bar_sync(1, kEpiThreads);
+      if (et == 0) {
+        uint32_t next, n;
+        if (pass == P_MINMAX) { next = P_SHIST; n = sample_count(nrange); }
+        else if (pass == P_SHIST || pass == P_FULL) {
+          // (FULL passes are bounded: each narrows the key range 128x; the cap only
+          // guards against a hang)
+          const uint32_t cap = DSV_FSEL_ABLATE ? 3u : 64u;
+          if (B.flag && B.nfull < cap) { next = P_FULL; n = nrange; ++B.nfull; } else { next = P_EMIT; n = nrange; }
+        } else { next = P_EXIT; n = 0; }
+        B.pass = next;
+        B.ntiles = n;
+      }
+    }
+    if (prof) { FPROF_AT(np, 7); }
+    if (pass == P_EMIT) {
+      // thresholds (one CTA of the cluster writes them)
+      if (warp >= 2 && me == 0) {
+        const int et = threadIdx.x - 64;
+        if (et < BM && m0 + et < G) out_thr[(long long)h * G + m0 + et] = key2f(R.T[et]);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+  if (S > 1) cluster_sync();   // no CTA exits while a peer may still read its shared memory
+}
+
+}  // namespace fsel
+}  // namespace dsv
+
+int dsv_select_fused_smem_bytes() { return dsv::fsel::SL::kBytes; }
+
+int dsv_debug_select_timeline_copy(void* dst, int bytes) {
+  const int n = (int)sizeof(g_fsel_prof) < bytes ? (int)sizeof(g_fsel_prof) : bytes;
+  if (cudaMemcpyFromSymbol(dst, g_fsel_prof, n) != cudaSuccess) return -1;
+  return n;
+}
+
+// grid = n_mt row tiles x S key-range CTAs (cluster of S along x)
+int dsv_select_fused_launch(const CUtensorMap* ta, const CUtensorMap* tb, int H, int G, int L,
+                            const int* kcount, int* out_idx, long long ldo, float* out_thr,
+                            int S, cudaStream_t st) {
+  using namespace dsv::fsel;
+  const int n_mt = H * ((G + BM - 1) / BM);
+  auto kern = select_fused_kernel;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SL::kBytes);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(n_mt * S), 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = SL::kBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return (int)cudaLaunchKernelEx(&cfg, kern, *ta, *tb, G, L, n_mt, kcount, out_idx, ldo, out_thr);
+}

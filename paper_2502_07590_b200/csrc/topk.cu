@@ -180,6 +180,8 @@ topk_rows_kernel(const float* __restrict__ scores, long long ld, int rows, int L
   const bool bulk = kSmem && (((ld * 4) & 15) == 0) &&
                     ((reinterpret_cast<uintptr_t>(scores) & 15) == 0) && L >= 4;
   const int n4 = L >> 2;
+  // bulk L2 prefetch of later rows needs 16-byte aligned row starts
+  const bool row_al16 = (((ld * 4) & 15) == 0) && ((reinterpret_cast<uintptr_t>(scores) & 15) == 0);
   const int seg = (((L + kWarps - 1) / kWarps) + 127) & ~127;  // contiguous warp segments (x128)
   const int s0 = warp * seg, s1 = min(L, s0 + seg);
   const uint32_t lt = (1u << lane) - 1u;
@@ -196,7 +198,7 @@ topk_rows_kernel(const float* __restrict__ scores, long long ld, int rows, int L
   for (int row = blockIdx.x; row < rows; row += gridDim.x) {
     const int k = k_per_head[row / rows_per_head];
     const float* grow = scores + (long long)row * ld;
-    if (tid == 0 && row + 2 * (int)gridDim.x < rows && n4 > 0)
+    if (tid == 0 && row + 2 * (int)gridDim.x < rows && n4 > 0 && row_al16)
       prefetch_l2(scores + (long long)(row + 2 * gridDim.x) * ld, (uint32_t)n4 * 16u);
 
     // ---- stage the row (raw fp32) in shared memory

@@ -110,7 +110,11 @@ class DSVAttentionLayer:
     def _scores_topk(self, qp, k_lr, return_scores):
         H, L, G = self.H, self.L, self.G
         hc = H if return_scores else self.score_heads_per_chunk()
-        if hc >= H:
+        if not return_scores and self.fused_select():
+            # K1b + K2 fused: scores recomputed on tcgen05 per pass, never stored
+            idx, thr = ops.select_fused(qp, k_lr, self.kcount, self.k_max)
+            scores = None
+        elif hc >= H:
             scores = ops.gemm_bf16(qp, k_lr, torch.float32)          # [H, G, L] fp32
             idx, thr = ops.topk_rows(scores.view(H * G, L), self.kcount, G, self.k_max)
         else:
@@ -128,6 +132,10 @@ class DSVAttentionLayer:
             scores = None
         sel = SelectedKV(idx.view(H, G, self.k_max), self.kcount, thr.view(H, G), self.ks)
         return (sel, scores) if return_scores else sel
+
+    def fused_select(self) -> bool:
+        """Fused K1b + K2 (select_fused.cu) unless DSV_FUSED_SELECT=0; r <= 16."""
+        return self.r <= 16 and os.environ.get("DSV_FUSED_SELECT", "1") != "0"
 
     def score_heads_per_chunk(self) -> int:
         """Heads scored per pass: the fp32 score matrices stay under DSV_SCORE_BYTES (16 GiB)."""

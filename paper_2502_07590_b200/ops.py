@@ -135,6 +135,37 @@ def topk_rows(scores: torch.Tensor, k_per_head: torch.Tensor, rows_per_head: int
     return idx, thr
 
 
+def select_fused(q_prox: torch.Tensor, k_lr: torch.Tensor, k_per_head: torch.Tensor,
+                 k_max: int | None = None, split: int = 0, out=None):
+    """K1b + K2 fused (select_fused.cu): exact top-k of q_prox[h] . k_lr[h]^T per row.
+
+    q_prox [H, G, r], k_lr [H, L, r] bf16 with unit stride along r (r <= 16). Same result as
+    topk_rows(gemm_bf16(q_prox, k_lr), k_per_head, G) without the [H, G, L] fp32 scores.
+    Returns (idx int32 [H*G, k_max], thr fp32 [H*G]); out: optional preallocated pair.
+    """
+    _require_cuda(q_prox, k_lr, k_per_head)
+    if q_prox.dtype != torch.bfloat16 or k_lr.dtype != torch.bfloat16:
+        raise ValueError("select_fused expects bf16 operands")
+    if q_prox.dim() != 3 or k_lr.dim() != 3 or q_prox.stride(2) != 1 or k_lr.stride(2) != 1:
+        raise ValueError("select_fused operands must be [H, rows, r] with unit stride along r")
+    H, G, r = q_prox.shape
+    H2, L, r2 = k_lr.shape
+    if H2 != H or r2 != r:
+        raise ValueError(f"select_fused shape mismatch {tuple(q_prox.shape)} x {tuple(k_lr.shape)}")
+    kp = k_per_head.to(device=q_prox.device, dtype=torch.int32).contiguous()
+    if k_max is None:
+        k_max = int(kp.max().item())
+    if out is None:
+        idx = torch.empty((H * G, k_max), device=q_prox.device, dtype=torch.int32)
+        thr = torch.empty((H * G,), device=q_prox.device, dtype=torch.float32)
+    else:
+        idx, thr = out
+    _lib.call("dsv_select_fused", _ptr(q_prox), q_prox.stride(1), q_prox.stride(0), _ptr(k_lr),
+              k_lr.stride(1), k_lr.stride(0), H, G, L, r, _ptr(kp), _ptr(idx), idx.stride(0),
+              _ptr(thr), int(split), _stream())
+    return idx, thr
+
+
 # ------------------------------------------------------------------- K3 attention
 def sparse_fwd(q, k, v, grp_rows, grp_size, idx, kcount, scale=None, kcount_hg=None):
     """Group-tiled sparse attention forward. q: [H, Lq, D], k/v: [H, Lk, D] bf16.

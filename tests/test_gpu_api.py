@@ -201,6 +201,7 @@ def test_layer_select_head_chunked_matches_whole(cuda, monkeypatch):
     x = torch.randn((grid.size, 5 * 128), generator=g).to(torch.bfloat16).to(cuda)
     wt = layer.predictor_weights(2)
     whole, _ = layer.select(x, wt, return_scores=True)
+    monkeypatch.setenv("DSV_FUSED_SELECT", "0")
     monkeypatch.setenv("DSV_SCORE_BYTES", str(2 * layer.G * layer.L * 4))
     assert layer.score_heads_per_chunk() == 2
     chunked = layer.select(x, wt)

@@ -54,6 +54,14 @@ def test_topk_random(cuda, L):
     _check_topk(scores, ks, R // 3, cuda)
 
 
+def test_topk_unaligned_row_stride_many_rows(cuda):
+    # row stride 4095 floats (rows not 16-byte aligned) and more rows than 2 x SMs, so the
+    # kernel's look-ahead L2 prefetch would be issued (it must skip unaligned rows)
+    rng = np.random.default_rng(4095)
+    scores = rng.standard_normal((600, 4095)).astype(np.float32)
+    _check_topk(scores, [409, 1, 4000], 200, cuda)
+
+
 def test_topk_global_path(cuda):
     rng = np.random.default_rng(5)
     L = 70000  # beyond the shared-memory row budget
