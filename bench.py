@@ -77,6 +77,9 @@ def _args():
                     help="replay the step as one captured CUDA graph")
     ap.add_argument("--scp", type=int, default=1,
                     help="g_s > 1: hybrid CP, N/g_s head groups x g_s selective-sequence groups")
+    ap.add_argument("--dense-heads", type=int, default=0,
+                    help="the first M heads are dense residual heads (sparsity 0); under --scp "
+                         "they run the ring KV pass (ring.py)")
     return ap.parse_args()
 
 
@@ -202,6 +205,11 @@ def run_gpu(args) -> None:
     grid = TokenGrid(*wl["grid"])
     L, H, D = grid.size, wl["heads"], HEAD_DIM
     sparsity = _sparsities(wl, H)
+    if args.dense_heads:
+        import numpy as np
+
+        sparsity = np.broadcast_to(np.asarray(sparsity, dtype=np.float64), (H,)).copy()
+        sparsity[:args.dense_heads] = 0.0
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
 
     def rnd(*shape):
@@ -248,7 +256,7 @@ def run_gpu(args) -> None:
         def step(ev=None):
             return cp.step(x, wt, q, k, v, do)
         launches_per_step = 8 + 8   # local layer + pack/unpack gathers
-        work = layer.work()
+        work = cp.work() if hasattr(cp, "work") else layer.work()
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -396,6 +404,7 @@ def run_gpu(args) -> None:
                    "parallelism": ("single" if world == 1 else f"hcp{world}" if args.scp == 1
                                    else f"hcp{world // args.scp}xscp{args.scp}"),
                    "head_plan": "balance_heads" if not args.unbalanced else "contiguous",
+                   **({"dense_heads": args.dense_heads} if args.dense_heads else {}),
                    "l2_note": f"inputs (X, Q, K, V, dO: {5 * L * H * D * 2 / 1e9:.2f} GB) exceed the 126 MB L2"},
         "effective_tflops": {"algorithmic": tot_flops / (ms / 1e3) / 1e12,
                              "dense_equivalent": dense_eq / (ms / 1e3) / 1e12},

@@ -26,6 +26,8 @@
  *                        critical-KV prefix length per scored row)
  *   dsv_copy_jobs        cpsim.py:147-156/284-299 HCP head exchange written straight into
  *                        the owners' buffers (peer pointers over NVLink)
+ *   dsv_ring_*           ring KV pass for dense residual heads under SCP (no reference
+ *                        counterpart; dense semantics of attention.py:95-109)
  */
 #ifndef DSV_H_
 #define DSV_H_
@@ -199,6 +201,22 @@ int dsv_debug_select_timeline(void* host_dst, int bytes);
 
 /* fp32 -> bf16 conversion of n contiguous elements. */
 int dsv_f32_to_bf16(const float* in, void* out, long long n, void* stream);
+
+/* Ring KV pass for dense residual heads (no reference counterpart: the
+ * reference only pins the dense semantics, attention.py:95-109 full_attention and
+ * tests/test_cpsim.py:75-88). Element kernels between the per-hop attention launches:
+ *   dsv_ring_lse_merge: merge one hop's partial rows part (bf16 [rows][D], normalised by
+ *     its own softmax sum) with LSE lse_part (log2 domain, as dsv_sparse_fwd writes it)
+ *     into the running fp32 acc [rows][D] / lse_in -> lse_out (first: acc := part);
+ *     out (optional, bf16 [rows][D]) receives the merged rows (the last hop).
+ *   dsv_ring_accum_bf16: acc (fp32) := (first ? 0 : acc) + x (bf16); out optional bf16(acc).
+ *   dsv_ring_accum_f32: acc := (first ? 0 : acc) + part; part := 0 (the traveling dK/dV
+ *     accumulator absorbs one hop's atomically-accumulated contribution). */
+int dsv_ring_lse_merge(float* acc, const float* lse_in, float* lse_out, const void* part,
+                       const float* lse_part, long long rows, int D, int first, void* out,
+                       void* stream);
+int dsv_ring_accum_bf16(float* acc, const void* x, long long n, int first, void* out, void* stream);
+int dsv_ring_accum_f32(float* acc, float* part, long long n, int first, void* stream);
 
 #ifdef __cplusplus
 }

@@ -65,6 +65,10 @@ SIGNATURES = {
     "dsv_gather_rows": [c_void_p, c_longlong, c_void_p, c_int, c_int, c_void_p, c_longlong,
                         c_void_p],
     "dsv_f32_to_bf16": [c_void_p, c_void_p, c_longlong, c_void_p],
+    "dsv_ring_lse_merge": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_longlong, c_int,
+                           c_int, c_void_p, c_void_p],
+    "dsv_ring_accum_bf16": [c_void_p, c_void_p, c_longlong, c_int, c_void_p, c_void_p],
+    "dsv_ring_accum_f32": [c_void_p, c_void_p, c_longlong, c_int, c_void_p],
 }
 _RESTYPES = {"dsv_last_error": ctypes.c_char_p}
 

@@ -30,8 +30,9 @@ import torch.distributed as dist
 from . import cpmodel
 
 PHASES = ("hcp_fwd", "scp_index_exchange", "scp_kv", "output_redistribute", "hcp_bwd_in",
-          "hcp_bwd_out", "scp_grad")   # scp_grad: dK/dV of gathered rows back to their owners
+          "hcp_bwd_out", "scp_grad",   # scp_grad: dK/dV of gathered rows back to their owners
                                        # (the reference simulator is forward-only)
+          "ring_kv", "ring_kv_bwd", "ring_grad")   # ring KV pass of dense heads (ring.py)
 
 
 @dataclass
@@ -637,7 +638,7 @@ class HybridExchange:
         """k_span, v_span [heads, span_len, D] (this rank's heads over its span).
         req: {peer group: [rows per head]} -> {peer group: (K rows, V rows) per head}."""
         dev, D = k_span.device, k_span.shape[2]
-        hp = len(self.heads)
+        hp = k_span.shape[0]          # this rank's sparse heads (dense ones take the ring)
         # 1. requested row lists (per head counts + ids) -> owners
         ids_parts, cnt_parts = [], []
         for g in range(self.g_s):
@@ -685,7 +686,7 @@ class HybridExchange:
         """Backward of fetch_kv: dk_rows/dv_rows {peer group: [rows grads per head]} (fp32)
         are sent to the owners, which add them into dk_span/dv_span [heads, span_len, D]."""
         dev, D = dk_span.device, dk_span.shape[2]
-        hp = len(self.heads)
+        hp = dk_span.shape[0]
         parts = []
         for g in range(self.g_s):
             if g == self.grp or g not in dk_rows:
@@ -852,16 +853,25 @@ class HybridDSV(_PhaseMarks):
     addressed by global token; the gradients of gathered rows go back to their owners
     and the outputs back to the token owners. The span must align with the voxel
     groups (L/g_s tokens = whole frames, a multiple of the voxel depth).
+
+    Dense residual heads (`dense` mask, default: sparsity <= 0, i.e. the heads the
+    dispatcher runs "full") skip selection and selective gathering: the g_s ranks that
+    share such a head pass its K/V chunks around a ring (ring.RingKV, NCCL P2P) and merge
+    the partial outputs by their LSE; the backward returns dK/dV with the ring.
     """
 
     def __init__(self, grid, heads: int, head_dim: int, d_lr: int, voxel, sparsity, g_h: int,
-                 g_s: int, balanced: bool = True, group=None, device="cuda"):
+                 g_s: int, balanced: bool = True, group=None, device="cuda", dense=None):
         from .grouping import build_groups
         from .layer import DSVAttentionLayer
+        from .ring import RingKV
 
         self.H, self.D, self.r, self.L = heads, head_dim, d_lr, grid.size
         sp = np.broadcast_to(np.asarray(sparsity, dtype=np.float64), (heads,)).copy()
-        self.assignment = plan_heads(sp, self.L, head_dim, g_h, balanced)
+        self.dense = (sp <= 0.0) if dense is None else np.broadcast_to(
+            np.asarray(dense, dtype=bool), (heads,)).copy()
+        self.sparsity = np.where(self.dense, 0.0, sp)
+        self.assignment = plan_heads(self.sparsity, self.L, head_dim, g_h, balanced)
         self.ex = HybridExchange(heads, self.L, self.assignment, g_h, g_s, "hcp-first", group)
         span = self.ex.span
         self.s0, self.span_len = int(span[0]), int(span.size)
@@ -875,41 +885,47 @@ class HybridDSV(_PhaseMarks):
             raise ValueError("the sequence span of an SCP group must hold whole voxel groups "
                              "(L / g_s tokens = a multiple of the voxel depth in frames)")
         self.heads = self.ex.heads
-        self.local = DSVAttentionLayer(grid, len(self.heads), head_dim, d_lr, voxel,
-                                       sp[self.heads], device, groups=inside)
         self.device = torch.device(device)
+        self.dloc = [i for i, h in enumerate(self.heads) if self.dense[h]]
+        self.sloc = [i for i, h in enumerate(self.heads) if not self.dense[h]]
+        self.local = (DSVAttentionLayer(grid, len(self.sloc), head_dim, d_lr, voxel,
+                                        sp[self.heads[self.sloc]], device, groups=inside)
+                      if self.sloc else None)
+        self.ring = RingKV(self.ex.scp_group, ledger=self.ex.ledger) if self.dloc else None
+        self._di = torch.tensor(self.dloc, dtype=torch.long, device=self.device)
+        self._si = torch.tensor(self.sloc, dtype=torch.long, device=self.device)
 
-    def step(self, x_local, wt, q, k, v, dout):
-        """x_local [L/N, H*D]; q, k, v, dout [H, L/N, D] -> (out, dq, dk, dv) [H, L/N, D]."""
+    def work(self) -> dict:
+        """Algorithmic work of this rank's heads over the whole sequence (sparse heads:
+        the layer's per-head terms; dense heads: 4 L^2 D forward, 10 L^2 D backward)."""
+        w = dict(self.local.work()) if self.local is not None else {
+            "projection_flops": 0, "estimation_flops": 0, "topk_bytes": 0, "fwd_flops": 0,
+            "bwd_flops": 0}
+        nd = len(self.dloc)
+        w["fwd_flops"] += 4 * nd * self.L * self.L * self.D
+        w["bwd_flops"] += 10 * nd * self.L * self.L * self.D
+        return w
+
+    def _sparse(self, ql, kl, vl, dol, qlr, klr):
+        """Selection + selective KV gathering + sparse attention for the sparse heads.
+        Inputs [hs, span_len, .]; returns (out, dq, dk, dv) [hs, span_len, D] bf16."""
         from . import ops
 
-        ex, hx = self.ex, self.ex.hcp
-        H, r, D, L = self.H, self.r, self.D, self.L
-        hp, dev = len(self.heads), q.device
-        chunk = hx.chunk
+        ex, L, r, D = self.ex, self.L, self.r, self.D
+        hs, dev = ql.shape[0], ql.device
         sl = slice(self.s0, self.s0 + self.span_len)
-        self._mark("start")
-        p = ops.project(x_local, wt)                                    # [L/N, 2 H r]
-        self._mark("project")
-        hm = hx.send_rows_headmajor(dev)
-        p_rows = p.view(chunk * 2 * H, r)
-        h = hx.finish(hx.to_heads_packed(
-            [(t.reshape(H * chunk, D), hm) for t in (q, k, v, dout)]
-            + [(p_rows, hx.send_rows_lowrank(0, dev)), (p_rows, hx.send_rows_lowrank(1, dev))],
-            "hcp_fwd"))
-        ql, kl, vl, dol, qlr, klr = h
-        full = lambda t: torch.empty((hp, L, t.shape[2]), dtype=t.dtype, device=dev)
+        full = lambda t: torch.empty((hs, L, t.shape[2]), dtype=t.dtype, device=dev)
         Qf, Kf, Vf, dOf, Qlr = full(ql), full(kl), full(vl), full(dol), full(qlr)
         for dst, src in ((Qf, ql), (Kf, kl), (Vf, vl), (dOf, dol), (Qlr, qlr)):
             dst[:, sl] = src
         # every key's K_lr for the selection: all-gather over the ranks holding these heads
         parts = [torch.empty_like(klr) for _ in range(ex.g_s)]
         dist.all_gather(parts, klr.contiguous(), group=ex.scp_group)
-        Klr = torch.cat([pp[:, None] for pp in parts], dim=1).reshape(hp, L, r)
+        Klr = torch.cat([pp[:, None] for pp in parts], dim=1).reshape(hs, L, r)
         self._mark("exchange_in")
         sel = self.local.select_from_lowrank(Qlr, Klr)
         self._mark("select")
-        counts = sel.kcount[:, None].expand(hp, self.local.G)
+        counts = sel.kcount[:, None].expand(hs, self.local.G)
         req = ex.requests_from_idx(sel.idx, counts)
         remote = ex.fetch_kv(kl, vl, req)
         for g, per_head in remote.items():
@@ -920,7 +936,7 @@ class HybridDSV(_PhaseMarks):
         self._mark("scp_fetch")
         out, lse = self.local.forward(Qf, Kf, Vf, sel)
         self._mark("fwd")
-        dk32 = torch.zeros((hp, L, D), dtype=torch.float32, device=dev)
+        dk32 = torch.zeros((hs, L, D), dtype=torch.float32, device=dev)
         dv32 = torch.zeros_like(dk32)
         dq, dk32, dv32 = ops.sparse_bwd(Qf, Kf, Vf, out, dOf, lse, self.local.grp_rows,
                                         self.local.grp_size, sel.idx, sel.kcount,
@@ -935,8 +951,46 @@ class HybridDSV(_PhaseMarks):
         dk = ops.f32_to_bf16(dk_span.contiguous())
         dv = ops.f32_to_bf16(dv_span.contiguous())
         self._mark("scp_grad")
-        h_o = hx.to_tokens_packed([out[:, sl].contiguous()], "output_redistribute")
-        grads = hx.finish(hx.to_tokens_packed([dq[:, sl].contiguous(), dk, dv], "hcp_bwd_out"))
+        return out[:, sl].contiguous(), dq[:, sl].contiguous(), dk, dv
+
+    def step(self, x_local, wt, q, k, v, dout):
+        """x_local [L/N, H*D]; q, k, v, dout [H, L/N, D] -> (out, dq, dk, dv) [H, L/N, D]."""
+        from . import ops
+
+        hx = self.ex.hcp
+        H, r, D = self.H, self.r, self.D
+        hp, dev = len(self.heads), q.device
+        chunk = hx.chunk
+        self._mark("start")
+        p = ops.project(x_local, wt)                                    # [L/N, 2 H r]
+        self._mark("project")
+        hm = hx.send_rows_headmajor(dev)
+        p_rows = p.view(chunk * 2 * H, r)
+        h = hx.finish(hx.to_heads_packed(
+            [(t.reshape(H * chunk, D), hm) for t in (q, k, v, dout)]
+            + [(p_rows, hx.send_rows_lowrank(0, dev)), (p_rows, hx.send_rows_lowrank(1, dev))],
+            "hcp_fwd"))
+        ql, kl, vl, dol, qlr, klr = h
+        if not self.dloc:
+            o, dq, dk, dv = self._sparse(ql, kl, vl, dol, qlr, klr)
+        else:
+            o, dq, dk, dv = (torch.empty((hp, self.span_len, D), dtype=torch.bfloat16, device=dev)
+                             for _ in range(4))
+            if self.sloc:
+                si = self._si
+                res = self._sparse(ql[si], kl[si], vl[si], dol[si], qlr[si], klr[si])
+                for dst, src in zip((o, dq, dk, dv), res):
+                    dst[si] = src
+            di = self._di
+            qd, kd, vd, dod = ql[di], kl[di], vl[di], dol[di]
+            od, lse = self.ring.forward(qd, kd, vd)
+            self._mark("ring_fwd")
+            res = (od, *self.ring.backward(qd, kd, vd, od, lse, dod))
+            self._mark("ring_bwd")
+            for dst, src in zip((o, dq, dk, dv), res):
+                dst[di] = src
+        h_o = hx.to_tokens_packed([o], "output_redistribute")
+        grads = hx.finish(hx.to_tokens_packed([dq, dk, dv], "hcp_bwd_out"))
         res = (hx.finish(h_o)[0], *grads)
         self._mark("exchange_out")
         return res

@@ -40,6 +40,10 @@ int dsv_attn_bwd_tc_launch(const void*, const void*, const void*, const void*, c
 int dsv_f32_to_bf16_launch(const float*, void*, long long, cudaStream_t);
 int dsv_select_fused_launch(const CUtensorMap*, const CUtensorMap*, int, int, int, const int*, int*,
                             long long, float*, int, cudaStream_t);
+int dsv_lse_merge_launch(float*, const float*, float*, const void*, const float*, long long, int,
+                         int, void*, cudaStream_t);
+int dsv_accum_bf16_launch(float*, const void*, long long, int, void*, cudaStream_t);
+int dsv_accum_f32_launch(float*, float*, long long, int, cudaStream_t);
 int dsv_proxy_scores_launch(const void*, long long, long long, const void*, long long, long long,
                             float*, long long, long long, int, int, int, cudaStream_t);
 
@@ -309,6 +313,31 @@ int dsv_rows_bwd(const void* q, const void* k, const void* v, const float* out, 
 
 int dsv_f32_to_bf16(const float* in, void* out, long long n, void* stream) {
   return cuda_status(dsv_f32_to_bf16_launch(in, out, n, S(stream)), "f32_to_bf16 launch");
+}
+
+int dsv_ring_lse_merge(float* acc, const float* lse_in, float* lse_out, const void* part,
+                       const float* lse_part, long long rows, int D, int first, void* out,
+                       void* stream) {
+  if (rows < 0 || (D != 64 && D != 128)) return fail(DSV_EINVAL, "ring_lse_merge: D must be 64 or 128");
+  if (!acc || !lse_out || !part || !lse_part || (!first && !lse_in))
+    return fail(DSV_EINVAL, "ring_lse_merge: null operand");
+  if (!al16(acc) || !al16(part) || (out && !al16(out)))
+    return fail(DSV_EINVAL, "ring_lse_merge: rows must be 16-byte aligned");
+  return cuda_status(dsv_lse_merge_launch(acc, lse_in, lse_out, part, lse_part, rows, D, first, out,
+                                          S(stream)), "ring_lse_merge launch");
+}
+
+int dsv_ring_accum_bf16(float* acc, const void* x, long long n, int first, void* out, void* stream) {
+  if (n < 0 || n % 8) return fail(DSV_EINVAL, "ring_accum_bf16: n must be a multiple of 8");
+  if (!al16(acc) || !al16(x) || (out && !al16(out)))
+    return fail(DSV_EINVAL, "ring_accum_bf16: operands must be 16-byte aligned");
+  return cuda_status(dsv_accum_bf16_launch(acc, x, n, first, out, S(stream)), "ring_accum_bf16 launch");
+}
+
+int dsv_ring_accum_f32(float* acc, float* part, long long n, int first, void* stream) {
+  if (n < 0 || n % 4) return fail(DSV_EINVAL, "ring_accum_f32: n must be a multiple of 4");
+  if (!al16(acc) || !al16(part)) return fail(DSV_EINVAL, "ring_accum_f32: operands must be 16-byte aligned");
+  return cuda_status(dsv_accum_f32_launch(acc, part, n, first, S(stream)), "ring_accum_f32 launch");
 }
 
 }  // extern "C"

@@ -299,3 +299,41 @@ def f32_to_bf16(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tenso
         out = torch.empty(x.shape, device=x.device, dtype=torch.bfloat16)
     _lib.call("dsv_f32_to_bf16", _ptr(x), _ptr(out), x.numel(), _stream())
     return out
+
+
+# ------------------------------------------------------------------- ring KV pass
+def _contig(*ts):
+    for t in ts:
+        if t is not None and not t.is_contiguous():
+            raise ValueError("ring kernels need contiguous tensors")
+
+
+def ring_lse_merge(acc, lse_in, lse_out, part, lse_part, first: bool, out=None) -> None:
+    """acc fp32 [..., D] / lse_in -> lse_out fp32 [...]: merge one hop's partial (part bf16,
+    lse_part log2 domain). first: acc := part. out (bf16, optional): the merged rows."""
+    _require_cuda(acc, part, lse_part, lse_out)
+    _contig(acc, lse_in, lse_out, part, lse_part, out)
+    D = acc.shape[-1]
+    rows = acc.numel() // D
+    if part.shape != acc.shape or lse_part.numel() != rows or lse_out.numel() != rows:
+        raise ValueError("ring_lse_merge: shape mismatch")
+    _lib.call("dsv_ring_lse_merge", _ptr(acc), _ptr(lse_in), _ptr(lse_out), _ptr(part),
+              _ptr(lse_part), rows, D, int(first), _ptr(out), _stream())
+
+
+def ring_accum_bf16(acc, x, first: bool, out=None) -> None:
+    """acc fp32 := (first ? 0 : acc) + x (bf16); out (bf16, optional) = the sum."""
+    _require_cuda(acc, x)
+    _contig(acc, x, out)
+    if x.numel() != acc.numel():
+        raise ValueError("ring_accum_bf16: shape mismatch")
+    _lib.call("dsv_ring_accum_bf16", _ptr(acc), _ptr(x), acc.numel(), int(first), _ptr(out), _stream())
+
+
+def ring_accum_f32(acc, part, first: bool) -> None:
+    """acc := (first ? 0 : acc) + part; part := 0."""
+    _require_cuda(acc, part)
+    _contig(acc, part)
+    if part.numel() != acc.numel():
+        raise ValueError("ring_accum_f32: shape mismatch")
+    _lib.call("dsv_ring_accum_f32", _ptr(acc), _ptr(part), acc.numel(), int(first), _stream())

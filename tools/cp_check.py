@@ -1,7 +1,9 @@
 """HCP on N GPUs vs the single-GPU layer on the same inputs (torchrun, NCCL).
 
 usage: torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/cp_check.py [--skewed] [--hybrid]
-(--hybrid: g_h = N/2 head groups x g_s = 2 selective-sequence groups, HybridDSV)
+                [--gs=G] [--dense=M]
+(--hybrid: g_h = N/G head groups x g_s = G (default 2) selective-sequence groups, HybridDSV;
+ --dense=M: the first M heads are dense residual heads, run by the ring KV pass)
 Every rank builds the same global inputs (seeded), keeps its L/N token chunk, runs
 HeadParallelDSV.step; the chunks of O, dQ, dK, dV are gathered and compared with
 DSVAttentionLayer.step on rank 0, and the exchange ledger with hcp_comm.
@@ -32,6 +34,9 @@ def main():
     H, D, r = 8, 128, 16
     L = grid.size
     sp = np.linspace(0.5, 0.95, H) if "--skewed" in sys.argv else np.full(H, 0.9)
+    n_dense = int(next((a.split("=")[1] for a in sys.argv if a.startswith("--dense=")), 0))
+    sp[:n_dense] = 0.0                      # dense residual heads (k = L on one GPU)
+    gs = int(next((a.split("=")[1] for a in sys.argv if a.startswith("--gs=")), 2))
     g = torch.Generator(device="cpu").manual_seed(0)
     x = torch.randn((L, H * D), generator=g).to(torch.bfloat16).to(dev)
     q, k, v, do = (torch.randn((H, L, D), generator=g).to(torch.bfloat16).to(dev) for _ in range(4))
@@ -39,7 +44,7 @@ def main():
     chunk = L // world
     sl = slice(rank * chunk, (rank + 1) * chunk)
     if hybrid:
-        cp = HybridDSV(grid, H, D, r, (8, 4, 4), sp, world // 2, 2, balanced=True, device=dev)
+        cp = HybridDSV(grid, H, D, r, (8, 4, 4), sp, world // gs, gs, balanced=True, device=dev)
     else:
         ov = next((a.split("=")[1] for a in sys.argv if a.startswith("--overlap=")), False)
         cp = HeadParallelDSV(grid, H, D, r, (8, 4, 4), sp, balanced=True, device=dev, overlap=ov)

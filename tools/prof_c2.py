@@ -25,6 +25,7 @@ def main(which):
     sc = ops.gemm_bf16(qp, klr, torch.float32).reshape(H * G, L)   # the layer's K1b path
     kp = torch.full((H,), k, dtype=torch.int32, device=dev)
     idx, _ = ops.topk_rows(sc, kp, G)
+    ops.select_fused(qp, klr, kp, k)                                 # the layer's default (fused K1b+K2)
     idx = idx.reshape(H, G, k)
     q, kk, v, do = (torch.randn((H, L, D), device=dev, generator=g).to(torch.bfloat16) for _ in range(4))
     rows, size = plan.tables(dev)
