@@ -239,7 +239,7 @@ def run_gpu(args) -> None:
     else:
         from paper_2502_07590_b200.cp import HeadParallelDSV, HybridDSV
 
-        if args.scp > 1:
+        if args.scp > 1 or args.dense_heads:   # dense residual heads: ring KV pass (g_s = 1: local)
             cp = HybridDSV(grid, H, D, D_LR, VOXEL, sparsity, world // args.scp, args.scp,
                            balanced=not args.unbalanced, device=dev)
         else:
@@ -256,7 +256,11 @@ def run_gpu(args) -> None:
         def step(ev=None):
             return cp.step(x, wt, q, k, v, do)
         launches_per_step = 8 + 8   # local layer + pack/unpack gathers
-        work = cp.work() if hasattr(cp, "work") else layer.work()
+        if args.dense_heads:        # ring: per hop attend + merge, grad + 2 accumulations; 2 converts
+            launches_per_step += 5 * args.scp + 2
+        # the kernel rooflines below are of the sparse kernels (the `fwd` / `bwd` stages);
+        # dense residual heads (ring stages) are counted in effective_tflops only
+        work = layer.work() if layer is not None else None
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -414,6 +418,7 @@ def run_gpu(args) -> None:
     }
     if stage_ms:
         res["stage_ms"] = stage_ms
+    if stage_ms and work is not None and "bwd" in stage_ms:
         # dominant kernel: sparse backward (tensor-bound by design; scatter-add to L2 limits it)
         bwd_ms = stage_ms["bwd"]
         achieved = work["bwd_flops"] / (bwd_ms / 1e3) / 1e12

@@ -103,7 +103,8 @@ int dsv_topk(const float* scores, long long ld, int rows, int L, const int* k_pe
 /* Group-tiled sparse attention forward (K3f), bf16, head dim D in {64, 128}.
  * q: [H][Lq][D], k, v: [H][Lk][D]; grp_rows: [G][128] int32 member token ids (entries past
  * grp_size[g] repeat a member); idx: [H][G][ldk] int32 ascending key ids with kcount[h] valid
- * entries per row (1..ldk), or, when kcount_hg != NULL, kcount_hg[h*G + g] valid entries.
+ * entries per row (1..ldk), or, when kcount_hg != NULL, kcount_hg[h*G + g] valid entries;
+ * ldk = 0: every (head, group) reads the same list (dense chunks of the ring KV pass).
  * out: [H][Lq][D] bf16; lse: [H][Lq] fp32, log2 domain of the scaled logits. */
 int dsv_sparse_fwd(const void* q, const void* k, const void* v, const int* grp_rows,
                    const int* grp_size, const int* idx, long long ldk, const int* kcount,

@@ -926,8 +926,8 @@ class HybridDSV(_PhaseMarks):
         sel = self.local.select_from_lowrank(Qlr, Klr)
         self._mark("select")
         counts = sel.kcount[:, None].expand(hs, self.local.G)
-        req = ex.requests_from_idx(sel.idx, counts)
-        remote = ex.fetch_kv(kl, vl, req)
+        req = ex.requests_from_idx(sel.idx, counts) if ex.g_s > 1 else {}
+        remote = ex.fetch_kv(kl, vl, req) if ex.g_s > 1 else {}
         for g, per_head in remote.items():
             for hi, (kr, vr) in enumerate(per_head):
                 rows = torch.from_numpy(req[g][hi]).to(dev)
@@ -947,7 +947,8 @@ class HybridDSV(_PhaseMarks):
         dv_rows = {g: [dv32[hi, torch.from_numpy(r).to(dev)] for hi, r in enumerate(per)]
                    for g, per in req.items()}
         dk_span, dv_span = dk32[:, sl], dv32[:, sl]
-        ex.return_grads(dk_rows, dv_rows, dk_span, dv_span)
+        if ex.g_s > 1:
+            ex.return_grads(dk_rows, dv_rows, dk_span, dv_span)
         dk = ops.f32_to_bf16(dk_span.contiguous())
         dv = ops.f32_to_bf16(dv_span.contiguous())
         self._mark("scp_grad")

@@ -261,7 +261,7 @@ int dsv_sparse_fwd(const void* q, const void* k, const void* v, const int* grp_r
                    const int* kcount_hg, int H, int G, int Lq, int Lk, int D, float scale,
                    void* out, float* lse, void* stream) {
   if (D != 64 && D != 128) return fail(DSV_EUNSUPPORTED, "sparse_fwd: head dim %d not 64/128", D);
-  if (H <= 0 || G <= 0 || Lq <= 0 || Lk <= 0 || ldk <= 0)
+  if (H <= 0 || G <= 0 || Lq <= 0 || Lk <= 0 || ldk < 0)
     return fail(DSV_EINVAL, "sparse_fwd: empty shape");
   if (!al16(q) || !al16(k) || !al16(v) || !al16(out) || !al16(grp_rows))
     return fail(DSV_EINVAL, "sparse_fwd: pointers must be 16-byte aligned");
@@ -278,7 +278,7 @@ int dsv_sparse_bwd(const void* q, const void* k, const void* v, const void* out,
                    int G, int Lq, int Lk, int D, float scale, void* dq, float* dk_acc,
                    float* dv_acc, void* stream) {
   if (D != 64 && D != 128) return fail(DSV_EUNSUPPORTED, "sparse_bwd: head dim %d not 64/128", D);
-  if (H <= 0 || G <= 0 || Lq <= 0 || Lk <= 0 || ldk <= 0)
+  if (H <= 0 || G <= 0 || Lq <= 0 || Lk <= 0 || ldk < 0)
     return fail(DSV_EINVAL, "sparse_bwd: empty shape");
   if (!al16(q) || !al16(k) || !al16(v) || !al16(out) || !al16(dout) || !al16(dq) ||
       !al16(dk_acc) || !al16(dv_acc) || !al16(grp_rows))
