@@ -682,6 +682,95 @@ class HybridExchange:
             out[g] = [(r[:, :D], r[:, D:]) for r in torch.split(rows, splits)]
         return out
 
+    # ------------------------------------------------------------------ device-vectorised path
+    def _dev_tables(self, device):
+        key = ("dev", str(device))
+        if getattr(self, "_dev_key", None) != key:
+            self._span_of_d = torch.from_numpy(self.span_of).to(device)
+            self._local_at_d = torch.from_numpy(self.local_at).to(device)
+            self._span_d = torch.from_numpy(self.span).to(device)
+            self._dev_key = key
+        return self._span_of_d, self._local_at_d, self._span_d
+
+    def requests_dev(self, mark):
+        """mark: bool [heads, L], the global key rows this span's queries selected, per local
+        head (any device). Returns (need, cnt): need int64 [n, 2] = (head, global row) of
+        the remote rows, grouped by owner group, then head, then row; cnt int64 host
+        [g_s, heads] = rows requested from each group per head. Same sets as
+        requests_from_idx, without per-head host loops (one host read)."""
+        span_of, _, _ = self._dev_tables(mark.device)
+        hp = mark.shape[0]
+        remote = mark & (span_of != self.grp)[None, :]
+        need = remote.nonzero()                                 # (head, row), row-major order
+        owner = span_of[need[:, 1]]
+        order = torch.sort(owner, stable=True).indices
+        need, owner = need[order], owner[order]
+        cnt = torch.zeros((self.g_s, hp), dtype=torch.int64, device=mark.device)
+        cnt.index_put_((owner, need[:, 0]), torch.ones_like(owner), accumulate=True)
+        return need, cnt.cpu()
+
+    def _a2a_fixed(self, send, recv_splits, send_splits):
+        recv = torch.empty((sum(recv_splits),) + tuple(send.shape[1:]), dtype=send.dtype,
+                           device=send.device)
+        dist.all_to_all_single(recv, send.contiguous(), recv_splits, send_splits,
+                               group=self.scp_group)
+        return recv
+
+    def fetch_kv_dev(self, k_span, v_span, need, cnt):
+        """Device form of fetch_kv: k_span, v_span [heads, span_len, D]; (need, cnt) from
+        requests_dev. Returns [n, 2 D] rows (K | V) aligned with `need`. Same bytes and
+        ledger entries as fetch_kv (8 B per head list + 4 B per index; 2 D elements per row)."""
+        dev, D = k_span.device, k_span.shape[2]
+        hp = k_span.shape[0]
+        _, local_at, _ = self._dev_tables(dev)
+        g_s = self.g_s
+        # 1. per-head counts, then the requested rows as indices inside the owner's span
+        rcnt = torch.empty_like(cnt.to(dev))
+        dist.all_to_all_single(rcnt, cnt.to(dev), group=self.scp_group)
+        rcnt = rcnt.cpu()
+        send_n = [int(cnt[g].sum()) for g in range(g_s)]
+        recv_n = [int(rcnt[g].sum()) for g in range(g_s)]
+        ids = local_at[need[:, 1]].to(torch.int32)
+        got_ids = self._a2a_fixed(ids, recv_n, send_n)
+        for g in range(g_s):
+            if g != self.grp:
+                self.ledger.add("scp_index_exchange", 8 * hp + 4 * send_n[g], 8 * hp + 4 * recv_n[g])
+        # 2. owners serve [K | V] rows in request order (one gather per tensor)
+        heads = torch.repeat_interleave(
+            torch.arange(hp, device=dev).repeat(g_s), rcnt.flatten().to(dev))
+        flat = heads * self.span_len + got_ids.long()
+        serve = torch.empty((flat.numel(), 2 * D), dtype=k_span.dtype, device=dev)
+        if flat.numel():
+            _gather_into(k_span.reshape(-1, D), flat, serve[:, :D])
+            _gather_into(v_span.reshape(-1, D), flat, serve[:, D:])
+        self._served_dev = (flat, recv_n)
+        es = k_span.element_size()
+        for g in range(g_s):
+            if g != self.grp:
+                self.ledger.add("scp_kv", recv_n[g] * 2 * D * es, send_n[g] * 2 * D * es)
+        return self._a2a_fixed(serve, send_n, recv_n)
+
+    def return_grads_dev(self, dk_full, dv_full, need, cnt, dk_span_flat_add):
+        """Backward of fetch_kv_dev: gathers the fp32 gradients of the fetched rows from
+        dk_full/dv_full [heads, L, D] (addressed by global row), sends them to the owners,
+        which add them with dk_span_flat_add(rows_flat_in_span, dk_rows, dv_rows)."""
+        dev, D = dk_full.device, dk_full.shape[2]
+        g_s = self.g_s
+        send_n = [int(cnt[g].sum()) for g in range(g_s)]
+        flat_g = need[:, 0] * self.L + need[:, 1]
+        rows = torch.empty((flat_g.numel(), 2 * D), dtype=dk_full.dtype, device=dev)
+        if flat_g.numel():
+            _gather_into(dk_full.reshape(-1, D), flat_g, rows[:, :D])
+            _gather_into(dv_full.reshape(-1, D), flat_g, rows[:, D:])
+        flat, recv_n = self._served_dev
+        got = self._a2a_fixed(rows, recv_n, send_n)
+        es = dk_full.element_size()
+        for g in range(g_s):
+            if g != self.grp:
+                self.ledger.add("scp_grad", send_n[g] * 2 * D * es, recv_n[g] * 2 * D * es)
+        if flat.numel():
+            dk_span_flat_add(flat, got[:, :D], got[:, D:])
+
     def return_grads(self, dk_rows, dv_rows, dk_span, dv_span):
         """Backward of fetch_kv: dk_rows/dv_rows {peer group: [rows grads per head]} (fp32)
         are sent to the owners, which add them into dk_span/dv_span [heads, span_len, D]."""
@@ -925,14 +1014,16 @@ class HybridDSV(_PhaseMarks):
         self._mark("exchange_in")
         sel = self.local.select_from_lowrank(Qlr, Klr)
         self._mark("select")
-        counts = sel.kcount[:, None].expand(hs, self.local.G)
-        req = ex.requests_from_idx(sel.idx, counts) if ex.g_s > 1 else {}
-        remote = ex.fetch_kv(kl, vl, req) if ex.g_s > 1 else {}
-        for g, per_head in remote.items():
-            for hi, (kr, vr) in enumerate(per_head):
-                rows = torch.from_numpy(req[g][hi]).to(dev)
-                Kf[hi, rows] = kr
-                Vf[hi, rows] = vr
+        if ex.g_s > 1:
+            # the union of the span's critical keys per head, then the remote ones fetched
+            mark = torch.zeros((hs, L), dtype=torch.bool, device=dev)
+            for hi, kh in enumerate(self.local.ks):
+                mark[hi].index_fill_(0, sel.idx[hi, :, :kh].reshape(-1).long(), True)
+            need, cnt = ex.requests_dev(mark)
+            got = ex.fetch_kv_dev(kl, vl, need, cnt)
+            flat = need[:, 0] * L + need[:, 1]
+            Kf.view(-1, D).index_copy_(0, flat, got[:, :D])
+            Vf.view(-1, D).index_copy_(0, flat, got[:, D:])
         self._mark("scp_fetch")
         out, lse = self.local.forward(Qf, Kf, Vf, sel)
         self._mark("fwd")
@@ -942,13 +1033,13 @@ class HybridDSV(_PhaseMarks):
                                         self.local.grp_size, sel.idx, sel.kcount,
                                         self.local.scale, dk32, dv32)
         self._mark("bwd")
-        dk_rows = {g: [dk32[hi, torch.from_numpy(r).to(dev)] for hi, r in enumerate(per)]
-                   for g, per in req.items()}
-        dv_rows = {g: [dv32[hi, torch.from_numpy(r).to(dev)] for hi, r in enumerate(per)]
-                   for g, per in req.items()}
         dk_span, dv_span = dk32[:, sl], dv32[:, sl]
         if ex.g_s > 1:
-            ex.return_grads(dk_rows, dv_rows, dk_span, dv_span)
+            def add_home(flat_span, dk_rows, dv_rows):     # rows addressed inside the span
+                glob = (flat_span // self.span_len) * L + self.s0 + flat_span % self.span_len
+                dk32.view(-1, D).index_add_(0, glob, dk_rows)
+                dv32.view(-1, D).index_add_(0, glob, dv_rows)
+            ex.return_grads_dev(dk32, dv32, need, cnt, add_home)
         dk = ops.f32_to_bf16(dk_span.contiguous())
         dv = ops.f32_to_bf16(dv_span.contiguous())
         self._mark("scp_grad")

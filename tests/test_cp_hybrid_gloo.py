@@ -89,6 +89,39 @@ def _worker(rank, world, port, placement, q):
                 np.add.at(asked[hi], ex.local_at[ids[o:o + c].numpy()], 1.0)
                 o += c
         np.testing.assert_array_equal(dks[:, :, 0].numpy(), asked)
+        # ---- the device-vectorised exchange HybridDSV runs (requests_dev / fetch_kv_dev /
+        # return_grads_dev): the same rows, the same adjoint, the same ledger
+        def run_dev(dtype):
+            ex = HybridExchange(H, S, g["assign"], 2, 2, placement)
+            loc = [torch.from_numpy(g[n][:, rows].copy()).to(dtype) for n in ("q", "k", "v")]
+            _, ks, vs = (ex.hcp.to_heads(t) for t in loc)
+            mark = torch.zeros((len(ex.heads), S), dtype=torch.bool)
+            for hi, h in enumerate(ex.heads):
+                for x in ex.span:
+                    mark[hi, torch.from_numpy(np.asarray(sets[h][x], dtype=np.int64))] = True
+            need, cnt = ex.requests_dev(mark)
+            return ex, ks, vs, need, cnt, ex.fetch_kv_dev(ks, vs, need, cnt)
+
+        exd, ksd, vsd, need, cnt, got = run_dev(torch.float64)
+        want = ~np.isnan(kf[:, :, 0])
+        want[:, ex.span] = False
+        nd = need.numpy()
+        assert sorted(map(tuple, nd.tolist())) == sorted(map(tuple, np.argwhere(want).tolist()))
+        np.testing.assert_array_equal(got[:, :D].numpy(), kf[nd[:, 0], nd[:, 1]])
+        np.testing.assert_array_equal(got[:, D:].numpy(), vf[nd[:, 0], nd[:, 1]])
+        dk_full = torch.zeros((hp, S, D), dtype=torch.float64)
+        dk_full[need[:, 0], need[:, 1]] = 1.0
+        dks_d = torch.zeros_like(ksd)
+
+        def add_home(flat, a, b):
+            dks_d.view(-1, D).index_add_(0, flat, a)
+        exd.return_grads_dev(dk_full, dk_full, need, cnt, add_home)
+        np.testing.assert_array_equal(dks_d[:, :, 0].numpy(), asked)
+        exd2 = run_dev(torch.float16)[0]
+        exd2.hcp.to_tokens(torch.zeros((len(exd2.heads), exd2.span_len, D), dtype=torch.float16))
+        for ph in PHASES:
+            assert exd2.ledger.sent.get(ph, 0) == g[f"{tag}_sent_{ph}"][rank], (ph, "sent", "dev")
+            assert exd2.ledger.received.get(ph, 0) == g[f"{tag}_recv_{ph}"][rank], (ph, "recv", "dev")
         # ---- byte ledger == reference simulator ledger (2-byte elements)
         ex2, _, _, _, _, _ = run(torch.float16)
         ex2.hcp.to_tokens(torch.zeros((len(ex2.heads), ex2.span_len, D), dtype=torch.float16))

@@ -30,13 +30,14 @@ def main():
     torch.cuda.set_device(dev)
     dist.init_process_group("nccl", device_id=dev)
     hybrid = "--hybrid" in sys.argv
-    grid = TokenGrid(16, 16, 16) if hybrid else TokenGrid(8, 16, 16)
+    gs = int(next((a.split("=")[1] for a in sys.argv if a.startswith("--gs=")), 2))
+    # hybrid: every SCP span must hold whole voxel groups (8 frames deep)
+    grid = TokenGrid(8 * gs, 16, 16) if hybrid else TokenGrid(8, 16, 16)
     H, D, r = 8, 128, 16
     L = grid.size
     sp = np.linspace(0.5, 0.95, H) if "--skewed" in sys.argv else np.full(H, 0.9)
     n_dense = int(next((a.split("=")[1] for a in sys.argv if a.startswith("--dense=")), 0))
     sp[:n_dense] = 0.0                      # dense residual heads (k = L on one GPU)
-    gs = int(next((a.split("=")[1] for a in sys.argv if a.startswith("--gs=")), 2))
     g = torch.Generator(device="cpu").manual_seed(0)
     x = torch.randn((L, H * D), generator=g).to(torch.bfloat16).to(dev)
     q, k, v, do = (torch.randn((H, L, D), generator=g).to(torch.bfloat16).to(dev) for _ in range(4))
