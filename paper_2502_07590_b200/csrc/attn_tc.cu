@@ -33,6 +33,7 @@
 // 2x the L2 reduction rate of row-per-thread atomics) by dedicated warps.
 
 #include <cuda.h>
+#include <cstdlib>
 #include "dsv_common.cuh"
 
 namespace dsv {
@@ -967,13 +968,18 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* O
   auto kern = sparse_bwd_kernel<D>;
   const int smem = BwdSmem<D>::kBytes;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  // conversion lag in heads: the converted head's CTAs precede the converter by >= 2 full
-  // waves of CTAs (one per SM), so they have finished (or are resident) — never waits on
-  // an undispatched CTA
+  // conversion lag in heads: the converted head's CTAs precede the converter by >= one
+  // full wave of CTAs (one per SM), so they have been dispatched (most have finished) —
+  // never waits on an undispatched CTA. DSV_CONV_WAVES overrides the wave count.
   int lag = H;
   if (head_done) {
-    lag = (2 * 148 + G - 1) / G;
-    if (lag < 2) lag = 2;
+    static const int waves = [] {
+      const char* e = getenv("DSV_CONV_WAVES");
+      const int w = e ? atoi(e) : 1;
+      return w < 1 ? 1 : w;
+    }();
+    lag = (waves * 148 + G - 1) / G;
+    if (lag < 1) lag = 1;
     if (lag > H) lag = H;
     cudaMemsetAsync(head_done, 0, sizeof(unsigned) * H, st);
   }

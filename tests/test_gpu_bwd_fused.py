@@ -25,9 +25,9 @@ def _rel(a, b):
     return ((a - b).norm() / b.norm().clamp_min(1e-30)).item()
 
 
-# (grid, H): G = 32 groups -> lag 10 (H = 6: tail only; H = 24: 14 heads in-kernel);
-# 16 groups of 64 tokens (H = 3: tail only); c2's grid, G = 260 -> lag 2 (H = 5: 3 in-kernel)
-@pytest.mark.parametrize("dims,H,sp", [((16, 16, 16), 6, 0.9), ((4, 16, 16), 3, 0.75),
+# (grid, H): G = 32 groups -> lag 5 (H = 6: 1 head in-kernel; H = 24: 19);
+# 4 groups (H = 3: tail only); c2's grid, G = 260 -> lag 1 (H = 5: 4 in-kernel)
+@pytest.mark.parametrize("dims,H,sp", [((16, 16, 16), 6, 0.9), ((8, 8, 8), 3, 0.75),
                                        ((8, 16, 16), 1, 0.5), ((16, 16, 16), 24, 0.9),
                                        ((16, 40, 50), 5, 0.9)])
 def test_fused_conversion_matches_unfused(cuda, dims, H, sp):
