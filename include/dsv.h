@@ -120,18 +120,6 @@ int dsv_sparse_bwd(const void* q, const void* k, const void* v, const void* out,
                    int G, int Lq, int Lk, int D, float scale, void* dq, float* dk_acc,
                    float* dv_acc, void* stream);
 
-/* Backward with the dK/dV conversion fused in: dk_acc, dv_acc are fp32 [H][Lk][D]
- * accumulators that must be ZERO on entry and are zero again on return (the kernel re-zeroes
- * them after converting); dk, dv: bf16 [H][Lk][D] results. head_done: workspace of H
- * unsigned (reset by the call). Equals dsv_sparse_bwd followed by an fp32 -> bf16 conversion
- * of the accumulators, without the separate fill and conversion passes. */
-int dsv_sparse_bwd_bf16(const void* q, const void* k, const void* v, const void* out,
-                        const void* dout, const float* lse, const int* grp_rows,
-                        const int* grp_size, const int* idx, long long ldk, const int* kcount,
-                        const int* kcount_hg, int H, int G, int Lq, int Lk, int D, float scale,
-                        void* dq, float* dk_acc, float* dv_acc, void* dk, void* dv,
-                        unsigned* head_done, void* stream);
-
 /* Ragged per-(head, query) CSR sparse attention on CUDA cores (fp32 math), any D <= 256.
  * ptr: [H*Lq + 1] int64 offsets into cols (int32 key ids); cols == NULL selects every key
  * (dense attention, ptr unused). out: [H][Lq][D] fp32,

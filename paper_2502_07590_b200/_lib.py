@@ -44,10 +44,6 @@ SIGNATURES = {
     "dsv_sparse_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                        c_void_p, c_void_p, c_longlong, c_void_p, c_void_p, c_int, c_int, c_int,
                        c_int, c_int, c_float, c_void_p, c_void_p, c_void_p, c_void_p],
-    "dsv_sparse_bwd_bf16": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                            c_void_p, c_void_p, c_longlong, c_void_p, c_void_p, c_int, c_int, c_int,
-                            c_int, c_int, c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                            c_void_p, c_void_p],
     "dsv_rows_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int,
                      c_int, c_float, c_int, c_void_p, c_void_p, c_void_p],
     "dsv_rows_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

@@ -33,7 +33,6 @@
 // 2x the L2 reduction rate of row-per-thread atomics) by dedicated warps.
 
 #include <cuda.h>
-#include <cstdlib>
 #include "dsv_common.cuh"
 
 namespace dsv {
@@ -530,53 +529,6 @@ DSV_DEV uint32_t stg_off(int p, int q) {
   return (uint32_t)(p * (D * 2) + ((q ^ (p & (kC - 1))) << 4));
 }
 
-// Fused accumulator epilogue of the backward: publish this CTA's dK/dV reductions, then
-// convert (and re-zero for the next pass) slice g of the head conv_lag behind, whose CTAs
-// have all finished — its fp32 accumulators are read while still L2-resident (head-major
-// order), replacing a separate fill + conversion pass over HBM. The last conv_lag heads
-// are converted by bwd_convert_tail_kernel. Out of line: keeps the main loop's registers.
-__device__ __noinline__ void bwd_fused_convert(float* dK, float* dV, __nv_bfloat16* dK16,
-                                               __nv_bfloat16* dV16, unsigned* head_done, int h,
-                                               int g, int G, int per_head, int conv_lag) {
-  __threadfence();                                   // this thread's red ops -> counter
-  __syncthreads();
-  if (threadIdx.x == 0) atomicAdd(head_done + h, 1u);
-  const int t = h - conv_lag;
-  if (t < 0) return;
-  if (threadIdx.x == 0) {
-    const unsigned* c = head_done + t;
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
-#ifdef DSV_WATCHDOG
-    const uint64_t t0 = globaltimer_ns();
-#endif
-    while (v < (unsigned)G) {
-      __nanosleep(256);
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
-#ifdef DSV_WATCHDOG
-      if (globaltimer_ns() - t0 > 4000000000ull) __trap();
-#endif
-    }
-    __threadfence();
-  }
-  __syncthreads();
-  const long long n4 = per_head / 4;                  // float4 per tensor per head
-  const long long per = (n4 + G - 1) / G;
-  const long long b0 = (long long)g * per, b1 = min(n4, b0 + per);
-  const long long base = (long long)t * n4;
-  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 1
-  for (int which = 0; which < 2; ++which) {
-    float4* acc = reinterpret_cast<float4*>(which ? dV : dK) + base;
-    uint2* out = reinterpret_cast<uint2*>(which ? dV16 : dK16) + base;
-    for (long long i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
-      const float4 a = acc[i];
-      out[i] = make_uint2(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w));
-      acc[i] = z;
-    }
-  }
-}
-
 template <int D>
 __global__ void __launch_bounds__(kBwdThreads, 1)
 sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __restrict__ dOg,
@@ -586,9 +538,7 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
                   const int* __restrict__ idx, long long ldk, const int* __restrict__ kcount,
                   const int* __restrict__ kcount_hg, int G, int Lq, int Lk, float scale,
                   float scale_log2,
-                  __nv_bfloat16* __restrict__ dQ, float* __restrict__ dK, float* __restrict__ dV,
-                  __nv_bfloat16* __restrict__ dK16, __nv_bfloat16* __restrict__ dV16,
-                  unsigned* __restrict__ head_done, int conv_lag) {
+                  __nv_bfloat16* __restrict__ dQ, float* __restrict__ dK, float* __restrict__ dV) {
   using SL = BwdSmem<D>;
   using GT = Gather<D, kBwdLoadThreads>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -897,23 +847,6 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   tc_fence_before();
   __syncthreads();
   if (warp == kBwdMmaWarp) tmem_dealloc(tmem, 512);
-  if (head_done != nullptr) bwd_fused_convert(dK, dV, dK16, dV16, head_done, h, g, G, Lk * D, conv_lag);
-}
-
-// The heads the backward's fused epilogue leaves (the last conv_lag): fp32 -> bf16 and
-// re-zero the accumulators. n4 = float4 count from head h0 on.
-__global__ void __launch_bounds__(256)
-bwd_convert_tail_kernel(float4* __restrict__ dK, float4* __restrict__ dV, uint2* __restrict__ dK16,
-                        uint2* __restrict__ dV16, long long n4) {
-  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
-       i += (long long)gridDim.x * blockDim.x) {
-    const float4 a = dK[i], b = dV[i];
-    dK16[i] = make_uint2(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w));
-    dV16[i] = make_uint2(pack_bf16(b.x, b.y), pack_bf16(b.z, b.w));
-    dK[i] = z;
-    dV[i] = z;
-  }
 }
 
 __global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
@@ -963,42 +896,15 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* O
                       const float* lse, const int* grp_rows, const int* grp_size, const int* idx,
                       long long ldk, const int* kcount, const int* kcount_hg, int H, int G, int Lq,
                       int Lk, float scale,
-                      float scale_log2, void* dQ, float* dK, float* dV, void* dK16, void* dV16,
-                      unsigned* head_done, cudaStream_t st) {
+                      float scale_log2, void* dQ, float* dK, float* dV, cudaStream_t st) {
   auto kern = sparse_bwd_kernel<D>;
   const int smem = BwdSmem<D>::kBytes;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  // conversion lag in heads: the converted head's CTAs precede the converter by >= one
-  // full wave of CTAs (one per SM), so they have been dispatched (most have finished) —
-  // never waits on an undispatched CTA. DSV_CONV_WAVES overrides the wave count.
-  int lag = H;
-  if (head_done) {
-    static const int waves = [] {
-      const char* e = getenv("DSV_CONV_WAVES");
-      const int w = e ? atoi(e) : 1;
-      return w < 1 ? 1 : w;
-    }();
-    lag = (waves * 148 + G - 1) / G;
-    if (lag < 1) lag = 1;
-    if (lag > H) lag = H;
-    cudaMemsetAsync(head_done, 0, sizeof(unsigned) * H, st);
-  }
   kern<<<H * G, kBwdThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)dO,
                                       (const __nv_bfloat16*)k, (const __nv_bfloat16*)v,
                                       (const __nv_bfloat16*)O, lse, grp_rows, grp_size, idx, ldk,
                                       kcount, kcount_hg, G, Lq, Lk, scale, scale_log2,
-                                      (__nv_bfloat16*)dQ, dK, dV, (__nv_bfloat16*)dK16,
-                                      (__nv_bfloat16*)dV16, head_done, lag);
-  if (head_done) {
-    const int h0 = H - lag;
-    const long long off = (long long)h0 * Lk * D / 4;
-    const long long n4 = (long long)lag * Lk * D / 4;
-    long long blocks = (n4 + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    bwd_convert_tail_kernel<<<(unsigned)blocks, 256, 0, st>>>(
-        reinterpret_cast<float4*>(dK) + off, reinterpret_cast<float4*>(dV) + off,
-        reinterpret_cast<uint2*>(dK16) + off, reinterpret_cast<uint2*>(dV16) + off, n4);
-  }
+                                      (__nv_bfloat16*)dQ, dK, dV);
   return (int)cudaGetLastError();
 }
 
@@ -1006,14 +912,13 @@ int dsv_attn_bwd_tc_launch(const void* q, const void* k, const void* v, const vo
                            const void* dO, const float* lse, const int* grp_rows,
                            const int* grp_size, const int* idx, long long ldk, const int* kcount,
                            const int* kcount_hg, int H, int G, int Lq, int Lk, int D, float scale,
-                           float scale_log2, void* dQ, float* dK, float* dV, void* dK16,
-                           void* dV16, unsigned* head_done, cudaStream_t st) {
+                           float scale_log2, void* dQ, float* dK, float* dV, cudaStream_t st) {
   if (D == 128)
     return bwd_launch<128>(q, k, v, O, dO, lse, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H,
-                           G, Lq, Lk, scale, scale_log2, dQ, dK, dV, dK16, dV16, head_done, st);
+                           G, Lq, Lk, scale, scale_log2, dQ, dK, dV, st);
   if (D == 64)
     return bwd_launch<64>(q, k, v, O, dO, lse, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H,
-                          G, Lq, Lk, scale, scale_log2, dQ, dK, dV, dK16, dV16, head_done, st);
+                          G, Lq, Lk, scale, scale_log2, dQ, dK, dV, st);
   return 1;
 }
 

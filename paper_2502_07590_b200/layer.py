@@ -149,30 +149,12 @@ class DSVAttentionLayer:
                               self.scale)
 
     def backward(self, q, k, v, out, lse, dout, sel: SelectedKV, dk_acc=None, dv_acc=None):
-        """-> (dq, dk, dv) bf16. Without caller accumulators the layer's own zero-invariant
-        fp32 accumulators are used and the kernel converts them itself (dsv_sparse_bwd_bf16:
-        no fill or conversion pass; DSV_FUSED_CONVERT=0 for the unfused path)."""
-        if dk_acc is None and os.environ.get("DSV_FUSED_CONVERT", "1") != "0":
-            acc = self._accumulators(k.shape[1], q.device)
-            return ops.sparse_bwd_bf16(q, k, v, out, dout, lse, self.grp_rows, self.grp_size,
-                                       sel.idx, sel.kcount, acc[0], acc[1], self.scale,
-                                       head_done=acc[2])
         if dk_acc is not None:
             dk_acc.zero_()
             dv_acc.zero_()
         dq, dk32, dv32 = ops.sparse_bwd(q, k, v, out, dout, lse, self.grp_rows, self.grp_size,
                                         sel.idx, sel.kcount, self.scale, dk_acc, dv_acc)
         return dq, ops.f32_to_bf16(dk32), ops.f32_to_bf16(dv32)
-
-    def _accumulators(self, n_keys: int, device):
-        """Persistent dK/dV fp32 accumulators (zero between calls: the fused backward
-        re-zeroes them) and the per-head completion counters."""
-        key = (int(n_keys), str(device))
-        if self.__dict__.get("_acc_key") != key:
-            z = torch.zeros((2, self.H, n_keys, self.D), device=device, dtype=torch.float32)
-            self._acc = (z[0], z[1], torch.zeros((self.H,), device=device, dtype=torch.int32))
-            self._acc_key = key
-        return self._acc
 
     def step(self, x, wt, q, k, v, dout, dk_acc=None, dv_acc=None):
         """One fwd+bwd pass of the layer (the bench's unit of work)."""

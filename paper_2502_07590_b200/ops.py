@@ -208,30 +208,6 @@ def sparse_bwd(q, k, v, out, dout, lse, grp_rows, grp_size, idx, kcount, scale=N
     return dq, dk_acc, dv_acc
 
 
-def sparse_bwd_bf16(q, k, v, out, dout, lse, grp_rows, grp_size, idx, kcount, dk_acc, dv_acc,
-                    scale=None, kcount_hg=None, head_done=None):
-    """Backward with the dK/dV conversion fused in (dsv_sparse_bwd_bf16). dk_acc/dv_acc fp32
-    [H, Lk, D] must be zero on entry and are zero again afterwards. Returns (dq, dk, dv) bf16."""
-    _require_cuda(q, k, v, out, dout, lse, dk_acc, dv_acc)
-    H, Lq, D = q.shape
-    Lk = k.shape[1]
-    G = grp_rows.shape[0]
-    if dk_acc.shape != (H, Lk, D) or dv_acc.shape != (H, Lk, D) or dk_acc.dtype != torch.float32:
-        raise ValueError("sparse_bwd_bf16: accumulators must be fp32 [H, Lk, D]")
-    if scale is None:
-        scale = 1.0 / math.sqrt(D)
-    if head_done is None:
-        head_done = torch.empty((H,), device=q.device, dtype=torch.int32)
-    dq = torch.empty_like(q)
-    dk = torch.empty((H, Lk, D), device=q.device, dtype=torch.bfloat16)
-    dv = torch.empty_like(dk)
-    _lib.call("dsv_sparse_bwd_bf16", _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(dout), _ptr(lse),
-              _ptr(grp_rows), _ptr(grp_size), _ptr(idx), idx.stride(1), _ptr(kcount),
-              _ptr(kcount_hg), H, G, Lq, Lk, D, float(scale), _ptr(dq), _ptr(dk_acc),
-              _ptr(dv_acc), _ptr(dk), _ptr(dv), _ptr(head_done), _stream())
-    return dq, dk, dv
-
-
 def rows_fwd(q, k, v, ptr, cols, scale=None):
     """Ragged CSR sparse attention forward on CUDA cores (cols None = every key).
 
