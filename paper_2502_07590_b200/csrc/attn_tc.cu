@@ -99,11 +99,16 @@ struct FwdBars {
   uint64_t s_full[kFwdSBufs], p_full[kFwdSBufs], pv_done[kFwdSBufs];
   uint64_t o_final;
   uint32_t tmem;
+  uint32_t ovf;             // lazy-max pass: some score exceeded the row's reference max by > 2^64
 };
 
 #ifndef DSV_FWD_ABLATE
 #define DSV_FWD_ABLATE 0   // 1: ablation build only (forward without the softmax math)
 #endif
+#ifndef DSV_FWD_LAZY
+#define DSV_FWD_LAZY 1     // 0: exchange the row max every key block (the exact-max pass only)
+#endif
+constexpr float kLazyLimit = 64.f;   // log2 headroom of the lazy-max pass
 // Optional in-kernel timeline (variant builds with -DDSV_BWD_PROF / -DDSV_FWD_PROF):
 // clock64 stamps of each role's phase boundaries for the first kProfCtas CTAs of the
 // backward (or forward) kernel, read back by dsv_debug_timeline.
@@ -244,19 +249,21 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   const int* irow = idx + ((long long)h * G + g) * ldk;
   const int* mrow = grp_rows + (long long)g * BQ;
 
-  if (warp == kFwdMmaWarp) {
-    if (lane == 0) {
-      mbar_init(&B.q_full, kProdThreads);
-      for (int s = 0; s < KST; ++s) { mbar_init(&B.k_full[s], kProdThreads / 2); mbar_init(&B.k_empty[s], 1); }
-      for (int s = 0; s < ST; ++s) { mbar_init(&B.v_full[s], kProdThreads / 2); mbar_init(&B.v_empty[s], 1); }
-      for (int s = 0; s < NS; ++s) {
-        mbar_init(&B.s_full[s], 1);
-        mbar_init(&B.p_full[s], kFwdSoftThreads);
-        mbar_init(&B.pv_done[s], 1);
-      }
-      mbar_init(&B.o_final, 1);
-      fence_barrier_init();
+  auto init_bars = [&]() {
+    mbar_init(&B.q_full, kProdThreads);
+    for (int s = 0; s < KST; ++s) { mbar_init(&B.k_full[s], kProdThreads / 2); mbar_init(&B.k_empty[s], 1); }
+    for (int s = 0; s < ST; ++s) { mbar_init(&B.v_full[s], kProdThreads / 2); mbar_init(&B.v_empty[s], 1); }
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&B.s_full[s], 1);
+      mbar_init(&B.p_full[s], kFwdSoftThreads);
+      mbar_init(&B.pv_done[s], 1);
     }
+    mbar_init(&B.o_final, 1);
+    B.ovf = 0u;
+    fence_barrier_init();
+  };
+  if (warp == kFwdMmaWarp) {
+    if (lane == 0) init_bars();
     __syncwarp();
     tmem_alloc(&B.tmem, 512);
   }
@@ -265,6 +272,16 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   tc_fence_after();
   const uint32_t tmem = B.tmem;
   const uint32_t tS0 = tmem, tO = tmem + NS * 128;   // S/P buffer b at tS0 + 128 b
+
+  // Pass 0 (lazy max): the row max is exchanged between the 16 softmax warps for key
+  // block 0 only; later blocks exponentiate against it without a barrier, each warp
+  // checking that its scores stay within 2^64 of it (P, O and the row sums are fp32 /
+  // bf16 with 2^127 range, and relative precision does not depend on the scale). A tile
+  // where some score exceeds that is flagged and re-run as pass 1, which exchanges the
+  // max every block and rescales O when it grows by > 2^8.
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+  const bool lazy = DSV_FWD_LAZY && pass == 0;
 
   if (warp >= kFwdProdWarp0) {
     // ------------------------------------------------------------ producers
@@ -356,6 +373,7 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
     constexpr int kOc = D / kFwdSoftWGs;              // O columns per warp (rescale, store)
     float m_run = -INFINITY, l_run = 0.f;
+    bool ovf_local = false;
     for (int j = 0; j < nblk; ++j) {
       const int kv = min(BKV, kh - j * BKV);
       const uint32_t tS = tS0 + (j % NS) * 128 + lane_off;
@@ -377,6 +395,10 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
         for (int i = 0; i < 32; ++i)
           if (cq * 32 + i < kv) mx = fmaxf(mx, __uint_as_float(r[i]));
       }
+      if (lazy && j > 0) {
+        // no exchange: this warp's 32 columns against the row's block-0 max
+        ovf_local |= mx * scale_log2 > m_run + kLazyLimit;
+      } else {
       // row max over the four column slices, through a parity double buffer
       float* xch = sMax + (j & 1) * (kFwdSoftWGs * 128);
       xch[cq * 128 + row] = mx;
@@ -405,6 +427,7 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
           tmem_st16(tO + lane_off + c, o);
         }
         m_run = mx;
+      }
       }
       // P = 2^(s scale_log2 - m) for keys [32 cq, +32): bf16 into columns [16 cq, +16)
       const f32x2 sc2 = f2(scale_log2, scale_log2), nm2 = f2(-m_run, -m_run);
@@ -456,9 +479,18 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
       }
     }
     if (cq == 0 && row < gsz) lse[(long long)h * Lq + tok] = m_run + __log2f(denom);
+    if (__any_sync(0xffffffffu, ovf_local) && lane == 0) atomicOr(&B.ovf, 1u);
   }
   tc_fence_before();
   __syncthreads();
+  if (!lazy || B.ovf == 0u) break;                   // uniform: read after the barrier
+  // flagged tile: every async op of pass 0 has completed (O final observed, producers
+  // drained their copies) -> re-arm the barriers and run the exact-max pass
+  if (warp == kFwdMmaWarp && lane == 0) init_bars();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  }
   if (warp == kFwdMmaWarp) tmem_dealloc(tmem, 512);
 }
 

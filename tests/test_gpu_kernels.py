@@ -227,10 +227,13 @@ def test_sparse_fwd_full_set_equals_dense(cuda):
     assert np.max(np.abs(out.float().cpu().numpy()[0] - ref)) < 3e-2
 
 
-def test_sparse_fwd_late_max_jump_on_some_rows(cuda):
-    # a few query rows meet a key in the last key block whose logit is far above the rows'
+@pytest.mark.parametrize("gain,where", [(1.0, "last"), (6.0, "last"), (6.0, "middle")])
+def test_sparse_fwd_late_max_jump_on_some_rows(cuda, gain, where):
+    # a few query rows meet a key in a later key block whose logit is far above the rows'
     # running max (online-softmax rescale), the other rows of the same warp do not: the
-    # rescale must stay warp-uniform (tcgen05.ld/st are warp-collective)
+    # rescale must stay warp-uniform (tcgen05.ld/st are warp-collective). gain 1: a jump
+    # of ~16 (log2) that the lazy-max pass absorbs; gain 6: ~98, beyond its 2^64 headroom,
+    # so the tile is flagged and re-run with the per-block max exchange.
     D, H = 128, 1
     plan = build_groups(TokenGrid(4, 8, 16), (2, 8, 8))
     L = plan.grid.size
@@ -238,7 +241,7 @@ def test_sparse_fwd_late_max_jump_on_some_rows(cuda):
     q, k, v, do = (rng.standard_normal((H, L, D)).astype(np.float32) for _ in range(4))
     hot = rng.choice(L, size=20, replace=False)
     for i, r in enumerate(hot):
-        k[0, L - 1 - i] = q[0, r]
+        k[0, (L - 1 - i) if where == "last" else (L // 2 + 3 * i)] = gain * q[0, r]
     idx = np.tile(np.arange(L, dtype=np.int32), (H, plan.n_groups, 1))
     rows, size = plan.tables(cuda)
     kc = torch.tensor([L], dtype=torch.int32, device=cuda)
