@@ -160,8 +160,10 @@ DSV_DEV float softmax_max_pass(uint32_t tS, int kv) {
 }
 
 #ifndef DSV_POLY_EVERY
-#define DSV_POLY_EVERY 4      // one pair in DSV_POLY_EVERY takes the polynomial (0: none)
-#endif
+#define DSV_POLY_EVERY 0      // one pair in DSV_POLY_EVERY takes the polynomial (0: none).
+#endif                        // With the lazy max (no per-block exchange) all-MUFU measured
+                              // fastest at c2: 1.431 ms vs 1.440 / 1.447 / 1.451 / 1.474
+                              // for one pair in 16 / 6 / 8 / 4 (tools/fwd_bench.py)
 #ifndef DSV_P_CHUNKS
 #define DSV_P_CHUNKS 2        // 32-column chunks loaded per TMEM wait in pass 2
 #endif
