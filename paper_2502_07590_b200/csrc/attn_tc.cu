@@ -359,7 +359,8 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
         const uint32_t tP = tS0 + (j % NS) * 128;
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_ts(tO, tP + kk * 8, sdesc_sw128(aV + kk * 2048, 128 * 128, 1024), idO, (j > 0 || kk > 0));
+          mma_ts(tO, tP + (kk >> 1) * 32 + (kk & 1) * 8, sdesc_sw128(aV + kk * 2048, 128 * 128, 1024),
+                 idO, (j > 0 || kk > 0));   // P of keys [32c, +32) sits in S columns [32c, +16)
         mma_commit(&B.v_empty[st]);
         mma_commit(&B.pv_done[j % NS]);
         if (j == nblk - 1) mma_commit(&B.o_final);
@@ -382,8 +383,6 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
       mbar_wait(&B.s_full[j % NS], (j / NS) & 1);
       tc_fence_after();
       if (warp == 0 && lane == 0) FPROF(j, 2);
-      // the 32 raw scores stay in registers across the max exchange, so the in-place
-      // P writes below cannot race with another warp's reads
       uint32_t r[32];
       tmem_ld32(tS + cq * 32, r);
       tmem_ld_wait();
@@ -431,7 +430,9 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
         m_run = mx;
       }
       }
-      // P = 2^(s scale_log2 - m) for keys [32 cq, +32): bf16 into columns [16 cq, +16)
+      // P = 2^(s scale_log2 - m) for keys [32 cq, +32): bf16 into columns [32 cq, +16),
+      // i.e. over this warp's own scores (already in registers) — no other warp reads
+      // them, so the lazy-max blocks need no barrier at all
       const f32x2 sc2 = f2(scale_log2, scale_log2), nm2 = f2(-m_run, -m_run);
       f32x2 lsum2 = f2(0.f, 0.f);
 #if DSV_FWD_ABLATE == 1
@@ -439,11 +440,11 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) pk[i] = r[2 * i] ^ r[2 * i + 1];
-        tmem_st16(tS + cq * 16, pk);
+        tmem_st16(tS + cq * 32, pk);
       }
 #else
-      if (kv == BKV) softmax_p_chunk<false>(r, tS + cq * 16, sc2, nm2, cq, kv, lsum2);
-      else softmax_p_chunk<true>(r, tS + cq * 16, sc2, nm2, cq, kv, lsum2);
+      if (kv == BKV) softmax_p_chunk<false>(r, tS + cq * 32, sc2, nm2, cq, kv, lsum2);
+      else softmax_p_chunk<true>(r, tS + cq * 32, sc2, nm2, cq, kv, lsum2);
 #endif
       const float2 ls = f2u(lsum2);
       l_run += ls.x + ls.y;

@@ -356,5 +356,8 @@ DSV_DEV void red_add_v4(float* addr, float a, float b, float c, float d) {
 DSV_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(nthreads) : "memory");
 }
+DSV_DEV void named_bar_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;" :: "r"(id), "r"(nthreads) : "memory");
+}
 
 }  // namespace dsv
