@@ -68,7 +68,10 @@ DSV_DEV void issue_tile(uint8_t* tile, const __nv_bfloat16* base,
 }
 
 // ====================================================================== fwd
-constexpr int kFwdKStages = 2;                                   // K_j frees after S_j
+#ifndef DSV_FWD_KSTAGES
+#define DSV_FWD_KSTAGES 3
+#endif
+constexpr int kFwdKStages = DSV_FWD_KSTAGES;                     // K_j frees after S_j
 constexpr int kFwdStages = 3;                                    // V ring (frees after PV_j)
 constexpr int kFwdSBufs = 3;                                     // S/P buffers in TMEM
 #ifndef DSV_FWD_SOFT_WGS
@@ -86,9 +89,13 @@ struct FwdSmem {
   static constexpr int kQ = 0;
   static constexpr int kK = kQ + kTile;
   static constexpr int kV = kK + kFwdKStages * kTile;
-  static constexpr int kMax = kV + kFwdStages * kTile;   // [2 parity][4 slices][128] fp32
-  static constexpr int kBar = kMax + 2 * kFwdSoftWGs * 128 * 4;
-  static constexpr int kBytes = kBar + 256 + 1024;
+  static constexpr int kMax = kV + kFwdStages * kTile;   // [4 slices][128] fp32 row exchange
+  static constexpr int kBar = kMax + kFwdSoftWGs * 128 * 4;
+  // Q + 3 K + 3 V tiles (D = 128: 224 KB) leave no room for alignment slack: the dynamic
+  // shared window starts 1024-aligned (checked at kernel entry)
+  static constexpr int kBytes = kBar + 256 + (kFwdKStages + kFwdStages >= 6 && D == 128 ? 0 : 1024);
+  static constexpr bool kSlack = !(kFwdKStages + kFwdStages >= 6 && D == 128);
+  static_assert(kBytes <= 232448, "forward shared memory over 227 KB");
 };
 
 struct FwdBars {
@@ -101,6 +108,7 @@ struct FwdBars {
   uint32_t tmem;
   uint32_t ovf;             // lazy-max pass: some score exceeded the row's reference max by > 2^64
 };
+static_assert(sizeof(FwdBars) <= 256, "forward barriers over their 256 B");
 
 #ifndef DSV_FWD_ABLATE
 #define DSV_FWD_ABLATE 0   // 1: ablation build only (forward without the softmax math)
@@ -237,7 +245,8 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   using GT = Gather<D>;
   constexpr int ST = kFwdStages, KST = kFwdKStages, NS = kFwdSBufs;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = aligned_smem(smem_raw);
+  uint8_t* smem = SL::kSlack ? aligned_smem(smem_raw) : smem_raw;
+  if (!SL::kSlack && (smem_u32(smem_raw) & 1023u)) __trap();    // see FwdSmem
   FwdBars& B = *reinterpret_cast<FwdBars*>(smem + SL::kBar);
   uint8_t* sQ = smem + SL::kQ;
   uint8_t* sK = smem + SL::kK;
@@ -400,12 +409,14 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
         // no exchange: this warp's 32 columns against the row's block-0 max
         ovf_local |= mx * scale_log2 > m_run + kLazyLimit;
       } else {
-      // row max over the four column slices, through a parity double buffer
-      float* xch = sMax + (j & 1) * (kFwdSoftWGs * 128);
+      // row max over the four column slices, through shared memory (one buffer: a
+      // second barrier frees it before the next exchange)
+      float* xch = sMax;
       xch[cq * 128 + row] = mx;
       if (warp == 0 && lane == 0) FPROF(j, 8);
       named_bar_sync(1, kFwdSoftThreads);
       mx = fmax3f(fmaxf(xch[row], xch[128 + row]), xch[256 + row], xch[384 + row]) * scale_log2;
+      named_bar_sync(1, kFwdSoftThreads);
       if (warp == 0 && lane == 0) FPROF(j, 3);
       if (j == 0) {
         m_run = mx;
@@ -457,7 +468,7 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
     // ---------------- epilogue: combine the slices' row sums, normalise, store
     mbar_wait(&B.o_final, 0);
     tc_fence_after();
-    float* lx = sMax + (nblk & 1) * (kFwdSoftWGs * 128);   // the buffer block nblk-2 used
+    float* lx = sMax;
     named_bar_sync(1, kFwdSoftThreads);
     lx[cq * 128 + row] = l_run;
     named_bar_sync(1, kFwdSoftThreads);
