@@ -234,7 +234,8 @@ def run_gpu(args) -> None:
             if ev is not None:
                 ev[2].record()
             return res
-        launches_per_step = 8   # project, gather, scores gemm, topk, fwd, bwd, 2x f32->bf16
+        # project, proxy gather, (scores gemm + topk | fused select), fwd, bwd, 2x f32->bf16
+        launches_per_step = 7 if layer.fused_select() else 8
         work = layer.work()
     else:
         from paper_2502_07590_b200.cp import HeadParallelDSV, HybridDSV

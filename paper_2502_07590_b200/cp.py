@@ -23,6 +23,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 import torch
 import torch.distributed as dist
@@ -266,7 +268,7 @@ class PeerExchange:
         self.hi_of = np.zeros(self.H, dtype=np.int64)
         for hs in self.heads_of:
             self.hi_of[hs] = np.arange(len(hs))
-        self.splits = int(splits)
+        self.splits = int(os.environ.get("DSV_COPY_SPLITS", splits))
         self.ledger = Ledger()
         nh_max = max(len(h) for h in self.heads_of)
         big, small, back = nh_max * self.L * self.D, nh_max * self.L * self.r, self.H * self.chunk * self.D
