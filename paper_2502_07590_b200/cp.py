@@ -312,15 +312,22 @@ class PeerExchange:
         return self.buf[o: o + self.H * self.chunk * self.D].view(self.H, self.chunk, self.D)
 
     # ------------------------------------------------------------------ job tables
-    def _table(self, key, build):
+    def _table(self, key, build, stream=None):
         """Device job table cached by the pointers it encodes. Uploaded from pinned host
-        memory (kept alive with the table), so a step can be captured in a CUDA graph."""
+        memory (kept alive with the table), so a step can be captured in a CUDA graph.
+        stream: the stream that will read the table (default: the current one); the upload
+        is ordered on it and the allocator told, so an evicted table is not reused while
+        that stream may still read it."""
         t = self._tables.get(key)
         if t is None:
             if len(self._tables) >= 16:
                 self._tables.clear()
             host = torch.from_numpy(build()).pin_memory()
-            t = (host.to(self.buf.device, non_blocking=True), host)
+            st = stream or torch.cuda.current_stream(self.buf.device)
+            with torch.cuda.stream(st):
+                dev = host.to(self.buf.device, non_blocking=True)
+            dev.record_stream(st)
+            t = (dev, host)
             self._tables[key] = t
         return t[0]
 
@@ -468,8 +475,9 @@ class PeerExchange:
         side = self._side
         ptrs = tuple(t.data_ptr() for t in (q, k, v, do, p))
         table = self._host_table if engine == "ce" else self._table
-        qkv = table(("qkv", engine) + ptrs, lambda: self._head_jobs((("q", q), ("k", k), ("v", v))))
-        dj = table(("do", engine) + ptrs, lambda: self._head_jobs((("do", do),)))
+        tkw = {} if engine == "ce" else {"stream": side}
+        qkv = table(("qkv", engine) + ptrs, lambda: self._head_jobs((("q", q), ("k", k), ("v", v))), **tkw)
+        dj = table(("do", engine) + ptrs, lambda: self._head_jobs((("do", do),)), **tkw)
 
         def send(jobs):
             if engine == "ce":
@@ -502,7 +510,9 @@ class PeerExchange:
         self._signal(1, step, side)
         ev_do.record(side)
         side.wait_event(ev_f)
-        oj = table(("o", engine, out.data_ptr()), lambda: self._back_jobs((out,), ("o",)))
+        oj = (self._host_table(("o", engine, out.data_ptr()), lambda: self._back_jobs((out,), ("o",)))
+              if engine == "ce" else
+              self._table(("o", engine, out.data_ptr()), lambda: self._back_jobs((out,), ("o",)), side))
         send(oj)
         self._signal(2, step, side)
         ev_o.record(side)
