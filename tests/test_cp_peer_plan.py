@@ -42,9 +42,13 @@ def _torch_np(t):
     return t.view(torch.int16).numpy()
 
 
-@pytest.mark.parametrize("world,plan", [(2, "balanced"), (4, "skewed"), (3, "contiguous"), (3, "balanced"), (4, "balanced")])
-def test_peer_job_tables_deliver_the_all_to_all_layout(world, plan):
-    H, D, r = 6, 16, 8
+@pytest.mark.parametrize("world,plan,H", [(2, "balanced", 6), (4, "skewed", 6), (3, "contiguous", 6),
+                                          (3, "balanced", 6), (4, "balanced", 6),
+                                          (8, "balanced", 24), (8, "skewed", 24), (8, "balanced", 6)])
+def test_peer_job_tables_deliver_the_all_to_all_layout(world, plan, H):
+    # world 8 with H = 24 is the driver's 8-GPU scaling run (3 heads per rank); H = 6 < 8
+    # leaves ranks without heads
+    D, r = 16, 8
     L = 24 * world
     chunk = L // world
     sp = np.linspace(0.5, 0.95, H) if plan == "skewed" else np.full(H, 0.9)
