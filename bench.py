@@ -73,8 +73,11 @@ def _args():
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--overlap", default=os.environ.get("DSV_OVERLAP", "none"), choices=["none", "sm", "ce"],
                     help="HCP exchange under the compute on a side stream (copy kernel / copy engines)")
-    ap.add_argument("--graph", action="store_true", default=os.environ.get("DSV_GRAPH", "0") == "1",
-                    help="replay the step as one captured CUDA graph")
+    ap.add_argument("--graph", dest="graph", action="store_true",
+                    default=os.environ.get("DSV_GRAPH", "1") == "1",
+                    help="replay the step as one captured CUDA graph (default; DSV_GRAPH=0 or "
+                         "--eager issues the kernels one by one)")
+    ap.add_argument("--eager", dest="graph", action="store_false")
     ap.add_argument("--scp", type=int, default=1,
                     help="g_s > 1: hybrid CP, N/g_s head groups x g_s selective-sequence groups")
     ap.add_argument("--dense-heads", type=int, default=0,
@@ -326,16 +329,22 @@ def run_gpu(args) -> None:
                     for i in range(args.steps)]
             stage_ms[name] = sum(vals) / len(vals)
     if args.graph and world == 1:
-        # per-stage times from one extra eager (untimed) step with events
-        ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        st0 = torch.cuda.Event(enable_timing=True)
-        st0.record()
-        eager_step(ev1)
+        # per-stage times from extra eager (untimed) steps with events, issued back to back
+        # (the host runs ahead, so no launch gap lands in a stage); median of steps 2..6
+        reps = 6
+        evr = [[torch.cuda.Event(enable_timing=True) for _ in range(len(eager_stage_names) + 1)]
+               for _ in range(reps)]
+        for i in range(reps):
+            evr[i][0].record()
+            eager_step(evr[i][1:])
         torch.cuda.synchronize()
-        stage_ms = {name: (st0 if i == 0 else ev1[i - 1]).elapsed_time(ev1[i])
-                    for i, name in enumerate(eager_stage_names)}
+        stage_ms = {}
+        for si, name in enumerate(eager_stage_names):
+            vals = sorted(evr[i][si].elapsed_time(evr[i][si + 1]) for i in range(1, reps))
+            stage_ms[name] = vals[len(vals) // 2]
     if world > 1:
-        # one extra (untimed) step with per-phase events on the compute stream
+        # extra (untimed) eager steps; per-phase events on the compute stream of the last
+        eager_step()
         cp.marks = []
         eager_step()
         stage_ms = cp.phase_ms()
