@@ -550,6 +550,19 @@ def plan_heads(sparsities, seq_len: int, head_dim: int, world: int, balanced: bo
     return cpmodel.balance_heads(loads, world).assignment
 
 
+def plan_heads_from_profile(profile, block: int, seq_len: int, head_dim: int, world: int,
+                            balanced: bool = True):
+    """Sparsity-aware head re-balancing from MEASURED sparsity: the EMA per head of one
+    transformer block in a `profiler.SparsityProfile` (filled by `measure_block_sparsity`
+    on the GPU, reference profiler.py:48-152) -> head loads (1 - s_h) S^2 d -> the
+    `balance_heads` assignment (cpmodel.py:73-210). Returns (assignment, sparsities); pass
+    the sparsities to HeadParallelDSV / HybridDSV / DSVAttentionLayer for the per-head k."""
+    sp = np.asarray(profile.head_emas(block), dtype=np.float64)
+    if sp.size == 0:
+        raise ValueError(f"no sparsity measured for block {block}")
+    return plan_heads(sp, seq_len, head_dim, world, balanced), sp
+
+
 class HybridExchange:
     """Hybrid head x selective-sequence CP: g_h-way HCP inside each of g_s SCP groups
     (cpsim.py:125-161), then selective KV gathering between the g_s ranks that hold the

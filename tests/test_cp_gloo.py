@@ -103,3 +103,23 @@ def test_plan_heads_balanced_vs_contiguous():
     ca = max(loads[a == r].sum() for r in range(4))
     cb = max(loads[b == r].sum() for r in range(4))
     assert ca <= cb
+
+
+def test_plan_heads_from_measured_profile():
+    # measured per-head sparsity (profiler EMA) drives the re-balancing
+    from paper_2502_07590_b200 import cpmodel
+    from paper_2502_07590_b200.cp import plan_heads, plan_heads_from_profile
+    from paper_2502_07590_b200.profiler import SparsityProfile
+
+    prof = SparsityProfile(alpha=0.5)
+    rng = np.random.default_rng(3)
+    for it in range(4):
+        prof.update_block(2, rng.uniform(0.5, 0.95, size=8), it)
+    assign, sp = plan_heads_from_profile(prof, 2, 4096, 64, 4)
+    np.testing.assert_array_equal(sp, prof.head_emas(2))
+    np.testing.assert_array_equal(assign, plan_heads(sp, 4096, 64, 4))
+    loads = cpmodel.head_loads(sp, 4096, 64)
+    naive = plan_heads(sp, 4096, 64, 4, balanced=False)
+    assert max(loads[assign == r].sum() for r in range(4)) <= max(loads[naive == r].sum() for r in range(4))
+    with pytest.raises(ValueError):
+        plan_heads_from_profile(prof, 7, 4096, 64, 4)

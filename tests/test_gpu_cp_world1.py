@@ -87,3 +87,24 @@ def test_hybrid_with_dense_heads_world1_matches_layer(cuda, pg):
     w = cp.work()
     L = grid.size
     assert w["fwd_flops"] >= 2 * 4 * L * L * D          # the two dense heads at least
+
+
+def test_measured_sparsity_drives_the_head_plan(cuda, pg):
+    # profiler on the GPU -> SparsityProfile EMA -> balance_heads plan -> HCP layer
+    from paper_2502_07590_b200.cp import HeadParallelDSV, plan_heads_from_profile
+    from paper_2502_07590_b200.profiler import SampleConfig, SparsityProfile, measure_block_sparsity
+
+    grid, H, D, r = TokenGrid(8, 16, 16), 4, 128, 16
+    x, wt, q, k, v, do = _inputs(grid, H, D, r, cuda, seed=2)
+    q = q * torch.tensor([0.5, 1.0, 2.0, 4.0], device=cuda, dtype=torch.bfloat16)[:, None, None]
+    samples = measure_block_sparsity(list(q), list(k), 0.9, SampleConfig(factor=16))
+    assert samples.shape == (H,) and np.all((samples >= 0) & (samples < 1))
+    assert samples[3] > samples[0]                   # sharper heads are sparser
+    prof = SparsityProfile(alpha=1.0)
+    prof.update_block(0, samples, 0)
+    assign, sp = plan_heads_from_profile(prof, 0, grid.size, D, 1)
+    cp = HeadParallelDSV(grid, H, D, r, (8, 4, 4), np.clip(sp, 0.0, 0.99), device=cuda,
+                         transport="all_to_all")
+    out = cp.step(x, wt, q, k, v, do)
+    torch.cuda.synchronize()
+    assert all(torch.isfinite(t.float()).all() for t in out)
