@@ -272,6 +272,8 @@ def run_gpu(args) -> None:
     if world > 1:
         dist.barrier()
     eager_step = step
+    if args.graph and (args.scp > 1 or args.dense_heads):
+        args.graph = False   # the hybrid layer sizes its selective exchanges on the host
     if args.graph:
         # one CUDA graph per step: the host issues one launch instead of ~20 kernels
         graph = torch.cuda.CUDAGraph()
