@@ -722,17 +722,25 @@ class HybridExchange:
         head (any device). Returns (need, cnt): need int64 [n, 2] = (head, global row) of
         the remote rows, grouped by owner group, then head, then row; cnt int64 host
         [g_s, heads] = rows requested from each group per head. Same sets as
-        requests_from_idx, without per-head host loops (one host read)."""
-        span_of, _, _ = self._dev_tables(mark.device)
+        requests_from_idx: the mark is regrouped as [owner group, head, span position] (one
+        gather; a view when the spans are contiguous and in group order), so a single
+        nonzero yields the rows already in request order."""
+        dev = mark.device
         hp = mark.shape[0]
-        remote = mark & (span_of != self.grp)[None, :]
-        need = remote.nonzero()                                 # (head, row), row-major order
-        owner = span_of[need[:, 1]]
-        order = torch.sort(owner, stable=True).indices
-        need, owner = need[order], owner[order]
-        cnt = torch.zeros((self.g_s, hp), dtype=torch.int64, device=mark.device)
-        cnt.index_put_((owner, need[:, 0]), torch.ones_like(owner), accumulate=True)
-        return need, cnt.cpu()
+        key = ("perm", str(dev))
+        if getattr(self, "_perm_key", None) != key:
+            perm = np.concatenate(self.spans)
+            self._perm_ident = bool(np.array_equal(perm, np.arange(self.L)))
+            self._perm_d = torch.from_numpy(perm).to(dev)
+            self._perm_key = key
+        m = mark if self._perm_ident else mark.index_select(1, self._perm_d)
+        mg = m.view(hp, self.g_s, self.span_len).transpose(0, 1).contiguous()   # [g_s, hp, span]
+        mg[self.grp] = False                                                     # own span: local
+        cnt = mg.sum(dim=2).cpu()                                                # [g_s, hp]
+        nz = mg.nonzero()                                                        # (g, h, p) sorted
+        rows = self._perm_d[nz[:, 0] * self.span_len + nz[:, 2]]
+        need = torch.stack([nz[:, 1], rows], dim=1)
+        return need, cnt
 
     def _a2a_fixed(self, send, recv_splits, send_splits):
         recv = torch.empty((sum(recv_splits),) + tuple(send.shape[1:]), dtype=send.dtype,
@@ -762,7 +770,8 @@ class HybridExchange:
                 self.ledger.add("scp_index_exchange", 8 * hp + 4 * send_n[g], 8 * hp + 4 * recv_n[g])
         # 2. owners serve [K | V] rows in request order (one gather per tensor)
         heads = torch.repeat_interleave(
-            torch.arange(hp, device=dev).repeat(g_s), rcnt.flatten().to(dev))
+            torch.arange(hp, device=dev).repeat(g_s), rcnt.flatten().to(dev),
+            output_size=int(sum(recv_n)))
         flat = heads * self.span_len + got_ids.long()
         serve = torch.empty((flat.numel(), 2 * D), dtype=k_span.dtype, device=dev)
         if flat.numel():
@@ -1042,8 +1051,13 @@ class HybridDSV(_PhaseMarks):
         if ex.g_s > 1:
             # the union of the span's critical keys per head, then the remote ones fetched
             mark = torch.zeros((hs, L), dtype=torch.bool, device=dev)
-            for hi, kh in enumerate(self.local.ks):
-                mark[hi].index_fill_(0, sel.idx[hi, :, :kh].reshape(-1).long(), True)
+            ks = self.local.ks
+            if len(set(ks)) == 1:      # one scatter over all heads (offset h * L)
+                off = torch.arange(hs, device=dev, dtype=torch.int64)[:, None, None] * L
+                mark.view(-1).index_fill_(0, (sel.idx[:, :, :ks[0]].long() + off).view(-1), True)
+            else:
+                for hi, kh in enumerate(ks):
+                    mark[hi].index_fill_(0, sel.idx[hi, :, :kh].reshape(-1).long(), True)
             need, cnt = ex.requests_dev(mark)
             got = ex.fetch_kv_dev(kl, vl, need, cnt)
             flat = need[:, 0] * L + need[:, 1]
