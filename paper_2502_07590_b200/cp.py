@@ -984,7 +984,8 @@ class HybridDSV(_PhaseMarks):
     """
 
     def __init__(self, grid, heads: int, head_dim: int, d_lr: int, voxel, sparsity, g_h: int,
-                 g_s: int, balanced: bool = True, group=None, device="cuda", dense=None):
+                 g_s: int, balanced: bool = True, group=None, device="cuda", dense=None,
+                 transport: str = "auto"):
         from .grouping import build_groups
         from .layer import DSVAttentionLayer
         from .ring import RingKV
@@ -1015,6 +1016,15 @@ class HybridDSV(_PhaseMarks):
                                         sp[self.heads[self.sloc]], device, groups=inside)
                       if self.sloc else None)
         self.ring = RingKV(self.ex.scp_group, ledger=self.ex.ledger) if self.dloc else None
+        # the HCP leg inside each SCP group: NVLink peer-memory copy kernels on CUDA (as in
+        # HeadParallelDSV), packed NCCL all-to-alls otherwise
+        if transport == "auto":
+            transport = "peer" if self.device.type == "cuda" else "all_to_all"
+        self.peer = None
+        if transport == "peer":
+            self.peer = PeerExchange(heads, self.span_len, head_dim, d_lr, self.assignment,
+                                     self.ex.hcp_group, self.device)
+            self.peer.ledger = self.ex.ledger
         self._di = torch.tensor(self.dloc, dtype=torch.long, device=self.device)
         self._si = torch.tensor(self.sloc, dtype=torch.long, device=self.device)
 
@@ -1095,13 +1105,16 @@ class HybridDSV(_PhaseMarks):
         self._mark("start")
         p = ops.project(x_local, wt)                                    # [L/N, 2 H r]
         self._mark("project")
-        hm = hx.send_rows_headmajor(dev)
-        p_rows = p.view(chunk * 2 * H, r)
-        h = hx.finish(hx.to_heads_packed(
-            [(t.reshape(H * chunk, D), hm) for t in (q, k, v, dout)]
-            + [(p_rows, hx.send_rows_lowrank(0, dev)), (p_rows, hx.send_rows_lowrank(1, dev))],
-            "hcp_fwd"))
-        ql, kl, vl, dol, qlr, klr = h
+        if self.peer is not None:
+            ql, kl, vl, dol, qlr, klr = self.peer.to_heads(q, k, v, dout, p)
+        else:
+            hm = hx.send_rows_headmajor(dev)
+            p_rows = p.view(chunk * 2 * H, r)
+            h = hx.finish(hx.to_heads_packed(
+                [(t.reshape(H * chunk, D), hm) for t in (q, k, v, dout)]
+                + [(p_rows, hx.send_rows_lowrank(0, dev)), (p_rows, hx.send_rows_lowrank(1, dev))],
+                "hcp_fwd"))
+            ql, kl, vl, dol, qlr, klr = h
         if not self.dloc:
             o, dq, dk, dv = self._sparse(ql, kl, vl, dol, qlr, klr)
         else:
@@ -1120,8 +1133,11 @@ class HybridDSV(_PhaseMarks):
             self._mark("ring_bwd")
             for dst, src in zip((o, dq, dk, dv), res):
                 dst[di] = src
-        h_o = hx.to_tokens_packed([o], "output_redistribute")
-        grads = hx.finish(hx.to_tokens_packed([dq, dk, dv], "hcp_bwd_out"))
-        res = (hx.finish(h_o)[0], *grads)
+        if self.peer is not None:
+            res = self.peer.to_tokens(o.contiguous(), dq.contiguous(), dk.contiguous(), dv.contiguous())
+        else:
+            h_o = hx.to_tokens_packed([o], "output_redistribute")
+            grads = hx.finish(hx.to_tokens_packed([dq, dk, dv], "hcp_bwd_out"))
+            res = (hx.finish(h_o)[0], *grads)
         self._mark("exchange_out")
         return res
