@@ -105,6 +105,7 @@ struct FwdBars {
   // per S/P buffer, so no barrier can run two phases ahead of its waiter
   uint64_t s_full[kFwdSBufs], p_full[kFwdSBufs], pv_done[kFwdSBufs];
   uint64_t o_final;
+  uint64_t q_empty, o_empty;  // persistent CTAs: Q / the O accumulator free for the next tile
   uint32_t tmem;
   uint32_t ovf;             // lazy-max pass: some score exceeded the row's reference max by > 2^64
 };
@@ -233,6 +234,14 @@ DSV_DEV float softmax_p_pass(uint32_t tS, float scale_log2, float m, int kv) {
 // TMEM holds three S/P buffers, and the MMA issues S_{j+3} right after PV_j: the
 // softmax of block j+1 never waits for PV_j to drain. O is rescaled (lazily, when
 // the running max grows by > 2^8) only after PV_{j-1} has completed.
+//
+// Persistent CTAs: each CTA walks tiles blockIdx.x, +gridDim.x, ... with every role
+// keeping running block counters, so the producers gather the next tile's Q and first
+// K/V blocks and the MMA warp computes its first S blocks while the softmax warps finish
+// the current tile (q_empty: every S of a tile has read Q; o_empty: the softmax epilogue
+// has read O out of TMEM). Lazy max (below) flags a tile whose scores exceed its
+// reference max by > 2^64 into ovf_list; the launcher re-runs those tiles with the exact
+// per-block max in list mode (list = ovf_list, read after the first launch).
 template <int D>
 __global__ void __launch_bounds__(kFwdThreads, 1)
 sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __restrict__ Kg,
@@ -240,7 +249,8 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
                   const int* __restrict__ grp_size, const int* __restrict__ idx, long long ldk,
                   const int* __restrict__ kcount, const int* __restrict__ kcount_hg, int G,
                   int Lq, int Lk, float scale_log2, __nv_bfloat16* __restrict__ O,
-                  float* __restrict__ lse) {
+                  float* __restrict__ lse, int n_tiles, const unsigned* __restrict__ list,
+                  unsigned* __restrict__ ovf_list) {
   using SL = FwdSmem<D>;
   using GT = Gather<D>;
   constexpr int ST = kFwdStages, KST = kFwdKStages, NS = kFwdSBufs;
@@ -254,14 +264,22 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   float* sMax = reinterpret_cast<float*>(smem + SL::kMax);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int h = blockIdx.x / G, g = blockIdx.x - h * G;
-  const int kh = kcount_hg ? kcount_hg[blockIdx.x] : kcount[h];
-  const int nblk = (kh + BKV - 1) / BKV;
-  const int* irow = idx + ((long long)h * G + g) * ldk;
-  const int* mrow = grp_rows + (long long)g * BQ;
+  // work items: tiles blockIdx.x, +gridDim.x, ... of all n_tiles (lazy max), or in list
+  // mode the flagged tiles list[1 + i] (exact per-block max)
+  const bool list_mode = list != nullptr;
+  const bool lazy = DSV_FWD_LAZY && !list_mode;
+  const int n_work = list_mode ? (int)list[0] : n_tiles;
+  if ((int)blockIdx.x >= n_work) return;                       // uniform
+  auto tile_of = [&](int it) -> int {
+    const long long i = (long long)blockIdx.x + (long long)it * gridDim.x;
+    if (i >= n_work) return -1;
+    return list_mode ? (int)list[1 + i] : (int)i;
+  };
 
   auto init_bars = [&]() {
     mbar_init(&B.q_full, kProdThreads);
+    mbar_init(&B.q_empty, 1);
+    mbar_init(&B.o_empty, kFwdSoftThreads);
     for (int s = 0; s < KST; ++s) { mbar_init(&B.k_full[s], kProdThreads / 2); mbar_init(&B.k_empty[s], 1); }
     for (int s = 0; s < ST; ++s) { mbar_init(&B.v_full[s], kProdThreads / 2); mbar_init(&B.v_empty[s], 1); }
     for (int s = 0; s < NS; ++s) {
@@ -284,15 +302,12 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   const uint32_t tmem = B.tmem;
   const uint32_t tS0 = tmem, tO = tmem + NS * 128;   // S/P buffer b at tS0 + 128 b
 
-  // Pass 0 (lazy max): the row max is exchanged between the 16 softmax warps for key
-  // block 0 only; later blocks exponentiate against it without a barrier, each warp
-  // checking that its scores stay within 2^64 of it (P, O and the row sums are fp32 /
-  // bf16 with 2^127 range, and relative precision does not depend on the scale). A tile
-  // where some score exceeds that is flagged and re-run as pass 1, which exchanges the
-  // max every block and rescales O when it grows by > 2^8.
-#pragma unroll 1
-  for (int pass = 0; pass < 2; ++pass) {
-  const bool lazy = DSV_FWD_LAZY && pass == 0;
+  // Lazy max: the row max is exchanged between the 16 softmax warps for key block 0
+  // only; later blocks exponentiate against it without a barrier, each warp checking
+  // that its scores stay within 2^64 of it (P, O and the row sums are fp32 / bf16 with
+  // 2^127 range, and relative precision does not depend on the scale). A tile where some
+  // score exceeds that is flagged for the exact pass (list mode), which exchanges the max
+  // every block and rescales O when it grows by > 2^8.
 
   if (warp >= kFwdProdWarp0) {
     // ------------------------------------------------------------ producers
@@ -302,14 +317,6 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
     // barrier asynchronously (cp.async.mbarrier.arrive.noinc, one per thread).
     using GH = Gather<D, kProdThreads / 2>;
     const int ptid = threadIdx.x - kFwdProdWarp0 * 32;
-    {
-      const int r0 = ptid / GT::kCPR;
-      int qrows[GT::kPer];
-#pragma unroll
-      for (int i = 0; i < GT::kPer; ++i) qrows[i] = h * Lq + __ldg(mrow + r0 + i * GT::kRowStep);
-      issue_tile<D>(sQ, Qg, qrows, ptid);
-      cp_async_arrive_noinc(&B.q_full);
-    }
     const bool is_v = ptid >= kProdThreads / 2;
     const int gtid = is_v ? ptid - kProdThreads / 2 : ptid;
     const int r0 = gtid / GH::kCPR;
@@ -318,17 +325,36 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
     uint64_t* full = is_v ? B.v_full : B.k_full;
     uint64_t* empty = is_v ? B.v_empty : B.k_empty;
     const int nst = is_v ? ST : KST;
-    const int kbase = h * Lk;
     int rows[GH::kPer];
-    for (int j = 0; j < nblk; ++j) {
-      const int st = j % nst;
+    int kb = 0;                                      // blocks through this ring so far
+    for (int it = 0;; ++it) {
+      const int tile = tile_of(it);
+      if (tile < 0) break;
+      const int h = tile / G, g = tile - h * G;
+      const int kh = kcount_hg ? kcount_hg[tile] : kcount[h];
+      const int nblk = (kh + BKV - 1) / BKV;
+      const int* irow = idx + ((long long)h * G + g) * ldk;
+      const int* mrow = grp_rows + (long long)g * BQ;
+      {   // Q of this tile, once every S of the previous tile has read the last one
+        const int qr0 = ptid / GT::kCPR;
+        int qrows[GT::kPer];
 #pragma unroll
-      for (int i = 0; i < GH::kPer; ++i)
-        rows[i] = kbase + __ldg(irow + min(j * BKV + r0 + i * GH::kRowStep, kh - 1));
-      if (j >= nst) mbar_wait(&empty[st], ((j / nst) - 1) & 1);
-      if (gtid == 0) FPROF(j, is_v ? 6 : 5);
-      issue_tile<D, kProdThreads / 2>(ring + st * SL::kTile, src, rows, gtid);
-      cp_async_arrive_noinc(&full[st]);
+        for (int i = 0; i < GT::kPer; ++i) qrows[i] = h * Lq + __ldg(mrow + qr0 + i * GT::kRowStep);
+        if (it > 0) mbar_wait(&B.q_empty, (it - 1) & 1);
+        issue_tile<D>(sQ, Qg, qrows, ptid);
+        cp_async_arrive_noinc(&B.q_full);
+      }
+      const int kbase = h * Lk;
+      for (int j = 0; j < nblk; ++j, ++kb) {
+        const int st = kb % nst;
+#pragma unroll
+        for (int i = 0; i < GH::kPer; ++i)
+          rows[i] = kbase + __ldg(irow + min(j * BKV + r0 + i * GH::kRowStep, kh - 1));
+        if (kb >= nst) mbar_wait(&empty[st], ((kb / nst) - 1) & 1);
+        if (gtid == 0) FPROF(j, is_v ? 6 : 5);
+        issue_tile<D, kProdThreads / 2>(ring + st * SL::kTile, src, rows, gtid);
+        cp_async_arrive_noinc(&full[st]);
+      }
     }
     cp_async_wait<0>();
   } else if (warp == kFwdMmaWarp) {
@@ -337,45 +363,56 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
     constexpr uint32_t idS = idesc_bf16_f32(128, BKV, 0, 0);
     constexpr uint32_t idO = idesc_bf16_f32(128, D, 0, 1);
     const uint32_t aQ = smem_u32(sQ);
+    int gb = 0;                                      // blocks of this CTA's earlier tiles
+    for (int it = 0;; ++it) {
+    const int tile = tile_of(it);
+    if (tile < 0) break;
+    const int h = tile / G;
+    const int kh = kcount_hg ? kcount_hg[tile] : kcount[h];
+    const int nblk = (kh + BKV - 1) / BKV;
     auto issue_s = [&](int s) {
-      const int st = s % KST;
-      mbar_wait(&B.k_full[st], (s / KST) & 1);
+      const int gs = gb + s, st = gs % KST;
+      mbar_wait(&B.k_full[st], (gs / KST) & 1);
       tc_fence_after();
       if (lane == 0) FPROF(s, 0);
       if (elect_one()) {
         const uint32_t aK = smem_u32(sK + st * SL::kTile);
-        const uint32_t dS = tS0 + (s % NS) * 128;
+        const uint32_t dS = tS0 + (gs % NS) * 128;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
           mma_ss(dS, sdesc_sw128(aQ + off, 16, 1024), sdesc_sw128(aK + off, 16, 1024), idS, kk > 0);
         }
-        mma_commit(&B.s_full[s % NS]);
+        mma_commit(&B.s_full[gs % NS]);
         mma_commit(&B.k_empty[st]);
+        if (s == nblk - 1) mma_commit(&B.q_empty);   // the tile's last read of Q
       }
       __syncwarp();
     };
-    mbar_wait(&B.q_full, 0);
+    mbar_wait(&B.q_full, it & 1);
     for (int s = 0; s < NS && s < nblk; ++s) issue_s(s);
     for (int j = 0; j < nblk; ++j) {
-      const int st = j % ST;
-      mbar_wait(&B.p_full[j % NS], (j / NS) & 1);
-      mbar_wait(&B.v_full[st], (j / ST) & 1);
+      const int gj = gb + j, st = gj % ST;
+      mbar_wait(&B.p_full[gj % NS], (gj / NS) & 1);
+      mbar_wait(&B.v_full[st], (gj / ST) & 1);
+      if (j == 0 && it > 0) mbar_wait(&B.o_empty, (it - 1) & 1);   // O read out
       tc_fence_after();
       if (lane == 0) FPROF(j, 1);
       if (elect_one()) {
         const uint32_t aV = smem_u32(sV + st * SL::kTile);
-        const uint32_t tP = tS0 + (j % NS) * 128;
+        const uint32_t tP = tS0 + (gj % NS) * 128;
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)
           mma_ts(tO, tP + (kk >> 1) * 32 + (kk & 1) * 8, sdesc_sw128(aV + kk * 2048, 128 * 128, 1024),
                  idO, (j > 0 || kk > 0));   // P of keys [32c, +32) sits in S columns [32c, +16)
         mma_commit(&B.v_empty[st]);
-        mma_commit(&B.pv_done[j % NS]);
+        mma_commit(&B.pv_done[gj % NS]);
         if (j == nblk - 1) mma_commit(&B.o_final);
       }
       __syncwarp();
       if (j + NS < nblk) issue_s(j + NS);
+    }
+    gb += nblk;
     }
   } else {
     // ------------------------------------------------------------ softmax warps
@@ -384,12 +421,21 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
     const int row = wq * 32 + lane;
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
     constexpr int kOc = D / kFwdSoftWGs;              // O columns per warp (rescale, store)
+    int gb = 0;
+    for (int it = 0;; ++it) {
+    const int tile = tile_of(it);
+    if (tile < 0) break;
+    const int h = tile / G, g = tile - h * G;
+    const int kh = kcount_hg ? kcount_hg[tile] : kcount[h];
+    const int nblk = (kh + BKV - 1) / BKV;
+    const int* mrow = grp_rows + (long long)g * BQ;
     float m_run = -INFINITY, l_run = 0.f;
     bool ovf_local = false;
     for (int j = 0; j < nblk; ++j) {
+      const int gj = gb + j;
       const int kv = min(BKV, kh - j * BKV);
-      const uint32_t tS = tS0 + (j % NS) * 128 + lane_off;
-      mbar_wait(&B.s_full[j % NS], (j / NS) & 1);
+      const uint32_t tS = tS0 + (gj % NS) * 128 + lane_off;
+      mbar_wait(&B.s_full[gj % NS], (gj / NS) & 1);
       tc_fence_after();
       if (warp == 0 && lane == 0) FPROF(j, 2);
       uint32_t r[32];
@@ -424,7 +470,7 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
         // rescale O (this warp's D/4 columns) once PV_{j-1} has landed. The decision is
         // warp-uniform: tcgen05.ld/st are warp-collective, so every lane takes the branch
         // and a row whose max did not grow rescales by alpha = 1.
-        mbar_wait(&B.pv_done[(j - 1) % NS], ((j - 1) / NS) & 1);
+        mbar_wait(&B.pv_done[(gj - 1) % NS], ((gj - 1) / NS) & 1);
         tc_fence_after();
         mx = fmaxf(mx, m_run);
         const float alpha = fast_exp2(m_run - mx);
@@ -462,17 +508,23 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
       if (warp == 0 && lane == 0) FPROF(j, 9);
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&B.p_full[j % NS]);
+      mbar_arrive(&B.p_full[gj % NS]);
       if (warp == 0 && lane == 0) FPROF(j, 4);
     }
     // ---------------- epilogue: combine the slices' row sums, normalise, store
-    mbar_wait(&B.o_final, 0);
+    mbar_wait(&B.o_final, it & 1);
     tc_fence_after();
     float* lx = sMax;
+    if (__any_sync(0xffffffffu, ovf_local) && lane == 0) B.ovf = 1u;
     named_bar_sync(1, kFwdSoftThreads);
     lx[cq * 128 + row] = l_run;
     named_bar_sync(1, kFwdSoftThreads);
     const float denom = (lx[row] + lx[128 + row]) + (lx[256 + row] + lx[384 + row]);
+    if (threadIdx.x == 0 && B.ovf) {                 // flag the tile for the exact pass
+      B.ovf = 0u;
+      ovf_list[1 + atomicAdd(ovf_list, 1u)] = (unsigned)tile;
+    }
+    named_bar_sync(1, kFwdSoftThreads);               // sMax / flag free for the next tile
     const float inv = denom > 0.f ? 1.f / denom : 0.f;
     const int gsz = grp_size[g];
     const int tok = mrow[row];
@@ -493,18 +545,13 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
       }
     }
     if (cq == 0 && row < gsz) lse[(long long)h * Lq + tok] = m_run + __log2f(denom);
-    if (__any_sync(0xffffffffu, ovf_local) && lane == 0) atomicOr(&B.ovf, 1u);
+    tc_fence_before();
+    mbar_arrive(&B.o_empty);                          // O is out of TMEM
+    gb += nblk;
+    }
   }
   tc_fence_before();
   __syncthreads();
-  if (!lazy || B.ovf == 0u) break;                   // uniform: read after the barrier
-  // flagged tile: every async op of pass 0 has completed (O final observed, producers
-  // drained their copies) -> re-arm the barriers and run the exact-max pass
-  if (warp == kFwdMmaWarp && lane == 0) init_bars();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  }
   if (warp == kFwdMmaWarp) tmem_dealloc(tmem, 512);
 }
 
@@ -915,25 +962,45 @@ template <int D>
 static int fwd_launch(const void* q, const void* k, const void* v, const int* grp_rows,
                       const int* grp_size, const int* idx, long long ldk, const int* kcount,
                       const int* kcount_hg, int H, int G, int Lq, int Lk, float scale_log2, void* O,
-                      float* lse, cudaStream_t st) {
+                      float* lse, unsigned* work, cudaStream_t st) {
   auto kern = sparse_fwd_kernel<D>;
   const int smem = FwdSmem<D>::kBytes;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  kern<<<H * G, kFwdThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
-                                      (const __nv_bfloat16*)v, grp_rows, grp_size, idx, ldk,
-                                      kcount, kcount_hg, G, Lq, Lk, scale_log2,
-                                      (__nv_bfloat16*)O, lse);
+  const int n_tiles = H * G;
+  // persistent grid: one CTA per SM (DSV_FWD_GRID=tiles: one CTA per tile, same kernel)
+  static const bool per_tile = [] {
+    const char* e = getenv("DSV_FWD_GRID");
+    return e && e[0] == 't';
+  }();
+  int sms = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int grid = per_tile ? n_tiles : (n_tiles < sms ? n_tiles : sms);
+  cudaMemsetAsync(work, 0, sizeof(unsigned), st);
+  kern<<<grid, kFwdThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
+                                     (const __nv_bfloat16*)v, grp_rows, grp_size, idx, ldk,
+                                     kcount, kcount_hg, G, Lq, Lk, scale_log2,
+                                     (__nv_bfloat16*)O, lse, n_tiles, nullptr, work);
+  // tiles flagged by the lazy max: exact per-block max (CTAs exit at once when none)
+  const int g2 = n_tiles < sms ? n_tiles : sms;
+  kern<<<g2, kFwdThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
+                                   (const __nv_bfloat16*)v, grp_rows, grp_size, idx, ldk,
+                                   kcount, kcount_hg, G, Lq, Lk, scale_log2,
+                                   (__nv_bfloat16*)O, lse, n_tiles, work, nullptr);
   return (int)cudaGetLastError();
 }
 
 int dsv_attn_fwd_tc_launch(const void* q, const void* k, const void* v, const int* grp_rows,
                            const int* grp_size, const int* idx, long long ldk, const int* kcount,
                            const int* kcount_hg, int H, int G, int Lq, int Lk, int D,
-                           float scale_log2, void* O, float* lse, cudaStream_t st) {
+                           float scale_log2, void* O, float* lse, unsigned* work, cudaStream_t st) {
   if (D == 128)
-    return fwd_launch<128>(q, k, v, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H, G, Lq, Lk, scale_log2, O, lse, st);
+    return fwd_launch<128>(q, k, v, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H, G, Lq, Lk, scale_log2, O, lse, work, st);
   if (D == 64)
-    return fwd_launch<64>(q, k, v, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H, G, Lq, Lk, scale_log2, O, lse, st);
+    return fwd_launch<64>(q, k, v, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H, G, Lq, Lk, scale_log2, O, lse, work, st);
   return 1;
 }
 
