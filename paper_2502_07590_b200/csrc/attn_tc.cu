@@ -611,6 +611,7 @@ struct BwdSmem {
 struct BwdBars {
   uint64_t q_full, k_full, v_full, k_empty, v_empty;
   uint64_t sdp_full, pds_full, mma_done, tmem_free;
+  uint64_t q_empty, dq_empty;                             // persistent CTAs: Q/dO, dQ free
   uint64_t stg_full[2], stg_free[2];                      // [0] = dV half, [1] = dK half
   uint32_t tmem;
 };
@@ -631,7 +632,8 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
                   const int* __restrict__ idx, long long ldk, const int* __restrict__ kcount,
                   const int* __restrict__ kcount_hg, int G, int Lq, int Lk, float scale,
                   float scale_log2,
-                  __nv_bfloat16* __restrict__ dQ, float* __restrict__ dK, float* __restrict__ dV) {
+                  __nv_bfloat16* __restrict__ dQ, float* __restrict__ dK, float* __restrict__ dV,
+                  int n_tiles) {
   using SL = BwdSmem<D>;
   using GT = Gather<D, kBwdLoadThreads>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -647,12 +649,23 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   float* sDelta = reinterpret_cast<float*>(smem + SL::kDelta);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int h = blockIdx.x / G, g = blockIdx.x - h * G;
-  const int kh = kcount_hg ? kcount_hg[blockIdx.x] : kcount[h];
-  const int nblk = (kh + BKV - 1) / BKV;
-  const int* irow = idx + ((long long)h * G + g) * ldk;
-  const int* mrow = grp_rows + (long long)g * BQ;
   constexpr int kCh = D / 32;                              // 32-column chunks per tensor
+  // persistent CTAs: tiles blockIdx.x, +gridDim.x, ...; every role keeps running block
+  // counters (gj) for the barrier parities, so the next tile's Q/dO and first K/V loads
+  // and its first MMAs overlap the current tile's last blocks and dQ epilogue
+  auto tile_of = [&](int it) -> int {
+    const long long t = (long long)blockIdx.x + (long long)it * gridDim.x;
+    return t < n_tiles ? (int)t : -1;
+  };
+#define DSV_BWD_TILE()                                                    \
+    const int tile = tile_of(it);                                           \
+    if (tile < 0) break;                                                    \
+    const int h = tile / G, g = tile - h * G;                               \
+    const int kh = kcount_hg ? kcount_hg[tile] : kcount[h];                 \
+    const int nblk = (kh + BKV - 1) / BKV;                                  \
+    const int* irow = idx + ((long long)h * G + g) * ldk;                   \
+    const int* mrow = grp_rows + (long long)g * BQ;                         \
+    (void)irow; (void)mrow; (void)nblk
 
   if (warp == kBwdMmaWarp) {
     if (lane == 0) {
@@ -665,6 +678,8 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
       mbar_init(&B.pds_full, kBwdWorkThreads);
       mbar_init(&B.mma_done, 1);
       mbar_init(&B.tmem_free, kBwdWorkThreads);
+      mbar_init(&B.q_empty, 1);
+      mbar_init(&B.dq_empty, kBwdWorkThreads);
       for (int t = 0; t < 2; ++t) {
         mbar_init(&B.stg_full[t], kBwdWorkThreads);   // every worker, once per half
         mbar_init(&B.stg_free[t], kBwdScatThreads);
@@ -679,20 +694,23 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   tc_fence_after();
   const uint32_t tmem = B.tmem;
   const uint32_t tA = tmem, tB = tmem + 128, tC = tmem + 256, tDq = tmem + 384;
-  const long long hoff = (long long)h * Lk * D;
 
   if (warp >= kBwdScatWarp0) {
     // ------------------------------------------------------------ scatter
     constexpr int RPW = 128 / kBwdScatWarps;        // staging rows per scatter warp
     const int pw = warp - kBwdScatWarp0;            // rows [RPW pw, RPW pw + RPW)
     const int stid = threadIdx.x - kBwdScatWarp0 * 32;
-    for (int jb = 0; jb < nblk; ++jb) {
+    int gj = 0;
+    for (int it = 0;; ++it) {
+    DSV_BWD_TILE();
+    const long long hoff = (long long)h * Lk * D;
+    for (int jb = 0; jb < nblk; ++jb, ++gj) {
       const int kv = min(BKV, kh - jb * BKV);
       const int myrow = pw * RPW + (lane % RPW);
       const int mykey = myrow < kv ? __ldg(irow + jb * BKV + myrow) : 0;
 #pragma unroll 1
       for (int t = 0; t < 2; ++t) {
-        mbar_wait(&B.stg_full[t], jb & 1);
+        mbar_wait(&B.stg_full[t], gj & 1);
         if (stid == 0) PROF(jb, 8 + t);
         float* acc = (t == 0 ? dV : dK) + hoff;
         const uint8_t* stg = sStg + t * (128 * D * 2);
@@ -727,30 +745,36 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
       }
       if (stid == 0) PROF(jb, 10);
     }
+    }
   } else if (warp >= kBwdLoadWarp0) {
     // ------------------------------------------------------------ gather producers
     const int ptid = threadIdx.x - kBwdLoadWarp0 * 32;
     const int r0 = ptid / GT::kCPR;
     int rows[GT::kPer];
+    int gj = 0;
+    for (int it = 0;; ++it) {
+    DSV_BWD_TILE();
     const int qbase = h * Lq;
 #pragma unroll
     for (int i = 0; i < GT::kPer; ++i) rows[i] = qbase + __ldg(mrow + r0 + i * GT::kRowStep);
+    if (it > 0) mbar_wait(&B.q_empty, (it - 1) & 1);   // the previous tile's MMAs are done with Q/dO
     issue_tile<D, kBwdLoadThreads>(sQ, Qg, rows, ptid);
     issue_tile<D, kBwdLoadThreads>(sdO, dOg, rows, ptid);
     cp_async_arrive_noinc(&B.q_full);
     const int kbase = h * Lk;
-    for (int j = 0; j < nblk; ++j) {
+    for (int j = 0; j < nblk; ++j, ++gj) {
 #pragma unroll
       for (int i = 0; i < GT::kPer; ++i)
         rows[i] = kbase + __ldg(irow + min(j * BKV + r0 + i * GT::kRowStep, kh - 1));
-      if (j > 0) mbar_wait(&B.v_empty, (j - 1) & 1);
+      if (gj > 0) mbar_wait(&B.v_empty, (gj - 1) & 1);
       if (ptid == 0) PROF(j, 0);
       issue_tile<D, kBwdLoadThreads>(sV, Vg, rows, ptid);
       cp_async_arrive_noinc(&B.v_full);
-      if (j > 0) mbar_wait(&B.k_empty, (j - 1) & 1);
+      if (gj > 0) mbar_wait(&B.k_empty, (gj - 1) & 1);
       if (ptid == 0) PROF(j, 1);
       issue_tile<D, kBwdLoadThreads>(sK, Kg, rows, ptid);
       cp_async_arrive_noinc(&B.k_full);
+    }
     }
     cp_async_wait<0>();
   } else if (warp == kBwdMmaWarp) {
@@ -760,11 +784,14 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
     constexpr uint32_t idDQ = idesc_bf16_f32(128, D, 1, 1);     // dS(MN smem) . K_j(MN)
     const uint32_t aQ = smem_u32(sQ), adO = smem_u32(sdO), adS = smem_u32(sdS);
     const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
-    mbar_wait(&B.q_full, 0);
-    for (int j = 0; j < nblk; ++j) {
-      mbar_wait(&B.k_full, j & 1);
-      mbar_wait(&B.v_full, j & 1);
-      if (j > 0) mbar_wait(&B.tmem_free, (j - 1) & 1);
+    int gj = 0;
+    for (int it = 0;; ++it) {
+    DSV_BWD_TILE();
+    mbar_wait(&B.q_full, it & 1);
+    for (int j = 0; j < nblk; ++j, ++gj) {
+      mbar_wait(&B.k_full, gj & 1);
+      mbar_wait(&B.v_full, gj & 1);
+      if (gj > 0) mbar_wait(&B.tmem_free, (gj - 1) & 1);
       tc_fence_after();
       if (lane == 0) PROF(j, 2);
       if (elect_one()) {
@@ -782,7 +809,8 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
         mma_commit(&B.v_empty);
       }
       __syncwarp();
-      mbar_wait(&B.pds_full, j & 1);
+      mbar_wait(&B.pds_full, gj & 1);
+      if (j == 0 && it > 0) mbar_wait(&B.dq_empty, (it - 1) & 1);   // dQ read out of TMEM
       tc_fence_after();
       if (lane == 0) PROF(j, 3);
       if (elect_one()) {
@@ -800,16 +828,22 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
         for (int kk = 0; kk < 8; ++kk)
           mma_ts(tB, tC + 64 + kk * 8, sdesc_sw128(aQ + kk * 2048, 128 * 128, 1024), idTS, kk > 0);
         mma_commit(&B.mma_done);
+        if (j == nblk - 1) mma_commit(&B.q_empty);     // the tile's last read of Q / dO
       }
       __syncwarp();
+    }
     }
   } else {
     // ------------------------------------------------------------ workers
     const int quarter = warp & 3, cg = warp >> 2;   // TMEM lane quarter, 32-column slice
     const int row = quarter * 32 + lane;            // query row (prologue/epilogue), key row (blocks)
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    int gj = 0;
+    for (int it = 0;; ++it) {
+    DSV_BWD_TILE();
     const int gsz = grp_size[g];
     const int tok = mrow[row];
+    if (it > 0) named_bar_sync(1, kBwdWorkThreads);   // every worker is past the last tile
     if (cg == 0) {
       // prologue: lse2 and Delta = rowsum(dO * O) for this query row
       float dlt = 0.f, l2 = INFINITY;
@@ -841,10 +875,10 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
             pack_bf16(__uint_as_float(r[8 * q + 4]), __uint_as_float(r[8 * q + 5])),
             pack_bf16(__uint_as_float(r[8 * q + 6]), __uint_as_float(r[8 * q + 7])));
     };
-    for (int j = 0; j < nblk; ++j) {
+    for (int j = 0; j < nblk; ++j, ++gj) {
       const int kv = min(BKV, kh - j * BKV);
       const bool kvalid = row < kv;
-      mbar_wait(&B.sdp_full, j & 1);
+      mbar_wait(&B.sdp_full, gj & 1);
       tc_fence_after();
       if (threadIdx.x == 0) PROF(j, 4);
       // ---- B: 16-query halves of this warp's 32-query slices, for its 32 keys
@@ -895,7 +929,7 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
       // ---- C': dV_j | dK_j 32-column chunks -> bf16 staging halves. Tasks n = cg,
       // cg + WPQ, ... of the 2 * kCh per quarter (t = n / kCh, chunk n % kCh); TMEM is
       // released after the last TMEM read, before that chunk is staged.
-      mbar_wait(&B.mma_done, j & 1);
+      mbar_wait(&B.mma_done, gj & 1);
       tc_fence_after();
       if (threadIdx.x == 0) PROF(j, 6);
       int cur_t = 0;
@@ -912,7 +946,7 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
         }
         if (t != cur_t) { mbar_arrive(&B.stg_full[0]); cur_t = 1; }
         if (n - kBwdWPQ < 0 || (n - kBwdWPQ) / kCh != t) {
-          if (j > 0) mbar_wait(&B.stg_free[t], (j - 1) & 1);   // first chunk of half t
+          if (gj > 0) mbar_wait(&B.stg_free[t], (gj - 1) & 1);   // first chunk of half t
         }
         stage(r, t, c);
       }
@@ -936,7 +970,11 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
               pack_bf16(__uint_as_float(r[i + 6]), __uint_as_float(r[i + 7])));
       }
     }
+    tc_fence_before();
+    mbar_arrive(&B.dq_empty);                          // dQ is out of TMEM
+    }
   }
+#undef DSV_BWD_TILE
   tc_fence_before();
   __syncthreads();
   if (warp == kBwdMmaWarp) tmem_dealloc(tmem, 512);
@@ -1013,11 +1051,23 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* O
   auto kern = sparse_bwd_kernel<D>;
   const int smem = BwdSmem<D>::kBytes;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  kern<<<H * G, kBwdThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)dO,
+  const int n_tiles = H * G;
+  static const bool per_tile = [] {          // DSV_BWD_GRID=tiles: one CTA per tile
+    const char* e = getenv("DSV_BWD_GRID");
+    return e && e[0] == 't';
+  }();
+  int sms = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int grid = per_tile ? n_tiles : (n_tiles < sms ? n_tiles : sms);
+  kern<<<grid, kBwdThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)dO,
                                       (const __nv_bfloat16*)k, (const __nv_bfloat16*)v,
                                       (const __nv_bfloat16*)O, lse, grp_rows, grp_size, idx, ldk,
                                       kcount, kcount_hg, G, Lq, Lk, scale, scale_log2,
-                                      (__nv_bfloat16*)dQ, dK, dV);
+                                      (__nv_bfloat16*)dQ, dK, dV, n_tiles);
   return (int)cudaGetLastError();
 }
 
