@@ -115,12 +115,13 @@ int dsv_sparse_fwd(const void* q, const void* k, const void* v, const int* grp_r
 
 /* Backward (K3b). dout: [H][Lq][D] bf16, out/lse from dsv_sparse_fwd. dq: [H][Lq][D] bf16
  * (every query of a group is written); dk_acc, dv_acc: [H][Lk][D] fp32 accumulators that the
- * caller zeroes; contributions are added atomically. */
+ * caller zeroes; contributions are added atomically. work: one device word (the persistent
+ * CTAs' tile counter; reset by the call). */
 int dsv_sparse_bwd(const void* q, const void* k, const void* v, const void* out,
                    const void* dout, const float* lse, const int* grp_rows, const int* grp_size,
                    const int* idx, long long ldk, const int* kcount, const int* kcount_hg, int H,
                    int G, int Lq, int Lk, int D, float scale, void* dq, float* dk_acc,
-                   float* dv_acc, void* stream);
+                   float* dv_acc, unsigned* work, void* stream);
 
 /* Ragged per-(head, query) CSR sparse attention on CUDA cores (fp32 math), any D <= 256.
  * ptr: [H*Lq + 1] int64 offsets into cols (int32 key ids); cols == NULL selects every key

@@ -612,9 +612,12 @@ struct BwdBars {
   uint64_t q_full, k_full, v_full, k_empty, v_empty;
   uint64_t sdp_full, pds_full, mma_done, tmem_free;
   uint64_t q_empty, dq_empty;                             // persistent CTAs: Q/dO, dQ free
+  uint64_t tq_full[4], tq_empty[4];                       // tile-id queue (dynamic schedule)
+  int tq[4];
   uint64_t stg_full[2], stg_free[2];                      // [0] = dV half, [1] = dK half
   uint32_t tmem;
 };
+static_assert(sizeof(BwdBars) <= 256, "backward barriers over their 256 B");
 
 // byte offset of 16-byte chunk q of staging row p (rows of D bf16, XOR-swizzled)
 template <int D>
@@ -633,7 +636,7 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
                   const int* __restrict__ kcount_hg, int G, int Lq, int Lk, float scale,
                   float scale_log2,
                   __nv_bfloat16* __restrict__ dQ, float* __restrict__ dK, float* __restrict__ dV,
-                  int n_tiles) {
+                  int n_tiles, unsigned* __restrict__ sched) {
   using SL = BwdSmem<D>;
   using GT = Gather<D, kBwdLoadThreads>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -653,9 +656,23 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   // persistent CTAs: tiles blockIdx.x, +gridDim.x, ...; every role keeps running block
   // counters (gj) for the barrier parities, so the next tile's Q/dO and first K/V loads
   // and its first MMAs overlap the current tile's last blocks and dQ epilogue
+  // Tiles are handed out dynamically (a global atomic counter, like the hardware block
+  // scheduler): with a static round-robin split the CTAs drift apart over their ~40
+  // tiles, more heads' dK/dV accumulators are live at once and fall out of L2. One
+  // producer lane draws the ids into a 4-slot shared queue that every thread reads.
   auto tile_of = [&](int it) -> int {
-    const long long t = (long long)blockIdx.x + (long long)it * gridDim.x;
-    return t < n_tiles ? (int)t : -1;
+    const int slot = it & 3;
+    mbar_wait(&B.tq_full[slot], (it >> 2) & 1);
+    const int t = *reinterpret_cast<volatile int*>(&B.tq[slot]);
+    mbar_arrive(&B.tq_empty[slot]);
+    return t;
+  };
+  auto draw_tile = [&](int it) {                   // the scheduler lane, ahead of everyone
+    const int slot = it & 3;
+    if (it >= 4) mbar_wait(&B.tq_empty[slot], ((it >> 2) - 1) & 1);
+    const unsigned t = atomicAdd(sched, 1u);
+    B.tq[slot] = t < (unsigned)n_tiles ? (int)t : -1;
+    mbar_arrive(&B.tq_full[slot]);                  // release: the id is visible to waiters
   };
 #define DSV_BWD_TILE()                                                    \
     const int tile = tile_of(it);                                           \
@@ -680,6 +697,10 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
       mbar_init(&B.tmem_free, kBwdWorkThreads);
       mbar_init(&B.q_empty, 1);
       mbar_init(&B.dq_empty, kBwdWorkThreads);
+      for (int t = 0; t < 4; ++t) {
+        mbar_init(&B.tq_full[t], 1);
+        mbar_init(&B.tq_empty[t], kBwdThreads);
+      }
       for (int t = 0; t < 2; ++t) {
         mbar_init(&B.stg_full[t], kBwdWorkThreads);   // every worker, once per half
         mbar_init(&B.stg_free[t], kBwdScatThreads);
@@ -753,6 +774,7 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
     int rows[GT::kPer];
     int gj = 0;
     for (int it = 0;; ++it) {
+    if (ptid == 0) draw_tile(it);
     DSV_BWD_TILE();
     const int qbase = h * Lq;
 #pragma unroll
@@ -1047,7 +1069,8 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* O
                       const float* lse, const int* grp_rows, const int* grp_size, const int* idx,
                       long long ldk, const int* kcount, const int* kcount_hg, int H, int G, int Lq,
                       int Lk, float scale,
-                      float scale_log2, void* dQ, float* dK, float* dV, cudaStream_t st) {
+                      float scale_log2, void* dQ, float* dK, float* dV, unsigned* sched,
+                      cudaStream_t st) {
   auto kern = sparse_bwd_kernel<D>;
   const int smem = BwdSmem<D>::kBytes;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1063,11 +1086,12 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* O
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int grid = per_tile ? n_tiles : (n_tiles < sms ? n_tiles : sms);
+  cudaMemsetAsync(sched, 0, sizeof(unsigned), st);
   kern<<<grid, kBwdThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)dO,
                                       (const __nv_bfloat16*)k, (const __nv_bfloat16*)v,
                                       (const __nv_bfloat16*)O, lse, grp_rows, grp_size, idx, ldk,
                                       kcount, kcount_hg, G, Lq, Lk, scale, scale_log2,
-                                      (__nv_bfloat16*)dQ, dK, dV, n_tiles);
+                                      (__nv_bfloat16*)dQ, dK, dV, n_tiles, sched);
   return (int)cudaGetLastError();
 }
 
@@ -1075,13 +1099,14 @@ int dsv_attn_bwd_tc_launch(const void* q, const void* k, const void* v, const vo
                            const void* dO, const float* lse, const int* grp_rows,
                            const int* grp_size, const int* idx, long long ldk, const int* kcount,
                            const int* kcount_hg, int H, int G, int Lq, int Lk, int D, float scale,
-                           float scale_log2, void* dQ, float* dK, float* dV, cudaStream_t st) {
+                           float scale_log2, void* dQ, float* dK, float* dV, unsigned* sched,
+                           cudaStream_t st) {
   if (D == 128)
     return bwd_launch<128>(q, k, v, O, dO, lse, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H,
-                           G, Lq, Lk, scale, scale_log2, dQ, dK, dV, st);
+                           G, Lq, Lk, scale, scale_log2, dQ, dK, dV, sched, st);
   if (D == 64)
     return bwd_launch<64>(q, k, v, O, dO, lse, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H,
-                          G, Lq, Lk, scale, scale_log2, dQ, dK, dV, st);
+                          G, Lq, Lk, scale, scale_log2, dQ, dK, dV, sched, st);
   return 1;
 }
 

@@ -36,7 +36,7 @@ int dsv_attn_fwd_tc_launch(const void*, const void*, const void*, const int*, co
 int dsv_attn_bwd_tc_launch(const void*, const void*, const void*, const void*, const void*,
                            const float*, const int*, const int*, const int*, long long,
                            const int*, const int*, int, int, int, int, int, float, float, void*,
-                           float*, float*, cudaStream_t);
+                           float*, float*, unsigned*, cudaStream_t);
 int dsv_f32_to_bf16_launch(const float*, void*, long long, cudaStream_t);
 int dsv_select_fused_launch(const CUtensorMap*, const CUtensorMap*, int, int, int, const int*, int*,
                             long long, float*, int, cudaStream_t);
@@ -278,17 +278,18 @@ int dsv_sparse_bwd(const void* q, const void* k, const void* v, const void* out,
                    const void* dout, const float* lse, const int* grp_rows, const int* grp_size,
                    const int* idx, long long ldk, const int* kcount, const int* kcount_hg, int H,
                    int G, int Lq, int Lk, int D, float scale, void* dq, float* dk_acc,
-                   float* dv_acc, void* stream) {
+                   float* dv_acc, unsigned* work, void* stream) {
   if (D != 64 && D != 128) return fail(DSV_EUNSUPPORTED, "sparse_bwd: head dim %d not 64/128", D);
   if (H <= 0 || G <= 0 || Lq <= 0 || Lk <= 0 || ldk < 0)
     return fail(DSV_EINVAL, "sparse_bwd: empty shape");
   if (!al16(q) || !al16(k) || !al16(v) || !al16(out) || !al16(dout) || !al16(dq) ||
       !al16(dk_acc) || !al16(dv_acc) || !al16(grp_rows))
     return fail(DSV_EINVAL, "sparse_bwd: pointers must be 16-byte aligned");
+  if (!work) return fail(DSV_EINVAL, "sparse_bwd: null workspace");
   const float scale_log2 = scale * 1.4426950408889634f;
   return cuda_status(dsv_attn_bwd_tc_launch(q, k, v, out, dout, lse, grp_rows, grp_size, idx, ldk,
                                             kcount, kcount_hg, H, G, Lq, Lk, D, scale, scale_log2,
-                                            dq, dk_acc, dv_acc, S(stream)),
+                                            dq, dk_acc, dv_acc, work, S(stream)),
                      "sparse_bwd launch");
 }
 

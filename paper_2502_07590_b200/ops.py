@@ -202,10 +202,11 @@ def sparse_bwd(q, k, v, out, dout, lse, grp_rows, grp_size, idx, kcount, scale=N
         dk_acc = torch.zeros((H, Lk, D), device=q.device, dtype=torch.float32)
     if dv_acc is None:
         dv_acc = torch.zeros((H, Lk, D), device=q.device, dtype=torch.float32)
+    work = torch.empty((4,), device=q.device, dtype=torch.int32)
     _lib.call("dsv_sparse_bwd", _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(dout), _ptr(lse),
               _ptr(grp_rows), _ptr(grp_size), _ptr(idx), idx.stride(1), _ptr(kcount),
               _ptr(kcount_hg), H, G, Lq, Lk, D, float(scale), _ptr(dq), _ptr(dk_acc), _ptr(dv_acc),
-              _stream())
+              _ptr(work), _stream())
     return dq, dk_acc, dv_acc
 
 
