@@ -106,8 +106,8 @@ int dsv_topk(const float* scores, long long ld, int rows, int L, const int* k_pe
  * entries per row (1..ldk), or, when kcount_hg != NULL, kcount_hg[h*G + g] valid entries;
  * ldk = 0: every (head, group) reads the same list (dense chunks of the ring KV pass).
  * out: [H][Lq][D] bf16; lse: [H][Lq] fp32, log2 domain of the scaled logits.
- * work: device workspace of >= H*G + 1 words (the persistent kernel's list of tiles that
- * need the exact-max pass; contents need no initialisation). */
+ * work: device workspace of >= H*G + 2 words (the persistent kernel's list of tiles that
+ * need the exact-max pass and its tile counter; contents need no initialisation). */
 int dsv_sparse_fwd(const void* q, const void* k, const void* v, const int* grp_rows,
                    const int* grp_size, const int* idx, long long ldk, const int* kcount,
                    const int* kcount_hg, int H, int G, int Lq, int Lk, int D, float scale,

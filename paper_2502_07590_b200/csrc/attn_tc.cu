@@ -106,6 +106,8 @@ struct FwdBars {
   uint64_t s_full[kFwdSBufs], p_full[kFwdSBufs], pv_done[kFwdSBufs];
   uint64_t o_final;
   uint64_t q_empty, o_empty;  // persistent CTAs: Q / the O accumulator free for the next tile
+  uint64_t tq_full[2], tq_empty[2];  // tile-id queue (dynamic schedule)
+  int tq[2];
   uint32_t tmem;
   uint32_t ovf;             // lazy-max pass: some score exceeded the row's reference max by > 2^64
 };
@@ -250,7 +252,7 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
                   const int* __restrict__ kcount, const int* __restrict__ kcount_hg, int G,
                   int Lq, int Lk, float scale_log2, __nv_bfloat16* __restrict__ O,
                   float* __restrict__ lse, int n_tiles, const unsigned* __restrict__ list,
-                  unsigned* __restrict__ ovf_list) {
+                  unsigned* __restrict__ ovf_list, unsigned* __restrict__ sched) {
   using SL = FwdSmem<D>;
   using GT = Gather<D>;
   constexpr int ST = kFwdStages, KST = kFwdKStages, NS = kFwdSBufs;
@@ -270,16 +272,37 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   const bool lazy = DSV_FWD_LAZY && !list_mode;
   const int n_work = list_mode ? (int)list[0] : n_tiles;
   if ((int)blockIdx.x >= n_work) return;                       // uniform
+  // normal mode: tiles drawn from a global atomic counter (one producer lane feeds a
+  // 2-slot shared-memory queue every thread reads; keeps the CTAs in step like the
+  // hardware block scheduler); list mode: a static split of the flagged list
   auto tile_of = [&](int it) -> int {
-    const long long i = (long long)blockIdx.x + (long long)it * gridDim.x;
-    if (i >= n_work) return -1;
-    return list_mode ? (int)list[1 + i] : (int)i;
+    if (list_mode) {
+      const long long i = (long long)blockIdx.x + (long long)it * gridDim.x;
+      return i < n_work ? (int)list[1 + i] : -1;
+    }
+    const int slot = it & 1;
+    mbar_wait(&B.tq_full[slot], (it >> 1) & 1);
+    const int t = *reinterpret_cast<volatile int*>(&B.tq[slot]);
+    mbar_arrive(&B.tq_empty[slot]);
+    return t;
+  };
+  auto draw_tile = [&](int it) {
+    if (list_mode) return;
+    const int slot = it & 1;
+    if (it >= 2) mbar_wait(&B.tq_empty[slot], ((it >> 1) - 1) & 1);
+    const unsigned t = atomicAdd(sched, 1u);
+    B.tq[slot] = t < (unsigned)n_tiles ? (int)t : -1;
+    mbar_arrive(&B.tq_full[slot]);
   };
 
   auto init_bars = [&]() {
     mbar_init(&B.q_full, kProdThreads);
     mbar_init(&B.q_empty, 1);
     mbar_init(&B.o_empty, kFwdSoftThreads);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&B.tq_full[t], 1);
+      mbar_init(&B.tq_empty[t], kFwdThreads);
+    }
     for (int s = 0; s < KST; ++s) { mbar_init(&B.k_full[s], kProdThreads / 2); mbar_init(&B.k_empty[s], 1); }
     for (int s = 0; s < ST; ++s) { mbar_init(&B.v_full[s], kProdThreads / 2); mbar_init(&B.v_empty[s], 1); }
     for (int s = 0; s < NS; ++s) {
@@ -328,6 +351,7 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
     int rows[GH::kPer];
     int kb = 0;                                      // blocks through this ring so far
     for (int it = 0;; ++it) {
+      if (ptid == 0) draw_tile(it);
       const int tile = tile_of(it);
       if (tile < 0) break;
       const int h = tile / G, g = tile - h * G;
@@ -1039,17 +1063,19 @@ static int fwd_launch(const void* q, const void* k, const void* v, const int* gr
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int grid = per_tile ? n_tiles : (n_tiles < sms ? n_tiles : sms);
+  unsigned* sched = work + n_tiles + 1;              // tile counter after the flag list
   cudaMemsetAsync(work, 0, sizeof(unsigned), st);
+  cudaMemsetAsync(sched, 0, sizeof(unsigned), st);
   kern<<<grid, kFwdThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
                                      (const __nv_bfloat16*)v, grp_rows, grp_size, idx, ldk,
                                      kcount, kcount_hg, G, Lq, Lk, scale_log2,
-                                     (__nv_bfloat16*)O, lse, n_tiles, nullptr, work);
+                                     (__nv_bfloat16*)O, lse, n_tiles, nullptr, work, sched);
   // tiles flagged by the lazy max: exact per-block max (CTAs exit at once when none)
   const int g2 = n_tiles < sms ? n_tiles : sms;
   kern<<<g2, kFwdThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
                                    (const __nv_bfloat16*)v, grp_rows, grp_size, idx, ldk,
                                    kcount, kcount_hg, G, Lq, Lk, scale_log2,
-                                   (__nv_bfloat16*)O, lse, n_tiles, work, nullptr);
+                                   (__nv_bfloat16*)O, lse, n_tiles, work, nullptr, nullptr);
   return (int)cudaGetLastError();
 }
 

@@ -265,8 +265,8 @@ int dsv_sparse_fwd(const void* q, const void* k, const void* v, const int* grp_r
     return fail(DSV_EINVAL, "sparse_fwd: empty shape");
   if (!al16(q) || !al16(k) || !al16(v) || !al16(out) || !al16(grp_rows))
     return fail(DSV_EINVAL, "sparse_fwd: pointers must be 16-byte aligned");
-  if (!work || work_words < (long long)H * G + 1)
-    return fail(DSV_EINVAL, "sparse_fwd: workspace needs H*G + 1 words");
+  if (!work || work_words < (long long)H * G + 2)
+    return fail(DSV_EINVAL, "sparse_fwd: workspace needs H*G + 2 words");
   const float scale_log2 = scale * 1.4426950408889634f;
   return cuda_status(dsv_attn_fwd_tc_launch(q, k, v, grp_rows, grp_size, idx, ldk, kcount,
                                             kcount_hg, H, G, Lq, Lk, D, scale_log2, out, lse,

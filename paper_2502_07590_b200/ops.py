@@ -181,7 +181,7 @@ def sparse_fwd(q, k, v, grp_rows, grp_size, idx, kcount, scale=None, kcount_hg=N
         scale = 1.0 / math.sqrt(D)
     out = torch.empty_like(q)
     lse = torch.empty((H, Lq), device=q.device, dtype=torch.float32)
-    work = torch.empty((H * G + 1,), device=q.device, dtype=torch.int32)
+    work = torch.empty((H * G + 2,), device=q.device, dtype=torch.int32)
     _lib.call("dsv_sparse_fwd", _ptr(q), _ptr(k), _ptr(v), _ptr(grp_rows), _ptr(grp_size),
               _ptr(idx), idx.stride(1), _ptr(kcount), _ptr(kcount_hg), H, G, Lq, Lk, D,
               float(scale), _ptr(out), _ptr(lse), _ptr(work), work.numel(), _stream())
