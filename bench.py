@@ -222,8 +222,6 @@ def run_gpu(args) -> None:
         layer = DSVAttentionLayer(grid, H, D, D_LR, VOXEL, sparsity, dev)
         wt = layer.predictor_weights(seed=0)
         x, q, k, v, do = rnd(L, H * D), rnd(H, L, D), rnd(H, L, D), rnd(H, L, D), rnd(H, L, D)
-        dk_acc = torch.zeros((H, L, D), device=dev, dtype=torch.float32)
-        dv_acc = torch.zeros_like(dk_acc)
         stage_names = ("select", "fwd", "bwd")
 
         def step(ev=None):
@@ -233,12 +231,13 @@ def run_gpu(args) -> None:
             out, lse = layer.forward(q, k, v, sel)
             if ev is not None:
                 ev[1].record()
-            res = layer.backward(q, k, v, out, lse, do, sel, dk_acc, dv_acc)
+            res = layer.backward(q, k, v, out, lse, do, sel)   # accumulators zeroed by forward
             if ev is not None:
                 ev[2].record()
             return res
-        # project, proxy gather, (scores gemm + topk | fused select), fwd, bwd, 2x f32->bf16
-        launches_per_step = 7 if layer.fused_select() else 8
+        # project, proxy gather, (scores gemm + topk | fused select), fwd (persistent + the
+        # list-mode re-run launch), bwd, 2x f32->bf16
+        launches_per_step = 8 if layer.fused_select() else 9
         work = layer.work()
     else:
         from paper_2502_07590_b200.cp import HeadParallelDSV, HybridDSV
@@ -363,7 +362,7 @@ def run_gpu(args) -> None:
 
         def dev_step(xb, qb, kb, vb, dob):
             if world == 1:
-                return layer.step(xb, wt, qb, kb, vb, dob, dk_acc=dk_acc, dv_acc=dv_acc)
+                return layer.step(xb, wt, qb, kb, vb, dob)
             return cp.step(xb, wt, qb, kb, vb, dob)
 
         for out in pipe.run(dev_step, [host] * 2):

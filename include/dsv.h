@@ -107,11 +107,14 @@ int dsv_topk(const float* scores, long long ld, int rows, int L, const int* k_pe
  * ldk = 0: every (head, group) reads the same list (dense chunks of the ring KV pass).
  * out: [H][Lq][D] bf16; lse: [H][Lq] fp32, log2 domain of the scaled logits.
  * work: device workspace of >= H*G + 2 words (the persistent kernel's list of tiles that
- * need the exact-max pass and its tile counter; contents need no initialisation). */
+ * need the exact-max pass and its tile counter; contents need no initialisation).
+ * zero_buf (optional): zero_floats fp32 set to 0 while the kernel runs (the backward's dK/dV
+ * accumulators; the writes hide under the gather-bound forward). */
 int dsv_sparse_fwd(const void* q, const void* k, const void* v, const int* grp_rows,
                    const int* grp_size, const int* idx, long long ldk, const int* kcount,
                    const int* kcount_hg, int H, int G, int Lq, int Lk, int D, float scale,
-                   void* out, float* lse, unsigned* work, long long work_words, void* stream);
+                   void* out, float* lse, unsigned* work, long long work_words, float* zero_buf,
+                   long long zero_floats, void* stream);
 
 /* Backward (K3b). dout: [H][Lq][D] bf16, out/lse from dsv_sparse_fwd. dq: [H][Lq][D] bf16
  * (every query of a group is written); dk_acc, dv_acc: [H][Lk][D] fp32 accumulators that the

@@ -1074,7 +1074,7 @@ class HybridDSV(_PhaseMarks):
             Kf.view(-1, D).index_copy_(0, flat, got[:, :D])
             Vf.view(-1, D).index_copy_(0, flat, got[:, D:])
         self._mark("scp_fetch")
-        out, lse = self.local.forward(Qf, Kf, Vf, sel)
+        out, lse = self.local.forward(Qf, Kf, Vf, sel, prepare_backward=False)
         self._mark("fwd")
         dk32 = torch.zeros((hs, L, D), dtype=torch.float32, device=dev)
         dv32 = torch.zeros_like(dk32)

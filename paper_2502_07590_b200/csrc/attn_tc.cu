@@ -252,7 +252,8 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
                   const int* __restrict__ kcount, const int* __restrict__ kcount_hg, int G,
                   int Lq, int Lk, float scale_log2, __nv_bfloat16* __restrict__ O,
                   float* __restrict__ lse, int n_tiles, const unsigned* __restrict__ list,
-                  unsigned* __restrict__ ovf_list, unsigned* __restrict__ sched) {
+                  unsigned* __restrict__ ovf_list, unsigned* __restrict__ sched,
+                  float4* __restrict__ zero_buf, long long zero_n4) {
   using SL = FwdSmem<D>;
   using GT = Gather<D>;
   constexpr int ST = kFwdStages, KST = kFwdKStages, NS = kFwdSBufs;
@@ -367,6 +368,14 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
         if (it > 0) mbar_wait(&B.q_empty, (it - 1) & 1);
         issue_tile<D>(sQ, Qg, qrows, ptid);
         cp_async_arrive_noinc(&B.q_full);
+      }
+      if (zero_buf != nullptr) {
+        // zero this tile's share of the backward's dK/dV accumulators: HBM writes that
+        // run under the gather-bound forward instead of a separate fill pass
+        const long long per = (zero_n4 + n_tiles - 1) / n_tiles;
+        const long long z0 = (long long)tile * per, z1 = min(zero_n4, z0 + per);
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (long long i = z0 + ptid; i < z1; i += kProdThreads) zero_buf[i] = z;
       }
       const int kbase = h * Lk;
       for (int j = 0; j < nblk; ++j, ++kb) {
@@ -1046,7 +1055,8 @@ template <int D>
 static int fwd_launch(const void* q, const void* k, const void* v, const int* grp_rows,
                       const int* grp_size, const int* idx, long long ldk, const int* kcount,
                       const int* kcount_hg, int H, int G, int Lq, int Lk, float scale_log2, void* O,
-                      float* lse, unsigned* work, cudaStream_t st) {
+                      float* lse, unsigned* work, float* zero_buf, long long zero_floats,
+                      cudaStream_t st) {
   auto kern = sparse_fwd_kernel<D>;
   const int smem = FwdSmem<D>::kBytes;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1069,24 +1079,29 @@ static int fwd_launch(const void* q, const void* k, const void* v, const int* gr
   kern<<<grid, kFwdThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
                                      (const __nv_bfloat16*)v, grp_rows, grp_size, idx, ldk,
                                      kcount, kcount_hg, G, Lq, Lk, scale_log2,
-                                     (__nv_bfloat16*)O, lse, n_tiles, nullptr, work, sched);
+                                     (__nv_bfloat16*)O, lse, n_tiles, nullptr, work, sched,
+                                     reinterpret_cast<float4*>(zero_buf), zero_floats / 4);
   // tiles flagged by the lazy max: exact per-block max (CTAs exit at once when none)
   const int g2 = n_tiles < sms ? n_tiles : sms;
   kern<<<g2, kFwdThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
                                    (const __nv_bfloat16*)v, grp_rows, grp_size, idx, ldk,
                                    kcount, kcount_hg, G, Lq, Lk, scale_log2,
-                                   (__nv_bfloat16*)O, lse, n_tiles, work, nullptr, nullptr);
+                                   (__nv_bfloat16*)O, lse, n_tiles, work, nullptr, nullptr,
+                                   nullptr, 0);
   return (int)cudaGetLastError();
 }
 
 int dsv_attn_fwd_tc_launch(const void* q, const void* k, const void* v, const int* grp_rows,
                            const int* grp_size, const int* idx, long long ldk, const int* kcount,
                            const int* kcount_hg, int H, int G, int Lq, int Lk, int D,
-                           float scale_log2, void* O, float* lse, unsigned* work, cudaStream_t st) {
+                           float scale_log2, void* O, float* lse, unsigned* work,
+                           float* zero_buf, long long zero_floats, cudaStream_t st) {
   if (D == 128)
-    return fwd_launch<128>(q, k, v, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H, G, Lq, Lk, scale_log2, O, lse, work, st);
+    return fwd_launch<128>(q, k, v, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H, G, Lq, Lk,
+                           scale_log2, O, lse, work, zero_buf, zero_floats, st);
   if (D == 64)
-    return fwd_launch<64>(q, k, v, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H, G, Lq, Lk, scale_log2, O, lse, work, st);
+    return fwd_launch<64>(q, k, v, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H, G, Lq, Lk,
+                          scale_log2, O, lse, work, zero_buf, zero_floats, st);
   return 1;
 }
 

@@ -32,7 +32,7 @@ int dsv_gemm_launch(const CUtensorMap*, const CUtensorMap*, const CUtensorMap*, 
                     long long, int, int, int, cudaStream_t);
 int dsv_attn_fwd_tc_launch(const void*, const void*, const void*, const int*, const int*,
                            const int*, long long, const int*, const int*, int, int, int, int, int,
-                           float, void*, float*, unsigned*, cudaStream_t);
+                           float, void*, float*, unsigned*, float*, long long, cudaStream_t);
 int dsv_attn_bwd_tc_launch(const void*, const void*, const void*, const void*, const void*,
                            const float*, const int*, const int*, const int*, long long,
                            const int*, const int*, int, int, int, int, int, float, float, void*,
@@ -259,7 +259,8 @@ int dsv_topk(const float* scores, long long ld, int rows, int L, const int* k_pe
 int dsv_sparse_fwd(const void* q, const void* k, const void* v, const int* grp_rows,
                    const int* grp_size, const int* idx, long long ldk, const int* kcount,
                    const int* kcount_hg, int H, int G, int Lq, int Lk, int D, float scale,
-                   void* out, float* lse, unsigned* work, long long work_words, void* stream) {
+                   void* out, float* lse, unsigned* work, long long work_words, float* zero_buf,
+                   long long zero_floats, void* stream) {
   if (D != 64 && D != 128) return fail(DSV_EUNSUPPORTED, "sparse_fwd: head dim %d not 64/128", D);
   if (H <= 0 || G <= 0 || Lq <= 0 || Lk <= 0 || ldk < 0)
     return fail(DSV_EINVAL, "sparse_fwd: empty shape");
@@ -267,10 +268,12 @@ int dsv_sparse_fwd(const void* q, const void* k, const void* v, const int* grp_r
     return fail(DSV_EINVAL, "sparse_fwd: pointers must be 16-byte aligned");
   if (!work || work_words < (long long)H * G + 2)
     return fail(DSV_EINVAL, "sparse_fwd: workspace needs H*G + 2 words");
+  if (zero_buf && (zero_floats < 0 || zero_floats % 4 || !al16(zero_buf)))
+    return fail(DSV_EINVAL, "sparse_fwd: zero_buf must be 16-byte aligned, a multiple of 4 floats");
   const float scale_log2 = scale * 1.4426950408889634f;
   return cuda_status(dsv_attn_fwd_tc_launch(q, k, v, grp_rows, grp_size, idx, ldk, kcount,
                                             kcount_hg, H, G, Lq, Lk, D, scale_log2, out, lse,
-                                            work, S(stream)),
+                                            work, zero_buf, zero_buf ? zero_floats : 0, S(stream)),
                      "sparse_fwd launch");
 }
 

@@ -154,22 +154,47 @@ class DSVAttentionLayer:
         return max(1, min(self.H, budget // per_head))
 
     # ------------------------------------------------------------- attention
-    def forward(self, q, k, v, sel: SelectedKV):
+    def forward(self, q, k, v, sel: SelectedKV, prepare_backward: bool = True):
+        """Sparse forward. prepare_backward: the kernel also zeroes the layer's dK/dV
+        accumulators for the coming backward (HBM writes hidden under the gather-bound
+        forward instead of a separate fill pass)."""
+        zero = None
+        if prepare_backward:
+            zero = self._accumulators(k.shape[1], k.device)
+            self._acc_zeroed = True
         return ops.sparse_fwd(q, k, v, self.grp_rows, self.grp_size, sel.idx, sel.kcount,
-                              self.scale)
+                              self.scale, zero=zero)
 
     def backward(self, q, k, v, out, lse, dout, sel: SelectedKV, dk_acc=None, dv_acc=None):
-        if dk_acc is not None:
+        """-> (dq, dk, dv) bf16. Without caller accumulators the layer's own are used (zeroed
+        by the preceding forward, or here if that did not happen)."""
+        if dk_acc is None:
+            acc = self._accumulators(k.shape[1], k.device)
+            if not getattr(self, "_acc_zeroed", False):
+                acc.zero_()
+            self._acc_zeroed = False
+            dk_acc, dv_acc = acc[0], acc[1]
+        else:
             dk_acc.zero_()
             dv_acc.zero_()
         dq, dk32, dv32 = ops.sparse_bwd(q, k, v, out, dout, lse, self.grp_rows, self.grp_size,
                                         sel.idx, sel.kcount, self.scale, dk_acc, dv_acc)
         return dq, ops.f32_to_bf16(dk32), ops.f32_to_bf16(dv32)
 
+    def _accumulators(self, n_keys: int, device):
+        """The layer's fp32 dK/dV accumulators [2, H, n_keys, D] (one contiguous buffer)."""
+        key = (int(n_keys), str(device))
+        if self.__dict__.get("_acc_key") != key:
+            self._acc = torch.empty((2, self.H, int(n_keys), self.D), device=device,
+                                    dtype=torch.float32)
+            self._acc_key = key
+            self._acc_zeroed = False
+        return self._acc
+
     def step(self, x, wt, q, k, v, dout, dk_acc=None, dv_acc=None):
         """One fwd+bwd pass of the layer (the bench's unit of work)."""
         sel = self.select(x, wt)
-        out, lse = self.forward(q, k, v, sel)
+        out, lse = self.forward(q, k, v, sel, prepare_backward=dk_acc is None)
         dq, dk, dv = self.backward(q, k, v, out, lse, dout, sel, dk_acc, dv_acc)
         return out, dq, dk, dv
 

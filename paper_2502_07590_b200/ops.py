@@ -167,13 +167,17 @@ def select_fused(q_prox: torch.Tensor, k_lr: torch.Tensor, k_per_head: torch.Ten
 
 
 # ------------------------------------------------------------------- K3 attention
-def sparse_fwd(q, k, v, grp_rows, grp_size, idx, kcount, scale=None, kcount_hg=None):
+def sparse_fwd(q, k, v, grp_rows, grp_size, idx, kcount, scale=None, kcount_hg=None, zero=None):
     """Group-tiled sparse attention forward. q: [H, Lq, D], k/v: [H, Lk, D] bf16.
 
     grp_rows int32 [G, 128], grp_size int32 [G], idx int32 [H, G, ldk], kcount int32 [H]
     (or per-row counts kcount_hg int32 [H, G]). Returns (out bf16 [H, Lq, D], lse2 fp32 [H, Lq]).
+    zero: optional contiguous fp32 tensor the kernel sets to 0 while it runs (the backward's
+    dK/dV accumulators).
     """
     _require_cuda(q, k, v, grp_rows, grp_size, idx, kcount)
+    if zero is not None and (zero.dtype != torch.float32 or not zero.is_contiguous()):
+        raise ValueError("sparse_fwd: zero must be a contiguous fp32 tensor")
     H, Lq, D = q.shape
     Lk = k.shape[1]
     G = grp_rows.shape[0]
@@ -184,7 +188,8 @@ def sparse_fwd(q, k, v, grp_rows, grp_size, idx, kcount, scale=None, kcount_hg=N
     work = torch.empty((H * G + 2,), device=q.device, dtype=torch.int32)
     _lib.call("dsv_sparse_fwd", _ptr(q), _ptr(k), _ptr(v), _ptr(grp_rows), _ptr(grp_size),
               _ptr(idx), idx.stride(1), _ptr(kcount), _ptr(kcount_hg), H, G, Lq, Lk, D,
-              float(scale), _ptr(out), _ptr(lse), _ptr(work), work.numel(), _stream())
+              float(scale), _ptr(out), _ptr(lse), _ptr(work), work.numel(), _ptr(zero),
+              0 if zero is None else zero.numel(), _stream())
     return out, lse
 
 
