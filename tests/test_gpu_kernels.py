@@ -303,3 +303,29 @@ def test_sparse_fwd_deterministic_repeated(cuda):
     for _ in range(8):
         out, lse = ops.sparse_fwd(q, kk, v, rows, size, idx, kc)
         assert torch.equal(out, out0) and torch.equal(lse, lse0)
+
+
+def test_layer_backward_accumulators_zeroed_by_forward_or_itself(cuda):
+    # the forward kernel zeroes the layer's dK/dV accumulators for the next backward; a
+    # second backward (no forward in between) must zero them itself, and explicit
+    # caller accumulators give the same gradients
+    from paper_2502_07590_b200.layer import DSVAttentionLayer
+
+    grid = TokenGrid(8, 16, 16)
+    H, D = 3, 128
+    layer = DSVAttentionLayer(grid, H, D, 16, (8, 4, 4), [0.5, 0.8, 0.9], cuda)
+    L = grid.size
+    g = torch.Generator(device="cpu").manual_seed(17)
+    x = torch.randn((L, H * D), generator=g).to(torch.bfloat16).to(cuda)
+    q, k, v, do = (torch.randn((H, L, D), generator=g).to(torch.bfloat16).to(cuda) for _ in range(4))
+    sel = layer.select(x, layer.predictor_weights(seed=2))
+    out, lse = layer.forward(q, k, v, sel)
+    a = layer.backward(q, k, v, out, lse, do, sel)
+    b = layer.backward(q, k, v, out, lse, do, sel)              # no forward in between
+    dk_acc = torch.full((H, L, D), 7.0, device=cuda)             # garbage: must be zeroed
+    dv_acc = torch.full((H, L, D), -3.0, device=cuda)
+    c = layer.backward(q, k, v, out, lse, do, sel, dk_acc, dv_acc)
+    torch.cuda.synchronize()
+    for x1, x2, x3 in zip(a, b, c):
+        assert _rel_l2(x2.float().cpu().numpy(), x1.float().cpu().numpy()) < 1e-3
+        assert _rel_l2(x3.float().cpu().numpy(), x1.float().cpu().numpy()) < 1e-3
