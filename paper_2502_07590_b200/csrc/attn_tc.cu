@@ -72,7 +72,10 @@ DSV_DEV void issue_tile(uint8_t* tile, const __nv_bfloat16* base,
 #define DSV_FWD_KSTAGES 3
 #endif
 constexpr int kFwdKStages = DSV_FWD_KSTAGES;                     // K_j frees after S_j
-constexpr int kFwdStages = 3;                                    // V ring (frees after PV_j)
+#ifndef DSV_FWD_VSTAGES
+#define DSV_FWD_VSTAGES 3
+#endif
+constexpr int kFwdStages = DSV_FWD_VSTAGES;                      // V ring (frees after PV_j)
 constexpr int kFwdSBufs = 3;                                     // S/P buffers in TMEM
 #ifndef DSV_FWD_SOFT_WGS
 #define DSV_FWD_SOFT_WGS 4
