@@ -165,7 +165,8 @@ class DSVAttentionLayer:
         return ops.sparse_fwd(q, k, v, self.grp_rows, self.grp_size, sel.idx, sel.kcount,
                               self.scale, zero=zero)
 
-    def backward(self, q, k, v, out, lse, dout, sel: SelectedKV, dk_acc=None, dv_acc=None):
+    def backward(self, q, k, v, out, lse, dout, sel: SelectedKV, dk_acc=None, dv_acc=None,
+                 kernel_done=None):
         """-> (dq, dk, dv) bf16. Without caller accumulators the layer's own are used (zeroed
         by the preceding forward, or here if that did not happen)."""
         if dk_acc is None:
@@ -179,6 +180,8 @@ class DSVAttentionLayer:
             dv_acc.zero_()
         dq, dk32, dv32 = ops.sparse_bwd(q, k, v, out, dout, lse, self.grp_rows, self.grp_size,
                                         sel.idx, sel.kcount, self.scale, dk_acc, dv_acc)
+        if kernel_done is not None:          # optional CUDA event after the kernel (timing)
+            kernel_done.record()
         return dq, ops.f32_to_bf16(dk32), ops.f32_to_bf16(dv32)
 
     def _accumulators(self, n_keys: int, device):
