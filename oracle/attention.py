@@ -70,8 +70,12 @@ def grouped_attention_bwd(q, k, v, members, group_sets, dout, scale=None):
         dp = do @ v[sel].T
         ds = p * (dp - (do * o).sum(axis=1, keepdims=True)) * scale
         dq[mem] = ds @ k[sel]
-        np.add.at(dk, sel, ds.T @ q[mem])
-        np.add.at(dv, sel, p.T @ do)
+        if sel.size < 2 or np.all(np.diff(sel) > 0):   # unique keys: plain fancy-index add
+            dk[sel] += ds.T @ q[mem]
+            dv[sel] += p.T @ do
+        else:
+            np.add.at(dk, sel, ds.T @ q[mem])
+            np.add.at(dv, sel, p.T @ do)
     return dq, dk, dv
 
 

@@ -32,3 +32,14 @@ def cuda():
 
     _lib.load()
     return torch.device("cuda:0")
+
+
+def parity_report(name: str, data: dict) -> None:
+    """Record measured errors of a GPU parity test (gpurun_out/parity/<name>.json; the
+    summaries committed under profiles/ are copied from there)."""
+    import json
+
+    out = ROOT / "gpurun_out" / "parity"
+    out.mkdir(parents=True, exist_ok=True)
+    (out / f"{name}.json").write_text(json.dumps(data, indent=1, sort_keys=True))
+    print(f"[parity] {name}: {json.dumps(data, sort_keys=True)}")
