@@ -28,6 +28,17 @@
  *                        the owners' buffers (peer pointers over NVLink)
  *   dsv_ring_*           ring KV pass for dense residual heads under SCP (no reference
  *                        counterpart; dense semantics of attention.py:95-109)
+ * Reference-precision (fp64) path for host fp64/fp32 callers (validate.py:10-25 computes in
+ * the caller's dtype):
+ *   dsv_gemm_f64         predictor.py:94-100 project; selection.py:149/204/222 score tiles;
+ *                        attention.py:112-115 logits (q @ k.T / sqrt(d))
+ *   dsv_softmax_rows_f64 attention.py:88-92 _stable_softmax_rows
+ *   dsv_topk_f64         selection.py:118-175 / 178-242 on fp64 scores (fp64 thresholds)
+ *   dsv_rows_*_f64       attention.py:95-109 / 153-187 and trainer.py:110-117 in fp64
+ *   dsv_sorted_stats_f64 attention.py:118-140 critical_kv_oracle prefix length;
+ *                        attention.py:208-212 analyze_distribution top-fraction mass
+ *   dsv_histogram_f64    attention.py:214-216 np.histogram
+ *   dsv_set_stats_f64    predictor.py:262-281 prediction_accuracy (recall / mass coverage)
  */
 #ifndef DSV_H_
 #define DSV_H_
@@ -224,6 +235,52 @@ int dsv_ring_lse_merge(float* acc, const float* lse_in, float* lse_out, const vo
                        void* stream);
 int dsv_ring_accum_bf16(float* acc, const void* x, long long n, int first, void* out, void* stream);
 int dsv_ring_accum_f32(float* acc, float* part, long long n, int first, void* stream);
+
+/* ---- reference-precision (fp64) path ------------------------------------------------- */
+/* C[b](m, n) = (sum_t A[b](m, t) B[b](t, n)) / div, fp64, fma in t order (deterministic).
+ * A(m, t) = A[m*sam + t*sat], B(t, n) = B[t*sbt + n*sbn] (element strides; transposes free),
+ * C row stride ldc, batch strides a_bs / b_bs / c_bs. */
+int dsv_gemm_f64(const double* A, long long sam, long long sat, long long a_bs, const double* B,
+                 long long sbt, long long sbn, long long b_bs, double* C, long long ldc,
+                 long long c_bs, int M, int N, int K, int nbatch, double div, void* stream);
+/* In place: x[r] <- softmax(x[r]) with the row max subtracted first. */
+int dsv_softmax_rows_f64(double* x, long long ld, int R, int N, void* stream);
+/* Exact top-k per row of fp64 scores S [R][L] (row stride lds); row r takes
+ * k = k_per[r / rows_per_k] (1 <= k <= L). out [R][>= k] int32 ascending, thr[r] = k-th
+ * largest score. Ties toward the lower index; -0.0 == +0.0. */
+int dsv_topk_f64(const double* S, long long lds, int R, int L, const int* k_per, int rows_per_k,
+                 int* out, long long ldo, double* thr, void* stream);
+/* Attention over CSR index lists in fp64 (cols == NULL: every key). q [H][Lq][Dk],
+ * k [H][Lk][Dk], v [H][Lk][Dv]; out [H][Lq][Dv], lse natural log of the scaled logits.
+ * Backward: dq [H][Lq][Dk]; dk_acc / dv_acc are accumulated into (caller zeroes them). */
+int dsv_rows_fwd_f64(const double* q, const double* k, const double* v, const long long* ptr,
+                     const int* cols, int H, int Lq, int Lk, int Dk, int Dv, double scale,
+                     double* out, double* lse, void* stream);
+int dsv_rows_bwd_f64(const double* q, const double* k, const double* v, const double* out,
+                     const double* lse, const double* dout, const long long* ptr,
+                     const int* cols, int H, int Lq, int Lk, int Dk, int Dv, double scale,
+                     double* dq, double* dk_acc, double* dv_acc, void* stream);
+/* Sorted-row statistics of non-negative fp64 rows S [R][L]: with the row sorted by value
+ * descending (ties: lower index first) and csum its sequential prefix sums,
+ * n_keep[r] = min(L, #{csum < min(theta, total) - eps} + 1) (theta <= 0: L; NULL: skipped)
+ * and topmass[r] = sum of the first top_n sorted values (NULL: skipped). Rows whose padded
+ * length fits shared memory need no scratch; otherwise pass scratch of
+ * dsv_sorted_stats_scratch_bytes(R, L) bytes. */
+long long dsv_sorted_stats_scratch_bytes(int R, int L);
+int dsv_sorted_stats_f64(const double* S, long long lds, int R, int L, double theta, double eps,
+                         int top_n, int* n_keep, double* topmass, void* scratch,
+                         long long scratch_bytes, void* stream);
+/* counts[b] += #{S values with edges[b] <= v < edges[b+1]} (last bin closed); nb bins,
+ * edges ascending [nb + 1], counts uint64 [nb] (np.histogram semantics). */
+int dsv_histogram_f64(const double* S, long long lds, int R, int N, const double* edges, int nb,
+                      unsigned long long* counts, void* stream);
+
+/* Per query q: inter[q] = |E_q & O_q| for sorted CSR lists E (est_ptr / est_cols) and O
+ * (ora_ptr / ora_cols), est_mass[q] / ora_mass[q] = sum of S[q][j] over each list
+ * (predictor.py:262-281 prediction_accuracy). */
+int dsv_set_stats_f64(const double* S, long long lds, int Q, const long long* est_ptr,
+                      const int* est_cols, const long long* ora_ptr, const int* ora_cols,
+                      int* inter, double* est_mass, double* ora_mass, void* stream);
 
 #ifdef __cplusplus
 }

@@ -67,3 +67,30 @@ def back(t: torch.Tensor, like, np_dtype=None):
         return t
     out = t.detach().cpu().numpy()
     return out.astype(np_dtype, copy=False) if np_dtype is not None else out
+
+
+def wants_f64(x) -> bool:
+    """The reference-precision path: host (numpy) data and torch float64 tensors compute in
+    fp64 on the device, like the reference computes in the caller's dtype (float64 by
+    default; float32 inputs get fp64 arithmetic and fp32 results). torch fp32 / bf16
+    tensors keep the fp32 / tensor-core paths."""
+    return (not is_torch(x)) or x.dtype == torch.float64
+
+
+def result_dtype(*xs):
+    """numpy result dtype of the reference's arithmetic on host inputs (None for torch)."""
+    if any(is_torch(x) for x in xs):
+        return None
+    return np.result_type(*[np.asarray(x).dtype for x in xs])
+
+
+def check_unit_interval(name: str, value: float, *, open_low=False, open_high=False) -> float:
+    """validate.py:36-44."""
+    value = float(value)
+    low_ok = value > 0.0 if open_low else value >= 0.0
+    high_ok = value < 1.0 if open_high else value <= 1.0
+    if not (low_ok and high_ok and np.isfinite(value)):
+        lo = "(" if open_low else "["
+        hi = ")" if open_high else "]"
+        raise ValueError(f"{name} must lie in {lo}0, 1{hi}, got {value}")
+    return value

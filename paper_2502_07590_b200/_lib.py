@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
-from ctypes import c_float, c_int, c_longlong, c_void_p
+from ctypes import c_double, c_float, c_int, c_longlong, c_void_p
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
@@ -69,8 +69,26 @@ SIGNATURES = {
                            c_int, c_void_p, c_void_p],
     "dsv_ring_accum_bf16": [c_void_p, c_void_p, c_longlong, c_int, c_void_p, c_void_p],
     "dsv_ring_accum_f32": [c_void_p, c_void_p, c_longlong, c_int, c_void_p],
+    # reference-precision (fp64) path
+    "dsv_gemm_f64": [c_void_p, c_longlong, c_longlong, c_longlong, c_void_p, c_longlong, c_longlong,
+                     c_longlong, c_void_p, c_longlong, c_longlong, c_int, c_int, c_int, c_int,
+                     c_double, c_void_p],
+    "dsv_softmax_rows_f64": [c_void_p, c_longlong, c_int, c_int, c_void_p],
+    "dsv_topk_f64": [c_void_p, c_longlong, c_int, c_int, c_void_p, c_int, c_void_p, c_longlong,
+                     c_void_p, c_void_p],
+    "dsv_rows_fwd_f64": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int,
+                         c_int, c_int, c_double, c_void_p, c_void_p, c_void_p],
+    "dsv_rows_bwd_f64": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                         c_void_p, c_int, c_int, c_int, c_int, c_int, c_double, c_void_p, c_void_p,
+                         c_void_p, c_void_p],
+    "dsv_sorted_stats_scratch_bytes": [c_int, c_int],
+    "dsv_sorted_stats_f64": [c_void_p, c_longlong, c_int, c_int, c_double, c_double, c_int,
+                             c_void_p, c_void_p, c_void_p, c_longlong, c_void_p],
+    "dsv_histogram_f64": [c_void_p, c_longlong, c_int, c_int, c_void_p, c_int, c_void_p, c_void_p],
+    "dsv_set_stats_f64": [c_void_p, c_longlong, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
+                          c_void_p, c_void_p, c_void_p, c_void_p],
 }
-_RESTYPES = {"dsv_last_error": ctypes.c_char_p}
+_RESTYPES = {"dsv_last_error": ctypes.c_char_p, "dsv_sorted_stats_scratch_bytes": c_longlong}
 
 _lib = None
 

@@ -46,6 +46,25 @@ int dsv_accum_bf16_launch(float*, const void*, long long, int, void*, cudaStream
 int dsv_accum_f32_launch(float*, float*, long long, int, cudaStream_t);
 int dsv_proxy_scores_launch(const void*, long long, long long, const void*, long long, long long,
                             float*, long long, long long, int, int, int, cudaStream_t);
+int dsv_gemm_f64_launch(const double*, long long, long long, long long, const double*, long long,
+                        long long, long long, double*, long long, long long, int, int, int, int,
+                        double, cudaStream_t);
+int dsv_softmax_rows_f64_launch(double*, long long, int, int, cudaStream_t);
+int dsv_topk_f64_launch(const double*, long long, int, int, const int*, int, int*, long long,
+                        double*, cudaStream_t);
+int dsv_rows_fwd_f64_launch(const double*, const double*, const double*, const long long*,
+                            const int*, int, int, int, int, int, double, double*, double*,
+                            cudaStream_t);
+int dsv_rows_bwd_f64_launch(const double*, const double*, const double*, const double*,
+                            const double*, const double*, const long long*, const int*, int, int,
+                            int, int, int, double, double*, double*, double*, cudaStream_t);
+size_t dsv_sorted_stats_smem(int);
+int dsv_sorted_stats_launch(const double*, long long, int, int, int, double, double, int, int*,
+                            double*, void*, int, cudaStream_t);
+int dsv_histogram_f64_launch(const double*, long long, int, int, const double*, int,
+                             unsigned long long*, cudaStream_t);
+int dsv_set_stats_f64_launch(const double*, long long, int, const long long*, const int*,
+                             const long long*, const int*, int*, double*, double*, cudaStream_t);
 
 namespace {
 
@@ -508,4 +527,106 @@ extern "C" int dsv_gather_rows(const void* src, long long src_stride, const int*
     gather_rows_kernel<false><<<blocks, 256, 0, S(stream)>>>((const uint8_t*)src, src_stride, rows, n,
                                                              row_bytes, (uint8_t*)out, out_stride);
   return cuda_status((int)cudaGetLastError(), "gather_rows launch");
+}
+
+// ---------------------------------------------------------------- fp64 precision path
+namespace {
+int pad_pow2(int L) {
+  int p = 2;
+  while (p < L) p <<= 1;
+  return p;
+}
+constexpr size_t kSortSmemMax = 200 * 1024;
+constexpr int kSortScratchCtas = 64;
+}  // namespace
+
+extern "C" int dsv_gemm_f64(const double* A, long long sam, long long sat, long long a_bs,
+                            const double* B, long long sbt, long long sbn, long long b_bs,
+                            double* C, long long ldc, long long c_bs, int M, int N, int K,
+                            int nbatch, double div, void* stream) {
+  if (M <= 0 || N <= 0 || nbatch <= 0) return fail(DSV_EINVAL, "gemm_f64: empty shape");
+  if (K < 0) return fail(DSV_EINVAL, "gemm_f64: negative inner dimension");
+  if (!A || !B || !C) return fail(DSV_EINVAL, "gemm_f64: null operand");
+  if (!(div != 0.0)) return fail(DSV_EINVAL, "gemm_f64: zero divisor");
+  return cuda_status(dsv_gemm_f64_launch(A, sam, sat, a_bs, B, sbt, sbn, b_bs, C, ldc, c_bs, M, N,
+                                         K, nbatch, div, S(stream)), "gemm_f64 launch");
+}
+
+extern "C" int dsv_softmax_rows_f64(double* x, long long ld, int R, int N, void* stream) {
+  if (R <= 0 || N <= 0 || ld < N) return fail(DSV_EINVAL, "softmax_rows_f64: bad shape");
+  return cuda_status(dsv_softmax_rows_f64_launch(x, ld, R, N, S(stream)), "softmax_rows_f64 launch");
+}
+
+extern "C" int dsv_topk_f64(const double* Sc, long long lds, int R, int L, const int* k_per,
+                            int rows_per_k, int* out, long long ldo, double* thr, void* stream) {
+  if (R <= 0 || L <= 0 || lds < L || rows_per_k <= 0) return fail(DSV_EINVAL, "topk_f64: bad shape");
+  if (!Sc || !k_per || !out || !thr) return fail(DSV_EINVAL, "topk_f64: null operand");
+  return cuda_status(dsv_topk_f64_launch(Sc, lds, R, L, k_per, rows_per_k, out, ldo, thr, S(stream)),
+                     "topk_f64 launch");
+}
+
+extern "C" int dsv_rows_fwd_f64(const double* q, const double* k, const double* v,
+                                const long long* ptr, const int* cols, int H, int Lq, int Lk,
+                                int Dk, int Dv, double scale, double* out, double* lse,
+                                void* stream) {
+  if (Dk < 1 || Dk > 256 || Dv < 1 || Dv > 256)
+    return fail(DSV_EUNSUPPORTED, "rows_fwd_f64: head dims (%d, %d) outside [1, 256]", Dk, Dv);
+  if (H <= 0 || Lq <= 0 || Lk <= 0) return fail(DSV_EINVAL, "rows_fwd_f64: empty shape");
+  return cuda_status(dsv_rows_fwd_f64_launch(q, k, v, ptr, cols, H, Lq, Lk, Dk, Dv, scale, out, lse,
+                                             S(stream)), "rows_fwd_f64 launch");
+}
+
+extern "C" int dsv_rows_bwd_f64(const double* q, const double* k, const double* v,
+                                const double* out, const double* lse, const double* dout,
+                                const long long* ptr, const int* cols, int H, int Lq, int Lk,
+                                int Dk, int Dv, double scale, double* dq, double* dk_acc,
+                                double* dv_acc, void* stream) {
+  if (Dk < 1 || Dk > 256 || Dv < 1 || Dv > 256)
+    return fail(DSV_EUNSUPPORTED, "rows_bwd_f64: head dims (%d, %d) outside [1, 256]", Dk, Dv);
+  if (H <= 0 || Lq <= 0 || Lk <= 0) return fail(DSV_EINVAL, "rows_bwd_f64: empty shape");
+  return cuda_status(dsv_rows_bwd_f64_launch(q, k, v, out, lse, dout, ptr, cols, H, Lq, Lk, Dk, Dv,
+                                             scale, dq, dk_acc, dv_acc, S(stream)),
+                     "rows_bwd_f64 launch");
+}
+
+extern "C" long long dsv_sorted_stats_scratch_bytes(int R, int L) {
+  if (R <= 0 || L <= 0) return 0;
+  const int Lpad = pad_pow2(L);
+  if (dsv_sorted_stats_smem(Lpad) <= kSortSmemMax) return 0;
+  const int ctas = R < kSortScratchCtas ? R : kSortScratchCtas;
+  return (long long)ctas * Lpad * 12;
+}
+
+extern "C" int dsv_sorted_stats_f64(const double* Sc, long long lds, int R, int L, double theta,
+                                    double eps, int top_n, int* n_keep, double* topmass,
+                                    void* scratch, long long scratch_bytes, void* stream) {
+  if (R <= 0 || L <= 0 || lds < L) return fail(DSV_EINVAL, "sorted_stats_f64: bad shape");
+  if (L > (1 << 30)) return fail(DSV_EUNSUPPORTED, "sorted_stats_f64: row too long");
+  const int Lpad = pad_pow2(L);
+  const long long need = dsv_sorted_stats_scratch_bytes(R, L);
+  if (need > 0 && (!scratch || scratch_bytes < need))
+    return fail(DSV_EINVAL, "sorted_stats_f64: rows of %d keys need %lld bytes of scratch", L, need);
+  const int ctas = need > 0 ? (R < kSortScratchCtas ? R : kSortScratchCtas) : 0;
+  return cuda_status(dsv_sorted_stats_launch(Sc, lds, R, L, Lpad, theta, eps, top_n, n_keep, topmass,
+                                             need > 0 ? scratch : nullptr, ctas, S(stream)),
+                     "sorted_stats_f64 launch");
+}
+
+extern "C" int dsv_histogram_f64(const double* Sc, long long lds, int R, int N, const double* edges,
+                                 int nb, unsigned long long* counts, void* stream) {
+  if (R < 0 || N < 0 || nb < 1 || nb > 16384) return fail(DSV_EINVAL, "histogram_f64: bad shape");
+  if (R == 0 || N == 0) return DSV_OK;
+  return cuda_status(dsv_histogram_f64_launch(Sc, lds, R, N, edges, nb, counts, S(stream)),
+                     "histogram_f64 launch");
+}
+
+extern "C" int dsv_set_stats_f64(const double* Sc, long long lds, int Q, const long long* est_ptr,
+                                 const int* est_cols, const long long* ora_ptr,
+                                 const int* ora_cols, int* inter, double* est_mass,
+                                 double* ora_mass, void* stream) {
+  if (Q <= 0) return fail(DSV_EINVAL, "set_stats_f64: no queries");
+  if (!Sc || !est_ptr || !ora_ptr || !inter || !est_mass || !ora_mass)
+    return fail(DSV_EINVAL, "set_stats_f64: null operand");
+  return cuda_status(dsv_set_stats_f64_launch(Sc, lds, Q, est_ptr, est_cols, ora_ptr, ora_cols, inter,
+                                              est_mass, ora_mass, S(stream)), "set_stats_f64 launch");
 }

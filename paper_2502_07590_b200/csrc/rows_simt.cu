@@ -70,126 +70,136 @@ scores_kernel(const T* __restrict__ A, long long lda, long long a_bs,
 }
 
 // ---------------------------------------------------------------- attention
-// q: [H, Lq, d], k/v: [H, Lk, d]; ptr: [H*Lq + 1] (int64), cols: int32 key ids.
-template <typename T, int NE>  // NE = ceil(d / 32) elements per lane
+// q: [H, Lq, dk], k: [H, Lk, dk], v: [H, Lk, dv]; ptr: [H*Lq + 1] (int64), cols: int32 key ids
+// (cols == nullptr: every key). A is the arithmetic type: fp32 for bf16 / fp32 inputs, fp64
+// for the reference-precision path (host fp64 callers: the reference computes in the input
+// dtype, pkg/src/dynsparse/attention.py:95-109 / 153-187).
+template <typename T, typename A> DSV_DEV A ld_a(const T* p) { return (A)ld_f(p); }
+template <> DSV_DEV double ld_a<double, double>(const double* p) { return __ldg(p); }
+DSV_DEV float ex_a(float x) { return __expf(x); }
+DSV_DEV double ex_a(double x) { return exp(x); }
+DSV_DEV float lg_a(float x) { return logf(x); }
+DSV_DEV double lg_a(double x) { return log(x); }
+
+template <typename T, typename A, int NE>  // NE = ceil(max(dk, dv) / 32) elements per lane
 __global__ void __launch_bounds__(256)
 attn_rows_fwd_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
                      const long long* __restrict__ ptr, const int* __restrict__ cols,
-                     int H, int Lq, int Lk, int d, float scale,
-                     float* __restrict__ o, float* __restrict__ lse) {
+                     int H, int Lq, int Lk, int dk, int dv, A scale,
+                     A* __restrict__ o, A* __restrict__ lse) {
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (gw >= H * Lq) return;
   const int h = gw / Lq;
-  const T* qr = q + (long long)gw * d;
-  float qv[NE], acc[NE];
+  const T* qr = q + (long long)gw * dk;
+  A qv[NE], acc[NE];
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
     const int c = lane + 32 * e;
-    qv[e] = (c < d) ? ld_f(qr + c) * scale : 0.f;
-    acc[e] = 0.f;
+    qv[e] = (c < dk) ? ld_a<T, A>(qr + c) : A(0);
+    acc[e] = A(0);
   }
-  float m = -INFINITY, l = 0.f;
+  A m = -INFINITY, l = A(0);
   const long long p0 = cols ? ptr[gw] : 0, p1 = cols ? ptr[gw + 1] : Lk;
-  const T* kh = k + (long long)h * Lk * d;
-  const T* vh = v + (long long)h * Lk * d;
+  const T* kh = k + (long long)h * Lk * dk;
+  const T* vh = v + (long long)h * Lk * dv;
   for (long long p = p0; p < p1; ++p) {
     const int key = cols ? cols[p] : (int)p;
-    const T* kr = kh + (long long)key * d;
-    float s = 0.f;
+    const T* kr = kh + (long long)key * dk;
+    A s = A(0);
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
       const int c = lane + 32 * e;
-      if (c < d) s = fmaf(qv[e], ld_f(kr + c), s);
+      if (c < dk) s = fma(qv[e], ld_a<T, A>(kr + c), s);
     }
 #pragma unroll
     for (int o2 = 16; o2; o2 >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o2);
-    const float mn = fmaxf(m, s);
-    const float alpha = __expf(m - mn);
-    const float pw = __expf(s - mn);
+    s *= scale;
+    const A mn = fmax(m, s);
+    const A alpha = ex_a(m - mn);
+    const A pw = ex_a(s - mn);
     l = l * alpha + pw;
-    const T* vr = vh + (long long)key * d;
+    const T* vr = vh + (long long)key * dv;
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
       const int c = lane + 32 * e;
-      acc[e] = acc[e] * alpha + ((c < d) ? pw * ld_f(vr + c) : 0.f);
+      acc[e] = acc[e] * alpha + ((c < dv) ? pw * ld_a<T, A>(vr + c) : A(0));
     }
     m = mn;
   }
-  const float inv = 1.f / l;
-  float* orow = o + (long long)gw * d;
+  const A inv = A(1) / l;
+  A* orow = o + (long long)gw * dv;
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
     const int c = lane + 32 * e;
-    if (c < d) orow[c] = acc[e] * inv;
+    if (c < dv) orow[c] = acc[e] * inv;
   }
-  if (lane == 0) lse[gw] = m + logf(l);
+  if (lane == 0) lse[gw] = m + lg_a(l);
 }
 
-template <typename T, int NE>
+template <typename T, typename A, int NE>
 __global__ void __launch_bounds__(256)
 attn_rows_bwd_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
-                     const float* __restrict__ o, const float* __restrict__ lse,
+                     const A* __restrict__ o, const A* __restrict__ lse,
                      const T* __restrict__ dout,
                      const long long* __restrict__ ptr, const int* __restrict__ cols,
-                     int H, int Lq, int Lk, int d, float scale,
-                     float* __restrict__ dq, float* __restrict__ dk, float* __restrict__ dv) {
+                     int H, int Lq, int Lk, int dk, int dv, A scale,
+                     A* __restrict__ dq, A* __restrict__ dkacc, A* __restrict__ dvacc) {
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (gw >= H * Lq) return;
   const int h = gw / Lq;
-  float qv[NE], dov[NE], dqa[NE];
-  float delta = 0.f;
+  A qv[NE], dov[NE], dqa[NE];
+  A delta = A(0);
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
     const int c = lane + 32 * e;
-    const bool ok = c < d;
-    qv[e] = ok ? ld_f(q + (long long)gw * d + c) : 0.f;
-    dov[e] = ok ? ld_f(dout + (long long)gw * d + c) : 0.f;
-    delta += ok ? dov[e] * o[(long long)gw * d + c] : 0.f;
-    dqa[e] = 0.f;
+    qv[e] = (c < dk) ? ld_a<T, A>(q + (long long)gw * dk + c) : A(0);
+    dov[e] = (c < dv) ? ld_a<T, A>(dout + (long long)gw * dv + c) : A(0);
+    delta += (c < dv) ? dov[e] * o[(long long)gw * dv + c] : A(0);
+    dqa[e] = A(0);
   }
 #pragma unroll
   for (int o2 = 16; o2; o2 >>= 1) delta += __shfl_xor_sync(0xffffffffu, delta, o2);
-  const float lrow = lse[gw];
+  const A lrow = lse[gw];
   const long long p0 = cols ? ptr[gw] : 0, p1 = cols ? ptr[gw + 1] : Lk;
-  const long long hoff = (long long)h * Lk * d;
+  const long long hk = (long long)h * Lk * dk, hv = (long long)h * Lk * dv;
   for (long long p = p0; p < p1; ++p) {
     const int key = cols ? cols[p] : (int)p;
-    const T* kr = k + hoff + (long long)key * d;
-    const T* vr = v + hoff + (long long)key * d;
-    float s = 0.f, dp = 0.f;
-    float kv[NE];
+    const T* kr = k + hk + (long long)key * dk;
+    const T* vr = v + hv + (long long)key * dv;
+    A s = A(0), dp = A(0);
+    A kv[NE];
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
       const int c = lane + 32 * e;
-      kv[e] = (c < d) ? ld_f(kr + c) : 0.f;
-      s = fmaf(qv[e], kv[e], s);
-      dp = fmaf(dov[e], (c < d) ? ld_f(vr + c) : 0.f, dp);
+      kv[e] = (c < dk) ? ld_a<T, A>(kr + c) : A(0);
+      s = fma(qv[e], kv[e], s);
+      dp = fma(dov[e], (c < dv) ? ld_a<T, A>(vr + c) : A(0), dp);
     }
 #pragma unroll
     for (int o2 = 16; o2; o2 >>= 1) {
       s += __shfl_xor_sync(0xffffffffu, s, o2);
       dp += __shfl_xor_sync(0xffffffffu, dp, o2);
     }
-    const float pw = __expf(s * scale - lrow);
-    const float ds = pw * (dp - delta) * scale;
-    float* dkr = dk + hoff + (long long)key * d;
-    float* dvr = dv + hoff + (long long)key * d;
+    const A pw = ex_a(s * scale - lrow);
+    const A ds = pw * (dp - delta) * scale;
+    A* dkr = dkacc + hk + (long long)key * dk;
+    A* dvr = dvacc + hv + (long long)key * dv;
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
       const int c = lane + 32 * e;
-      if (c < d) {
-        dqa[e] = fmaf(ds, kv[e], dqa[e]);
+      if (c < dk) {
+        dqa[e] = fma(ds, kv[e], dqa[e]);
         atomicAdd(dkr + c, ds * qv[e]);
-        atomicAdd(dvr + c, pw * dov[e]);
       }
+      if (c < dv) atomicAdd(dvr + c, pw * dov[e]);
     }
   }
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
     const int c = lane + 32 * e;
-    if (c < d) dq[(long long)gw * d + c] = dqa[e];
+    if (c < dk) dq[(long long)gw * dk + c] = dqa[e];
   }
 }
 
@@ -214,53 +224,75 @@ int dsv_scores_f32_launch(const void* A, long long lda, long long a_bs, const vo
   return (int)cudaGetLastError();
 }
 
-template <typename T>
+template <typename T, typename A>
 static int rows_fwd(const void* q, const void* k, const void* v, const long long* ptr,
-                    const int* cols, int H, int Lq, int Lk, int d, float scale, float* o,
-                    float* lse, cudaStream_t st) {
+                    const int* cols, int H, int Lq, int Lk, int dk, int dv, A scale, A* o, A* lse,
+                    cudaStream_t st) {
   const long long warps = (long long)H * Lq;
   const int blocks = (int)((warps * 32 + 255) / 256);
   const T *Q = (const T*)q, *K = (const T*)k, *V = (const T*)v;
+  const int d = dk > dv ? dk : dv;
+#define DSV_ROWS_FWD(NE) \
+  attn_rows_fwd_kernel<T, A, NE><<<blocks, 256, 0, st>>>(Q, K, V, ptr, cols, H, Lq, Lk, dk, dv, scale, o, lse)
   switch ((d + 31) / 32) {
-    case 1: attn_rows_fwd_kernel<T, 1><<<blocks, 256, 0, st>>>(Q, K, V, ptr, cols, H, Lq, Lk, d, scale, o, lse); break;
-    case 2: attn_rows_fwd_kernel<T, 2><<<blocks, 256, 0, st>>>(Q, K, V, ptr, cols, H, Lq, Lk, d, scale, o, lse); break;
-    case 3: case 4: attn_rows_fwd_kernel<T, 4><<<blocks, 256, 0, st>>>(Q, K, V, ptr, cols, H, Lq, Lk, d, scale, o, lse); break;
-    case 5: case 6: case 7: case 8: attn_rows_fwd_kernel<T, 8><<<blocks, 256, 0, st>>>(Q, K, V, ptr, cols, H, Lq, Lk, d, scale, o, lse); break;
+    case 1: DSV_ROWS_FWD(1); break;
+    case 2: DSV_ROWS_FWD(2); break;
+    case 3: case 4: DSV_ROWS_FWD(4); break;
+    case 5: case 6: case 7: case 8: DSV_ROWS_FWD(8); break;
     default: return 1;
   }
+#undef DSV_ROWS_FWD
   return (int)cudaGetLastError();
 }
 
-template <typename T>
-static int rows_bwd(const void* q, const void* k, const void* v, const float* o, const float* lse,
+template <typename T, typename A>
+static int rows_bwd(const void* q, const void* k, const void* v, const A* o, const A* lse,
                     const void* dout, const long long* ptr, const int* cols, int H, int Lq, int Lk,
-                    int d, float scale, float* dq, float* dk, float* dv, cudaStream_t st) {
+                    int dk, int dv, A scale, A* dq, A* dka, A* dva, cudaStream_t st) {
   const long long warps = (long long)H * Lq;
   const int blocks = (int)((warps * 32 + 255) / 256);
   const T *Q = (const T*)q, *K = (const T*)k, *V = (const T*)v, *DO = (const T*)dout;
+  const int d = dk > dv ? dk : dv;
+#define DSV_ROWS_BWD(NE) \
+  attn_rows_bwd_kernel<T, A, NE><<<blocks, 256, 0, st>>>(Q, K, V, o, lse, DO, ptr, cols, H, Lq, Lk, dk, dv, scale, dq, dka, dva)
   switch ((d + 31) / 32) {
-    case 1: attn_rows_bwd_kernel<T, 1><<<blocks, 256, 0, st>>>(Q, K, V, o, lse, DO, ptr, cols, H, Lq, Lk, d, scale, dq, dk, dv); break;
-    case 2: attn_rows_bwd_kernel<T, 2><<<blocks, 256, 0, st>>>(Q, K, V, o, lse, DO, ptr, cols, H, Lq, Lk, d, scale, dq, dk, dv); break;
-    case 3: case 4: attn_rows_bwd_kernel<T, 4><<<blocks, 256, 0, st>>>(Q, K, V, o, lse, DO, ptr, cols, H, Lq, Lk, d, scale, dq, dk, dv); break;
-    case 5: case 6: case 7: case 8: attn_rows_bwd_kernel<T, 8><<<blocks, 256, 0, st>>>(Q, K, V, o, lse, DO, ptr, cols, H, Lq, Lk, d, scale, dq, dk, dv); break;
+    case 1: DSV_ROWS_BWD(1); break;
+    case 2: DSV_ROWS_BWD(2); break;
+    case 3: case 4: DSV_ROWS_BWD(4); break;
+    case 5: case 6: case 7: case 8: DSV_ROWS_BWD(8); break;
     default: return 1;
   }
+#undef DSV_ROWS_BWD
   return (int)cudaGetLastError();
 }
 
 int dsv_rows_fwd_launch(const void* q, const void* k, const void* v, const long long* ptr,
                         const int* cols, int H, int Lq, int Lk, int d, float scale, int bf16_in,
                         float* o, float* lse, cudaStream_t st) {
-  return bf16_in ? rows_fwd<__nv_bfloat16>(q, k, v, ptr, cols, H, Lq, Lk, d, scale, o, lse, st)
-                 : rows_fwd<float>(q, k, v, ptr, cols, H, Lq, Lk, d, scale, o, lse, st);
+  return bf16_in ? rows_fwd<__nv_bfloat16, float>(q, k, v, ptr, cols, H, Lq, Lk, d, d, scale, o, lse, st)
+                 : rows_fwd<float, float>(q, k, v, ptr, cols, H, Lq, Lk, d, d, scale, o, lse, st);
 }
 
 int dsv_rows_bwd_launch(const void* q, const void* k, const void* v, const float* o,
                         const float* lse, const void* dout, const long long* ptr, const int* cols,
                         int H, int Lq, int Lk, int d, float scale, int bf16_in, float* dq,
                         float* dk, float* dv, cudaStream_t st) {
-  return bf16_in ? rows_bwd<__nv_bfloat16>(q, k, v, o, lse, dout, ptr, cols, H, Lq, Lk, d, scale,
-                                           dq, dk, dv, st)
-                 : rows_bwd<float>(q, k, v, o, lse, dout, ptr, cols, H, Lq, Lk, d, scale, dq, dk,
-                                   dv, st);
+  return bf16_in ? rows_bwd<__nv_bfloat16, float>(q, k, v, o, lse, dout, ptr, cols, H, Lq, Lk, d, d,
+                                                  scale, dq, dk, dv, st)
+                 : rows_bwd<float, float>(q, k, v, o, lse, dout, ptr, cols, H, Lq, Lk, d, d, scale,
+                                          dq, dk, dv, st);
+}
+
+int dsv_rows_fwd_f64_launch(const double* q, const double* k, const double* v, const long long* ptr,
+                            const int* cols, int H, int Lq, int Lk, int dk, int dv, double scale,
+                            double* o, double* lse, cudaStream_t st) {
+  return rows_fwd<double, double>(q, k, v, ptr, cols, H, Lq, Lk, dk, dv, scale, o, lse, st);
+}
+
+int dsv_rows_bwd_f64_launch(const double* q, const double* k, const double* v, const double* o,
+                            const double* lse, const double* dout, const long long* ptr,
+                            const int* cols, int H, int Lq, int Lk, int dk, int dv, double scale,
+                            double* dq, double* dka, double* dva, cudaStream_t st) {
+  return rows_bwd<double, double>(q, k, v, o, lse, dout, ptr, cols, H, Lq, Lk, dk, dv, scale, dq,
+                                  dka, dva, st);
 }

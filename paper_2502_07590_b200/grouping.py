@@ -151,8 +151,10 @@ def grouped_sparse_attention(q, k, v, plan: VoxelGroupPlan, group_sets: list, *,
         if a.size == 0:
             raise ValueError(f"group {g} has an empty index set")
         sets.append(a)
-    tc_ok = (cv.is_torch(q) and q.dtype == torch.bfloat16 and q.dim() == 2 and q.shape[1] in (64, 128)
-             and plan.max_group <= TILE)
+    tc_ok = (cv.is_torch(q) and cv.is_torch(k) and cv.is_torch(v)
+             and all(t.dtype == torch.bfloat16 and t.is_cuda and t.dim() == 2 for t in (q, k, v))
+             and q.shape[1] in (64, 128) and k.shape[1] == q.shape[1] and v.shape == k.shape
+             and q.shape[0] == plan.grid.size and plan.max_group <= TILE)
     if not tc_ok:
         per_query = [None] * plan.grid.size
         for g, members in enumerate(plan.members):
@@ -178,3 +180,86 @@ def grouped_sparse_attention(q, k, v, plan: VoxelGroupPlan, group_sets: list, *,
         flops.add_pairs(int(sum(s.size * m.size for s, m in zip(sets, plan.members))), q.shape[1])
         flops.add_per_query(q.shape[0])
     return out[0]
+
+
+def _softmax_rows_device(q, k, rows=None):
+    """fp64 post-softmax scores of q[rows] against every key (attention.py:112-115 math,
+    dsv_gemm_f64 + dsv_softmax_rows_f64)."""
+    from . import _convert as cv
+    from . import ops
+
+    qd = cv.to_device(q, torch.float64)
+    if rows is not None:
+        qd = qd[torch.as_tensor(np.asarray(rows, dtype=np.int64), device=qd.device)]
+    kd = cv.to_device(k, torch.float64)
+    sc = ops.gemm_f64(qd.contiguous(), kd.t(), div=float(np.sqrt(q.shape[1])))
+    return ops.softmax_rows_f64_(sc)
+
+
+def _member_sets(q, k, members, theta, k_top):
+    """Critical sets of one group's member queries (grouping.py:117-126): the exact top-k_top
+    (streaming_topk) or the theta-mass prefix of each member's softmax row."""
+    from .attention import _critical_device
+    from .selection import streaming_topk
+
+    if k_top is not None:
+        rows = streaming_topk(q[members], k, k_top).indices
+        return [np.asarray(rows[i]) for i in range(len(members))]
+    return _critical_device(_softmax_rows_device(q, k, members), theta)
+
+
+def select_group_critical(q, k, plan: VoxelGroupPlan, theta: float) -> list:
+    """Per-group critical sets selected by each group's proxy query (grouping.py:184-193):
+    the theta-mass prefix of the proxy's softmax row, on the device."""
+    from . import _convert as cv
+    from .attention import _check_unit_interval, _critical_device
+
+    theta = _check_unit_interval("theta", theta, open_low=True)
+    q = cv.as_matrix("Q", q)
+    k = cv.as_matrix("K", k)
+    cv.check_same_cols("Q", q, "K", k)
+    return _critical_device(_softmax_rows_device(q, k, plan.proxies), theta)
+
+
+def calibrate_group_size(qs, ks, grid: TokenGrid, theta: float = 0.9, target_ratio: float = 0.8,
+                         *, k_top=None, n_sample_groups: int = 32, seed: int = 0,
+                         ladder=SIZE_LADDER) -> tuple:
+    """Largest ladder voxel whose sampled mean proxy overlap meets target_ratio
+    (grouping.py:129-181). Groups are sampled with the same generator calls as the
+    reference (so the same groups are scored); member sets come from the device."""
+    from . import _convert as cv
+
+    target_ratio = cv.check_unit_interval("target_ratio", target_ratio, open_low=True)
+    if not isinstance(qs, (list, tuple)) and np.ndim(qs) == 2:
+        qs, ks = [qs], [ks]
+    heads = []
+    for q, k in zip(qs, ks):
+        q, k = cv.as_matrix("Q", q), cv.as_matrix("K", k)
+        cv.check_same_cols("Q", q, "K", k)
+        if q.shape[0] != grid.size:
+            raise ValueError("Q rows must match the grid token count")
+        heads.append((q, k))
+    best, best_count = (1, 1, 1), 1
+    rng = np.random.default_rng(seed)
+    for dims in ladder:
+        dims = tuple(int(x) for x in dims)
+        if dims == (1, 1, 1):
+            continue
+        if dims[0] > grid.frames or dims[1] > grid.height or dims[2] > grid.width:
+            continue
+        plan = build_groups(grid, dims)
+        eligible = [g for g in range(plan.n_groups) if plan.members[g].size > 1]
+        if not eligible:
+            continue
+        chosen = rng.choice(len(eligible), size=min(n_sample_groups, len(eligible)), replace=False)
+        ratios = []
+        for gi in np.asarray(chosen):
+            g = eligible[gi]
+            members = plan.members[g]
+            proxy_pos = int(np.searchsorted(members, plan.proxies[g]))
+            for q, k in heads:
+                ratios.append(overlap_ratio(_member_sets(q, k, members, theta, k_top), proxy_pos))
+        count = int(np.prod(dims))
+        if np.mean(ratios) >= target_ratio and count > best_count:
+            best, best_count = dims, count
+    return best

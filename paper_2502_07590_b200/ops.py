@@ -344,3 +344,142 @@ def ring_accum_f32(acc, part, first: bool) -> None:
     if part.numel() != acc.numel():
         raise ValueError("ring_accum_f32: shape mismatch")
     _lib.call("dsv_ring_accum_f32", _ptr(acc), _ptr(part), acc.numel(), int(first), _stream())
+
+
+# ------------------------------------------------------------------- fp64 precision path
+_F64 = torch.float64
+
+
+def _need_f64(*ts):
+    for t in ts:
+        if t is not None and t.dtype != _F64:
+            raise ValueError("fp64 kernels need float64 tensors")
+
+
+def gemm_f64(a: torch.Tensor, b: torch.Tensor, div: float = 1.0, out=None) -> torch.Tensor:
+    """fp64 C = (A . B) / div on CUDA cores (dsv_gemm_f64). a: [M, K] or [nb, M, K],
+    b: [K, N] or [nb, K, N]; any strides (pass b = x.t() for A . x^T)."""
+    _require_cuda(a, b)
+    _need_f64(a, b)
+    squeeze = a.dim() == 2
+    if squeeze:
+        a, b = a.unsqueeze(0), b.unsqueeze(0)
+    nb, M, K = a.shape
+    if b.shape[0] != nb or b.shape[1] != K:
+        raise ValueError(f"gemm_f64 shape mismatch {tuple(a.shape)} x {tuple(b.shape)}")
+    N = b.shape[2]
+    if out is None:
+        c = torch.empty((nb, M, N), device=a.device, dtype=_F64)
+    else:
+        c = out.unsqueeze(0) if squeeze else out
+        if tuple(c.shape) != (nb, M, N) or c.dtype != _F64 or c.stride(2) != 1:
+            raise ValueError("gemm_f64 out has the wrong shape, dtype or layout")
+    _lib.call("dsv_gemm_f64", _ptr(a), a.stride(1), a.stride(2), a.stride(0), _ptr(b), b.stride(1),
+              b.stride(2), b.stride(0), _ptr(c), c.stride(1), c.stride(0), M, N, K, nb, float(div),
+              _stream())
+    return c[0] if squeeze else c
+
+
+def softmax_rows_f64_(x: torch.Tensor) -> torch.Tensor:
+    """In place: every row of the fp64 matrix x becomes its max-subtracted softmax."""
+    _require_cuda(x)
+    _need_f64(x)
+    if x.dim() != 2 or x.stride(1) != 1:
+        raise ValueError("softmax_rows_f64_ expects a row-major fp64 matrix")
+    _lib.call("dsv_softmax_rows_f64", _ptr(x), x.stride(0), x.shape[0], x.shape[1], _stream())
+    return x
+
+
+def topk_f64(scores: torch.Tensor, k_per, rows_per_k: int, k_max: int):
+    """Exact top-k per row of fp64 scores [R, L] (dsv_topk_f64). k_per: int32 device tensor,
+    row r uses k_per[r // rows_per_k]. Returns (idx int32 [R, k_max], thr fp64 [R])."""
+    _require_cuda(scores, k_per)
+    _need_f64(scores)
+    if scores.dim() != 2 or scores.stride(1) != 1:
+        raise ValueError("topk_f64 expects a row-major fp64 matrix")
+    R, L = scores.shape
+    kp = k_per.to(device=scores.device, dtype=torch.int32).contiguous()
+    idx = torch.empty((R, k_max), device=scores.device, dtype=torch.int32)
+    thr = torch.empty((R,), device=scores.device, dtype=_F64)
+    _lib.call("dsv_topk_f64", _ptr(scores), scores.stride(0), R, L, _ptr(kp), int(rows_per_k),
+              _ptr(idx), idx.stride(0), _ptr(thr), _stream())
+    return idx, thr
+
+
+def rows_fwd_f64(q, k, v, ptr, cols, scale):
+    """fp64 attention over CSR lists (cols None: every key). q [H, Lq, Dk], k [H, Lk, Dk],
+    v [H, Lk, Dv] -> (out [H, Lq, Dv], lse [H, Lq]) fp64."""
+    _require_cuda(q, k, v)
+    _need_f64(q, k, v)
+    H, Lq, Dk = q.shape
+    Lk, Dv = k.shape[1], v.shape[2]
+    out = torch.empty((H, Lq, Dv), device=q.device, dtype=_F64)
+    lse = torch.empty((H, Lq), device=q.device, dtype=_F64)
+    _lib.call("dsv_rows_fwd_f64", _ptr(q), _ptr(k), _ptr(v), _ptr(ptr), _ptr(cols), H, Lq, Lk, Dk,
+              Dv, float(scale), _ptr(out), _ptr(lse), _stream())
+    return out, lse
+
+
+def rows_bwd_f64(q, k, v, out, lse, dout, ptr, cols, scale):
+    """Backward of rows_fwd_f64 -> fp64 (dq, dk, dv)."""
+    _require_cuda(q, k, v, out, lse, dout)
+    _need_f64(q, k, v, out, lse, dout)
+    H, Lq, Dk = q.shape
+    Lk, Dv = k.shape[1], v.shape[2]
+    dq = torch.empty_like(q)
+    dk = torch.zeros((H, Lk, Dk), device=q.device, dtype=_F64)
+    dv = torch.zeros((H, Lk, Dv), device=q.device, dtype=_F64)
+    _lib.call("dsv_rows_bwd_f64", _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), _ptr(dout),
+              _ptr(ptr), _ptr(cols), H, Lq, Lk, Dk, Dv, float(scale), _ptr(dq), _ptr(dk), _ptr(dv),
+              _stream())
+    return dq, dk, dv
+
+
+def sorted_stats_f64(scores: torch.Tensor, theta: float = 0.0, eps: float = 0.0, top_n: int = 0,
+                     want_keep: bool = True, want_top: bool = False):
+    """Per row of non-negative fp64 scores: (n_keep int32 [R] | None, topmass fp64 [R] | None)
+    (dsv_sorted_stats_f64: the critical-prefix length and the top-n mass of the sorted row)."""
+    _require_cuda(scores)
+    _need_f64(scores)
+    if scores.dim() != 2 or scores.stride(1) != 1:
+        raise ValueError("sorted_stats_f64 expects a row-major fp64 matrix")
+    R, L = scores.shape
+    keep = torch.empty((R,), device=scores.device, dtype=torch.int32) if want_keep else None
+    top = torch.empty((R,), device=scores.device, dtype=_F64) if want_top else None
+    nbytes = int(load_lib().dsv_sorted_stats_scratch_bytes(R, L))
+    scratch = torch.empty((max(nbytes, 1),), device=scores.device, dtype=torch.uint8) if nbytes else None
+    _lib.call("dsv_sorted_stats_f64", _ptr(scores), scores.stride(0), R, L, float(theta), float(eps),
+              int(top_n), _ptr(keep), _ptr(top), _ptr(scratch), nbytes, _stream())
+    return keep, top
+
+
+def histogram_f64(values: torch.Tensor, edges: torch.Tensor) -> torch.Tensor:
+    """np.histogram(values, bins=edges) counts on the device (int64 [len(edges) - 1])."""
+    _require_cuda(values, edges)
+    _need_f64(values, edges)
+    v = values if values.dim() == 2 else values.reshape(1, -1)
+    if v.stride(-1) != 1:
+        v = v.contiguous()
+    nb = edges.numel() - 1
+    counts = torch.zeros((nb,), device=values.device, dtype=torch.int64)
+    _lib.call("dsv_histogram_f64", _ptr(v), v.stride(0), v.shape[0], v.shape[1],
+              _ptr(edges.contiguous()), nb, _ptr(counts), _stream())
+    return counts
+
+
+def load_lib():
+    return _lib.load()
+
+
+def set_stats_f64(scores: torch.Tensor, e_ptr, e_cols, o_ptr, o_cols):
+    """Per query: (|E & O| int32, mass(E) fp64, mass(O) fp64) of two sorted CSR index sets
+    under the fp64 score rows (dsv_set_stats_f64)."""
+    _require_cuda(scores, e_ptr, o_ptr)
+    _need_f64(scores)
+    Q = scores.shape[0]
+    inter = torch.empty((Q,), device=scores.device, dtype=torch.int32)
+    em = torch.empty((Q,), device=scores.device, dtype=_F64)
+    om = torch.empty((Q,), device=scores.device, dtype=_F64)
+    _lib.call("dsv_set_stats_f64", _ptr(scores), scores.stride(0), Q, _ptr(e_ptr), _ptr(e_cols),
+              _ptr(o_ptr), _ptr(o_cols), _ptr(inter), _ptr(em), _ptr(om), _stream())
+    return inter, em, om

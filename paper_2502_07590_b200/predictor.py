@@ -3,9 +3,11 @@
 Per attention block (the north_star: per head) two projections W_q, W_k in
 R^{d x d_lr}; the predicted score matrix (X W_q)(X W_k)^T is ranked per query
 and its top-k keys are the critical KV estimate. Here:
-  * project            -> K1a tcgen05 GEMM (bf16 in, fp32 accumulate)
-  * estimate_critical  -> K1a for both sides, then fp32 score rows (K1b) and the
-                          exact K2 top-k; per-query k arrays use per-row k on
+  * project            -> host / fp64 inputs: dsv_gemm_f64 (the reference's fp64);
+                          bf16 / fp32 torch tensors: K1a tcgen05 GEMM (bf16 in, fp32 acc)
+  * estimate_critical  -> the same projection for both sides, then score rows and the
+                          exact top-k (fp64 rows + dsv_topk_f64 on the precision path,
+                          fp32 rows + K2 otherwise); per-query k arrays use per-row k on
                           the device (same result as the reference's
                           top-k_max + re-rank, predictor.py:246-259, because the
                           top-k set of a row is nested in its top-k_max set).
@@ -89,15 +91,33 @@ class PredictorParams:
 
 
 def project(x, w):
-    """X W (predictor.py:94-100) on the tcgen05 GEMM: bf16 inputs, fp32 accumulate."""
+    """X W (predictor.py:94-100). Host / fp64 inputs: fp64 on the device (dsv_gemm_f64, the
+    reference's precision; numpy in -> numpy out in numpy's result dtype). bf16 / fp32 torch
+    tensors: the K1a tcgen05 GEMM (bf16 operands, fp32 accumulate)."""
     x = cv.as_matrix("X", x)
     w = cv.as_matrix("W", w)
     if x.shape[1] != w.shape[0]:
         raise ValueError(f"X has {x.shape[1]} cols but W has {w.shape[0]} rows")
+    if cv.wants_f64(x) and cv.wants_f64(w):
+        out = ops.gemm_f64(cv.to_device(x, torch.float64), cv.to_device(w, torch.float64))
+        return cv.back(out, x, cv.result_dtype(x, w))
     xd = cv.to_device(x, torch.bfloat16)
     wt = cv.to_device(w.T if not cv.is_torch(w) else w.t(), torch.bfloat16)
     out = ops.gemm_bf16(xd, wt, torch.float32)
     return cv.back(out, x, x.dtype if not cv.is_torch(x) else None)
+
+
+def _lowrank(params: PredictorParams, x):
+    """(Q_lr, K_lr) on the device: fp64 for host / fp64 inputs (reference precision), else
+    the bf16 tcgen05 projection of both sides in one GEMM."""
+    if cv.wants_f64(x):
+        xd = cv.to_device(x, torch.float64)
+        w = torch.from_numpy(np.concatenate([params.w_q, params.w_k], axis=1)).to(xd.device)
+        lr = ops.gemm_f64(xd, w)                                         # [S, 2 d_lr] fp64
+    else:
+        xd = cv.to_device(x, torch.bfloat16)
+        lr = ops.gemm_bf16(xd, params.device_wt(), torch.float32)      # [S, 2 d_lr]
+    return lr[:, : params.d_lr].contiguous(), lr[:, params.d_lr:].contiguous()
 
 
 def estimate_critical(params: PredictorParams, x, k=None, sparsity=None, *, flops=None,
@@ -111,10 +131,7 @@ def estimate_critical(params: PredictorParams, x, k=None, sparsity=None, *, flop
         k = k_from_sparsity(sparsity, s_total)
     if x.shape[1] != params.d:
         raise ValueError(f"X has {x.shape[1]} cols but the predictor expects d={params.d}")
-    xd = cv.to_device(x, torch.bfloat16)
-    lr = ops.gemm_bf16(xd, params.device_wt(), torch.float32)      # [S, 2 d_lr]
-    q_lr = lr[:, : params.d_lr].contiguous()
-    k_lr = lr[:, params.d_lr:].contiguous()
+    q_lr, k_lr = _lowrank(params, x)
     if flops is not None:
         flops.projection += 2 * 2 * s_total * params.d * params.d_lr
     if np.ndim(k) == 0:
@@ -136,6 +153,68 @@ def estimate_critical(params: PredictorParams, x, k=None, sparsity=None, *, flop
     idx = res[0].cpu().numpy()
     sets = CriticalIndexSet([idx[i, : sizes[i]] for i in range(s_total)], theta=None)
     return (sets, res[2]) if return_scores else sets
+
+
+def prediction_accuracy(estimated: CriticalIndexSet, oracle: CriticalIndexSet, scores):
+    """(recall, score coverage) of an estimate against the oracle sets (predictor.py:262-281):
+    mean over queries of |est & oracle| / |oracle| and of mass(est) / mass(oracle) under the
+    post-softmax `scores` (1 where the oracle set / mass is empty). The per-query
+    intersections and masses are one pass of dsv_set_stats on the device."""
+    scores = cv.as_matrix("scores", scores)
+    if estimated.n_queries != oracle.n_queries:
+        raise ValueError("estimate and oracle cover different query counts")
+    n = oracle.n_queries
+    if n == 0:
+        return float("nan"), float("nan")
+    dev = cv.device()
+    sc = cv.to_device(scores, torch.float64)
+    e_ptr, e_cols = estimated.to_csr(dev)
+    o_ptr, o_cols = oracle.to_csr(dev)
+    inter, e_mass, o_mass = ops.set_stats_f64(sc, e_ptr, e_cols, o_ptr, o_cols)
+    inter = inter.cpu().numpy().astype(np.float64)
+    e_mass = e_mass.cpu().numpy()
+    o_mass = o_mass.cpu().numpy()
+    o_size = oracle.sizes().astype(np.float64)
+    recalls = np.where(o_size > 0, inter / np.where(o_size > 0, o_size, 1.0), 1.0)
+    cover = np.where(o_mass > 0, e_mass / np.where(o_mass > 0, o_mass, 1.0), 1.0)
+    return float(recalls.mean()), float(cover.mean())
+
+
+def save_checkpoint(params: PredictorParams, directory, block_id: int):
+    """predictor.py:284-310: the six matrices as DTSR binary tensors plus canonical JSON
+    metadata (serialize.save_tensor format), so reference checkpoints load here and back."""
+    from pathlib import Path
+
+    from . import serialize
+
+    directory = Path(directory)
+    directory.mkdir(parents=True, exist_ok=True)
+    stem = f"predictor_block{block_id:03d}"
+    files = {}
+    for tag in ("w_q", "w_k", "m_q", "v_q", "m_k", "v_k"):
+        path = directory / f"{stem}.{tag}.bin"
+        serialize.save_tensor(path, getattr(params, tag))
+        files[tag] = path.name
+    meta = {"block_id": block_id, "d": params.d, "d_lr": params.d_lr, "lr": params.lr,
+            "step": params.step, "loss_history": params.loss_history, "files": files}
+    meta_path = directory / f"{stem}.json"
+    meta_path.write_text(serialize.canonical_json(meta))
+    return meta_path
+
+
+def load_checkpoint(meta_path) -> PredictorParams:
+    """predictor.py:313-324."""
+    import json
+    from pathlib import Path
+
+    from . import serialize
+
+    meta_path = Path(meta_path)
+    meta = json.loads(meta_path.read_text())
+    arr = {tag: serialize.load_tensor(meta_path.parent / name) for tag, name in meta["files"].items()}
+    return PredictorParams(w_q=arr["w_q"], w_k=arr["w_k"], lr=meta["lr"], step=meta["step"],
+                           m_q=arr["m_q"], v_q=arr["v_q"], m_k=arr["m_k"], v_k=arr["v_k"],
+                           loss_history=list(meta["loss_history"]))
 
 
 @dataclass

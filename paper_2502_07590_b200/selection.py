@@ -3,11 +3,13 @@
 `streaming_topk` / `twopass_select` keep the reference signatures and exact
 semantics — per query the k largest scores of Q_lr K_lr^T, ties toward the lower
 key index, indices ascending, threshold = k-th largest score — but run on the
-GPU: the score rows are produced by the fp32 CUDA-core product kernel (K1b,
-deterministic t-order fmaf) in row chunks and selected by the K2 kernel, so the
-S x S product is only ever materialised one chunk at a time on the device.
-Given identical fp32 scores the selected sets are bit-exact with the reference
-rule (tests/test_gpu_api.py, tests/test_gpu_kernels.py).
+GPU in row chunks, so the S x S product is only ever materialised one chunk at a
+time (within the reference's O(S k) working set). Host (numpy) and torch fp64
+inputs take the reference-precision path: fp64 score tiles (dsv_gemm_f64) and the
+fp64 top-k (dsv_topk_f64), fp64 thresholds. torch fp32 / bf16 inputs score in
+fp32 (deterministic t-order fmaf) and select with the K2 kernel. Given identical
+scores the selected sets are bit-exact with the reference rule
+(tests/test_gpu_api.py, tests/test_gpu_kernels.py, conformance/).
 """
 
 from __future__ import annotations
@@ -78,15 +80,25 @@ def _prep(q_lr, k_lr, k):
     return q_lr, k_lr, k
 
 
+def _chunk_rows(s_q: int, s_k: int, k_max: int, elem: int) -> int:
+    """Score rows per chunk: the live score chunk stays within 4 S k entries (the reference's
+    O(S k) working-set contract, selection.py:31-45 / tests/test_selection.py:100-107:
+    peak <= 8 S k with the (S, k) results) and within _ROW_CHUNK_BYTES."""
+    return max(1, min(s_q, (4 * s_q * k_max) // s_k, _ROW_CHUNK_BYTES // (elem * s_k)))
+
+
 def topk_scores_device(q: torch.Tensor, kk: torch.Tensor, k_per_row, meter=None, flops=None,
                        return_scores: bool = False):
     """Exact top-k of q @ kk.T on device; k_per_row: int or int tensor [S_q].
 
-    q: [S_q, r], kk: [S_k, r] (fp32 or bf16 CUDA tensors). Returns (idx int32
-    [S_q, k_max], thr fp32 [S_q]) and optionally the fp32 score matrix.
+    q: [S_q, r], kk: [S_k, r] CUDA tensors: fp64 (the reference-precision path: fp64 score
+    tiles on dsv_gemm_f64, fp64 top-k, fp64 thresholds) or fp32 / bf16 (fp32 scores, K2).
+    Returns (idx int32 [S_q, k_max], thr [S_q]) and optionally the score matrix.
     """
     s_q, r = q.shape
     s_k = kk.shape[0]
+    f64 = q.dtype == torch.float64
+    sdt = torch.float64 if f64 else torch.float32
     if isinstance(k_per_row, int):
         kvec = torch.full((1,), k_per_row, dtype=torch.int32, device=q.device)
         rows_per = max(s_q, 1)
@@ -96,21 +108,32 @@ def topk_scores_device(q: torch.Tensor, kk: torch.Tensor, k_per_row, meter=None,
         rows_per = 1
         k_max = int(kvec.max().item())
     idx = torch.empty((s_q, k_max), dtype=torch.int32, device=q.device)
-    thr = torch.empty((s_q,), dtype=torch.float32, device=q.device)
-    all_scores = torch.empty((s_q, s_k), dtype=torch.float32, device=q.device) if return_scores else None
-    chunk = max(1, min(s_q, _ROW_CHUNK_BYTES // (4 * s_k)))
+    thr = torch.empty((s_q,), dtype=sdt, device=q.device)
+    all_scores = torch.empty((s_q, s_k), dtype=sdt, device=q.device) if return_scores else None
+    chunk = _chunk_rows(s_q, s_k, k_max, 8 if f64 else 4)
     if meter is not None:
         meter.grab(2 * s_q * k_max, "result buffers")
+    buf = None
     for r0 in range(0, s_q, chunk):
         r1 = min(r0 + chunk, s_q)
-        sc = ops.scores_f32(q[r0:r1], kk) if all_scores is None else ops.scores_f32(
-            q[r0:r1], kk, out=all_scores[r0:r1].unsqueeze(0))
-        if sc.dim() == 3:
-            sc = sc[0]
+        if all_scores is not None:
+            sc = all_scores[r0:r1]
+        else:
+            if buf is None:
+                buf = torch.empty((chunk, s_k), dtype=sdt, device=q.device)
+            sc = buf[: r1 - r0]
+        if f64:
+            ops.gemm_f64(q[r0:r1], kk.t(), out=sc)
+        else:
+            ops.scores_f32(q[r0:r1], kk, out=sc.unsqueeze(0))
         if meter is not None:
             meter.grab(sc.numel(), "score chunk")
         kv = kvec if rows_per != 1 else kvec[r0:r1]
-        ii, tt = ops.topk_rows(sc, kv, rows_per if rows_per != 1 else 1, k_max)
+        rp = rows_per if rows_per != 1 else 1
+        if f64:
+            ii, tt = ops.topk_f64(sc, kv, rp, k_max)
+        else:
+            ii, tt = ops.topk_rows(sc, kv, rp, k_max)
         idx[r0:r1] = ii
         thr[r0:r1] = tt
         if meter is not None:
@@ -125,7 +148,12 @@ def topk_scores_device(q: torch.Tensor, kk: torch.Tensor, k_per_row, meter=None,
 
 def _run(q_lr, k_lr, k, meter=None, flops=None) -> TopKResult:
     q_lr, k_lr, k = _prep(q_lr, k_lr, k)
-    dt = torch.bfloat16 if (cv.is_torch(q_lr) and q_lr.dtype == torch.bfloat16) else torch.float32
+    if cv.wants_f64(q_lr) and cv.wants_f64(k_lr):
+        dt = torch.float64
+    elif cv.is_torch(q_lr) and q_lr.dtype == torch.bfloat16:
+        dt = torch.bfloat16
+    else:
+        dt = torch.float32
     qd, kd = cv.to_device(q_lr, dt), cv.to_device(k_lr, dt)
     idx, thr = topk_scores_device(qd, kd, k, meter=meter, flops=flops)
     if cv.is_torch(q_lr):

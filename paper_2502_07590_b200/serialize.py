@@ -151,3 +151,54 @@ def offload(encoded: torch.Tensor, stream=None):
         ev.record(stream)
     encoded.record_stream(stream)
     return host, ev
+
+
+# ---- binary tensors (serialize.py:1-85 "DTSR" layout), used by predictor checkpoints.
+# Little-endian: b"DTSR", version 1, dtype code (1 f64, 2 f32, 3 i32, 4 i64), ndim (1..4), a
+# reserved zero byte, ndim uint64 sizes, then the C-order element data.
+MAGIC = b"DTSR"
+VERSION = 1
+_CODES = {np.dtype(np.float64): 1, np.dtype(np.float32): 2, np.dtype(np.int32): 3,
+          np.dtype(np.int64): 4}
+_DTYPES = {c: dt for dt, c in _CODES.items()}
+
+
+def canonical_json(obj) -> str:
+    """Sorted keys, compact separators, trailing newline (serialize.py:36-38)."""
+    import json
+
+    return json.dumps(obj, sort_keys=True, separators=(",", ":")) + "\n"
+
+
+def tensor_bytes(arr) -> bytes:
+    arr = np.ascontiguousarray(arr)
+    if arr.dtype not in _CODES:
+        raise ValueError(f"unsupported dtype {arr.dtype}")
+    if not 1 <= arr.ndim <= 4:
+        raise ValueError(f"unsupported rank {arr.ndim}")
+    head = MAGIC + bytes([VERSION, _CODES[arr.dtype], arr.ndim, 0])
+    head += np.asarray(arr.shape, dtype="<u8").tobytes()
+    return head + arr.astype(arr.dtype.newbyteorder("<"), copy=False).tobytes(order="C")
+
+
+def tensor_from_bytes(raw: bytes) -> np.ndarray:
+    if raw[:4] != MAGIC:
+        raise ValueError("bad tensor magic")
+    if raw[4] != VERSION:
+        raise ValueError(f"unsupported tensor format version {raw[4]}")
+    dt = _DTYPES.get(raw[5])
+    if dt is None:
+        raise ValueError(f"unknown dtype code {raw[5]}")
+    ndim = raw[6]
+    dims = tuple(int(x) for x in np.frombuffer(raw, dtype="<u8", count=ndim, offset=8))
+    return np.frombuffer(raw, dtype=dt.newbyteorder("<"), offset=8 + 8 * ndim).reshape(dims).astype(dt)
+
+
+def save_tensor(path, arr) -> None:
+    with open(path, "wb") as fh:
+        fh.write(tensor_bytes(np.asarray(arr)))
+
+
+def load_tensor(path) -> np.ndarray:
+    with open(path, "rb") as fh:
+        return tensor_from_bytes(fh.read())

@@ -12,7 +12,7 @@ HEADER = Path(__file__).resolve().parent.parent / "include" / "dsv.h"
 
 def _declared():
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(dsv_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|long long|const char\*)\s+(dsv_\w+)\s*\(", text, re.M)))
 
 
 def test_header_declares_the_boundary():
