@@ -97,11 +97,20 @@ int dsv_scores_f32(const void* A, long long lda, long long a_bs, const void* B, 
  * r <= 64) without materialising them. Same scores (same tcgen05 sequence) and the same
  * selection semantics as dsv_gemm_bf16 (fp32 out) followed by dsv_topk with
  * rows_per_head = G: out_idx[h*G + g][0..k_h) ascending, out_thr[h*G + g].
- * split: CTAs per 128-row tile splitting the key range (cluster), 0 = automatic. */
+ * split: CTAs per 128-row tile splitting the key range (cluster), 0 = automatic.
+ * workspace (dsv_select_fused_workspace_size bytes for the largest k, or NULL): enables the single-pass
+ * mode — sample passes pick a key band around the k-th score, one collect pass writes a
+ * per-row bitmap of the keys at or above the band plus the band entries, a finish kernel
+ * selects the k-th score among the band and emits from the bitmap; row tiles whose band
+ * missed it re-run the exact multi-pass algorithm (same results either way). NULL: the
+ * multi-pass algorithm only (sample, band refinement, candidates, emission passes).
+ * The workspace size is 0 where the single pass is not worthwhile (the band would hold too
+ * large a share of the keys, or need more than 1 GiB): pass NULL then. */
+long long dsv_select_fused_workspace_size(int H, int G, int L, int k_max, int split);
 int dsv_select_fused(const void* q_prox, long long ldq, long long q_bs, const void* k_lr,
                      long long ldk, long long k_bs, int H, int G, int L, int r,
                      const int* k_per_head, int* out_idx, long long out_ld, float* out_thr,
-                     int split, void* stream);
+                     int split, void* workspace, long long ws_bytes, void* stream);
 
 /* Exact top-k per row of an fp32 score matrix (K2).
  * scores: [rows][ld] fp32; row r uses k = k_per_head[r / rows_per_head] (1 <= k <= L).

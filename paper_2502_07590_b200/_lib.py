@@ -35,7 +35,8 @@ SIGNATURES = {
                        c_void_p],
     "dsv_select_fused": [c_void_p, c_longlong, c_longlong, c_void_p, c_longlong, c_longlong, c_int,
                          c_int, c_int, c_int, c_void_p, c_void_p, c_longlong, c_void_p, c_int,
-                         c_void_p],
+                         c_void_p, c_longlong, c_void_p],
+    "dsv_select_fused_workspace_size": [c_int, c_int, c_int, c_int, c_int],
     "dsv_topk": [c_void_p, c_longlong, c_int, c_int, c_void_p, c_int, c_void_p, c_longlong,
                  c_void_p, c_void_p],
     "dsv_sparse_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_longlong,
@@ -88,7 +89,8 @@ SIGNATURES = {
     "dsv_set_stats_f64": [c_void_p, c_longlong, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
                           c_void_p, c_void_p, c_void_p, c_void_p],
 }
-_RESTYPES = {"dsv_last_error": ctypes.c_char_p, "dsv_sorted_stats_scratch_bytes": c_longlong}
+_RESTYPES = {"dsv_last_error": ctypes.c_char_p, "dsv_sorted_stats_scratch_bytes": c_longlong,
+             "dsv_select_fused_workspace_size": c_longlong}
 
 _lib = None
 

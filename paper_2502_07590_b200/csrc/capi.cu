@@ -39,7 +39,8 @@ int dsv_attn_bwd_tc_launch(const void*, const void*, const void*, const void*, c
                            float*, float*, unsigned*, cudaStream_t);
 int dsv_f32_to_bf16_launch(const float*, void*, long long, cudaStream_t);
 int dsv_select_fused_launch(const CUtensorMap*, const CUtensorMap*, int, int, int, const int*, int*,
-                            long long, float*, int, cudaStream_t);
+                            long long, float*, int, void*, long long, cudaStream_t);
+long long dsv_select_fused_ws_bytes(int, int, int, int, int);
 int dsv_lse_merge_launch(float*, const float*, float*, const void*, const float*, long long, int,
                          int, void*, cudaStream_t);
 int dsv_accum_bf16_launch(float*, const void*, long long, int, void*, cudaStream_t);
@@ -224,10 +225,34 @@ int dsv_proxy_scores(const void* q_prox, long long ldq, long long q_bs, const vo
                      "proxy_scores launch");
 }
 
+static int select_split(int H, int G, int L, int split) {
+  // key-range split per 128-row tile (a cluster of `split` CTAs): fewest waves per unit
+  // of per-CTA work, at least one 128-key tile per CTA
+  const int n_mt = H * ((G + 127) / 128), nt = (L + 127) / 128;
+  int ns = split;
+  if (ns <= 0) {
+    int sms = dsv_device_sm_count();
+    if (sms <= 0) sms = 148;        // no device visible: size for a B200
+    double best = 1e30;
+    for (int s = 1; s <= 4 && s <= nt; ++s) {
+      const double cost = (double)((n_mt * s + sms - 1) / sms) / s;
+      if (cost < best - 1e-9) { best = cost; ns = s; }
+    }
+  }
+  return ns;
+}
+
+long long dsv_select_fused_workspace_size(int H, int G, int L, int k_max, int split) {
+  if (H <= 0 || G <= 0 || L <= 0 || k_max < 1 || k_max > L) return 0;
+  const int ns = select_split(H, G, L, split);
+  if (ns < 1 || ns > 8) return 0;
+  return dsv_select_fused_ws_bytes(H, G, L, k_max, ns);
+}
+
 int dsv_select_fused(const void* q_prox, long long ldq, long long q_bs, const void* k_lr,
                      long long ldk, long long k_bs, int H, int G, int L, int r,
                      const int* k_per_head, int* out_idx, long long out_ld, float* out_thr,
-                     int split, void* stream) {
+                     int split, void* workspace, long long ws_bytes, void* stream) {
   if (H <= 0 || G <= 0 || L <= 0) return fail(DSV_EINVAL, "select_fused: empty shape");
   if (r < 1 || r > 16) return fail(DSV_EUNSUPPORTED, "select_fused: predictor rank %d (1..16)", r);
   if (!al16(q_prox) || !al16(k_lr) || (ldq * 2) % 16 || (ldk * 2) % 16 || (q_bs * 2) % 16 ||
@@ -248,21 +273,11 @@ int dsv_select_fused(const void* q_prox, long long ldq, long long q_bs, const vo
     if (!make_map(&tb, k_lr, 3, dims, st, box, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, CU_TENSOR_MAP_SWIZZLE_32B))
       return fail(DSV_EINVAL, "select_fused: tensor map K");
   }
-  // key-range split per 128-row tile (a cluster of `split` CTAs): fewest waves per unit
-  // of per-CTA work, at least one 128-key tile per CTA
-  const int n_mt = H * ((G + 127) / 128), nt = (L + 127) / 128;
-  int ns = split;
-  if (ns <= 0) {
-    const int sms = dsv_device_sm_count();
-    double best = 1e30;
-    for (int s = 1; s <= 4 && s <= nt; ++s) {
-      const double cost = (double)((n_mt * s + sms - 1) / sms) / s;
-      if (cost < best - 1e-9) { best = cost; ns = s; }
-    }
-  }
+  const int nt = (L + 127) / 128;
+  const int ns = select_split(H, G, L, split);
   if (ns < 1 || ns > 8 || ns > nt) return fail(DSV_EINVAL, "select_fused: split %d", ns);
   return cuda_status(dsv_select_fused_launch(&ta, &tb, H, G, L, k_per_head, out_idx, out_ld,
-                                             out_thr, ns, S(stream)),
+                                             out_thr, ns, workspace, ws_bytes, S(stream)),
                      "select_fused launch");
 }
 

@@ -61,6 +61,9 @@ constexpr int kCols = BN / kParts;            // columns per thread per tile
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kThreads = 64 + kEpiThreads;
 constexpr int kBuckets = 128;
+// histogram row stride (words): padded so that lanes = rows hitting the same bucket index
+// land in different shared-memory banks
+constexpr int kHistStride = kBuckets + 1;
 constexpr int kCap = 128;                     // candidates per row (cluster-wide) = bucket words
 constexpr int kSampleTiles = 48;
 constexpr int kFlushTiles = 8;                // tiles per emission flush (1024 columns)
@@ -82,13 +85,16 @@ constexpr uint32_t KEY_NEG0 = 0x7FFFFFFFu;    // the key no float maps to (-0.0 
 #endif
 
 enum : uint32_t { ST_REFINE = 0, ST_CAND = 1, ST_DONE = 2 };
-enum : uint32_t { P_MINMAX = 0, P_SHIST = 1, P_FULL = 2, P_EMIT = 3, P_EXIT = 4 };
+enum : uint32_t { P_MINMAX = 0, P_SHIST = 1, P_FULL = 2, P_EMIT = 3, P_EXIT = 4, P_COLLECT = 5 };
+// launch modes: exact multi-pass (classic), single collect pass + select_finish_kernel (fast),
+// classic restricted to the row tiles the finish kernel flagged (list)
+enum : int { M_CLASSIC = 0, M_FAST = 1, M_LIST = 2 };
 
 struct SL {
   static constexpr int kA = 0;
   static constexpr int kB = kA + BM * BK * 2;
   static constexpr int kU = kB + kStages * BN * BK * 2;              // hist / candidates
-  static constexpr int kStage = kU + BM * kBuckets * 4;              // emission masks
+  static constexpr int kStage = kU + ((BM * kHistStride * 4 + 15) / 16) * 16;  // emission masks
   static constexpr int kRows = kStage + ((BM * kStageStride * 4 + 15) / 16) * 16;
   static constexpr int kRowArrays = 20;                              // see Rows
   static constexpr int kScr = kRows + kRowArrays * BM * 4;          // band-element scratch
@@ -176,7 +182,11 @@ DSV_DEV uint32_t ld_peer(const uint32_t* p, uint32_t rank, uint32_t me) {
 DSV_DEV int range_lo(int nt, int S, int s) { return (int)(((long long)nt * s) / S); }
 // i-th sample tile of a range [t0, t1)
 // 1/8 of the range, at least 8 and at most kSampleTiles tiles
-DSV_DEV int sample_count(int n) { return min(n, max(8, min(kSampleTiles, n / 8))); }
+__host__ __device__ __forceinline__ int sample_count(int n) {
+  const int a = n / 8 < kSampleTiles ? n / 8 : kSampleTiles;
+  const int b = a > 8 ? a : 8;
+  return n < b ? n : b;
+}
 DSV_DEV int sample_tile(int t0, int n, int ns, int i) { return t0 + (int)(((long long)i * n) / ns); }
 
 // tile processed at step i of the current pass
@@ -217,7 +227,7 @@ DSV_DEV uint32_t warp_suffix(uint32_t v, int lane) {
 }
 
 DSV_DEV void finalize_row(Rows& R, uint32_t* U, int r, int lane, uint32_t pass, uint32_t S,
-                          uint32_t me, uint32_t ns, int L) {
+                          uint32_t me, uint32_t ns, int L, int mode) {
   const uint32_t st = R.state[r];
   if (pass == P_MINMAX) {
     if (lane == 0) {
@@ -232,7 +242,7 @@ DSV_DEV void finalize_row(Rows& R, uint32_t* U, int r, int lane, uint32_t pass, 
     return;
   }
   if (st == ST_DONE) return;
-  const uint32_t* hrow = U + r * kBuckets + 4 * lane;
+  const uint32_t* hrow = U + r * kHistStride + 4 * lane;
   uint32_t c[4] = {0u, 0u, 0u, 0u};
   if (pass == P_SHIST || st == ST_REFINE) {
     for (uint32_t s = 0; s < S; ++s) {
@@ -245,7 +255,10 @@ DSV_DEV void finalize_row(Rows& R, uint32_t* U, int r, int lane, uint32_t pass, 
   if (pass == P_SHIST) {
     const float lo = R.smin[r], hi = R.smax[r];
     const double tgt = (double)R.k[r] * ns / L;
-    const double marg = 4.0 * sqrt(fmax(tgt * (1.0 - tgt / ns), 0.0)) + 4.0;
+    // band half-width in sample ranks: 4 sigma (+4) when a miss only costs another FULL
+    // pass; 5.5 sigma (+8) for the single collect pass, where a miss re-runs the tile
+    const double sig = sqrt(fmax(tgt * (1.0 - tgt / ns), 0.0));
+    const double marg = mode == M_FAST ? 5.5 * sig + 8.0 : 4.0 * sig + 4.0;
     const double hi_rank = tgt - marg, lo_rank = tgt + marg;
     // highest bucket with cum > hi_rank / cum >= lo_rank
     int bh = -1, bl = -1;
@@ -329,7 +342,7 @@ DSV_DEV void finalize_row(Rows& R, uint32_t* U, int r, int lane, uint32_t pass, 
         for (int q = 0; q < 4; ++q)
           if (4 * lane + q > pick) part += ld_peer(hrow + q, s, me);
         const uint32_t gt = warp_sum(part) + ld_peer(R.cta_above + r, s, me);
-        const uint32_t eq = ld_peer(U + r * kBuckets + pick, s, me);
+        const uint32_t eq = ld_peer(U + r * kHistStride + pick, s, me);
         const uint32_t qv = eq_before >= need ? 0u : min(eq, need - eq_before);
         if (s < me) pos += gt + qv; else my_quota = qv;
         eq_before += eq;
@@ -353,7 +366,7 @@ DSV_DEV void finalize_row(Rows& R, uint32_t* U, int r, int lane, uint32_t pass, 
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const uint32_t i = (uint32_t)(lane + 32 * q);
-      if (i >= n && i < n + ns && i < (uint32_t)kCap) { cv[q] = ld_peer(U + r * kBuckets + (i - n), s, me); cs[q] = s; }
+      if (i >= n && i < n + ns && i < (uint32_t)kCap) { cv[q] = ld_peer(U + r * kHistStride + (i - n), s, me); cs[q] = s; }
     }
     n += ns;
   }
@@ -397,7 +410,9 @@ DSV_DEV void finalize_row(Rows& R, uint32_t* U, int r, int lane, uint32_t pass, 
 __global__ void __launch_bounds__(kThreads, 1)
 select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     int G, int L, int n_mt, const int* __restrict__ kcount,
-                    int* __restrict__ out_idx, long long ldo, float* __restrict__ out_thr) {
+                    int* __restrict__ out_idx, long long ldo, float* __restrict__ out_thr,
+                    int mode, uint32_t* __restrict__ bitmap, int nwords, uint2* __restrict__ stash,
+                    int cap, uint32_t* __restrict__ counts, const int* __restrict__ tile_fail) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Bars& B = *reinterpret_cast<Bars*>(smem + SL::kBar);
@@ -409,6 +424,7 @@ select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const uint32_t S = gridDim.x / (uint32_t)(n_mt);   // cluster size (grid = n_mt x S)
   const uint32_t me = S > 1 ? cluster_rank() : 0u;
   const int tile_id = blockIdx.x / S;
+  if (mode == M_LIST && tile_fail[tile_id] == 0) return;   // every CTA of the cluster agrees
   const int h = tile_id / ((G + BM - 1) / BM);
   const int m0 = (tile_id - h * ((G + BM - 1) / BM)) * BM;
   const int nt = (L + BN - 1) / BN;
@@ -439,7 +455,7 @@ select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     R.state[r] = live ? ST_REFINE : ST_DONE;
     R.T[r] = 0; R.pos[r] = 0; R.quota[r] = 0; R.taken[r] = 0; R.ncand[r] = 0;
   }
-  for (int i = threadIdx.x; i < BM * kBuckets; i += kThreads) U[i] = 0;
+  for (int i = threadIdx.x; i < BM * kHistStride; i += kThreads) U[i] = 0;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -522,8 +538,8 @@ select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       }
       uint32_t cnt = 0;
       float mn = __int_as_float(0x7f800000), mx = __int_as_float(0xff800000);
-      uint32_t* hist = U + row * kBuckets;
-      uint32_t* cand = U + row * kBuckets;    // candidates reuse the row's histogram space
+      uint32_t* hist = U + row * kHistStride;
+      uint32_t* cand = U + row * kHistStride;    // candidates reuse the row's histogram space
       uint32_t* scr = reinterpret_cast<uint32_t*>(smem + SL::kScr) + (threadIdx.x - 64) * kScratch;
       int ft = 0, flush_t0 = t0;
       const bool warp_idle = __all_sync(0xffffffffu, st == ST_DONE);
@@ -589,6 +605,46 @@ select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                     ++slot;
                   } while (bb);
                 }
+              }
+            }
+          }
+        } else if (pass == P_COLLECT) {
+          // one pass for the fast mode: bit (s >= lo) per column into the row's bitmap (the
+          // keys above the band are kept whatever T is), and every band entry (col, key)
+          // appended to this CTA's stash segment of the row; select_finish_kernel picks T
+          // among the stash and emits from the bitmap
+          if (!warp_idle && st != ST_DONE) {
+            const long long grow = (long long)h * G + m0 + row;
+            uint32_t* brow = bitmap + grow * nwords;
+            uint2* srow = stash + (grow * S + me) * cap;
+#pragma unroll
+            for (int c = 0; c < kCols / 32; ++c) {
+              uint32_t gm[4] = {0u, 0u, 0u, 0u}, bm[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const float s = __uint_as_float(v[c * 32 + j]);
+                const bool gt = s > hi_f;
+                if (gt) gm[j & 3] |= 1u << j;
+                if (!gt && s >= lo_f) bm[j & 3] |= 1u << j;
+              }
+              const uint32_t gt = (gm[0] | gm[1]) | (gm[2] | gm[3]);
+              const uint32_t band = (bm[0] | bm[1]) | (bm[2] | bm[3]);
+              const int cbase = col0 + c * 32;
+              if ((cbase >> 5) < nwords) brow[cbase >> 5] = gt | band;
+              if (band) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 4)
+                  *reinterpret_cast<uint4*>(scr + j) = make_uint4(v[c * 32 + j], v[c * 32 + j + 1],
+                                                                  v[c * 32 + j + 2], v[c * 32 + j + 3]);
+                uint32_t bb = band;
+                uint32_t slot = atomicAdd(R.ncand + row, (uint32_t)__popc(bb));
+                do {
+                  const int j = __ffs(bb) - 1;
+                  bb &= bb - 1;
+                  if (slot < (uint32_t)cap)
+                    srow[slot] = make_uint2((uint32_t)(cbase + j), f2key(__uint_as_float(scr[j])));
+                  ++slot;
+                } while (bb);
               }
             }
           }
@@ -696,6 +752,12 @@ select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         reinterpret_cast<float*>(stage)[part * BM + row] = mx;
       }
       named_bar_sync(1, kEpiThreads);
+      if (pass == P_COLLECT && part == 0 && m0 + row < G) {
+        const long long grow = (long long)h * G + m0 + row;
+        counts[grow * S + me] = R.ncand[row];
+        if (me == 0) reinterpret_cast<uint2*>(counts + (long long)gridDim.x * BM)[grow] =
+            make_uint2(R.klo[row], R.khi[row]);       // the band, for the finish kernel
+      }
       if (part == 0) {
         if (pass == P_FULL) {
           uint32_t c = 0;
@@ -717,9 +779,9 @@ select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     if (prof) FPROF_AT(np, 3);
     if (S > 1) cluster_sync(); else __syncthreads();
     if (prof) FPROF_AT(np, 4);
-    if (warp >= 2 && pass != P_EMIT) {
+    if (warp >= 2 && pass != P_EMIT && pass != P_COLLECT) {
       for (int r = warp - 2; r < BM; r += kEpiWarps)
-        finalize_row(R, U, r, lane, pass, S, me, ns_total, L);
+        finalize_row(R, U, r, lane, pass, S, me, ns_total, L, mode);
     }
     if (prof) FPROF_AT(np, 5);
     if (S > 1) cluster_sync(); else __syncthreads();
@@ -727,7 +789,7 @@ select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     // clear this CTA's partials for the next pass; choose the next pass
     if (warp >= 2) {
       const int et = threadIdx.x - 64;
-      for (int i = et; i < BM * kBuckets; i += kEpiThreads) U[i] = 0;
+      for (int i = et; i < BM * kHistStride; i += kEpiThreads) U[i] = 0;
       for (int r = et; r < BM; r += kEpiThreads) R.ncand[r] = 0;
       if (et == 0) B.flag = 0;
       named_bar_sync(1, kEpiThreads);
@@ -736,6 +798,8 @@ select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       if (et == 0) {
         uint32_t next, n;
         if (pass == P_MINMAX) { next = P_SHIST; n = sample_count(nrange); }
+        else if (pass == P_SHIST && mode == M_FAST) { next = P_COLLECT; n = nrange; }
+        else if (pass == P_COLLECT) { next = P_EXIT; n = 0; }
         else if (pass == P_SHIST || pass == P_FULL) {
           // (FULL passes are bounded: each narrows the key range 128x; the cap only
           // guards against a hang)
@@ -762,6 +826,252 @@ select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   if (S > 1) cluster_sync();   // no CTA exits while a peer may still read its shared memory
 }
 
+
+// ------------------------------------------------------------------ fast-mode finish
+// One warp per (head, proxy) row, after the collect pass: the row's bitmap marks every key
+// with s >= lo (all of S CTAs' key ranges) and the stash segments hold the band entries
+// (lo <= s <= hi) as (column, order key). With n_ge set bits and B band entries,
+// above = n_ge - B keys lie above the band, so T is the m-th largest band key, m = k - above
+// (1 <= m <= B when the band brackets T). Ties at T are kept in column order up to the
+// quota: need = m - #(band > T); when more band entries equal T, the need-th smallest tie
+// column bounds the kept ones. Dropped band entries are cleared from the bitmap, which then
+// holds exactly the k kept keys; a warp-wide scan over its words emits them ascending.
+// A row whose band missed T or overflowed its stash flags its row tile for the exact
+// multi-pass re-run (M_LIST launch).
+constexpr int kFinThreads = 256;
+constexpr int kFinDigit = 11;                        // radix digit (2048-bucket histogram)
+constexpr int kFinBuckets = 1 << kFinDigit;
+
+struct FinShared {
+  uint32_t hist[kFinBuckets];
+  uint32_t red[2][kFinThreads / 32];
+  uint32_t b, above;
+};
+
+// m-th largest (1-based) key among n entries passing `keyf`, all keys in [kmin, kmin + range]:
+// radix select on key - kmin with 11-bit digits from the top of the range (two rounds for
+// the band's ~2^22-ulp spread). *rem = m minus the number of entries strictly above it.
+template <typename AtF, typename KeyF>
+DSV_DEV uint32_t block_select(AtF at, uint32_t n, uint32_t m, uint32_t kmin, uint32_t range,
+                              FinShared& F, KeyF keyf, uint32_t* rem) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kPer = kFinBuckets / kFinThreads;    // buckets per thread (8)
+  const int top = range ? 31 - __clz(range) : 0;
+  uint32_t prefix = 0, remaining = m;
+  for (int sh = top + 1 - kFinDigit; sh > -kFinDigit; sh -= kFinDigit) {
+    const int shift = sh > 0 ? sh : 0;
+    const uint32_t mask_hi = sh + kFinDigit >= 32 ? 0u : (0xffffffffu << (sh + kFinDigit));
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) F.hist[tid * kPer + j] = 0u;
+    __syncthreads();
+    for (uint32_t i = tid; i < n; i += kFinThreads) {
+      uint32_t key;
+      if (keyf(at(i), key)) {
+        const uint32_t x = key - kmin;
+        if ((x & mask_hi) == prefix) atomicAdd(&F.hist[(x >> shift) & (kFinBuckets - 1)], 1u);
+      }
+    }
+    __syncthreads();
+    // thread t owns buckets (top down) kFinBuckets-1-kPer*t ..; block scan of their counts
+    uint32_t c[kPer], tot = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) { c[j] = F.hist[kFinBuckets - 1 - kPer * tid - j]; tot += c[j]; }
+    uint32_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) F.red[0][warp] = incl;
+    __syncthreads();
+    uint32_t wb = 0;
+#pragma unroll
+    for (int w = 0; w < kFinThreads / 32; ++w) wb += w < warp ? F.red[0][w] : 0u;
+    incl += wb;
+    const uint32_t excl = incl - tot;
+    if (excl < remaining && incl >= remaining) {
+      uint32_t run = excl;
+      int j = 0;
+      while (run + c[j] < remaining) { run += c[j]; ++j; }
+      F.b = kFinBuckets - 1 - kPer * tid - j;
+      F.above = run;
+    }
+    __syncthreads();
+    prefix |= F.b << shift;
+    remaining -= F.above;
+    __syncthreads();
+  }
+  *rem = remaining;
+  return prefix + kmin;
+}
+
+DSV_DEV uint32_t block_sum(uint32_t v, FinShared& F) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) F.red[1][warp] = v;
+  __syncthreads();
+  uint32_t t = 0;
+#pragma unroll
+  for (int w = 0; w < kFinThreads / 32; ++w) t += F.red[1][w];
+  __syncthreads();
+  return t;
+}
+
+// One CTA (256 threads) per (head, proxy) row, after the collect pass: the row's bitmap marks
+// every key with s >= lo (all S key ranges) and the stash segments hold the band entries
+// (lo <= s <= hi) as (column, order key). With n_ge set bits and B band entries,
+// above = n_ge - B keys lie above the band, so T is the m-th largest band key, m = k - above
+// (1 <= m <= B when the band brackets T). Ties at T are kept in column order up to the
+// quota: need = m - #(band > T); when more band entries equal T, the need-th smallest tie
+// column bounds the kept ones. Dropped band entries are cleared from the shared copy of the
+// bitmap, which then holds exactly the k kept keys, emitted ascending by a block scan.
+// A row whose band missed T (or overflowed its stash) flags its row tile for the exact
+// multi-pass re-run (M_LIST launch).
+__global__ void __launch_bounds__(kFinThreads)
+select_finish_kernel(int H, int G, int L, uint32_t S, const int* __restrict__ kcount,
+                     const uint32_t* __restrict__ bitmap, int nwords,
+                     const uint2* __restrict__ stash, int cap, const uint32_t* __restrict__ counts,
+                     const uint2* __restrict__ bandlim, int* __restrict__ out_idx, long long ldo,
+                     float* __restrict__ out_thr, int* __restrict__ tile_fail, int smem_cap) {
+  __shared__ FinShared F;
+  extern __shared__ __align__(16) uint8_t fin_smem[];
+  const int tid = threadIdx.x;
+  const int nw4 = (nwords + 3) & ~3;
+  uint32_t* bits = reinterpret_cast<uint32_t*>(fin_smem);
+  uint2* sband = reinterpret_cast<uint2*>(bits + nw4);
+  const long long row = blockIdx.x;
+  const int h = (int)(row / G), g = (int)(row % G);
+  int* fail = tile_fail + h * ((G + BM - 1) / BM) + g / BM;
+  const int kh = kcount[h];
+  const uint32_t k = (uint32_t)(kh < 1 ? 1 : (kh > L ? L : kh));
+  uint32_t segn[8];
+  uint32_t B = 0;
+  bool over = false;
+#pragma unroll
+  for (uint32_t s = 0; s < 8; ++s) {
+    segn[s] = 0;
+    if (s >= S) continue;
+    const uint32_t n = counts[row * S + s];
+    over |= n > (uint32_t)cap;
+    segn[s] = n > (uint32_t)cap ? (uint32_t)cap : n;
+    B += segn[s];
+  }
+  if (over) {
+    if (tid == 0) atomicExch(fail, 1);
+    return;
+  }
+  // stage the bitmap and (when they fit) the band entries in shared memory
+  const uint4* brow = reinterpret_cast<const uint4*>(bitmap + row * nwords);
+  uint32_t nge = 0;
+  if ((nwords & 3) == 0 && ((row * nwords) & 3) == 0) {
+    for (int w = tid; w < nwords / 4; w += kFinThreads) {
+      const uint4 x = brow[w];
+      reinterpret_cast<uint4*>(bits)[w] = x;
+      nge += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+    }
+  } else {
+    const uint32_t* b1 = bitmap + row * nwords;
+    for (int w = tid; w < nwords; w += kFinThreads) {
+      const uint32_t x = b1[w];
+      bits[w] = x;
+      nge += __popc(x);
+    }
+  }
+  const uint2* gbase = stash + row * S * cap;
+  const bool staged = B <= (uint32_t)smem_cap;
+  uint32_t sstart[8];
+  {
+    uint32_t off = 0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) { sstart[s] = off; off += segn[s]; }
+  }
+  if (staged) {
+    // band entries: four loads in flight per thread before their shared-memory stores
+    for (uint32_t s = 0; s < S; ++s) {
+      const uint2* src = gbase + (size_t)s * cap;
+      for (uint32_t i0 = 0; i0 < segn[s]; i0 += 4 * kFinThreads) {
+        uint2 v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t i = i0 + j * kFinThreads + tid;
+          if (i < segn[s]) v[j] = src[i];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t i = i0 + j * kFinThreads + tid;
+          if (i < segn[s]) sband[sstart[s] + i] = v[j];
+        }
+      }
+    }
+  }
+  // entry i of the row's band: shared copy, or its stash segment (rows too large to stage)
+  auto at = [&](uint32_t i) -> uint2 {
+    if (staged) return sband[i];
+    uint32_t s = 0;
+    while (s + 1 < S && i >= sstart[s + 1]) ++s;
+    return gbase[(size_t)s * cap + (i - sstart[s])];
+  };
+  nge = block_sum(nge, F);       // (its barriers also publish the staged copies)
+  const uint32_t above = nge - B;
+  if (nge < B || above >= k || above + B < k) {
+    if (tid == 0) atomicExch(fail, 1);
+    return;
+  }
+  const uint32_t m = k - above;
+  const uint2 lim = bandlim[row];
+  uint32_t need;
+  const uint32_t T = block_select(at, B, m, lim.x, lim.y - lim.x, F,
+                                  [](uint2 e, uint32_t& key) { key = e.y; return true; }, &need);
+  uint32_t eq = 0;
+  for (uint32_t i = tid; i < B; i += kFinThreads) eq += at(i).y == T;
+  eq = block_sum(eq, F);
+  uint32_t col_max = 0xffffffffu;
+  if (eq > need) {
+    uint32_t dummy;
+    const uint32_t cmin = ~(uint32_t)(L - 1);         // ~col lies in [~(L-1), ~0]
+    col_max = ~block_select(at, B, need, cmin, (uint32_t)(L - 1), F,
+                            [T](uint2 e, uint32_t& key) { key = ~e.x; return e.y == T; }, &dummy);
+  }
+  for (uint32_t i = tid; i < B; i += kFinThreads) {
+    const uint2 e = at(i);
+    if (!(e.y > T || (e.y == T && e.x <= col_max))) atomicAnd(bits + (e.x >> 5), ~(1u << (e.x & 31)));
+  }
+  __syncthreads();
+  // emit: thread t owns a contiguous run of words; block exclusive scan of their popcounts
+  const int wpt = (nwords + kFinThreads - 1) / kFinThreads;
+  const int w0 = tid * wpt, w1 = min(nwords, w0 + wpt);
+  uint32_t c = 0;
+  for (int w = w0; w < w1; ++w) c += __popc(bits[w]);
+  const int lane = tid & 31, warp = tid >> 5;
+  uint32_t incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) F.red[1][warp] = incl;
+  __syncthreads();
+  uint32_t wbase = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < kFinThreads / 32; ++w) {
+    if (w < warp) wbase += F.red[1][w];
+    total += F.red[1][w];
+  }
+  if (total != k) {                    // cannot happen when the band brackets T; be exact
+    if (tid == 0) atomicExch(fail, 1);
+    return;
+  }
+  int* op = out_idx + row * ldo + (wbase + incl - c);
+  for (int w = w0; w < w1; ++w) {
+    uint32_t word = bits[w];
+    const int cb = w * 32;
+    while (word) {
+      *op++ = cb + __ffs(word) - 1;
+      word &= word - 1;
+    }
+  }
+  if (tid == 0) out_thr[row] = key2f(T);
+}
 }  // namespace fsel
 }  // namespace dsv
 
@@ -774,9 +1084,10 @@ int dsv_debug_select_timeline_copy(void* dst, int bytes) {
 }
 
 // grid = n_mt row tiles x S key-range CTAs (cluster of S along x)
-int dsv_select_fused_launch(const CUtensorMap* ta, const CUtensorMap* tb, int H, int G, int L,
-                            const int* kcount, int* out_idx, long long ldo, float* out_thr,
-                            int S, cudaStream_t st) {
+static int launch_select(const CUtensorMap* ta, const CUtensorMap* tb, int H, int G, int L,
+                         const int* kcount, int* out_idx, long long ldo, float* out_thr, int S,
+                         int mode, uint32_t* bitmap, int nwords, uint2* stash, int cap,
+                         uint32_t* counts, const int* tile_fail, cudaStream_t st) {
   using namespace dsv::fsel;
   const int n_mt = H * ((G + BM - 1) / BM);
   auto kern = select_fused_kernel;
@@ -793,5 +1104,85 @@ int dsv_select_fused_launch(const CUtensorMap* ta, const CUtensorMap* tb, int H,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return (int)cudaLaunchKernelEx(&cfg, kern, *ta, *tb, G, L, n_mt, kcount, out_idx, ldo, out_thr);
+  return (int)cudaLaunchKernelEx(&cfg, kern, *ta, *tb, G, L, n_mt, kcount, out_idx, ldo, out_thr,
+                                 mode, bitmap, nwords, stash, cap, counts, tile_fail);
+}
+
+// fast-mode workspace: [tile_fail n_mt ints | counts rows*S u32 | bitmap rows*nwords u32 |
+// stash rows*S*cap uint2], each part 256-byte aligned; cap (band entries per row and CTA)
+// is what the remaining bytes hold
+static long long align256(long long x) { return (x + 255) & ~255LL; }
+
+static long long fixed_ws_bytes(int H, int G, int L, int S) {
+  const long long rows = (long long)H * G, n_mt = (long long)H * ((G + 127) / 128);
+  return align256(n_mt * 4) + align256(n_mt * S * 128 * 4 + rows * 8) +
+         align256(rows * ((L + 31) / 32) * 4);
+}
+
+// Expected band entries per (row, CTA): the sample passes pick a band of +-(5.5 sigma + 8)
+// sample ranks around the k-th (binomial sigma of the sample count above it), widened to
+// the 128-bucket grid of the sample histogram; cap = twice that (0 = the single pass is
+// not worthwhile: the band would hold too large a share of the keys, or too many bytes).
+long long dsv_select_fused_ws_bytes(int H, int G, int L, int k_max, int S) {
+  using namespace dsv::fsel;
+  const int nt = (L + BN - 1) / BN;
+  const int n = (nt + S - 1) / S;
+  const double ns = (double)S * sample_count(n) * BN;
+  const double pk = fmin((double)k_max, (double)(L - k_max)) / L;
+  const double sig = sqrt(fmax(ns * pk * (1.0 - pk), 0.0));
+  const double frac = 2.0 * (5.5 * sig + 8.0) / ns + 4.0 / kBuckets;
+  if (frac > 0.15) return 0;
+  const long long band = (long long)(frac * L / S) + 64;
+  const long long cap = ((2 * band + 255) / 256) * 256;
+  const long long rows = (long long)H * G;
+  const long long bytes = fixed_ws_bytes(H, G, L, S) + align256(rows * S * cap * 8);
+  return bytes > (1LL << 30) ? 0 : bytes;
+}
+
+int dsv_select_fused_launch(const CUtensorMap* ta, const CUtensorMap* tb, int H, int G, int L,
+                            const int* kcount, int* out_idx, long long ldo, float* out_thr,
+                            int S, void* ws, long long ws_bytes, cudaStream_t st) {
+  using namespace dsv::fsel;
+  const long long rows = (long long)H * G, n_mt = (long long)H * ((G + BM - 1) / BM);
+  const long long fixed = fixed_ws_bytes(H, G, L, S);
+  const long long capl = ws ? (ws_bytes - fixed) / (rows * S * 8) : 0;
+  if (capl < 256)
+    return launch_select(ta, tb, H, G, L, kcount, out_idx, ldo, out_thr, S, M_CLASSIC, nullptr, 0,
+                         nullptr, 0, nullptr, nullptr, st);
+  const int cap = (int)(capl > (1 << 24) ? (1 << 24) : capl);
+  const int nwords = (L + 31) / 32;
+  uint8_t* p = reinterpret_cast<uint8_t*>(ws);
+  int* tile_fail = reinterpret_cast<int*>(p);
+  p += align256(n_mt * 4);
+  // counts [rows][S] (row tiles x BM x S words reserved: the kernel addresses the band limits
+  // [rows] uint2 right after gridDim.x * BM words) then the band limits
+  uint32_t* counts = reinterpret_cast<uint32_t*>(p);
+  const uint2* bandlim = reinterpret_cast<const uint2*>(counts + n_mt * S * BM);
+  p += align256(n_mt * S * 128 * 4 + rows * 8);
+  uint32_t* bitmap = reinterpret_cast<uint32_t*>(p);
+  p += align256(rows * nwords * 4);
+  uint2* stash = reinterpret_cast<uint2*>(p);
+  cudaMemsetAsync(tile_fail, 0, n_mt * 4, st);
+  int rc = launch_select(ta, tb, H, G, L, kcount, out_idx, ldo, out_thr, S, M_FAST, bitmap, nwords,
+                         stash, cap, counts, tile_fail, st);
+  if (rc) return rc;
+  // one CTA per row: its bitmap and band entries staged in shared memory (<= 36 KB with the
+  // static part, so six CTAs share an SM); rows with more band entries read them from the
+  // workspace
+  const int nw4 = (nwords + 3) & ~3;
+  long long smem_cap = (36 * 1024 - 8400 - nw4 * 4) / 8;
+  if (smem_cap > (long long)S * cap) smem_cap = (long long)S * cap;
+  if (smem_cap < 0) smem_cap = 0;
+  const size_t fin_smem = (size_t)nw4 * 4 + (size_t)smem_cap * 8;
+  if (fin_smem > 200 * 1024) return (int)cudaErrorInvalidValue;
+  cudaFuncSetAttribute(select_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)fin_smem);
+  select_finish_kernel<<<(unsigned)rows, kFinThreads, fin_smem, st>>>(
+      H, G, L, (uint32_t)S, kcount, bitmap, nwords, stash, cap, counts, bandlim, out_idx, ldo,
+      out_thr, tile_fail, (int)smem_cap);
+  rc = (int)cudaGetLastError();
+  if (rc) return rc;
+  // exact multi-pass re-run of flagged row tiles (its CTAs exit at once when none is)
+  return launch_select(ta, tb, H, G, L, kcount, out_idx, ldo, out_thr, S, M_LIST, nullptr, 0,
+                       nullptr, 0, nullptr, tile_fail, st);
 }

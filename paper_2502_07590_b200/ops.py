@@ -135,13 +135,50 @@ def topk_rows(scores: torch.Tensor, k_per_head: torch.Tensor, rows_per_head: int
     return idx, thr
 
 
+_WS_CACHE = {}
+
+
+def select_workspace(H: int, G: int, L: int, k_max: int, split: int, device) -> torch.Tensor | None:
+    """Device workspace of the single-pass fused selection (cached per shape / device); None
+    where the library advises the multi-pass algorithm."""
+    key = (H, G, L, k_max, split, str(device))
+    if key not in _WS_CACHE:
+        n = int(_lib.load().dsv_select_fused_workspace_size(H, G, L, k_max, split))
+        _WS_CACHE[key] = torch.empty((n,), dtype=torch.uint8, device=device) if n > 0 else None
+    return _WS_CACHE[key]
+
+
+def select_fast_fallbacks(H: int, G: int, L: int, k_max: int, split: int, device) -> int:
+    """Row tiles the last single-pass selection of this shape re-ran with the multi-pass
+    algorithm (the workspace's leading tile-flag array; diagnostics). -1: no workspace."""
+    ws = _WS_CACHE.get((H, G, L, k_max, split, str(device)))
+    if ws is None:
+        return -1
+    n_mt = H * ((G + 127) // 128)
+    return int(ws[: 4 * n_mt].view(torch.int32).ne(0).sum().item())
+
+
+def select_band_stats(H: int, G: int, L: int, k_max: int, split: int, S: int, device):
+    """(mean, max) band entries per (row, CTA) of the last single-pass selection of this shape
+    (the workspace's count array; diagnostics for the band sizing)."""
+    ws = _WS_CACHE.get((H, G, L, k_max, split, str(device)))
+    if ws is None:
+        return None
+    n_mt = H * ((G + 127) // 128)
+    off = (n_mt * 4 + 255) // 256 * 256
+    c = ws[off: off + 4 * H * G * S].view(torch.int32).double()
+    return float(c.mean().item()), int(c.max().item())
+
+
 def select_fused(q_prox: torch.Tensor, k_lr: torch.Tensor, k_per_head: torch.Tensor,
-                 k_max: int | None = None, split: int = 0, out=None):
+                 k_max: int | None = None, split: int = 0, out=None, mode: str = "auto"):
     """K1b + K2 fused (select_fused.cu): exact top-k of q_prox[h] . k_lr[h]^T per row.
 
     q_prox [H, G, r], k_lr [H, L, r] bf16 with unit stride along r (r <= 16). Same result as
     topk_rows(gemm_bf16(q_prox, k_lr), k_per_head, G) without the [H, G, L] fp32 scores.
     Returns (idx int32 [H*G, k_max], thr fp32 [H*G]); out: optional preallocated pair.
+    mode: "fast" (single collect pass + finish, a cached workspace), "multipass" (no
+    workspace), "auto" = fast unless DSV_SELECT_MULTIPASS=1. Results are identical.
     """
     _require_cuda(q_prox, k_lr, k_per_head)
     if q_prox.dtype != torch.bfloat16 or k_lr.dtype != torch.bfloat16:
@@ -160,9 +197,14 @@ def select_fused(q_prox: torch.Tensor, k_lr: torch.Tensor, k_per_head: torch.Ten
         thr = torch.empty((H * G,), device=q_prox.device, dtype=torch.float32)
     else:
         idx, thr = out
+    if mode == "auto":
+        import os
+
+        mode = "multipass" if os.environ.get("DSV_SELECT_MULTIPASS") == "1" else "fast"
+    ws = select_workspace(H, G, L, int(k_max), int(split), q_prox.device) if mode == "fast" else None
     _lib.call("dsv_select_fused", _ptr(q_prox), q_prox.stride(1), q_prox.stride(0), _ptr(k_lr),
               k_lr.stride(1), k_lr.stride(0), H, G, L, r, _ptr(kp), _ptr(idx), idx.stride(0),
-              _ptr(thr), int(split), _stream())
+              _ptr(thr), int(split), _ptr(ws), 0 if ws is None else ws.numel(), _stream())
     return idx, thr
 
 

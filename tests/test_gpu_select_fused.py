@@ -25,19 +25,25 @@ def _operands(H, G, L, r, seed, ints=False, dev="cuda"):
 
 
 def _compare(q, k, ks, split=0, check_oracle=False):
+    for mode in ("fast", "multipass"):
+        _compare_mode(q, k, ks, split, check_oracle, mode)
+
+
+def _compare_mode(q, k, ks, split, check_oracle, mode):
     H, G, _ = q.shape
     L = k.shape[1]
     kc = torch.tensor(ks, dtype=torch.int32, device=q.device)
     kmax = max(ks)
     scores = ops.gemm_bf16(q, k, torch.float32)
     ref_idx, ref_thr = ops.topk_rows(scores.view(H * G, L), kc, G, kmax)
-    idx, thr = ops.select_fused(q, k, kc, kmax, split=split)
+    idx, thr = ops.select_fused(q, k, kc, kmax, split=split, mode=mode)
     torch.cuda.synchronize()
     ri, rt, fi, ft = ref_idx.cpu().numpy(), ref_thr.cpu().numpy(), idx.cpu().numpy(), thr.cpu().numpy()
     for h in range(H):
         kh = ks[h]
         rows = slice(h * G, (h + 1) * G)
-        np.testing.assert_array_equal(fi[rows, :kh], ri[rows, :kh], err_msg=f"head {h} k={kh} split={split}")
+        np.testing.assert_array_equal(fi[rows, :kh], ri[rows, :kh],
+                                      err_msg=f"head {h} k={kh} split={split} mode={mode}")
     assert np.all(ft == rt)
     if check_oracle:
         sc = scores.cpu().numpy()
@@ -96,3 +102,13 @@ def test_fused_c5_row_length():
     q, k = _operands(3, 130, 524288, 16, seed=15)
     q[2, :40] = torch.round(q[2, :40] * 2) / 2
     _compare(q, k, [52429, 1, 524287], split=0)
+
+
+def test_fast_mode_c2_needs_no_fallback():
+    # c2's selection shape on random scores: the sampled band brackets every row's k-th
+    # score, so the single-pass mode finishes every row tile itself
+    q, k = _operands(24, 260, 32000, 16, seed=21)
+    kc = torch.full((24,), 3200, dtype=torch.int32, device=q.device)
+    ops.select_fused(q, k, kc, 3200, mode="fast")
+    torch.cuda.synchronize()
+    assert ops.select_fast_fallbacks(24, 260, 32000, 3200, 0, q.device) == 0
