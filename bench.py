@@ -10,8 +10,9 @@ backward (dQ, dK, dV). With N > 1 (torchrun) the same layer runs head-parallel
 (HCP): each rank holds L/N tokens, NCCL all-to-alls reshard to the heads that
 the sparsity-aware planner assigned to it and back (strong scaling).
 
-Prints one JSON line (rank 0). `--impl reference` times the reference's CPU
-implementation of the path (the numpy oracle restatement) on the host cores.
+Prints one JSON line (rank 0). `--impl reference` times the reference's own CPU
+implementation of the path (the unmodified `dynsparse` package installed into
+baseline/_ref) on a bounded sample of the same workload, on the host cores.
 """
 
 from __future__ import annotations
@@ -93,17 +94,108 @@ def _cores() -> int:
         return os.cpu_count() or 1
 
 
-# ---------------------------------------------------------------- CPU oracle timing
+# ---------------------------------------------------------------- CPU reference timing
 _SAMPLE = {}
+REF_DIR = ROOT / "baseline" / "_ref"
+
+
+class RefLayerSample:
+    """The UNMODIFIED reference (`dynsparse` installed into baseline/_ref from
+    /root/reference/pkg) on a bounded sample of the c2 layer, in its
+    float32 throughput mode (validate.py:16-19 keeps float32):
+      project   predictor.project(X, W_q), project(X, W_k)          one head per sample
+      select    selection.streaming_topk(Q_lr[proxies], K_lr, k)     the sampled groups
+      fwd       attention.sparse_attention(Q[members], K, V, set)    = grouped_sparse_attention's
+                                                                     per-group expansion
+      bwd       the reference trainer's sparse autograd (trainer.py:110-117: gather, einsum,
+                softmax, einsum) run by torch-CPU on the same group; `_Block.attention` itself
+                is self-attention over all S rows (S x k x d gathers: 52 GB at c2), so the
+                formulation runs on the sampled queries against all keys
+    extrapolated to 24 heads x 260 groups. Without baseline/_ref (not installed) the oracle
+    port (oracle.pipeline) stands in and the record says kind "port"."""
+
+    def __init__(self):
+        import numpy as np
+
+        sys.path.insert(0, str(REF_DIR))
+        from dynsparse import attention, grid, grouping, predictor, selection
+
+        self.mod = {"attention": attention, "predictor": predictor, "selection": selection}
+        plan = grouping.build_groups(grid.TokenGrid(*GRID), VOXEL)
+        self.members, self.proxies = plan.members, plan.proxies
+        self.L = int(np.prod(GRID))
+        self.k = selection.k_from_sparsity(SPARSITY, self.L)
+        rng = np.random.default_rng(0)
+        d_model = HEADS * HEAD_DIM
+        self.x = rng.standard_normal((self.L, d_model), dtype=np.float32)
+        self.wq, self.wk = (rng.standard_normal((d_model, D_LR), dtype=np.float32) / np.float32(np.sqrt(d_model))
+                            for _ in range(2))
+        self.q, self.kk, self.v, self.do = (rng.standard_normal((self.L, HEAD_DIM), dtype=np.float32)
+                                            for _ in range(4))
+        self.kind = "reference"
+
+    @property
+    def n_groups(self) -> int:
+        return len(self.members)
+
+    def run(self, groups) -> dict:
+        import numpy as np
+        import torch
+
+        A, P, Sel = self.mod["attention"], self.mod["predictor"], self.mod["selection"]
+        t0 = time.perf_counter()
+        q_lr = P.project(self.x, self.wq)
+        k_lr = P.project(self.x, self.wk)
+        t1 = time.perf_counter()
+        sets = Sel.streaming_topk(q_lr[self.proxies[groups]], k_lr, self.k).indices
+        t2 = time.perf_counter()
+        for i, g in enumerate(groups):
+            mem = self.members[g]
+            A.sparse_attention(self.q[mem], self.kk, self.v, A.CriticalIndexSet([sets[i]] * mem.size))
+        t3 = time.perf_counter()
+        t_bwd = 0.0
+        kt = torch.from_numpy(self.kk)[None, None].requires_grad_(True)    # [B, H, S, dk]
+        vt = torch.from_numpy(self.v)[None, None].requires_grad_(True)
+        for i, g in enumerate(groups):
+            mem = self.members[g]
+            qt = torch.from_numpy(self.q[mem])[None, None].requires_grad_(True)
+            idx = torch.from_numpy(np.asarray(sets[i], dtype=np.int64)).expand(mem.size, -1)
+            k_sel = torch.stack([kt[0][:, idx]])
+            v_sel = torch.stack([vt[0][:, idx]])
+            logits = torch.einsum("bhqd,bhqkd->bhqk", qt, k_sel) / math.sqrt(HEAD_DIM)
+            out = torch.einsum("bhqk,bhqkd->bhqd", torch.softmax(logits, dim=-1), v_sel)
+            dout = torch.from_numpy(self.do[mem])[None, None]
+            tb = time.perf_counter()
+            out.backward(dout)
+            t_bwd += time.perf_counter() - tb
+        return {"project": t1 - t0, "select": t2 - t1, "fwd": t3 - t2, "bwd": t_bwd,
+                "groups": len(groups)}
+
+    def layer_seconds(self, timing: dict) -> float:
+        per_group = (timing["select"] + timing["fwd"] + timing["bwd"]) / timing["groups"]
+        return HEADS * (timing["project"] + per_group * self.n_groups)
+
+
+def _sample():
+    if "s" not in _SAMPLE:
+        if (REF_DIR / "dynsparse").is_dir():
+            _SAMPLE["s"] = RefLayerSample()
+        else:
+            from oracle.pipeline import LayerSample
+
+            smp = LayerSample(GRID, HEADS, HEAD_DIM, D_LR, VOXEL, SPARSITY)
+            smp.kind = "port"
+            _SAMPLE["s"] = smp
+    return _SAMPLE["s"]
 
 
 def cpu_oracle(budget_s: float, warm: bool = True) -> dict:
-    """Reference CPU path (oracle port) on a bounded sample of the c2 workload."""
-    from oracle.pipeline import LayerSample
+    """The reference CPU path on a bounded sample of the c2 workload (RefLayerSample)."""
+    import numpy as np  # noqa: F401  (RefLayerSample.run)
+    import torch
 
-    if "s" not in _SAMPLE:
-        _SAMPLE["s"] = LayerSample(GRID, HEADS, HEAD_DIM, D_LR, VOXEL, SPARSITY)
-    smp = _SAMPLE["s"]
+    torch.set_num_threads(_cores())
+    smp = _sample()
     if warm:
         smp.run([0])
     tot = {"project": 0.0, "select": 0.0, "fwd": 0.0, "bwd": 0.0, "groups": 0}
@@ -111,21 +203,24 @@ def cpu_oracle(budget_s: float, warm: bool = True) -> dict:
     t_start = time.perf_counter()
     n_proj = 0
     while True:
-        groups = [(g + i) % smp.n_groups for i in range(4)]
+        groups = [(g + i * 67) % smp.n_groups for i in range(4)]
         t = smp.run(groups)
         for key in ("project", "select", "fwd", "bwd"):
             tot[key] += t[key]
         tot["groups"] += t["groups"]
         n_proj += 1
-        g += 4
+        g += 1
         if time.perf_counter() - t_start >= budget_s:
             break
     tot["project"] /= n_proj
     layer_s = smp.layer_seconds(tot)
-    return {"tokens_per_s": smp.L / layer_s, "layer_seconds": layer_s,
-            "sample": (f"{tot['groups']} (head, group) query tiles of 128 + {n_proj} one-head "
-                       f"projections, fp32 numpy/BLAS (reference throughput mode), extrapolated to "
-                       f"24 heads x 260 groups"),
+    what = ("unmodified reference (baseline/_ref dynsparse: project, streaming_topk, "
+            "sparse_attention; trainer autograd formulation for the backward), float32"
+            if smp.kind == "reference" else "oracle port (oracle.pipeline), float32")
+    return {"tokens_per_s": smp.L / layer_s, "layer_seconds": layer_s, "kind": smp.kind,
+            "sample": (f"{tot['groups']} (head, group) query tiles of <= 128 + {n_proj} one-head "
+                       f"projections, {what}; extrapolated to 24 heads x 260 groups"),
+            "stage_s": {k: tot[k] for k in ("select", "fwd", "bwd")},
             "wall_s": time.perf_counter() - t_start}
 
 
@@ -354,7 +449,7 @@ def run_gpu(args) -> None:
         stage_ms = cp.phase_ms()
         cp.marks = None
 
-    # ---- e2e through the public layer API with host-resident inputs
+    # ---- e2e through the public layer API with host-resident inputs and outputs
     e2e = None
     if not args.no_e2e:
         from paper_2502_07590_b200.layer import HostPipeline
@@ -368,18 +463,21 @@ def run_gpu(args) -> None:
                 return layer.step(xb, wt, qb, kb, vb, dob)
             return cp.step(xb, wt, qb, kb, vb, dob)
 
-        for out in pipe.run(dev_step, [host] * 2):
-            float(out[1].float().sum().item())
+        for _ in pipe.run(dev_step, [host] * 2):
+            pass
+        pipe.drain()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         n_e2e = max(3, args.steps // 2)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        # every step: pinned H2D of its own inputs (overlapping the previous step)
-        # and a D2H read of its result; the clock starts before the first copy
+        # every step: pinned H2D of its own inputs (overlapping the previous step) and the D2H
+        # of its results O, dQ, dK, dV into pinned host buffers (overlapping the next step);
+        # the clock starts before the first copy and stops after the last result landed
         a.record()
-        for out in pipe.run(dev_step, [host] * n_e2e):
-            float(out[1].float().sum().item())   # D2H: the step's scalar result
+        for _ in pipe.run(dev_step, [host] * n_e2e):
+            pass
+        pipe.drain()
         b.record()
         torch.cuda.synchronize()
         e_ms = a.elapsed_time(b) / n_e2e
@@ -388,9 +486,10 @@ def run_gpu(args) -> None:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e_ms = float(tt.item())
         e2e = {"value": L / (e_ms / 1e3), "unit": "tokens/s", "ms_per_step": e_ms,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": pipe.d2h_bytes,
                "api": ("DSVAttentionLayer.step" if world == 1 else "HeadParallelDSV.step")
-               + " via HostPipeline (pinned H2D of step i+1 overlaps step i)"}
+               + " via HostPipeline (pinned H2D of step i+1 and D2H of step i-1's O, dQ, dK, dV "
+                 "overlap step i; full-duplex PCIe)"}
 
     if rank != 0:
         if world > 1:
@@ -466,8 +565,9 @@ def run_gpu(args) -> None:
     if world == 1 and args.workload == "c2" and os.environ.get("DSV_CPU_BASELINE", "1") != "0":
         cb = cpu_oracle(args.cpu_budget)
         res["cpu_baseline"] = {"value": cb["tokens_per_s"], "unit": "tokens/s", "cores": _cores(),
-                               "kind": "port", "sample": cb["sample"],
-                               "threads_note": "numpy/OpenBLAS default threads = all cores"}
+                               "kind": cb["kind"], "sample": cb["sample"], "same_config": True,
+                               "threads_note": "numpy/OpenBLAS default threads = all cores; "
+                                               "torch.set_num_threads(cores)"}
     print(json.dumps(res))
     if world > 1:
         dist.barrier()
@@ -488,7 +588,7 @@ def run_reference(args) -> None:
         r = cpu_oracle(budget, warm=False)
         vals.append(r["tokens_per_s"])
         walls.append(r["layer_seconds"])
-        sample = r["sample"]
+        sample, kind = r["sample"], r["kind"]
     value = statistics.median(vals)
     res = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
            "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
@@ -497,8 +597,8 @@ def run_reference(args) -> None:
            "data": "synthetic: N(0,1) X, Q, K, V, dO (float32, reference throughput mode)",
            "config": {"workload": WORKLOAD, "tokens": 32000, "heads": HEADS, "head_dim": HEAD_DIM,
                       "sparsity": SPARSITY, "voxel": list(VOXEL)},
-           "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": _cores(), "kind": "port",
-                            "sample": sample},
+           "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": _cores(), "kind": kind,
+                            "sample": sample, "same_config": True},
            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(res))

@@ -221,21 +221,25 @@ class DSVAttentionLayer:
 
 
 class HostPipeline:
-    """Runs a device step over host-resident batches, H2D of batch i+1 overlapping step i.
+    """Runs a device step over host-resident batches: H2D of batch i+1 and D2H of step i's
+    results overlap step i+1 / step i on two copy streams.
 
-    Two device buffer sets; the copies run on a side stream from pinned host memory
-    (the sequence of `step` calls on the current stream is unchanged). Each yielded
-    result is whatever `step(*device_inputs)` returned, already synchronised by the
-    caller's own D2H read.
+    Two device input buffer sets filled from pinned host memory on the H2D stream; each
+    step's result tensors are copied back into one of two pinned host output sets on the D2H
+    stream (full-duplex PCIe: both directions at once). Yields each step's host output set;
+    its contents are valid once `drain()` (or a later synchronize) returns.
     """
 
     def __init__(self, like, device):
         dev = torch.device(device)
         self.bufs = [[torch.empty(t.shape, dtype=t.dtype, device=dev) for t in like] for _ in range(2)]
         self.copy = torch.cuda.Stream(dev)
+        self.d2h = torch.cuda.Stream(dev)
         self.ready = [torch.cuda.Event(), torch.cuda.Event()]
         self.free = [None, None]
         self.h2d_bytes = sum(t.numel() * t.element_size() for t in like)
+        self.d2h_bytes = 0
+        self.host_out = [None, None]
 
     def _stage(self, slot, host):
         with torch.cuda.stream(self.copy):
@@ -247,7 +251,24 @@ class HostPipeline:
                 dst.copy_(src, non_blocking=True)
             self.ready[slot].record(self.copy)
 
-    def run(self, step, batches):
+    def _fetch(self, slot, res):
+        """D2H of the step's result tensors into pinned host set `slot` on the D2H stream."""
+        res = [t for t in (res if isinstance(res, (tuple, list)) else (res,)) if torch.is_tensor(t)]
+        if self.host_out[slot] is None:
+            self.host_out[slot] = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in res]
+            self.d2h_bytes = sum(t.numel() * t.element_size() for t in res)
+        self.d2h.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.d2h):
+            for t, h in zip(res, self.host_out[slot]):
+                h.copy_(t, non_blocking=True)
+                t.record_stream(self.d2h)
+        return self.host_out[slot]
+
+    def drain(self):
+        """Make the current stream wait for every issued D2H copy."""
+        torch.cuda.current_stream().wait_stream(self.d2h)
+
+    def run(self, step, batches, fetch: bool = True):
         it = iter(batches)
         nxt = next(it, None)
         slot = 0
@@ -263,5 +284,5 @@ class HostPipeline:
             ev = torch.cuda.Event()
             ev.record(cur)
             self.free[slot] = ev
-            yield res
+            yield self._fetch(slot, res) if fetch else res
             slot ^= 1
