@@ -81,6 +81,9 @@ def _args():
     ap.add_argument("--eager", dest="graph", action="store_false")
     ap.add_argument("--scp", type=int, default=1,
                     help="g_s > 1: hybrid CP, N/g_s head groups x g_s selective-sequence groups")
+    ap.add_argument("--voxel", default=None,
+                    help="voxel group shape t,h,w (default 8,4,4); the ladder's 8,8,4 / 8,8,8 groups "
+                         "span several 128-query tiles")
     ap.add_argument("--dense-heads", type=int, default=0,
                     help="the first M heads are dense residual heads (sparsity 0); under --scp "
                          "they run the ring KV pass (ring.py)")
@@ -283,6 +286,7 @@ def _traffic() -> dict:
 
 
 def run_gpu(args) -> None:
+    global VOXEL
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -295,6 +299,8 @@ def run_gpu(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.voxel:
+        VOXEL = tuple(int(x) for x in args.voxel.split(","))
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
@@ -518,6 +524,8 @@ def run_gpu(args) -> None:
                    "k_per_group": all_ks[0] if args.workload == "c2" else all_ks,
                    "voxel": list(VOXEL),
                    "groups": layer.G if world == 1 else len(build_groups(grid, VOXEL).members),
+                   **({"voxel_override": True, "tiles_per_head": int(layer.grp_rows.shape[0])}
+                      if args.voxel else {}),
                    "parallelism": ("single" if world == 1 else f"hcp{world}" if args.scp == 1
                                    else f"hcp{world // args.scp}xscp{args.scp}"),
                    "head_plan": "balance_heads" if not args.unbalanced else "contiguous",

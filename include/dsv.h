@@ -129,12 +129,15 @@ int dsv_topk(const float* scores, long long ld, int rows, int L, const int* k_pe
  * work: device workspace of >= H*G + 2 words (the persistent kernel's list of tiles that
  * need the exact-max pass and its tile counter; contents need no initialisation).
  * zero_buf (optional): zero_floats fp32 set to 0 while the kernel runs (the backward's dK/dV
- * accumulators; the writes hide under the gather-bound forward). */
+ * accumulators; the writes hide under the gather-bound forward).
+ * tile_grp (optional, int32 [G]): the G tiles are 128-query pieces of n_groups voxel groups
+ * (grouping.py:22-32 ladder shapes up to 8x8x8 = 512 queries); tile g reads index row
+ * tile_grp[g] of idx [H][n_groups][ldk] (and kcount_hg [H][n_groups]). NULL: tile = group. */
 int dsv_sparse_fwd(const void* q, const void* k, const void* v, const int* grp_rows,
                    const int* grp_size, const int* idx, long long ldk, const int* kcount,
                    const int* kcount_hg, int H, int G, int Lq, int Lk, int D, float scale,
                    void* out, float* lse, unsigned* work, long long work_words, float* zero_buf,
-                   long long zero_floats, void* stream);
+                   long long zero_floats, const int* tile_grp, int n_groups, void* stream);
 
 /* Backward (K3b). dout: [H][Lq][D] bf16, out/lse from dsv_sparse_fwd. dq: [H][Lq][D] bf16
  * (every query of a group is written); dk_acc, dv_acc: [H][Lk][D] fp32 accumulators that the
@@ -144,7 +147,7 @@ int dsv_sparse_bwd(const void* q, const void* k, const void* v, const void* out,
                    const void* dout, const float* lse, const int* grp_rows, const int* grp_size,
                    const int* idx, long long ldk, const int* kcount, const int* kcount_hg, int H,
                    int G, int Lq, int Lk, int D, float scale, void* dq, float* dk_acc,
-                   float* dv_acc, unsigned* work, void* stream);
+                   float* dv_acc, unsigned* work, const int* tile_grp, int n_groups, void* stream);
 
 /* Ragged per-(head, query) CSR sparse attention on CUDA cores (fp32 math), any D <= 256.
  * ptr: [H*Lq + 1] int64 offsets into cols (int32 key ids); cols == NULL selects every key

@@ -1080,7 +1080,7 @@ class HybridDSV(_PhaseMarks):
         dv32 = torch.zeros_like(dk32)
         dq, dk32, dv32 = ops.sparse_bwd(Qf, Kf, Vf, out, dOf, lse, self.local.grp_rows,
                                         self.local.grp_size, sel.idx, sel.kcount,
-                                        self.local.scale, dk32, dv32)
+                                        self.local.scale, dk32, dv32, tile_grp=self.local.tile_grp)
         self._mark("bwd")
         dk_span, dv_span = dk32[:, sl], dv32[:, sl]
         if ex.g_s > 1:

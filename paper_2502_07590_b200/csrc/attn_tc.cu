@@ -247,6 +247,14 @@ DSV_DEV float softmax_p_pass(uint32_t tS, float scale_log2, float m, int kv) {
 // has read O out of TMEM). Lazy max (below) flags a tile whose scores exceed its
 // reference max by > 2^64 into ovf_list; the launcher re-runs those tiles with the exact
 // per-block max in list mode (list = ovf_list, read after the first launch).
+// Index-list row of a (head, tile): tiles are the 128-query pieces of the voxel groups; a group
+// larger than 128 queries spans several tiles that share its row (tile_grp: tile -> group,
+// nullptr = one tile per group), so idx / kcount_hg are [H, Gs, ...] over the Gs groups.
+DSV_DEV long long sel_row(int tile, int G, const int* tile_grp, int Gs) {
+  const int h = tile / G, g = tile - h * G;
+  return (long long)h * Gs + (tile_grp ? __ldg(tile_grp + g) : g);
+}
+
 template <int D>
 __global__ void __launch_bounds__(kFwdThreads, 1)
 sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __restrict__ Kg,
@@ -256,7 +264,8 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
                   int Lq, int Lk, float scale_log2, __nv_bfloat16* __restrict__ O,
                   float* __restrict__ lse, int n_tiles, const unsigned* __restrict__ list,
                   unsigned* __restrict__ ovf_list, unsigned* __restrict__ sched,
-                  float4* __restrict__ zero_buf, long long zero_n4) {
+                  float4* __restrict__ zero_buf, long long zero_n4,
+                  const int* __restrict__ tile_grp, int Gs) {
   using SL = FwdSmem<D>;
   using GT = Gather<D>;
   constexpr int ST = kFwdStages, KST = kFwdKStages, NS = kFwdSBufs;
@@ -359,9 +368,9 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
       const int tile = tile_of(it);
       if (tile < 0) break;
       const int h = tile / G, g = tile - h * G;
-      const int kh = kcount_hg ? kcount_hg[tile] : kcount[h];
+      const int kh = kcount_hg ? kcount_hg[sel_row(tile, G, tile_grp, Gs)] : kcount[h];
       const int nblk = (kh + BKV - 1) / BKV;
-      const int* irow = idx + ((long long)h * G + g) * ldk;
+      const int* irow = idx + sel_row(tile, G, tile_grp, Gs) * ldk;
       const int* mrow = grp_rows + (long long)g * BQ;
       {   // Q of this tile, once every S of the previous tile has read the last one
         const int qr0 = ptid / GT::kCPR;
@@ -404,7 +413,7 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
     const int tile = tile_of(it);
     if (tile < 0) break;
     const int h = tile / G;
-    const int kh = kcount_hg ? kcount_hg[tile] : kcount[h];
+    const int kh = kcount_hg ? kcount_hg[sel_row(tile, G, tile_grp, Gs)] : kcount[h];
     const int nblk = (kh + BKV - 1) / BKV;
     auto issue_s = [&](int s) {
       const int gs = gb + s, st = gs % KST;
@@ -462,7 +471,7 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
     const int tile = tile_of(it);
     if (tile < 0) break;
     const int h = tile / G, g = tile - h * G;
-    const int kh = kcount_hg ? kcount_hg[tile] : kcount[h];
+    const int kh = kcount_hg ? kcount_hg[sel_row(tile, G, tile_grp, Gs)] : kcount[h];
     const int nblk = (kh + BKV - 1) / BKV;
     const int* mrow = grp_rows + (long long)g * BQ;
     float m_run = -INFINITY, l_run = 0.f;
@@ -672,7 +681,8 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
                   const int* __restrict__ kcount_hg, int G, int Lq, int Lk, float scale,
                   float scale_log2,
                   __nv_bfloat16* __restrict__ dQ, float* __restrict__ dK, float* __restrict__ dV,
-                  int n_tiles, unsigned* __restrict__ sched) {
+                  int n_tiles, unsigned* __restrict__ sched, const int* __restrict__ tile_grp,
+                  int Gs) {
   using SL = BwdSmem<D>;
   using GT = Gather<D, kBwdLoadThreads>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -714,9 +724,9 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
     const int tile = tile_of(it);                                           \
     if (tile < 0) break;                                                    \
     const int h = tile / G, g = tile - h * G;                               \
-    const int kh = kcount_hg ? kcount_hg[tile] : kcount[h];                 \
+    const int kh = kcount_hg ? kcount_hg[sel_row(tile, G, tile_grp, Gs)] : kcount[h];                 \
     const int nblk = (kh + BKV - 1) / BKV;                                  \
-    const int* irow = idx + ((long long)h * G + g) * ldk;                   \
+    const int* irow = idx + sel_row(tile, G, tile_grp, Gs) * ldk;                   \
     const int* mrow = grp_rows + (long long)g * BQ;                         \
     (void)irow; (void)mrow; (void)nblk
 
@@ -1059,7 +1069,7 @@ static int fwd_launch(const void* q, const void* k, const void* v, const int* gr
                       const int* grp_size, const int* idx, long long ldk, const int* kcount,
                       const int* kcount_hg, int H, int G, int Lq, int Lk, float scale_log2, void* O,
                       float* lse, unsigned* work, float* zero_buf, long long zero_floats,
-                      cudaStream_t st) {
+                      const int* tile_grp, int Gs, cudaStream_t st) {
   auto kern = sparse_fwd_kernel<D>;
   const int smem = FwdSmem<D>::kBytes;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1083,14 +1093,15 @@ static int fwd_launch(const void* q, const void* k, const void* v, const int* gr
                                      (const __nv_bfloat16*)v, grp_rows, grp_size, idx, ldk,
                                      kcount, kcount_hg, G, Lq, Lk, scale_log2,
                                      (__nv_bfloat16*)O, lse, n_tiles, nullptr, work, sched,
-                                     reinterpret_cast<float4*>(zero_buf), zero_floats / 4);
+                                     reinterpret_cast<float4*>(zero_buf), zero_floats / 4,
+                                     tile_grp, Gs);
   // tiles flagged by the lazy max: exact per-block max (CTAs exit at once when none)
   const int g2 = n_tiles < sms ? n_tiles : sms;
   kern<<<g2, kFwdThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
                                    (const __nv_bfloat16*)v, grp_rows, grp_size, idx, ldk,
                                    kcount, kcount_hg, G, Lq, Lk, scale_log2,
                                    (__nv_bfloat16*)O, lse, n_tiles, work, nullptr, nullptr,
-                                   nullptr, 0);
+                                   nullptr, 0, tile_grp, Gs);
   return (int)cudaGetLastError();
 }
 
@@ -1098,13 +1109,14 @@ int dsv_attn_fwd_tc_launch(const void* q, const void* k, const void* v, const in
                            const int* grp_size, const int* idx, long long ldk, const int* kcount,
                            const int* kcount_hg, int H, int G, int Lq, int Lk, int D,
                            float scale_log2, void* O, float* lse, unsigned* work,
-                           float* zero_buf, long long zero_floats, cudaStream_t st) {
+                           float* zero_buf, long long zero_floats, const int* tile_grp, int Gs,
+                           cudaStream_t st) {
   if (D == 128)
     return fwd_launch<128>(q, k, v, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H, G, Lq, Lk,
-                           scale_log2, O, lse, work, zero_buf, zero_floats, st);
+                           scale_log2, O, lse, work, zero_buf, zero_floats, tile_grp, Gs, st);
   if (D == 64)
     return fwd_launch<64>(q, k, v, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H, G, Lq, Lk,
-                          scale_log2, O, lse, work, zero_buf, zero_floats, st);
+                          scale_log2, O, lse, work, zero_buf, zero_floats, tile_grp, Gs, st);
   return 1;
 }
 
@@ -1114,7 +1126,7 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* O
                       long long ldk, const int* kcount, const int* kcount_hg, int H, int G, int Lq,
                       int Lk, float scale,
                       float scale_log2, void* dQ, float* dK, float* dV, unsigned* sched,
-                      cudaStream_t st) {
+                      const int* tile_grp, int Gs, cudaStream_t st) {
   auto kern = sparse_bwd_kernel<D>;
   const int smem = BwdSmem<D>::kBytes;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1135,7 +1147,7 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* O
                                       (const __nv_bfloat16*)k, (const __nv_bfloat16*)v,
                                       (const __nv_bfloat16*)O, lse, grp_rows, grp_size, idx, ldk,
                                       kcount, kcount_hg, G, Lq, Lk, scale, scale_log2,
-                                      (__nv_bfloat16*)dQ, dK, dV, n_tiles, sched);
+                                      (__nv_bfloat16*)dQ, dK, dV, n_tiles, sched, tile_grp, Gs);
   return (int)cudaGetLastError();
 }
 
@@ -1144,13 +1156,13 @@ int dsv_attn_bwd_tc_launch(const void* q, const void* k, const void* v, const vo
                            const int* grp_size, const int* idx, long long ldk, const int* kcount,
                            const int* kcount_hg, int H, int G, int Lq, int Lk, int D, float scale,
                            float scale_log2, void* dQ, float* dK, float* dV, unsigned* sched,
-                           cudaStream_t st) {
+                           const int* tile_grp, int Gs, cudaStream_t st) {
   if (D == 128)
     return bwd_launch<128>(q, k, v, O, dO, lse, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H,
-                           G, Lq, Lk, scale, scale_log2, dQ, dK, dV, sched, st);
+                           G, Lq, Lk, scale, scale_log2, dQ, dK, dV, sched, tile_grp, Gs, st);
   if (D == 64)
     return bwd_launch<64>(q, k, v, O, dO, lse, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H,
-                          G, Lq, Lk, scale, scale_log2, dQ, dK, dV, sched, st);
+                          G, Lq, Lk, scale, scale_log2, dQ, dK, dV, sched, tile_grp, Gs, st);
   return 1;
 }
 

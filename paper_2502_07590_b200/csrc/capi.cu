@@ -32,11 +32,12 @@ int dsv_gemm_launch(const CUtensorMap*, const CUtensorMap*, const CUtensorMap*, 
                     long long, int, int, int, cudaStream_t);
 int dsv_attn_fwd_tc_launch(const void*, const void*, const void*, const int*, const int*,
                            const int*, long long, const int*, const int*, int, int, int, int, int,
-                           float, void*, float*, unsigned*, float*, long long, cudaStream_t);
+                           float, void*, float*, unsigned*, float*, long long, const int*, int,
+                           cudaStream_t);
 int dsv_attn_bwd_tc_launch(const void*, const void*, const void*, const void*, const void*,
                            const float*, const int*, const int*, const int*, long long,
                            const int*, const int*, int, int, int, int, int, float, float, void*,
-                           float*, float*, unsigned*, cudaStream_t);
+                           float*, float*, unsigned*, const int*, int, cudaStream_t);
 int dsv_f32_to_bf16_launch(const float*, void*, long long, cudaStream_t);
 int dsv_select_fused_launch(const CUtensorMap*, const CUtensorMap*, int, int, int, const int*, int*,
                             long long, float*, int, void*, long long, cudaStream_t);
@@ -294,8 +295,9 @@ int dsv_sparse_fwd(const void* q, const void* k, const void* v, const int* grp_r
                    const int* grp_size, const int* idx, long long ldk, const int* kcount,
                    const int* kcount_hg, int H, int G, int Lq, int Lk, int D, float scale,
                    void* out, float* lse, unsigned* work, long long work_words, float* zero_buf,
-                   long long zero_floats, void* stream) {
+                   long long zero_floats, const int* tile_grp, int n_groups, void* stream) {
   if (D != 64 && D != 128) return fail(DSV_EUNSUPPORTED, "sparse_fwd: head dim %d not 64/128", D);
+  if (tile_grp && n_groups <= 0) return fail(DSV_EINVAL, "sparse_fwd: tile_grp needs n_groups > 0");
   if (H <= 0 || G <= 0 || Lq <= 0 || Lk <= 0 || ldk < 0)
     return fail(DSV_EINVAL, "sparse_fwd: empty shape");
   if (!al16(q) || !al16(k) || !al16(v) || !al16(out) || !al16(grp_rows))
@@ -307,7 +309,8 @@ int dsv_sparse_fwd(const void* q, const void* k, const void* v, const int* grp_r
   const float scale_log2 = scale * 1.4426950408889634f;
   return cuda_status(dsv_attn_fwd_tc_launch(q, k, v, grp_rows, grp_size, idx, ldk, kcount,
                                             kcount_hg, H, G, Lq, Lk, D, scale_log2, out, lse,
-                                            work, zero_buf, zero_buf ? zero_floats : 0, S(stream)),
+                                            work, zero_buf, zero_buf ? zero_floats : 0, tile_grp,
+                                            tile_grp ? n_groups : G, S(stream)),
                      "sparse_fwd launch");
 }
 
@@ -315,8 +318,9 @@ int dsv_sparse_bwd(const void* q, const void* k, const void* v, const void* out,
                    const void* dout, const float* lse, const int* grp_rows, const int* grp_size,
                    const int* idx, long long ldk, const int* kcount, const int* kcount_hg, int H,
                    int G, int Lq, int Lk, int D, float scale, void* dq, float* dk_acc,
-                   float* dv_acc, unsigned* work, void* stream) {
+                   float* dv_acc, unsigned* work, const int* tile_grp, int n_groups, void* stream) {
   if (D != 64 && D != 128) return fail(DSV_EUNSUPPORTED, "sparse_bwd: head dim %d not 64/128", D);
+  if (tile_grp && n_groups <= 0) return fail(DSV_EINVAL, "sparse_bwd: tile_grp needs n_groups > 0");
   if (H <= 0 || G <= 0 || Lq <= 0 || Lk <= 0 || ldk < 0)
     return fail(DSV_EINVAL, "sparse_bwd: empty shape");
   if (!al16(q) || !al16(k) || !al16(v) || !al16(out) || !al16(dout) || !al16(dq) ||
@@ -326,7 +330,8 @@ int dsv_sparse_bwd(const void* q, const void* k, const void* v, const void* out,
   const float scale_log2 = scale * 1.4426950408889634f;
   return cuda_status(dsv_attn_bwd_tc_launch(q, k, v, out, dout, lse, grp_rows, grp_size, idx, ldk,
                                             kcount, kcount_hg, H, G, Lq, Lk, D, scale, scale_log2,
-                                            dq, dk_acc, dv_acc, work, S(stream)),
+                                            dq, dk_acc, dv_acc, work, tile_grp,
+                                            tile_grp ? n_groups : G, S(stream)),
                      "sparse_bwd launch");
 }
 

@@ -20,10 +20,12 @@ from . import ops
 
 class _GroupSparseAttention(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, q, k, v, grp_rows, grp_size, idx, kcount, kcount_hg, scale):
-        out, lse = ops.sparse_fwd(q, k, v, grp_rows, grp_size, idx, kcount, scale, kcount_hg)
+    def forward(ctx, q, k, v, grp_rows, grp_size, idx, kcount, kcount_hg, scale, tile_grp):
+        out, lse = ops.sparse_fwd(q, k, v, grp_rows, grp_size, idx, kcount, scale, kcount_hg,
+                                  tile_grp=tile_grp)
         ctx.save_for_backward(q, k, v, out, lse, grp_rows, grp_size, idx, kcount)
         ctx.kcount_hg = kcount_hg
+        ctx.tile_grp = tile_grp
         ctx.scale = scale
         return out
 
@@ -31,18 +33,19 @@ class _GroupSparseAttention(torch.autograd.Function):
     def backward(ctx, dout):
         q, k, v, out, lse, grp_rows, grp_size, idx, kcount = ctx.saved_tensors
         dq, dk32, dv32 = ops.sparse_bwd(q, k, v, out, dout.contiguous(), lse, grp_rows, grp_size,
-                                        idx, kcount, ctx.scale, kcount_hg=ctx.kcount_hg)
+                                        idx, kcount, ctx.scale, kcount_hg=ctx.kcount_hg,
+                                        tile_grp=ctx.tile_grp)
         return (dq, ops.f32_to_bf16(dk32), ops.f32_to_bf16(dv32),
-                None, None, None, None, None, None)
+                None, None, None, None, None, None, None)
 
 
 def group_sparse_attention(q, k, v, plan, idx, kcount, kcount_hg=None, scale=None):
     """Differentiable group-tiled sparse attention. q, k, v: [H, L, D] bf16 CUDA."""
     if scale is None:
         scale = 1.0 / math.sqrt(q.shape[-1])
-    rows, size = plan.tables(q.device)
+    rows, size, tg = plan.tile_tables(q.device)
     return _GroupSparseAttention.apply(q.contiguous(), k.contiguous(), v.contiguous(), rows, size,
-                                       idx, kcount, kcount_hg, float(scale))
+                                       idx, kcount, kcount_hg, float(scale), tg)
 
 
 class _RowsSparseAttention(torch.autograd.Function):

@@ -1,12 +1,14 @@
 """Voxel query grouping (reference pkg/src/dynsparse/grouping.py).
 
-A voxel group is the tensor-core query tile: its members (<= 128 queries) share
-one critical-KV index list, selected by the group's proxy query. The plan is
-built on the host (cheap integer work) and uploaded once as two small device
-tables consumed by the K3 kernels:
+A voxel group's members share one critical-KV index list, selected by the group's
+proxy query; the tensor-core query tile is 128 queries, so a group of the larger
+ladder shapes ((8,8,4) = 256, (8,8,8) = 512 members) spans several tiles that read
+the same index row. The plan is built on the host (cheap integer work) and uploaded
+once as small device tables consumed by the K3 kernels:
 
-    grp_rows int32 [G, 128]  member token ids, padded by repeating the last member
-    grp_size int32 [G]       live members per group
+    grp_rows int32 [T, 128]  member token ids per tile, padded by repeating the last member
+    grp_size int32 [T]       live members per tile
+    tile_grp int32 [T]       the group (index row) of each tile (None when T == G)
 """
 
 from __future__ import annotations
@@ -57,12 +59,23 @@ class VoxelGroupPlan:
         return plan
 
     def tables(self, device) -> tuple[torch.Tensor, torch.Tensor]:
-        """(grp_rows [G, 128], grp_size [G]) int32 on `device` (cached)."""
-        key = str(device)
+        """(grp_rows [G, 128], grp_size [G]) int32 on `device` (cached) — one tile per group;
+        plans with groups of more than 128 members use tile_tables."""
+        rows, size, tg = self.tile_tables(device)
+        if tg is not None:
+            raise ValueError(f"groups of up to {self.max_group} members span several 128-query "
+                             f"tiles: use tile_tables")
+        return rows, size
+
+    def tile_tables(self, device, groups=None):
+        """(grp_rows [T, 128], grp_size [T], tile_grp [T] | None) int32 on `device` (cached) for
+        all groups or the listed subset (tile_grp then indexes the subset)."""
+        key = (str(device), None if groups is None else tuple(int(g) for g in groups))
         if key not in self._device:
-            rows, size = group_tables(self.members)
-            self._device[key] = (torch.from_numpy(rows).to(device),
-                                 torch.from_numpy(size).to(device))
+            mem = self.members if groups is None else [self.members[int(g)] for g in groups]
+            rows, size, tg = group_tables(mem, split=True)
+            self._device[key] = (torch.from_numpy(rows).to(device), torch.from_numpy(size).to(device),
+                                 None if tg is None else torch.from_numpy(tg).to(device))
         return self._device[key]
 
     def proxies_tensor(self, device) -> torch.Tensor:
@@ -98,19 +111,29 @@ def build_groups(grid: TokenGrid, dims) -> VoxelGroupPlan:
                           proxies=np.asarray(proxies, dtype=np.int64))
 
 
-def group_tables(members) -> tuple[np.ndarray, np.ndarray]:
-    """Pad member lists to the 128-query tile (host-side)."""
-    G = len(members)
-    rows = np.empty((G, TILE), dtype=np.int32)
-    size = np.empty(G, dtype=np.int32)
+def group_tables(members, split: bool = False):
+    """Pad member lists to the 128-query tile (host-side). split: a group of more than 128
+    members becomes consecutive 128-member tiles of its sorted member list, and the result
+    gains the tile -> group map (None when every group is one tile)."""
+    tiles, parent = [], []
     for g, m in enumerate(members):
         m = np.asarray(m, dtype=np.int64)
-        if m.size == 0 or m.size > TILE:
+        if m.size == 0 or (m.size > TILE and not split):
             raise ValueError(f"group {g} has {m.size} members; tiles hold 1..{TILE}")
-        rows[g, : m.size] = m
-        rows[g, m.size:] = m[-1]
-        size[g] = m.size
-    return rows, size
+        for t0 in range(0, m.size, TILE):
+            tiles.append(m[t0:t0 + TILE])
+            parent.append(g)
+    T = len(tiles)
+    rows = np.empty((T, TILE), dtype=np.int32)
+    size = np.empty(T, dtype=np.int32)
+    for t, m in enumerate(tiles):
+        rows[t, : m.size] = m
+        rows[t, m.size:] = m[-1]
+        size[t] = m.size
+    if not split:
+        return rows, size
+    tg = None if T == len(members) else np.asarray(parent, dtype=np.int32)
+    return rows, size, tg
 
 
 def overlap_ratio(member_sets: list, proxy_pos: int) -> float:
@@ -135,7 +158,8 @@ def grouped_sparse_attention(q, k, v, plan: VoxelGroupPlan, group_sets: list, *,
     """Sparse attention where each group's members share one index set (grouping.py:196-216).
 
     bf16 CUDA tensors with head dim 64/128 run the group-tiled tcgen05 kernel
-    directly (one 128-query tile per group, ragged per-group set sizes); other
+    directly (128-query tiles; a group of the larger ladder shapes spans several tiles that
+    share its index row; ragged per-group set sizes); other
     inputs (numpy / fp32) run the fp32 CUDA-core kernel on the expanded per-query
     lists, matching the reference's expansion (grouping.py:209-216).
     """
@@ -154,7 +178,7 @@ def grouped_sparse_attention(q, k, v, plan: VoxelGroupPlan, group_sets: list, *,
     tc_ok = (cv.is_torch(q) and cv.is_torch(k) and cv.is_torch(v)
              and all(t.dtype == torch.bfloat16 and t.is_cuda and t.dim() == 2 for t in (q, k, v))
              and q.shape[1] in (64, 128) and k.shape[1] == q.shape[1] and v.shape == k.shape
-             and q.shape[0] == plan.grid.size and plan.max_group <= TILE)
+             and q.shape[0] == plan.grid.size)
     if not tc_ok:
         per_query = [None] * plan.grid.size
         for g, members in enumerate(plan.members):
@@ -171,11 +195,11 @@ def grouped_sparse_attention(q, k, v, plan: VoxelGroupPlan, group_sets: list, *,
             raise ValueError(f"group {g}: indices must be sorted, unique and inside K")
         idx[0, g, : s.size] = s
         counts[0, g] = s.size
-    rows, size = plan.tables(dev)
+    rows, size, tg = plan.tile_tables(dev)
     out, _ = ops.sparse_fwd(q.unsqueeze(0).contiguous(), k.unsqueeze(0).contiguous(),
                             v.unsqueeze(0).contiguous(), rows, size, torch.from_numpy(idx).to(dev),
                             torch.tensor([k_max], dtype=torch.int32, device=dev),
-                            kcount_hg=torch.from_numpy(counts).to(dev))
+                            kcount_hg=torch.from_numpy(counts).to(dev), tile_grp=tg)
     if flops is not None:
         flops.add_pairs(int(sum(s.size * m.size for s, m in zip(sets, plan.members))), q.shape[1])
         flops.add_per_query(q.shape[0])

@@ -58,13 +58,13 @@ class DSVAttentionLayer:
         self.ks = [k_from_sparsity(float(s), self.L) for s in sp]
         self.kcount = torch.tensor(self.ks, dtype=torch.int32, device=self.device)
         self.k_max = max(self.ks)
-        self.grp_rows, self.grp_size = self.plan.tables(self.device)
+        # query tiles of 128 (groups of the (8,8,4) / (8,8,8) ladder shapes span several tiles
+        # sharing their index row, tile_grp: tile -> group); a `groups` subset keeps its tiles
+        self.grp_rows, self.grp_size, self.tile_grp = self.plan.tile_tables(self.device, groups)
         self.proxies = self.plan.proxies_tensor(self.device)
         self._G = self.plan.n_groups
         if groups is not None:
             sel = torch.as_tensor(np.asarray(groups, dtype=np.int64), device=self.device)
-            self.grp_rows = self.grp_rows[sel].contiguous()
-            self.grp_size = self.grp_size[sel].contiguous()
             self.proxies = self.proxies[sel].contiguous()
             self._G = int(sel.numel())
         self.scale = 1.0 / math.sqrt(self.D)
@@ -163,7 +163,7 @@ class DSVAttentionLayer:
             zero = self._accumulators(k.shape[1], k.device)
             self._acc_zeroed = True
         return ops.sparse_fwd(q, k, v, self.grp_rows, self.grp_size, sel.idx, sel.kcount,
-                              self.scale, zero=zero)
+                              self.scale, zero=zero, tile_grp=self.tile_grp)
 
     def backward(self, q, k, v, out, lse, dout, sel: SelectedKV, dk_acc=None, dv_acc=None,
                  kernel_done=None):
@@ -179,7 +179,8 @@ class DSVAttentionLayer:
             dk_acc.zero_()
             dv_acc.zero_()
         dq, dk32, dv32 = ops.sparse_bwd(q, k, v, out, dout, lse, self.grp_rows, self.grp_size,
-                                        sel.idx, sel.kcount, self.scale, dk_acc, dv_acc)
+                                        sel.idx, sel.kcount, self.scale, dk_acc, dv_acc,
+                                        tile_grp=self.tile_grp)
         if kernel_done is not None:          # optional CUDA event after the kernel (timing)
             kernel_done.record()
         return dq, ops.f32_to_bf16(dk32), ops.f32_to_bf16(dv32)
@@ -240,6 +241,8 @@ class HostPipeline:
         self.h2d_bytes = sum(t.numel() * t.element_size() for t in like)
         self.d2h_bytes = 0
         self.host_out = [None, None]
+        self.held = [None, None]            # device results still being copied out
+        self.fetched = [None, None]         # D2H completion of each slot
 
     def _stage(self, slot, host):
         with torch.cuda.stream(self.copy):
@@ -252,7 +255,9 @@ class HostPipeline:
             self.ready[slot].record(self.copy)
 
     def _fetch(self, slot, res):
-        """D2H of the step's result tensors into pinned host set `slot` on the D2H stream."""
+        """D2H of the step's result tensors into pinned host set `slot` on the D2H stream. The
+        device tensors stay referenced until the compute stream has waited for the copy (the
+        slot's next step), so the allocator never hands their memory out while it is read."""
         res = [t for t in (res if isinstance(res, (tuple, list)) else (res,)) if torch.is_tensor(t)]
         if self.host_out[slot] is None:
             self.host_out[slot] = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in res]
@@ -261,7 +266,10 @@ class HostPipeline:
         with torch.cuda.stream(self.d2h):
             for t, h in zip(res, self.host_out[slot]):
                 h.copy_(t, non_blocking=True)
-                t.record_stream(self.d2h)
+            ev = torch.cuda.Event()
+            ev.record(self.d2h)
+        self.held[slot] = res
+        self.fetched[slot] = ev
         return self.host_out[slot]
 
     def drain(self):
@@ -280,6 +288,9 @@ class HostPipeline:
                 self._stage(slot ^ 1, nxt)
             cur = torch.cuda.current_stream()
             cur.wait_event(self.ready[slot])
+            if self.fetched[slot] is not None:      # the slot's previous results are copied out
+                cur.wait_event(self.fetched[slot])
+                self.held[slot] = None
             res = step(*self.bufs[slot])
             ev = torch.cuda.Event()
             ev.record(cur)

@@ -209,13 +209,16 @@ def select_fused(q_prox: torch.Tensor, k_lr: torch.Tensor, k_per_head: torch.Ten
 
 
 # ------------------------------------------------------------------- K3 attention
-def sparse_fwd(q, k, v, grp_rows, grp_size, idx, kcount, scale=None, kcount_hg=None, zero=None):
+def sparse_fwd(q, k, v, grp_rows, grp_size, idx, kcount, scale=None, kcount_hg=None, zero=None,
+               tile_grp=None):
     """Group-tiled sparse attention forward. q: [H, Lq, D], k/v: [H, Lk, D] bf16.
 
     grp_rows int32 [G, 128], grp_size int32 [G], idx int32 [H, G, ldk], kcount int32 [H]
     (or per-row counts kcount_hg int32 [H, G]). Returns (out bf16 [H, Lq, D], lse2 fp32 [H, Lq]).
     zero: optional contiguous fp32 tensor the kernel sets to 0 while it runs (the backward's
     dK/dV accumulators).
+    tile_grp: optional int32 [G] tile -> voxel group map (groups of more than 128 queries span
+    several tiles that share the group's idx row; idx / kcount_hg are then per group).
     """
     _require_cuda(q, k, v, grp_rows, grp_size, idx, kcount)
     if zero is not None and (zero.dtype != torch.float32 or not zero.is_contiguous()):
@@ -231,12 +234,13 @@ def sparse_fwd(q, k, v, grp_rows, grp_size, idx, kcount, scale=None, kcount_hg=N
     _lib.call("dsv_sparse_fwd", _ptr(q), _ptr(k), _ptr(v), _ptr(grp_rows), _ptr(grp_size),
               _ptr(idx), idx.stride(1), _ptr(kcount), _ptr(kcount_hg), H, G, Lq, Lk, D,
               float(scale), _ptr(out), _ptr(lse), _ptr(work), work.numel(), _ptr(zero),
-              0 if zero is None else zero.numel(), _stream())
+              0 if zero is None else zero.numel(), _ptr(tile_grp),
+              0 if tile_grp is None else idx.shape[1], _stream())
     return out, lse
 
 
 def sparse_bwd(q, k, v, out, dout, lse, grp_rows, grp_size, idx, kcount, scale=None,
-               dk_acc=None, dv_acc=None, kcount_hg=None):
+               dk_acc=None, dv_acc=None, kcount_hg=None, tile_grp=None):
     """Backward of sparse_fwd. Returns (dq bf16, dk_acc fp32, dv_acc fp32)."""
     _require_cuda(q, k, v, out, dout, lse)
     H, Lq, D = q.shape
@@ -253,7 +257,7 @@ def sparse_bwd(q, k, v, out, dout, lse, grp_rows, grp_size, idx, kcount, scale=N
     _lib.call("dsv_sparse_bwd", _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(dout), _ptr(lse),
               _ptr(grp_rows), _ptr(grp_size), _ptr(idx), idx.stride(1), _ptr(kcount),
               _ptr(kcount_hg), H, G, Lq, Lk, D, float(scale), _ptr(dq), _ptr(dk_acc), _ptr(dv_acc),
-              _ptr(work), _stream())
+              _ptr(work), _ptr(tile_grp), 0 if tile_grp is None else idx.shape[1], _stream())
     return dq, dk_acc, dv_acc
 
 

@@ -250,3 +250,49 @@ def test_mixed_k_ragged_counts_multi_tile(cuda, D):
     parity_report(f"mixed_k_ragged_D{D}", {"tiles": H * G, "tol": TOL, **errs})
     for name, e in errs.items():
         _assert_tol(e, name)
+
+
+@pytest.mark.parametrize("grid_dims,voxel", [((16, 16, 16), (8, 8, 4)), ((16, 16, 16), (8, 8, 8)),
+                                              ((12, 12, 10), (8, 8, 4))])
+def test_ladder_voxels_over_128_members(cuda, grid_dims, voxel):
+    # reference SIZE_LADDER shapes above 128 queries (grouping.py:22-32): each group spans
+    # several 128-query tiles that share the group's index row (tile_grp), on tcgen05
+    grid = TokenGrid(*grid_dims)
+    H, D = 2, 128
+    layer = DSVAttentionLayer(grid, H, D, 16, voxel, [0.9, 0.75], cuda)
+    assert layer.tile_grp is not None and layer.plan.max_group > 128
+    L, G = grid.size, layer.G
+    g = torch.Generator(device=cuda).manual_seed(5)
+
+    def rnd(*shape):
+        return torch.randn(shape, device=cuda, generator=g).to(torch.bfloat16)
+
+    x, q, k, v, do = rnd(L, H * D), rnd(H, L, D), rnd(H, L, D), rnd(H, L, D), rnd(H, L, D)
+    sel, scores = layer.select(x, layer.predictor_weights(seed=2), return_scores=True)
+    out, lse = layer.forward(q, k, v, sel)
+    dq, dk, dv = layer.backward(q, k, v, out, lse, do, sel)
+    torch.cuda.synchronize()
+    idx, sc = sel.idx.cpu().numpy(), scores.cpu().numpy()
+    errs = {}
+    for h in range(H):
+        kh = layer.ks[h]
+        ri, _ = oracle.topk_from_scores(sc[h], kh)
+        np.testing.assert_array_equal(idx[h, :, :kh], ri)
+        hd = {"q": q[h].double().cpu().numpy(), "k": k[h].double().cpu().numpy(),
+              "v": v[h].double().cpu().numpy(), "do": do[h].double().cpu().numpy(),
+              "out": out[h].float().cpu().numpy(), "lse": lse[h].cpu().numpy(),
+              "dq": dq[h].float().cpu().numpy(), "dk": dk[h].float().cpu().numpy(),
+              "dv": dv[h].float().cpu().numpy(), "dk32": layer._acc[0, h].cpu().numpy(),
+              "dv32": layer._acc[1, h].cpu().numpy()}
+        sets = [idx[h, gi, :kh] for gi in range(G)]
+        members = layer.plan.members
+        ref, ref_lse = oracle.grouped_attention_fwd(hd["q"], hd["k"], hd["v"], members, sets)
+        rdq, rdk, rdv = oracle.grouped_attention_bwd(hd["q"], hd["k"], hd["v"], members, sets, hd["do"])
+        e = {"o_max_abs": float(np.max(np.abs(hd["out"] - ref))), "o_rel_l2": _rel_l2(hd["out"], ref),
+             "lse_max_abs": float(np.max(np.abs(hd["lse"] * math.log(2.0) - ref_lse))),
+             "dq_rel_l2": _rel_l2(hd["dq"], rdq), "dk_rel_l2": _rel_l2(hd["dk"], rdk),
+             "dv_rel_l2": _rel_l2(hd["dv"], rdv)}
+        errs[f"head{h}"] = e
+        _assert_tol(e, f"{voxel} head {h}")
+    parity_report(f"ladder_{voxel[0]}x{voxel[1]}x{voxel[2]}_{grid_dims[0]}x{grid_dims[1]}x{grid_dims[2]}",
+                  {"groups": G, "tiles": int(layer.grp_rows.shape[0]), **errs})

@@ -1,13 +1,12 @@
-"""Timeline of HostPipeline at c2: copy-stream and compute-stream events per step."""
-import math
+"""Timeline of HostPipeline at c2 with the D2H of each step's results: per-step compute
+(start, end) and D2H (end) events, relative to the first copy. python tools/e2e_probe.py"""
 import sys
-import time
 
 import torch
 
 sys.path.insert(0, ".")
-from paper_2502_07590_b200.grid import TokenGrid
-from paper_2502_07590_b200.layer import DSVAttentionLayer, HostPipeline
+from paper_2502_07590_b200.grid import TokenGrid  # noqa: E402
+from paper_2502_07590_b200.layer import DSVAttentionLayer, HostPipeline  # noqa: E402
 
 
 def main():
@@ -20,41 +19,34 @@ def main():
     g = torch.Generator().manual_seed(0)
     host = [torch.randn(s, generator=g).to(torch.bfloat16).pin_memory()
             for s in ((L, H * D), (H, L, D), (H, L, D), (H, L, D), (H, L, D))]
-    dk = torch.zeros((H, L, D), device=dev)
-    dv = torch.zeros_like(dk)
     pipe = HostPipeline(host, dev)
     marks = []
 
     def step(*b):
-        e0 = torch.cuda.Event(enable_timing=True); e0.record()
-        out = layer.step(b[0], wt, *b[1:], dk_acc=dk, dv_acc=dv)
-        e1 = torch.cuda.Event(enable_timing=True); e1.record()
-        marks.append((e0, e1))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = layer.step(b[0], wt, *b[1:])
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        marks.append([e0, e1])
         return out
 
-    for mode in ("pipe", "pipe"):
+    for rep in range(2):
         marks.clear()
-        t0 = torch.cuda.Event(enable_timing=True); t0.record()
-        w0 = time.perf_counter()
-        for out in pipe.run(step, [host] * 5):
-            float(out[1].float().sum().item())
-        t1 = torch.cuda.Event(enable_timing=True); t1.record()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in pipe.run(step, [host] * 6):
+            e2 = torch.cuda.Event(enable_timing=True)
+            e2.record(pipe.d2h)
+            marks[-1].append(e2)
+        pipe.drain()
+        t1 = torch.cuda.Event(enable_timing=True)
+        t1.record()
         torch.cuda.synchronize()
-        w1 = time.perf_counter()
-        print(f"{mode}: total {t0.elapsed_time(t1):.2f} ms (wall {1e3 * (w1 - w0):.2f}) for 5 steps")
-        for i, (a, b) in enumerate(marks):
-            print(f"  step {i}: start {t0.elapsed_time(a):7.2f}  end {t0.elapsed_time(b):7.2f}")
-    # plain sequential copy then step
-    bufs = pipe.bufs[0]
-    t0 = torch.cuda.Event(enable_timing=True); t0.record()
-    for _ in range(5):
-        for s_, d_ in zip(host, bufs):
-            d_.copy_(s_, non_blocking=True)
-        out = layer.step(bufs[0], wt, *bufs[1:], dk_acc=dk, dv_acc=dv)
-        float(out[1].float().sum().item())
-    t1 = torch.cuda.Event(enable_timing=True); t1.record()
-    torch.cuda.synchronize()
-    print(f"sequential: {t0.elapsed_time(t1) / 5:.2f} ms/step")
+        print(f"rep {rep}: {t0.elapsed_time(t1) / 6:.2f} ms/step")
+        for i, (a, b, c) in enumerate(marks):
+            print(f"  step {i}: compute {t0.elapsed_time(a):7.2f} .. {t0.elapsed_time(b):7.2f}  "
+                  f"d2h done {t0.elapsed_time(c):7.2f}")
 
 
 if __name__ == "__main__":
