@@ -72,8 +72,6 @@ def _args():
     ap.add_argument("--cpu-budget", type=float, default=float(os.environ.get("DSV_CPU_BUDGET", 12)))
     ap.add_argument("--unbalanced", action="store_true", help="contiguous head split (no rebalance)")
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--overlap", default=os.environ.get("DSV_OVERLAP", "none"), choices=["none", "sm", "ce"],
-                    help="HCP exchange under the compute on a side stream (copy kernel / copy engines)")
     ap.add_argument("--graph", dest="graph", action="store_true",
                     default=os.environ.get("DSV_GRAPH", "1") == "1",
                     help="replay the step as one captured CUDA graph (default; DSV_GRAPH=0 or "
@@ -351,8 +349,7 @@ def run_gpu(args) -> None:
                            balanced=not args.unbalanced, device=dev)
         else:
             cp = HeadParallelDSV(grid, H, D, D_LR, VOXEL, sparsity, balanced=not args.unbalanced,
-                                 device=dev,
-                                 overlap=False if args.overlap == "none" else args.overlap)
+                                 device=dev)
         layer = cp.local
         chunk = L // world
         g0 = torch.Generator(device="cpu").manual_seed(0)

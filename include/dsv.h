@@ -210,16 +210,20 @@ typedef struct dsv_copy_job {
  * `splits` blocks cooperate on each job (1..1024). */
 int dsv_copy_jobs(const dsv_copy_job* jobs, int njobs, int splits, void* stream);
 
-/* The same job semantics from a HOST job table, executed by the copy engines (one
- * cudaMemcpyAsync per flat job, cudaMemcpy2DAsync per strided job) on `stream`: no SM
- * time, so an exchange can run underneath the attention kernels. */
-int dsv_copy_jobs_ce(const dsv_copy_job* jobs, int njobs, void* stream);
-
-/* Stream memory operations for cross-GPU signalling without SM time: write `value` to
- * a 4-byte device (or peer-mapped) word after all prior work of `stream`, and make
- * `stream` wait until a word is >= value (monotone step counters). */
-int dsv_stream_write_u32(void* addr, unsigned int value, void* stream);
-int dsv_stream_wait_u32_geq(const void* addr, unsigned int value, void* stream);
+/* Peer memory for the NVLink exchanges (one process per GPU): dsv_peer_alloc returns a
+ * zeroed device buffer and its 64-byte CUDA IPC handle, which a peer process maps with
+ * dsv_peer_open (unmap: dsv_peer_close; owner: dsv_peer_free). dsv_peer_barrier is a
+ * device-side barrier over those buffers: peer_slots is a DEVICE array of `world` pointers
+ * (rank r's slot array as mapped here), my_slots this rank's own array of `world` u32 and
+ * epoch a u32 device counter; all ranks must issue their barriers in the same order. Writes
+ * of earlier kernels on `stream` (including peer writes) are visible to every rank's later
+ * kernels. Graph-capturable (the epoch advances on the device). */
+int dsv_peer_alloc(long long bytes, void** ptr, void* handle);
+int dsv_peer_open(const void* handle, void** ptr);
+int dsv_peer_close(void* ptr);
+int dsv_peer_free(void* ptr);
+int dsv_peer_barrier(unsigned* const* peer_slots, unsigned* my_slots, unsigned* epoch, int world,
+                     int rank, void* stream);
 
 /* Diagnostics: copy the backward kernel's phase timeline (clock64 stamps, filled only
  * by builds with -DDSV_BWD_PROF; layout [8 CTAs][32 blocks][12 events] int64) into a

@@ -62,9 +62,11 @@ SIGNATURES = {
                           c_void_p],
     "dsv_critical_counts": [c_void_p, c_longlong, c_int, c_int, ctypes.c_double, ctypes.c_double,
                             c_void_p, c_void_p],
-    "dsv_copy_jobs_ce": [c_void_p, c_int, c_void_p],
-    "dsv_stream_write_u32": [c_void_p, ctypes.c_uint, c_void_p],
-    "dsv_stream_wait_u32_geq": [c_void_p, ctypes.c_uint, c_void_p],
+    "dsv_peer_alloc": [c_longlong, c_void_p, c_void_p],
+    "dsv_peer_open": [c_void_p, c_void_p],
+    "dsv_peer_close": [c_void_p],
+    "dsv_peer_free": [c_void_p],
+    "dsv_peer_barrier": [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p],
     "dsv_gather_rows": [c_void_p, c_longlong, c_void_p, c_int, c_int, c_void_p, c_longlong,
                         c_void_p],
     "dsv_f32_to_bf16": [c_void_p, c_void_p, c_longlong, c_void_p],

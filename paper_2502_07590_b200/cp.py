@@ -29,7 +29,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from . import cpmodel
+from . import _lib, cpmodel
 
 PHASES = ("hcp_fwd", "scp_index_exchange", "scp_kv", "output_redistribute", "hcp_bwd_in",
           "hcp_bwd_out", "scp_grad",   # scp_grad: dK/dV of gathered rows back to their owners
@@ -228,10 +228,56 @@ class HeadParallelExchange:
         return cpmodel.hcp_comm(self.H, len(self.my_heads), self.L, d, self.world, elem_width)
 
 
+class _CudaArray:
+    """Minimal __cuda_array_interface__ view of raw device memory (int16 elements)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i2", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class _PeerBuffer:
+    """This rank's peer-mapped device buffer plus every peer's, mapped into this process with
+    CUDA IPC through libdsv (dsv_peer_alloc / dsv_peer_open; handles exchanged with
+    all_gather_object). `tensor` is a bf16 view of the local buffer; `ptrs[r]` the address of
+    rank r's buffer in this process."""
+
+    def __init__(self, nbytes: int, group, device):
+        import ctypes
+
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        ptr, handle = ctypes.c_void_p(), ctypes.create_string_buffer(64)
+        with torch.cuda.device(device):
+            _lib.call("dsv_peer_alloc", int(nbytes), ctypes.byref(ptr), handle)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, handle.raw, group=group)
+        self.ptrs, self._opened = [], []
+        with torch.cuda.device(device):
+            for r, h in enumerate(handles):
+                if r == self.rank:
+                    self.ptrs.append(int(ptr.value))
+                    continue
+                p = ctypes.c_void_p()
+                _lib.call("dsv_peer_open", ctypes.create_string_buffer(h, 64), ctypes.byref(p))
+                self.ptrs.append(int(p.value))
+                self._opened.append(int(p.value))
+        self._own = int(ptr.value)
+        self.tensor = torch.as_tensor(_CudaArray(self._own, nbytes // 2), device=device).view(torch.bfloat16)
+
+    def __del__(self):
+        try:
+            for p in self._opened:
+                _lib.load().dsv_peer_close(p)
+            self.tensor = None
+            _lib.load().dsv_peer_free(self._own)
+        except Exception:
+            pass
+
+
 class PeerExchange:
     """HCP exchange over NVLink peer memory (one process per GPU, B200 NVSwitch).
 
-    Every rank owns one symmetric buffer holding the regions the DSV layer reads
+    Every rank owns one peer-mapped buffer (CUDA IPC) holding the regions the DSV layer reads
     and returns: Q, K, V, dO [heads, L, D] and Q_lr, K_lr [heads, L, r] for its
     heads, and O, dQ, dK, dV [H, L/N, D] for its tokens. A sender writes its rows
     straight into the owner's region (dsv_copy_jobs on peer pointers), so pack,
@@ -274,7 +320,7 @@ class PeerExchange:
         big, small, back = nh_max * self.L * self.D, nh_max * self.L * self.r, self.H * self.chunk * self.D
         names = [("q", big), ("k", big), ("v", big), ("do", big), ("qlr", small), ("klr", small),
                  ("o", back), ("dq", back), ("dk", back), ("dv", back),
-                 ("flags", 2 * 3 * self.world)]          # int32 [3 kinds][world] arrival flags
+                 ("flags", 2 * (self.world + 1))]        # u32 [world] barrier slots + epoch
         self.off, tot = {}, 0
         for n, sz in names:
             self.off[n] = tot
@@ -282,24 +328,26 @@ class PeerExchange:
         self.total_elems = tot
         self._tables = {}
         if plan_only is not None:
-            self.buf, self.hdl = None, None
+            self.buf, self.peer = None, None
             self.ptrs = np.asarray(plan_only[2], dtype=np.int64)
             return
-        import torch.distributed._symmetric_memory as symm
-
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.buf = symm.empty(tot, dtype=torch.bfloat16, device=dev)
-        if hasattr(symm, "enable_symm_mem_for_group"):
-            try:
-                symm.enable_symm_mem_for_group(self.group.group_name)
-            except Exception:   # newer torch: implicit
-                pass
-        self.hdl = symm.rendezvous(self.buf, self.group)
-        self.ptrs = np.asarray([int(p) for p in self.hdl.buffer_ptrs], dtype=np.int64)
-        self.buf[self.off["flags"]: self.off["flags"] + 2 * 3 * self.world].zero_()
+        self.peer = _PeerBuffer(2 * tot, self.group, dev)
+        self.buf = self.peer.tensor
+        self.ptrs = np.asarray(self.peer.ptrs, dtype=np.int64)
+        # barrier slots: [world] u32 arrival epochs + one u32 epoch counter (device side)
+        so = 2 * self.off["flags"]
+        self._slots_tab = torch.tensor([int(p) + so for p in self.ptrs], dtype=torch.int64, device=dev)
+        self._my_slots = int(self.ptrs[self.rank]) + so
+        self._epoch = self._my_slots + 4 * self.world
         torch.cuda.synchronize(dev)
         dist.barrier(self.group)
         self._step = 0
+
+    def _barrier(self):
+        """Device barrier over the ranks' peer buffers on the current stream."""
+        _lib.call("dsv_peer_barrier", self._slots_tab.data_ptr(), self._my_slots, self._epoch,
+                  self.world, self.rank, torch.cuda.current_stream(self.buf.device).cuda_stream)
 
     # ------------------------------------------------------------------ views
     def region(self, name: str) -> torch.Tensor:
@@ -399,9 +447,9 @@ class PeerExchange:
     def _run(self, table):
         from . import ops
 
-        self.hdl.barrier(channel=0)          # owners are done reading the previous contents
+        self._barrier()                      # owners are done reading the previous contents
         ops.copy_jobs(table, self.splits)
-        self.hdl.barrier(channel=0)          # every writer is done: regions are complete
+        self._barrier()                      # every writer is done: regions are complete
 
     # ------------------------------------------------------------------ exchanges
     def to_heads(self, q, k, v, do, p):
@@ -429,105 +477,6 @@ class PeerExchange:
         key = ("b",) + tuple(t.data_ptr() for t in (o, dq, dk, dv))
         self._run(self._table(key, lambda: self._back_jobs((o, dq, dk, dv))))
         self._account(("output_redistribute", self.D), ("hcp_bwd_out", 3 * self.D), to_heads=False)
-        return tuple(self.region(n) for n in ("o", "dq", "dk", "dv"))
-
-    # ------------------------------------------------------------------ overlapped step
-    def _flag(self, rank: int, kind: int, src: int) -> int:
-        """Address of rank's arrival flag for data of `kind` (0 Q/K/V, 1 dO, 2 O) from src."""
-        return int(self.ptrs[rank]) + 2 * self.off["flags"] + 4 * (kind * self.world + src)
-
-    def _signal(self, kind: int, step: int, stream) -> None:
-        from . import _lib
-
-        for r in range(self.world):
-            if r != self.rank:
-                _lib.call("dsv_stream_write_u32", self._flag(r, kind, self.rank), step, stream.cuda_stream)
-
-    def _await(self, kind: int, step: int, stream) -> None:
-        from . import _lib
-
-        for r in range(self.world):
-            if r != self.rank:
-                _lib.call("dsv_stream_wait_u32_geq", self._flag(self.rank, kind, r), step, stream.cuda_stream)
-
-    def overlapped(self, q, k, v, do, p, select, forward, backward, engine: str = "sm"):
-        """One HCP step with the bulk of the exchange under the compute, moved either by the
-        copy kernel on a side stream (engine "sm") or by the copy engines ("ce"):
-
-        compute stream: barrier | Q_lr/K_lr rows (copy kernel) | barrier | select |
-                        wait Q,K,V | forward | wait dO | backward | dQ,dK,dV (copy kernel) |
-                        barrier | wait O
-        side stream:    Q,K,V | signal | dO | signal | wait fwd | O | signal
-
-        Arrival is signalled with stream memory operations (a value write into each
-        owner's flag word, a wait-until->= on the consumer's stream): no kernel spins on
-        an SM while the attention kernels run.
-
-        select/forward/backward are callables on the compute stream (the local layer).
-        Returns (O, dQ, dK, dV) views [H, L/N, D] of this rank's tokens.
-        """
-        from . import ops
-
-        self._check_in(q, k, v, do, p)
-        cur = torch.cuda.current_stream()
-        if getattr(self, "_side", None) is None:
-            self._side = torch.cuda.Stream(device=self.buf.device)
-        side = self._side
-        ptrs = tuple(t.data_ptr() for t in (q, k, v, do, p))
-        table = self._host_table if engine == "ce" else self._table
-        tkw = {} if engine == "ce" else {"stream": side}
-        qkv = table(("qkv", engine) + ptrs, lambda: self._head_jobs((("q", q), ("k", k), ("v", v))), **tkw)
-        dj = table(("do", engine) + ptrs, lambda: self._head_jobs((("do", do),)), **tkw)
-
-        def send(jobs):
-            if engine == "ce":
-                ops.copy_jobs_ce(jobs, side)
-            else:
-                with torch.cuda.stream(side):
-                    ops.copy_jobs(jobs, self.splits)
-        lr = self._table(("lr",) + ptrs, lambda: self._lowrank_jobs(p))
-        # host issue order keeps the GPU busy: the select kernels are queued before the
-        # (slow to issue) copy-engine jobs, the forward before the dO / O jobs
-        self.hdl.barrier(channel=0)                   # everyone is done with the last step
-        ev0 = torch.cuda.Event()
-        ev0.record(cur)
-        ev_qkv, ev_do, ev_f, ev_o = (torch.cuda.Event() for _ in range(4))
-        self._step += 1
-        step = self._step
-        ops.copy_jobs(lr, self.splits)
-        self.hdl.barrier(channel=0)
-        ql, kl, vl, dom, qlr, klr = (self.region(n) for n in ("q", "k", "v", "do", "qlr", "klr"))
-        sel = select(qlr, klr)
-        side.wait_event(ev0)
-        send(qkv)
-        self._signal(0, step, side)
-        ev_qkv.record(side)
-        cur.wait_event(ev_qkv)                        # this rank's own (local) copies
-        self._await(0, step, cur)
-        out, lse = forward(ql, kl, vl, sel)
-        ev_f.record(cur)
-        send(dj)
-        self._signal(1, step, side)
-        ev_do.record(side)
-        side.wait_event(ev_f)
-        oj = (self._host_table(("o", engine, out.data_ptr()), lambda: self._back_jobs((out,), ("o",)))
-              if engine == "ce" else
-              self._table(("o", engine, out.data_ptr()), lambda: self._back_jobs((out,), ("o",)), side))
-        send(oj)
-        self._signal(2, step, side)
-        ev_o.record(side)
-        cur.wait_event(ev_do)
-        self._await(1, step, cur)
-        dq, dk, dv = backward(ql, kl, vl, out, lse, dom, sel)
-        gj = self._table(("g",) + tuple(t.data_ptr() for t in (dq, dk, dv)),
-                         lambda: self._back_jobs((dq, dk, dv), ("dq", "dk", "dv")))
-        ops.copy_jobs(gj, self.splits)
-        self.hdl.barrier(channel=0)
-        cur.wait_event(ev_o)
-        self._await(2, step, cur)
-        self._account(("hcp_fwd", 3 * self.D + 2 * self.r), ("hcp_bwd_in", self.D), to_heads=True)
-        self._account(("output_redistribute", self.D), ("hcp_bwd_out", 3 * self.D), to_heads=False)
-        self._keep = (out, dq, dk, dv)                # alive until the side stream has read them
         return tuple(self.region(n) for n in ("o", "dq", "dk", "dv"))
 
     def _account(self, *phases, to_heads: bool):
@@ -856,7 +805,7 @@ class HeadParallelDSV(_PhaseMarks):
 
     def __init__(self, grid, heads: int, head_dim: int, d_lr: int = 16, voxel=(8, 4, 4),
                  sparsity=0.9, balanced: bool = True, group=None, device="cuda",
-                 transport: str = "auto", overlap: bool = False):
+                 transport: str = "auto"):
         from .layer import DSVAttentionLayer
 
         self.world = dist.get_world_size(group)
@@ -867,9 +816,6 @@ class HeadParallelDSV(_PhaseMarks):
         if transport not in ("peer", "all_to_all"):
             raise ValueError(f"unknown transport {transport!r}")
         self.transport = transport
-        # overlap: False, True / "sm" (copy kernel on a side stream) or "ce" (copy engines)
-        self.overlap = bool(overlap) and transport == "peer"
-        self.overlap_engine = overlap if isinstance(overlap, str) else "sm"
         if transport == "peer":
             self.ex = PeerExchange(heads, grid.size, head_dim, d_lr, self.assignment, group, device)
         else:
@@ -929,28 +875,6 @@ class HeadParallelDSV(_PhaseMarks):
         self._mark("start")
         p = ops.project(x_local, wt)                                   # [L/N, 2 H r]
         self._mark("project")
-        if self.overlap:
-            # copy-engine exchange under the compute (measured slower on B200 at 2-4 GPUs:
-            # the copy engines move ~200 GB/s here vs ~570 GB/s for the copy kernel)
-            def select(qlr, klr):
-                r = loc.select_from_lowrank(qlr, klr)
-                self._mark("select")   # includes the Q_lr/K_lr exchange
-                return r
-
-            def forward(ql, kl, vl, sel):
-                r = loc.forward(ql, kl, vl, sel)
-                self._mark("fwd")
-                return r
-
-            def backward(*a):
-                r = loc.backward(*a)
-                self._mark("bwd")
-                return r
-
-            res = self.ex.overlapped(q, k, v, dout, p, select, forward, backward,
-                                     engine=self.overlap_engine)
-            self._mark("grads_exchange")
-            return res
         ql, kl, vl, dout_m, qlr, klr = self.ex.to_heads(q, k, v, dout, p)
         self._mark("exchange_in")
         sel = loc.select_from_lowrank(qlr, klr)

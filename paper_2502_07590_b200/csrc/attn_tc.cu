@@ -116,9 +116,6 @@ struct FwdBars {
 };
 static_assert(sizeof(FwdBars) <= 256, "forward barriers over their 256 B");
 
-#ifndef DSV_FWD_ABLATE
-#define DSV_FWD_ABLATE 0   // 1: ablation build only (forward without the softmax math)
-#endif
 #ifndef DSV_FWD_LAZY
 #define DSV_FWD_LAZY 1     // 0: exchange the row max every key block (the exact-max pass only)
 #endif
@@ -173,16 +170,13 @@ DSV_DEV float softmax_max_pass(uint32_t tS, int kv) {
   return mx;
 }
 
-#ifndef DSV_POLY_EVERY
-#define DSV_POLY_EVERY 0      // one pair in DSV_POLY_EVERY takes the polynomial (0: none).
-#endif                        // With the lazy max (no per-block exchange) all-MUFU measured
-                              // fastest at c2: 1.431 ms vs 1.440 / 1.447 / 1.451 / 1.474
-                              // for one pair in 16 / 6 / 8 / 4 (tools/fwd_bench.py)
+// All exponentials on the MUFU: with the lazy max (no per-block exchange) all-MUFU measured
+// fastest at c2 (1.431 ms vs 1.440 / 1.447 / 1.451 / 1.474 ms with one pair in 16 / 6 / 8 / 4
+// on an FMA-pipe polynomial, round 1, tools/fwd_bench.py).
 #ifndef DSV_P_CHUNKS
 #define DSV_P_CHUNKS 2        // 32-column chunks loaded per TMEM wait in pass 2
 #endif
-// P for one 32-column chunk of raw scores: 2^(s*scale_log2 - m) with packed FMAs; one
-// pair in four takes the polynomial exp2 on the FMA pipe, the rest the MUFU.
+// P for one 32-column chunk of raw scores: 2^(s*scale_log2 - m) (packed FMAs, MUFU ex2).
 template <bool kMasked>
 DSV_DEV void softmax_p_chunk(const uint32_t (&r)[32], uint32_t tdst, f32x2 sc2, f32x2 nm2, int c,
                              int kv, f32x2& lsum2) {
@@ -190,13 +184,8 @@ DSV_DEV void softmax_p_chunk(const uint32_t (&r)[32], uint32_t tdst, f32x2 sc2, 
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     const f32x2 x = ffma2(f2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), sc2, nm2);
-    float2 p;
-    if (DSV_POLY_EVERY > 0 && (i % (DSV_POLY_EVERY > 0 ? DSV_POLY_EVERY : 1)) == DSV_POLY_EVERY - 1) {
-      p = f2u(exp2_poly2(x));
-    } else {
-      const float2 xv = f2u(x);
-      p = make_float2(fast_exp2(xv.x), fast_exp2(xv.y));
-    }
+    const float2 xv = f2u(x);
+    float2 p = make_float2(fast_exp2(xv.x), fast_exp2(xv.y));
     if constexpr (kMasked) {
       if (c * 32 + 2 * i >= kv) p.x = 0.f;
       if (c * 32 + 2 * i + 1 >= kv) p.y = 0.f;
@@ -537,17 +526,8 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
       // them, so the lazy-max blocks need no barrier at all
       const f32x2 sc2 = f2(scale_log2, scale_log2), nm2 = f2(-m_run, -m_run);
       f32x2 lsum2 = f2(0.f, 0.f);
-#if DSV_FWD_ABLATE == 1
-      {   // ablation build: no exponentials (P = raw bits), measures the MMA/load pipeline
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) pk[i] = r[2 * i] ^ r[2 * i + 1];
-        tmem_st16(tS + cq * 32, pk);
-      }
-#else
       if (kv == BKV) softmax_p_chunk<false>(r, tS + cq * 32, sc2, nm2, cq, kv, lsum2);
       else softmax_p_chunk<true>(r, tS + cq * 32, sc2, nm2, cq, kv, lsum2);
-#endif
       const float2 ls = f2u(lsum2);
       l_run += ls.x + ls.y;
       if (warp == 0 && lane == 0) FPROF(j, 9);
@@ -633,9 +613,6 @@ constexpr int kBwdScatWarps = DSV_BWD_SCAT_WARPS;
 constexpr int kBwdScatThreads = kBwdScatWarps * 32;
 constexpr int kBwdThreads = (kBwdScatWarp0 + kBwdScatWarps) * 32;   // 864 by default
 
-#ifndef DSV_BWD_SCATTER
-#define DSV_BWD_SCATTER 0   // 1: ablation build only (no global adds)
-#endif
 
 template <int D>
 struct BwdSmem {
@@ -788,12 +765,8 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
             const int key = __shfl_sync(0xffffffffu, mykey, rr);
             if (p < kv) {
               const uint2 v = *reinterpret_cast<const uint2*>(stg + stg_off<D>(p, lane >> 1) + (lane & 1) * 8);
-#if DSV_BWD_SCATTER == 1
-              if (v.x == 0x7fc17fc1u) acc[0] = 0.f;   // ablation: no global traffic
-#else
               red_add_v4(acc + (long long)key * D + lane * 4, bf16lo(v.x), bf16hi(v.x),
                          bf16lo(v.y), bf16hi(v.y));
-#endif
             }
           }
         } else {

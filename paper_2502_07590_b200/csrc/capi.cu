@@ -104,20 +104,6 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// Stream memory operations (executed by the GPU front end, no SM time): a peer's copy
-// engines signal data arrival with a value write, the consumer's stream waits on it.
-using WriteValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-template <typename Fn>
-Fn driver_fn(const char* name) {
-  void* p = nullptr;
-  cudaDriverEntryPointQueryResult q;
-  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess &&
-      q == cudaDriverEntryPointSuccess)
-    return reinterpret_cast<Fn>(p);
-  return nullptr;
-}
-
 // bf16 tensor map with up to 3 dims: dims[0] innermost (elements), strides in bytes for
 // dims 1..rank-1, 128B swizzle.
 bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
@@ -485,44 +471,6 @@ extern "C" int dsv_critical_counts(const float* scores, long long ld, int rows, 
                      "critical_counts launch");
 }
 
-extern "C" int dsv_stream_write_u32(void* addr, unsigned int value, void* stream) {
-  static WriteValueFn fn = driver_fn<WriteValueFn>("cuStreamWriteValue32");
-  if (!fn) return fail(DSV_EUNSUPPORTED, "stream_write_u32: driver entry point missing");
-  if (!addr || (reinterpret_cast<uintptr_t>(addr) & 3)) return fail(DSV_EINVAL, "stream_write_u32: bad address");
-  const CUresult r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(addr), value,
-                        CU_STREAM_WRITE_VALUE_DEFAULT);
-  return r == CUDA_SUCCESS ? DSV_OK : fail(DSV_ECUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
-}
-
-extern "C" int dsv_stream_wait_u32_geq(const void* addr, unsigned int value, void* stream) {
-  static WaitValueFn fn = driver_fn<WaitValueFn>("cuStreamWaitValue32");
-  if (!fn) return fail(DSV_EUNSUPPORTED, "stream_wait_u32: driver entry point missing");
-  if (!addr || (reinterpret_cast<uintptr_t>(addr) & 3)) return fail(DSV_EINVAL, "stream_wait_u32: bad address");
-  const CUresult r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(addr), value,
-                        CU_STREAM_WAIT_VALUE_GEQ);
-  return r == CUDA_SUCCESS ? DSV_OK : fail(DSV_ECUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
-}
-
-extern "C" int dsv_copy_jobs_ce(const dsv_copy_job* jobs, int njobs, void* stream) {
-  if (njobs <= 0) return DSV_OK;
-  if (!jobs) return fail(DSV_EINVAL, "copy_jobs_ce: null job table");
-  for (int i = 0; i < njobs; ++i) {
-    const dsv_copy_job& j = jobs[i];
-    if (j.rows <= 0 || j.row_bytes <= 0) continue;
-    cudaError_t e;
-    if (j.rows == 1 || (j.src_stride == j.row_bytes && j.dst_stride == j.row_bytes)) {
-      e = cudaMemcpyAsync(reinterpret_cast<void*>(j.dst), reinterpret_cast<const void*>(j.src),
-                          (size_t)(j.rows * j.row_bytes), cudaMemcpyDeviceToDevice, S(stream));
-    } else {
-      e = cudaMemcpy2DAsync(reinterpret_cast<void*>(j.dst), (size_t)j.dst_stride,
-                            reinterpret_cast<const void*>(j.src), (size_t)j.src_stride,
-                            (size_t)j.row_bytes, (size_t)j.rows, cudaMemcpyDeviceToDevice, S(stream));
-    }
-    if (e != cudaSuccess) return cuda_status((int)e, "copy_jobs_ce");
-  }
-  return DSV_OK;
-}
-
 extern "C" int dsv_copy_jobs(const dsv_copy_job* jobs, int njobs, int splits, void* stream) {
   if (njobs <= 0) return DSV_OK;
   if (!jobs || splits < 1 || splits > 1024)
@@ -530,6 +478,70 @@ extern "C" int dsv_copy_jobs(const dsv_copy_job* jobs, int njobs, int splits, vo
   dim3 grid(njobs, splits);
   copy_jobs_kernel<<<grid, 256, 0, S(stream)>>>(jobs);
   return cuda_status((int)cudaGetLastError(), "copy_jobs launch");
+}
+
+// ---------------------------------------------------------------- peer memory (NVLink)
+// One buffer per rank, mapped into every peer process with CUDA IPC (public runtime API;
+// replaces torch's private symmetric-memory module). The device barrier orders the copy
+// kernels' peer writes: rank r stores its arrival epoch into slot r of every peer's slot
+// array (system-scope release after a system fence), then waits until all of its own slots
+// reached the epoch (acquire). Epochs live in device memory, so a captured graph's replays
+// keep counting.
+namespace {
+__global__ void peer_barrier_kernel(unsigned* const* __restrict__ peer_slots,
+                                    unsigned* __restrict__ my_slots, unsigned* __restrict__ epoch,
+                                    int world, int rank) {
+  if (threadIdx.x != 0) return;
+  const unsigned e = *epoch + 1u;
+  __threadfence_system();
+  for (int r = 0; r < world; ++r)
+    asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(peer_slots[r] + rank), "r"(e) : "memory");
+  for (int r = 0; r < world; ++r) {
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(my_slots + r) : "memory");
+    } while ((int)(v - e) < 0);
+  }
+  *epoch = e;
+  __threadfence_system();
+}
+}  // namespace
+
+extern "C" int dsv_peer_alloc(long long bytes, void** ptr, void* handle) {
+  if (bytes <= 0 || !ptr || !handle) return fail(DSV_EINVAL, "peer_alloc: bad arguments");
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, (size_t)bytes);
+  if (e != cudaSuccess) return cuda_status((int)e, "peer_alloc cudaMalloc");
+  e = cudaMemset(p, 0, (size_t)bytes);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle), p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return cuda_status((int)e, "peer_alloc cudaIpcGetMemHandle");
+  }
+  *ptr = p;
+  return DSV_OK;
+}
+
+extern "C" int dsv_peer_open(const void* handle, void** ptr) {
+  if (!handle || !ptr) return fail(DSV_EINVAL, "peer_open: bad arguments");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  return cuda_status((int)cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess),
+                     "peer_open cudaIpcOpenMemHandle");
+}
+
+extern "C" int dsv_peer_close(void* ptr) {
+  return cuda_status((int)cudaIpcCloseMemHandle(ptr), "peer_close");
+}
+
+extern "C" int dsv_peer_free(void* ptr) { return cuda_status((int)cudaFree(ptr), "peer_free"); }
+
+extern "C" int dsv_peer_barrier(unsigned* const* peer_slots, unsigned* my_slots, unsigned* epoch,
+                                int world, int rank, void* stream) {
+  if (world < 1 || rank < 0 || rank >= world || !peer_slots || !my_slots || !epoch)
+    return fail(DSV_EINVAL, "peer_barrier: bad arguments");
+  peer_barrier_kernel<<<1, 32, 0, S(stream)>>>(peer_slots, my_slots, epoch, world, rank);
+  return cuda_status((int)cudaGetLastError(), "peer_barrier launch");
 }
 
 extern "C" int dsv_gather_rows(const void* src, long long src_stride, const int* rows, int n,

@@ -82,27 +82,6 @@ DSV_DEV float fmax3f(float a, float b, float c) {
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
   return r;
 }
-// 2^x on the FMA/ALU pipes for a pair (x <= 0 in the softmax): round-to-nearest split
-// through the 1.5*2^23 magic add (no FRND/F2I, which share the quarter-rate unit with
-// MUFU), degree-3 minimax for 2^f on [-1/2, 1/2] (max rel. error 7.5e-5, far below
-// bf16's 3.9e-3), exponent added as integer bits. Offloads part of the exponentials
-// from the 16/clk/SM MUFU unit.
-DSV_DEV f32x2 exp2_poly2(f32x2 x) {
-  float2 v = f2u(x);
-  v.x = fmaxf(v.x, -125.f);
-  v.y = fmaxf(v.y, -125.f);
-  const f32x2 magic = f2(12582912.f, 12582912.f);
-  const f32x2 xc = f2(v.x, v.y);
-  const f32x2 t = fadd2(xc, magic);
-  const f32x2 jf = fadd2(t, f2(-12582912.f, -12582912.f));
-  const f32x2 fr = ffma2(jf, f2(-1.f, -1.f), xc);
-  f32x2 p = ffma2(fr, f2(0.05517044f, 0.05517044f), f2(0.2426081f, 0.2426081f));
-  p = ffma2(fr, p, f2(0.69326096f, 0.69326096f));
-  p = ffma2(fr, p, f2(0.99992834f, 0.99992834f));
-  const float2 q = f2u(p), tt = f2u(t);
-  return f2(__int_as_float(__float_as_int(q.x) + (__float_as_int(tt.x) << 23)),
-            __int_as_float(__float_as_int(q.y) + (__float_as_int(tt.y) << 23)));
-}
 DSV_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
 }

@@ -80,9 +80,6 @@ constexpr uint32_t KEY_NEG0 = 0x7FFFFFFFu;    // the key no float maps to (-0.0 
 #else
 #define FSEL_WAIT mbar_wait
 #endif
-#ifndef DSV_FSEL_ABLATE
-#define DSV_FSEL_ABLATE 0          // 1: epilogue skips the per-element work (pipeline only)
-#endif
 
 enum : uint32_t { ST_REFINE = 0, ST_CAND = 1, ST_DONE = 2 };
 enum : uint32_t { P_MINMAX = 0, P_SHIST = 1, P_FULL = 2, P_EMIT = 3, P_EXIT = 4, P_COLLECT = 5 };
@@ -561,9 +558,7 @@ select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 #pragma unroll
           for (int j = 0; j < kCols; ++j) if (col0 + j >= L) v[j] = 0x7fc00000u;   // NaN
         }
-        if (DSV_FSEL_ABLATE) {
-          if (v[0] == 0x12345678u && v[kCols - 1] == 0x9abcdef0u) cnt += 1;   // keep the loads
-        } else if (pass == P_FULL) {
+        if (pass == P_FULL) {
           if (!warp_idle) {
             // per 32 columns: count above the band (predicated adds) and a band bit mask;
             // the band entries (rare after the first refinement) are handled per set bit
@@ -803,7 +798,7 @@ select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         else if (pass == P_SHIST || pass == P_FULL) {
           // (FULL passes are bounded: each narrows the key range 128x; the cap only
           // guards against a hang)
-          const uint32_t cap = DSV_FSEL_ABLATE ? 3u : 64u;
+          const uint32_t cap = 64u;
           if (B.flag && B.nfull < cap) { next = P_FULL; n = nrange; ++B.nfull; } else { next = P_EMIT; n = nrange; }
         } else { next = P_EXIT; n = 0; }
         B.pass = next;

@@ -333,18 +333,6 @@ def copy_jobs(jobs: torch.Tensor, splits: int = 16) -> None:
     _lib.call("dsv_copy_jobs", _ptr(jobs), jobs.shape[0], int(splits), _stream())
 
 
-def copy_jobs_ce(jobs_host, stream=None) -> None:
-    """Run a host [njobs, 6] int64 job table on the copy engines (dsv_copy_jobs_ce) on
-    `stream` (default: current stream); the table must stay alive until the call returns."""
-    import numpy as np
-
-    jobs_host = np.ascontiguousarray(jobs_host, dtype=np.int64)
-    if jobs_host.ndim != 2 or jobs_host.shape[1] != 6:
-        raise ValueError("copy_jobs_ce: expected an [njobs, 6] int64 table")
-    st = (stream or torch.cuda.current_stream()).cuda_stream
-    _lib.call("dsv_copy_jobs_ce", jobs_host.ctypes.data, jobs_host.shape[0], st)
-
-
 def f32_to_bf16(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     _require_cuda(x)
     x = x.contiguous()

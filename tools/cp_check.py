@@ -1,7 +1,7 @@
 """HCP on N GPUs vs the single-GPU layer on the same inputs (torchrun, NCCL).
 
 usage: torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/cp_check.py [--skewed] [--hybrid]
-                [--gs=G] [--dense=M]
+                [--gs=G] [--dense=M] [--transport=peer|all_to_all]
 (--hybrid: g_h = N/G head groups x g_s = G (default 2) selective-sequence groups, HybridDSV;
  --dense=M: the first M heads are dense residual heads, run by the ring KV pass)
 Every rank builds the same global inputs (seeded), keeps its L/N token chunk, runs
@@ -47,8 +47,8 @@ def main():
     if hybrid:
         cp = HybridDSV(grid, H, D, r, (8, 4, 4), sp, world // gs, gs, balanced=True, device=dev)
     else:
-        ov = next((a.split("=")[1] for a in sys.argv if a.startswith("--overlap=")), False)
-        cp = HeadParallelDSV(grid, H, D, r, (8, 4, 4), sp, balanced=True, device=dev, overlap=ov)
+        tr = next((a.split("=")[1] for a in sys.argv if a.startswith("--transport=")), "auto")
+        cp = HeadParallelDSV(grid, H, D, r, (8, 4, 4), sp, balanced=True, device=dev, transport=tr)
     outs = cp.step(x[sl].contiguous(), wt, *(t[:, sl].contiguous() for t in (q, k, v, do)))
     gathered = []
     for t in outs:
