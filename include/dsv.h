@@ -132,12 +132,18 @@ int dsv_topk(const float* scores, long long ld, int rows, int L, const int* k_pe
  * accumulators; the writes hide under the gather-bound forward).
  * tile_grp (optional, int32 [G]): the G tiles are 128-query pieces of n_groups voxel groups
  * (grouping.py:22-32 ladder shapes up to 8x8x8 = 512 queries); tile g reads index row
- * tile_grp[g] of idx [H][n_groups][ldk] (and kcount_hg [H][n_groups]). NULL: tile = group. */
+ * tile_grp[g] of idx [H][n_groups][ldk] (and kcount_hg [H][n_groups]). NULL: tile = group.
+ * o_tab (optional, int64 device table [H][o_n] of addresses): each output row (h, tok) is
+ * also stored at o_tab[h*o_n + tok/o_chunk] + (tok % o_chunk) * D elements — the token
+ * owners' buffers under head-parallel CP (peer-mapped), so the output redistribution rides
+ * on the epilogue's stores (cpsim.py:284-299). dsv_sparse_bwd's dq_tab does the same for dQ
+ * (dQ is then written only there). */
 int dsv_sparse_fwd(const void* q, const void* k, const void* v, const int* grp_rows,
                    const int* grp_size, const int* idx, long long ldk, const int* kcount,
                    const int* kcount_hg, int H, int G, int Lq, int Lk, int D, float scale,
                    void* out, float* lse, unsigned* work, long long work_words, float* zero_buf,
-                   long long zero_floats, const int* tile_grp, int n_groups, void* stream);
+                   long long zero_floats, const int* tile_grp, int n_groups,
+                   const long long* o_tab, int o_n, int o_chunk, void* stream);
 
 /* Backward (K3b). dout: [H][Lq][D] bf16, out/lse from dsv_sparse_fwd. dq: [H][Lq][D] bf16
  * (every query of a group is written); dk_acc, dv_acc: [H][Lk][D] fp32 accumulators that the
@@ -147,7 +153,8 @@ int dsv_sparse_bwd(const void* q, const void* k, const void* v, const void* out,
                    const void* dout, const float* lse, const int* grp_rows, const int* grp_size,
                    const int* idx, long long ldk, const int* kcount, const int* kcount_hg, int H,
                    int G, int Lq, int Lk, int D, float scale, void* dq, float* dk_acc,
-                   float* dv_acc, unsigned* work, const int* tile_grp, int n_groups, void* stream);
+                   float* dv_acc, unsigned* work, const int* tile_grp, int n_groups,
+                   const long long* dq_tab, int dq_n, int dq_chunk, void* stream);
 
 /* Ragged per-(head, query) CSR sparse attention on CUDA cores (fp32 math), any D <= 256.
  * ptr: [H*Lq + 1] int64 offsets into cols (int32 key ids); cols == NULL selects every key
@@ -209,6 +216,11 @@ typedef struct dsv_copy_job {
  * row_bytes must be a multiple of 16 and rows * row_bytes / 16 < 2^31 per job.
  * `splits` blocks cooperate on each job (1..1024). */
 int dsv_copy_jobs(const dsv_copy_job* jobs, int njobs, int splits, void* stream);
+
+/* fp32 [H][L][D] rows -> bf16 rows at tab[h*n + tok/chunk] + (tok % chunk) * D (D = 64 or
+ * 128): the dK / dV conversion writing straight into the token owners' buffers. */
+int dsv_f32_to_bf16_rows(const float* in, int H, int L, int D, const long long* tab, int n,
+                         int chunk, void* stream);
 
 /* Peer memory for the NVLink exchanges (one process per GPU): dsv_peer_alloc returns a
  * zeroed device buffer and its 64-byte CUDA IPC handle, which a peer process maps with

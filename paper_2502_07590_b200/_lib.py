@@ -42,11 +42,11 @@ SIGNATURES = {
     "dsv_sparse_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_longlong,
                        c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_float, c_void_p,
                        c_void_p, c_void_p, c_longlong, c_void_p, c_longlong, c_void_p, c_int,
-                       c_void_p],
+                       c_void_p, c_int, c_int, c_void_p],
     "dsv_sparse_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                        c_void_p, c_void_p, c_longlong, c_void_p, c_void_p, c_int, c_int, c_int,
                        c_int, c_int, c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                       c_int, c_void_p],
+                       c_int, c_void_p, c_int, c_int, c_void_p],
     "dsv_rows_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int,
                      c_int, c_float, c_int, c_void_p, c_void_p, c_void_p],
     "dsv_rows_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
@@ -70,6 +70,7 @@ SIGNATURES = {
     "dsv_gather_rows": [c_void_p, c_longlong, c_void_p, c_int, c_int, c_void_p, c_longlong,
                         c_void_p],
     "dsv_f32_to_bf16": [c_void_p, c_void_p, c_longlong, c_void_p],
+    "dsv_f32_to_bf16_rows": [c_void_p, c_int, c_int, c_int, c_void_p, c_int, c_int, c_void_p],
     "dsv_ring_lse_merge": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_longlong, c_int,
                            c_int, c_void_p, c_void_p],
     "dsv_ring_accum_bf16": [c_void_p, c_void_p, c_longlong, c_int, c_void_p, c_void_p],

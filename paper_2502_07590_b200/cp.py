@@ -435,6 +435,31 @@ class PeerExchange:
             jobs.append(j)
         return np.ascontiguousarray(np.concatenate(jobs))
 
+    def rows(self, name: str):
+        """(tab int64 [my_heads * world], world, chunk): where row (local head hi, token t) of a
+        [my_heads, L, D] result lands in its token owner's `name` region — the address table the
+        fused epilogues (dsv_sparse_fwd o_tab, dsv_sparse_bwd dq_tab, dsv_f32_to_bf16_rows) store
+        through, so the output redistribution needs no separate copy."""
+        rt = self.__dict__.setdefault("_row_tabs", {})      # kept for the exchange's lifetime
+        t = rt.get(name)
+        if t is None:
+            hs = self.my_heads.astype(np.int64)
+            tab = (self.ptrs[None, :] + 2 * (self.off[name] + hs[:, None] * self.chunk * self.D)
+                   ).reshape(-1)
+            t = rt[name] = torch.from_numpy(np.ascontiguousarray(tab)).to(self.buf.device)
+        return t, self.world, self.chunk
+
+    def begin_tokens(self):
+        """Fused output redistribution: the kernels about to run store into the token owners'
+        regions (every rank is past the previous step: the to_heads barrier ordered that)."""
+
+    def finish_tokens(self):
+        """After the fused epilogues: a device barrier publishes the peer stores; returns the
+        views O, dQ, dK, dV [H, L/N, D] of this rank's tokens."""
+        self._barrier()
+        self._account(("output_redistribute", self.D), ("hcp_bwd_out", 3 * self.D), to_heads=False)
+        return tuple(self.region(n) for n in ("o", "dq", "dk", "dv"))
+
     def _host_table(self, key, build):
         t = self._tables.get(key)
         if t is None:
@@ -805,7 +830,7 @@ class HeadParallelDSV(_PhaseMarks):
 
     def __init__(self, grid, heads: int, head_dim: int, d_lr: int = 16, voxel=(8, 4, 4),
                  sparsity=0.9, balanced: bool = True, group=None, device="cuda",
-                 transport: str = "auto"):
+                 transport: str = "auto", fused_out: bool | None = None):
         from .layer import DSVAttentionLayer
 
         self.world = dist.get_world_size(group)
@@ -816,6 +841,11 @@ class HeadParallelDSV(_PhaseMarks):
         if transport not in ("peer", "all_to_all"):
             raise ValueError(f"unknown transport {transport!r}")
         self.transport = transport
+        # peer transport: the output redistribution rides on the kernels' epilogue stores
+        # (DSV_FUSED_OUT=0 keeps the separate copy kernel for comparison)
+        if fused_out is None:
+            fused_out = os.environ.get("DSV_FUSED_OUT", "1") != "0"
+        self.fused_out = bool(fused_out) and transport == "peer"
         if transport == "peer":
             self.ex = PeerExchange(heads, grid.size, head_dim, d_lr, self.assignment, group, device)
         else:
@@ -879,11 +909,24 @@ class HeadParallelDSV(_PhaseMarks):
         self._mark("exchange_in")
         sel = loc.select_from_lowrank(qlr, klr)
         self._mark("select")
+        ex = self.ex
+        if self.fused_out:
+            # output redistribution fused into the kernels: the forward epilogue also stores O
+            # at the token owners, the backward's dQ epilogue and the dK / dV conversion store
+            # there directly (NVLink peer stores), then one device barrier
+            out, lse = loc.forward(ql, kl, vl, sel, out_rows=ex.rows("o"))
+            self._mark("fwd")
+            loc.backward(ql, kl, vl, out, lse, dout_m, sel, dq_rows=ex.rows("dq"),
+                         dkdv_rows=(ex.rows("dk"), ex.rows("dv")))
+            self._mark("bwd")
+            res = ex.finish_tokens()
+            self._mark("exchange_out")
+            return res
         out, lse = loc.forward(ql, kl, vl, sel)
         self._mark("fwd")
         dq, dk, dv = loc.backward(ql, kl, vl, out, lse, dout_m, sel)
         self._mark("bwd")
-        res = self.ex.to_tokens(out, dq, dk, dv)
+        res = ex.to_tokens(out, dq, dk, dv)
         self._mark("exchange_out")
         return res
 
@@ -909,7 +952,7 @@ class HybridDSV(_PhaseMarks):
 
     def __init__(self, grid, heads: int, head_dim: int, d_lr: int, voxel, sparsity, g_h: int,
                  g_s: int, balanced: bool = True, group=None, device="cuda", dense=None,
-                 transport: str = "auto"):
+                 transport: str = "auto", fused_out: bool | None = None):
         from .grouping import build_groups
         from .layer import DSVAttentionLayer
         from .ring import RingKV

@@ -239,6 +239,20 @@ DSV_DEV float softmax_p_pass(uint32_t tS, float scale_log2, float m, int kv) {
 // Index-list row of a (head, tile): tiles are the 128-query pieces of the voxel groups; a group
 // larger than 128 queries spans several tiles that share its row (tile_grp: tile -> group,
 // nullptr = one tile per group), so idx / kcount_hg are [H, Gs, ...] over the Gs groups.
+// Rows written to other ranks' buffers (HCP output redistribution fused into the kernels'
+// epilogues): row (h, tok) of a [H, L, D] bf16 result goes to tab[h * n + tok / chunk] +
+// (tok % chunk) * D — peer-mapped addresses of the token owners' regions. tab == nullptr:
+// not used.
+struct RowOut {
+  const long long* tab;
+  int n, chunk;
+};
+template <int D>
+DSV_DEV __nv_bfloat16* row_out(const RowOut& ro, int h, int tok) {
+  const int o = tok / ro.chunk;
+  return reinterpret_cast<__nv_bfloat16*>(ro.tab[h * ro.n + o]) + (long long)(tok - o * ro.chunk) * D;
+}
+
 DSV_DEV long long sel_row(int tile, int G, const int* tile_grp, int Gs) {
   const int h = tile / G, g = tile - h * G;
   return (long long)h * Gs + (tile_grp ? __ldg(tile_grp + g) : g);
@@ -254,7 +268,7 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
                   float* __restrict__ lse, int n_tiles, const unsigned* __restrict__ list,
                   unsigned* __restrict__ ovf_list, unsigned* __restrict__ sched,
                   float4* __restrict__ zero_buf, long long zero_n4,
-                  const int* __restrict__ tile_grp, int Gs) {
+                  const int* __restrict__ tile_grp, int Gs, RowOut oremote) {
   using SL = FwdSmem<D>;
   using GT = Gather<D>;
   constexpr int ST = kFwdStages, KST = kFwdKStages, NS = kFwdSBufs;
@@ -554,6 +568,7 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
     const int gsz = grp_size[g];
     const int tok = mrow[row];
     __nv_bfloat16* orow = O + ((long long)h * Lq + tok) * D;
+    __nv_bfloat16* rrow = oremote.tab ? row_out<D>(oremote, h, tok) : nullptr;
 #pragma unroll 1
     for (int c = cq * kOc; c < (cq + 1) * kOc; c += 16) {
       uint32_t o[16];
@@ -561,12 +576,15 @@ sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
       tmem_ld_wait();
       if (row < gsz) {
 #pragma unroll
-        for (int i = 0; i < 16; i += 8)
-          *reinterpret_cast<uint4*>(orow + c + i) =
+        for (int i = 0; i < 16; i += 8) {
+          const uint4 pk =
               make_uint4(pack_bf16(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv),
                          pack_bf16(__uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv),
                          pack_bf16(__uint_as_float(o[i + 4]) * inv, __uint_as_float(o[i + 5]) * inv),
                          pack_bf16(__uint_as_float(o[i + 6]) * inv, __uint_as_float(o[i + 7]) * inv));
+          *reinterpret_cast<uint4*>(orow + c + i) = pk;
+          if (rrow) *reinterpret_cast<uint4*>(rrow + c + i) = pk;   // the token owner (NVLink)
+        }
       }
     }
     if (cq == 0 && row < gsz) lse[(long long)h * Lq + tok] = m_run + __log2f(denom);
@@ -659,7 +677,7 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
                   float scale_log2,
                   __nv_bfloat16* __restrict__ dQ, float* __restrict__ dK, float* __restrict__ dV,
                   int n_tiles, unsigned* __restrict__ sched, const int* __restrict__ tile_grp,
-                  int Gs) {
+                  int Gs, RowOut dqremote) {
   using SL = BwdSmem<D>;
   using GT = Gather<D, kBwdLoadThreads>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -995,7 +1013,8 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
       mbar_arrive(&B.stg_full[1]);
     }
     // ---------------- dQ epilogue (query rows); the last mma_done covered dQ
-    __nv_bfloat16* qrow = dQ + ((long long)h * Lq + tok) * D;
+    __nv_bfloat16* qrow = dqremote.tab ? row_out<D>(dqremote, h, tok)   // the token owner
+                                       : dQ + ((long long)h * Lq + tok) * D;
 #pragma unroll 1
     for (int c = cg; c < D / 32; c += 4) {
       uint32_t r[32];
@@ -1032,6 +1051,25 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* 
   }
 }
 
+// fp32 [H, L, D] rows -> bf16 rows at their token owners (RowOut), one warp per row (D = 64
+// or 128: 2 or 4 floats per lane).
+template <int D>
+__global__ void f32_to_bf16_rows_kernel(const float* __restrict__ in, long long rows, int L,
+                                        RowOut out) {
+  const long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const int h = (int)(r / L), tok = (int)(r - (long long)h * L);
+  __nv_bfloat16* dst = row_out<D>(out, h, tok);
+  if constexpr (D == 128) {
+    const float4 v = reinterpret_cast<const float4*>(in + r * D)[lane];
+    reinterpret_cast<uint2*>(dst)[lane] = make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+  } else {
+    const float2 v = reinterpret_cast<const float2*>(in + r * D)[lane];
+    reinterpret_cast<uint32_t*>(dst)[lane] = pack_bf16(v.x, v.y);
+  }
+}
+
 }  // namespace attn
 }  // namespace dsv
 
@@ -1042,7 +1080,7 @@ static int fwd_launch(const void* q, const void* k, const void* v, const int* gr
                       const int* grp_size, const int* idx, long long ldk, const int* kcount,
                       const int* kcount_hg, int H, int G, int Lq, int Lk, float scale_log2, void* O,
                       float* lse, unsigned* work, float* zero_buf, long long zero_floats,
-                      const int* tile_grp, int Gs, cudaStream_t st) {
+                      const int* tile_grp, int Gs, RowOut oremote, cudaStream_t st) {
   auto kern = sparse_fwd_kernel<D>;
   const int smem = FwdSmem<D>::kBytes;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1067,14 +1105,14 @@ static int fwd_launch(const void* q, const void* k, const void* v, const int* gr
                                      kcount, kcount_hg, G, Lq, Lk, scale_log2,
                                      (__nv_bfloat16*)O, lse, n_tiles, nullptr, work, sched,
                                      reinterpret_cast<float4*>(zero_buf), zero_floats / 4,
-                                     tile_grp, Gs);
+                                     tile_grp, Gs, oremote);
   // tiles flagged by the lazy max: exact per-block max (CTAs exit at once when none)
   const int g2 = n_tiles < sms ? n_tiles : sms;
   kern<<<g2, kFwdThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
                                    (const __nv_bfloat16*)v, grp_rows, grp_size, idx, ldk,
                                    kcount, kcount_hg, G, Lq, Lk, scale_log2,
                                    (__nv_bfloat16*)O, lse, n_tiles, work, nullptr, nullptr,
-                                   nullptr, 0, tile_grp, Gs);
+                                   nullptr, 0, tile_grp, Gs, oremote);
   return (int)cudaGetLastError();
 }
 
@@ -1083,13 +1121,14 @@ int dsv_attn_fwd_tc_launch(const void* q, const void* k, const void* v, const in
                            const int* kcount_hg, int H, int G, int Lq, int Lk, int D,
                            float scale_log2, void* O, float* lse, unsigned* work,
                            float* zero_buf, long long zero_floats, const int* tile_grp, int Gs,
-                           cudaStream_t st) {
+                           const long long* o_tab, int o_n, int o_chunk, cudaStream_t st) {
+  const RowOut ro{o_tab, o_n, o_chunk};
   if (D == 128)
     return fwd_launch<128>(q, k, v, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H, G, Lq, Lk,
-                           scale_log2, O, lse, work, zero_buf, zero_floats, tile_grp, Gs, st);
+                           scale_log2, O, lse, work, zero_buf, zero_floats, tile_grp, Gs, ro, st);
   if (D == 64)
     return fwd_launch<64>(q, k, v, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H, G, Lq, Lk,
-                          scale_log2, O, lse, work, zero_buf, zero_floats, tile_grp, Gs, st);
+                          scale_log2, O, lse, work, zero_buf, zero_floats, tile_grp, Gs, ro, st);
   return 1;
 }
 
@@ -1099,7 +1138,7 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* O
                       long long ldk, const int* kcount, const int* kcount_hg, int H, int G, int Lq,
                       int Lk, float scale,
                       float scale_log2, void* dQ, float* dK, float* dV, unsigned* sched,
-                      const int* tile_grp, int Gs, cudaStream_t st) {
+                      const int* tile_grp, int Gs, RowOut dqremote, cudaStream_t st) {
   auto kern = sparse_bwd_kernel<D>;
   const int smem = BwdSmem<D>::kBytes;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1120,7 +1159,8 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* O
                                       (const __nv_bfloat16*)k, (const __nv_bfloat16*)v,
                                       (const __nv_bfloat16*)O, lse, grp_rows, grp_size, idx, ldk,
                                       kcount, kcount_hg, G, Lq, Lk, scale, scale_log2,
-                                      (__nv_bfloat16*)dQ, dK, dV, n_tiles, sched, tile_grp, Gs);
+                                      (__nv_bfloat16*)dQ, dK, dV, n_tiles, sched, tile_grp, Gs,
+                                      dqremote);
   return (int)cudaGetLastError();
 }
 
@@ -1129,13 +1169,15 @@ int dsv_attn_bwd_tc_launch(const void* q, const void* k, const void* v, const vo
                            const int* grp_size, const int* idx, long long ldk, const int* kcount,
                            const int* kcount_hg, int H, int G, int Lq, int Lk, int D, float scale,
                            float scale_log2, void* dQ, float* dK, float* dV, unsigned* sched,
-                           const int* tile_grp, int Gs, cudaStream_t st) {
+                           const int* tile_grp, int Gs, const long long* dq_tab, int dq_n,
+                           int dq_chunk, cudaStream_t st) {
+  const RowOut ro{dq_tab, dq_n, dq_chunk};
   if (D == 128)
     return bwd_launch<128>(q, k, v, O, dO, lse, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H,
-                           G, Lq, Lk, scale, scale_log2, dQ, dK, dV, sched, tile_grp, Gs, st);
+                           G, Lq, Lk, scale, scale_log2, dQ, dK, dV, sched, tile_grp, Gs, ro, st);
   if (D == 64)
     return bwd_launch<64>(q, k, v, O, dO, lse, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H,
-                          G, Lq, Lk, scale, scale_log2, dQ, dK, dV, sched, tile_grp, Gs, st);
+                          G, Lq, Lk, scale, scale_log2, dQ, dK, dV, sched, tile_grp, Gs, ro, st);
   return 1;
 }
 
@@ -1143,6 +1185,18 @@ int dsv_debug_timeline_copy(void* dst, int bytes) {
   const int n = (int)sizeof(g_bwd_prof) < bytes ? (int)sizeof(g_bwd_prof) : bytes;
   if (cudaMemcpyFromSymbol(dst, g_bwd_prof, n) != cudaSuccess) return -1;
   return n;
+}
+
+int dsv_f32_to_bf16_rows_launch(const float* in, int H, int L, int D, const long long* tab, int n,
+                                int chunk, cudaStream_t st) {
+  const long long rows = (long long)H * L;
+  if (rows <= 0) return 0;
+  const RowOut ro{tab, n, chunk};
+  const unsigned blocks = (unsigned)((rows * 32 + 255) / 256);
+  if (D == 128) f32_to_bf16_rows_kernel<128><<<blocks, 256, 0, st>>>(in, rows, L, ro);
+  else if (D == 64) f32_to_bf16_rows_kernel<64><<<blocks, 256, 0, st>>>(in, rows, L, ro);
+  else return 1;
+  return (int)cudaGetLastError();
 }
 
 int dsv_f32_to_bf16_launch(const float* in, void* out, long long n, cudaStream_t st) {

@@ -33,11 +33,14 @@ int dsv_gemm_launch(const CUtensorMap*, const CUtensorMap*, const CUtensorMap*, 
 int dsv_attn_fwd_tc_launch(const void*, const void*, const void*, const int*, const int*,
                            const int*, long long, const int*, const int*, int, int, int, int, int,
                            float, void*, float*, unsigned*, float*, long long, const int*, int,
-                           cudaStream_t);
+                           const long long*, int, int, cudaStream_t);
 int dsv_attn_bwd_tc_launch(const void*, const void*, const void*, const void*, const void*,
                            const float*, const int*, const int*, const int*, long long,
                            const int*, const int*, int, int, int, int, int, float, float, void*,
-                           float*, float*, unsigned*, const int*, int, cudaStream_t);
+                           float*, float*, unsigned*, const int*, int, const long long*, int, int,
+                           cudaStream_t);
+int dsv_f32_to_bf16_rows_launch(const float*, int, int, int, const long long*, int, int,
+                                cudaStream_t);
 int dsv_f32_to_bf16_launch(const float*, void*, long long, cudaStream_t);
 int dsv_select_fused_launch(const CUtensorMap*, const CUtensorMap*, int, int, int, const int*, int*,
                             long long, float*, int, void*, long long, cudaStream_t);
@@ -281,8 +284,11 @@ int dsv_sparse_fwd(const void* q, const void* k, const void* v, const int* grp_r
                    const int* grp_size, const int* idx, long long ldk, const int* kcount,
                    const int* kcount_hg, int H, int G, int Lq, int Lk, int D, float scale,
                    void* out, float* lse, unsigned* work, long long work_words, float* zero_buf,
-                   long long zero_floats, const int* tile_grp, int n_groups, void* stream) {
+                   long long zero_floats, const int* tile_grp, int n_groups,
+                   const long long* o_tab, int o_n, int o_chunk, void* stream) {
   if (D != 64 && D != 128) return fail(DSV_EUNSUPPORTED, "sparse_fwd: head dim %d not 64/128", D);
+  if (o_tab && (o_n < 1 || o_chunk < 1 || (long long)o_n * o_chunk < Lq))
+    return fail(DSV_EINVAL, "sparse_fwd: o_tab needs n * chunk >= Lq");
   if (tile_grp && n_groups <= 0) return fail(DSV_EINVAL, "sparse_fwd: tile_grp needs n_groups > 0");
   if (H <= 0 || G <= 0 || Lq <= 0 || Lk <= 0 || ldk < 0)
     return fail(DSV_EINVAL, "sparse_fwd: empty shape");
@@ -296,7 +302,8 @@ int dsv_sparse_fwd(const void* q, const void* k, const void* v, const int* grp_r
   return cuda_status(dsv_attn_fwd_tc_launch(q, k, v, grp_rows, grp_size, idx, ldk, kcount,
                                             kcount_hg, H, G, Lq, Lk, D, scale_log2, out, lse,
                                             work, zero_buf, zero_buf ? zero_floats : 0, tile_grp,
-                                            tile_grp ? n_groups : G, S(stream)),
+                                            tile_grp ? n_groups : G, o_tab, o_n, o_chunk,
+                                            S(stream)),
                      "sparse_fwd launch");
 }
 
@@ -304,8 +311,11 @@ int dsv_sparse_bwd(const void* q, const void* k, const void* v, const void* out,
                    const void* dout, const float* lse, const int* grp_rows, const int* grp_size,
                    const int* idx, long long ldk, const int* kcount, const int* kcount_hg, int H,
                    int G, int Lq, int Lk, int D, float scale, void* dq, float* dk_acc,
-                   float* dv_acc, unsigned* work, const int* tile_grp, int n_groups, void* stream) {
+                   float* dv_acc, unsigned* work, const int* tile_grp, int n_groups,
+                   const long long* dq_tab, int dq_n, int dq_chunk, void* stream) {
   if (D != 64 && D != 128) return fail(DSV_EUNSUPPORTED, "sparse_bwd: head dim %d not 64/128", D);
+  if (dq_tab && (dq_n < 1 || dq_chunk < 1 || (long long)dq_n * dq_chunk < Lq))
+    return fail(DSV_EINVAL, "sparse_bwd: dq_tab needs n * chunk >= Lq");
   if (tile_grp && n_groups <= 0) return fail(DSV_EINVAL, "sparse_bwd: tile_grp needs n_groups > 0");
   if (H <= 0 || G <= 0 || Lq <= 0 || Lk <= 0 || ldk < 0)
     return fail(DSV_EINVAL, "sparse_bwd: empty shape");
@@ -317,7 +327,8 @@ int dsv_sparse_bwd(const void* q, const void* k, const void* v, const void* out,
   return cuda_status(dsv_attn_bwd_tc_launch(q, k, v, out, dout, lse, grp_rows, grp_size, idx, ldk,
                                             kcount, kcount_hg, H, G, Lq, Lk, D, scale, scale_log2,
                                             dq, dk_acc, dv_acc, work, tile_grp,
-                                            tile_grp ? n_groups : G, S(stream)),
+                                            tile_grp ? n_groups : G, dq_tab, dq_n, dq_chunk,
+                                            S(stream)),
                      "sparse_bwd launch");
 }
 
@@ -340,6 +351,15 @@ int dsv_rows_bwd(const void* q, const void* k, const void* v, const float* out, 
   return cuda_status(dsv_rows_bwd_launch(q, k, v, out, lse, dout, ptr, cols, H, Lq, Lk, D, scale,
                                          in_dtype == DSV_DTYPE_BF16, dq, dk_acc, dv_acc, S(stream)),
                      "rows_bwd launch");
+}
+
+int dsv_f32_to_bf16_rows(const float* in, int H, int L, int D, const long long* tab, int n,
+                         int chunk, void* stream) {
+  if (D != 64 && D != 128) return fail(DSV_EUNSUPPORTED, "f32_to_bf16_rows: D must be 64 or 128");
+  if (!in || !tab || n < 1 || chunk < 1 || (long long)n * chunk < L)
+    return fail(DSV_EINVAL, "f32_to_bf16_rows: bad arguments");
+  return cuda_status(dsv_f32_to_bf16_rows_launch(in, H, L, D, tab, n, chunk, S(stream)),
+                     "f32_to_bf16_rows launch");
 }
 
 int dsv_f32_to_bf16(const float* in, void* out, long long n, void* stream) {

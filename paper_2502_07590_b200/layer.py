@@ -154,21 +154,24 @@ class DSVAttentionLayer:
         return max(1, min(self.H, budget // per_head))
 
     # ------------------------------------------------------------- attention
-    def forward(self, q, k, v, sel: SelectedKV, prepare_backward: bool = True):
+    def forward(self, q, k, v, sel: SelectedKV, prepare_backward: bool = True, out_rows=None):
         """Sparse forward. prepare_backward: the kernel also zeroes the layer's dK/dV
         accumulators for the coming backward (HBM writes hidden under the gather-bound
-        forward instead of a separate fill pass)."""
+        forward instead of a separate fill pass). out_rows: (tab, n, chunk) row addresses the
+        epilogue also stores O at (the token owners under head-parallel CP)."""
         zero = None
         if prepare_backward:
             zero = self._accumulators(k.shape[1], k.device)
             self._acc_zeroed = True
         return ops.sparse_fwd(q, k, v, self.grp_rows, self.grp_size, sel.idx, sel.kcount,
-                              self.scale, zero=zero, tile_grp=self.tile_grp)
+                              self.scale, zero=zero, tile_grp=self.tile_grp, out_rows=out_rows)
 
     def backward(self, q, k, v, out, lse, dout, sel: SelectedKV, dk_acc=None, dv_acc=None,
-                 kernel_done=None):
+                 kernel_done=None, dq_rows=None, dkdv_rows=None):
         """-> (dq, dk, dv) bf16. Without caller accumulators the layer's own are used (zeroed
-        by the preceding forward, or here if that did not happen)."""
+        by the preceding forward, or here if that did not happen). dq_rows / dkdv_rows:
+        (tab, n, chunk) row addresses dQ / (dK, dV) go to instead (the token owners under
+        head-parallel CP); the corresponding results are then None."""
         if dk_acc is None:
             acc = self._accumulators(k.shape[1], k.device)
             if not getattr(self, "_acc_zeroed", False):
@@ -180,10 +183,14 @@ class DSVAttentionLayer:
             dv_acc.zero_()
         dq, dk32, dv32 = ops.sparse_bwd(q, k, v, out, dout, lse, self.grp_rows, self.grp_size,
                                         sel.idx, sel.kcount, self.scale, dk_acc, dv_acc,
-                                        tile_grp=self.tile_grp)
+                                        tile_grp=self.tile_grp, dq_rows=dq_rows)
         if kernel_done is not None:          # optional CUDA event after the kernel (timing)
             kernel_done.record()
-        return dq, ops.f32_to_bf16(dk32), ops.f32_to_bf16(dv32)
+        if dkdv_rows is not None:
+            ops.f32_to_bf16_rows(dk32, dkdv_rows[0])
+            ops.f32_to_bf16_rows(dv32, dkdv_rows[1])
+            return (None if dq_rows is not None else dq), None, None
+        return (None if dq_rows is not None else dq), ops.f32_to_bf16(dk32), ops.f32_to_bf16(dv32)
 
     def _accumulators(self, n_keys: int, device):
         """The layer's fp32 dK/dV accumulators [2, H, n_keys, D] (one contiguous buffer)."""

@@ -210,7 +210,7 @@ def select_fused(q_prox: torch.Tensor, k_lr: torch.Tensor, k_per_head: torch.Ten
 
 # ------------------------------------------------------------------- K3 attention
 def sparse_fwd(q, k, v, grp_rows, grp_size, idx, kcount, scale=None, kcount_hg=None, zero=None,
-               tile_grp=None):
+               tile_grp=None, out_rows=None):
     """Group-tiled sparse attention forward. q: [H, Lq, D], k/v: [H, Lk, D] bf16.
 
     grp_rows int32 [G, 128], grp_size int32 [G], idx int32 [H, G, ldk], kcount int32 [H]
@@ -219,6 +219,8 @@ def sparse_fwd(q, k, v, grp_rows, grp_size, idx, kcount, scale=None, kcount_hg=N
     dK/dV accumulators).
     tile_grp: optional int32 [G] tile -> voxel group map (groups of more than 128 queries span
     several tiles that share the group's idx row; idx / kcount_hg are then per group).
+    out_rows: optional (tab int64 [H * n], n, chunk): output rows are also stored at the token
+    owners' addresses (fused HCP output redistribution).
     """
     _require_cuda(q, k, v, grp_rows, grp_size, idx, kcount)
     if zero is not None and (zero.dtype != torch.float32 or not zero.is_contiguous()):
@@ -235,12 +237,21 @@ def sparse_fwd(q, k, v, grp_rows, grp_size, idx, kcount, scale=None, kcount_hg=N
               _ptr(idx), idx.stride(1), _ptr(kcount), _ptr(kcount_hg), H, G, Lq, Lk, D,
               float(scale), _ptr(out), _ptr(lse), _ptr(work), work.numel(), _ptr(zero),
               0 if zero is None else zero.numel(), _ptr(tile_grp),
-              0 if tile_grp is None else idx.shape[1], _stream())
+              0 if tile_grp is None else idx.shape[1], *_rows_args(out_rows), _stream())
     return out, lse
 
 
+def _rows_args(rows):
+    if rows is None:
+        return 0, 0, 0
+    tab, n, chunk = rows
+    if tab.dtype != torch.int64 or not tab.is_cuda:
+        raise ValueError("row table must be an int64 CUDA tensor")
+    return tab.data_ptr(), int(n), int(chunk)
+
+
 def sparse_bwd(q, k, v, out, dout, lse, grp_rows, grp_size, idx, kcount, scale=None,
-               dk_acc=None, dv_acc=None, kcount_hg=None, tile_grp=None):
+               dk_acc=None, dv_acc=None, kcount_hg=None, tile_grp=None, dq_rows=None):
     """Backward of sparse_fwd. Returns (dq bf16, dk_acc fp32, dv_acc fp32)."""
     _require_cuda(q, k, v, out, dout, lse)
     H, Lq, D = q.shape
@@ -257,7 +268,8 @@ def sparse_bwd(q, k, v, out, dout, lse, grp_rows, grp_size, idx, kcount, scale=N
     _lib.call("dsv_sparse_bwd", _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(dout), _ptr(lse),
               _ptr(grp_rows), _ptr(grp_size), _ptr(idx), idx.stride(1), _ptr(kcount),
               _ptr(kcount_hg), H, G, Lq, Lk, D, float(scale), _ptr(dq), _ptr(dk_acc), _ptr(dv_acc),
-              _ptr(work), _ptr(tile_grp), 0 if tile_grp is None else idx.shape[1], _stream())
+              _ptr(work), _ptr(tile_grp), 0 if tile_grp is None else idx.shape[1],
+              *_rows_args(dq_rows), _stream())
     return dq, dk_acc, dv_acc
 
 
@@ -331,6 +343,16 @@ def copy_jobs(jobs: torch.Tensor, splits: int = 16) -> None:
     if jobs.dtype != torch.int64 or jobs.dim() != 2 or jobs.shape[1] != 6 or not jobs.is_contiguous():
         raise ValueError("copy_jobs: expected a contiguous [njobs, 6] int64 table")
     _lib.call("dsv_copy_jobs", _ptr(jobs), jobs.shape[0], int(splits), _stream())
+
+
+def f32_to_bf16_rows(x: torch.Tensor, rows) -> None:
+    """fp32 [H, L, D] -> bf16 rows at the (tab, n, chunk) addresses (dsv_f32_to_bf16_rows)."""
+    _require_cuda(x)
+    if x.dtype != torch.float32 or x.dim() != 3 or not x.is_contiguous():
+        raise ValueError("f32_to_bf16_rows expects a contiguous fp32 [H, L, D] tensor")
+    tab, n, chunk = _rows_args(rows)
+    _lib.call("dsv_f32_to_bf16_rows", _ptr(x), x.shape[0], x.shape[1], x.shape[2], tab, n, chunk,
+              _stream())
 
 
 def f32_to_bf16(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:

@@ -43,5 +43,5 @@ def test_invalid_arguments_are_reported_not_launched():
     assert rc == _lib.DSV_EINVAL
     assert b"topk" in lib.dsv_last_error()
     rc = lib.dsv_sparse_fwd(None, None, None, None, None, None, 1, None, None, 1, 1, 1, 1, 96,
-                            ctypes.c_float(0.1), None, None, None, 0, None, 0, None, 0, None)
+                            ctypes.c_float(0.1), None, None, None, 0, None, 0, None, 0, None, 0, 0, None)
     assert rc == _lib.DSV_EUNSUPPORTED
