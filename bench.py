@@ -372,8 +372,8 @@ def run_gpu(args) -> None:
     if world > 1:
         dist.barrier()
     eager_step = step
-    if args.graph and (args.scp > 1 or args.dense_heads):
-        args.graph = False   # the hybrid layer sizes its selective exchanges on the host
+    if args.graph and args.dense_heads:
+        args.graph = False   # the ring KV pass issues host-sized NCCL P2P hops
     if args.graph:
         # one CUDA graph per step: the host issues one launch instead of ~20 kernels
         graph = torch.cuda.CUDAGraph()
@@ -494,6 +494,9 @@ def run_gpu(args) -> None:
                + " via HostPipeline (pinned H2D of step i+1 and D2H of step i-1's O, dQ, dK, dV "
                  "overlap step i; full-duplex PCIe)"}
 
+    if args.graph:
+        del graph                        # release the captured graph before the groups go
+        torch.cuda.synchronize()
     if rank != 0:
         if world > 1:
             dist.barrier()

@@ -217,6 +217,21 @@ typedef struct dsv_copy_job {
  * `splits` blocks cooperate on each job (1..1024). */
 int dsv_copy_jobs(const dsv_copy_job* jobs, int njobs, int splits, void* stream);
 
+/* Selective KV gathering (SCP, cpsim.py:164-216) over NVLink, one-sided: each rank of an SCP
+ * group holds full-length buffers [hs][L][D] addressed by global token (K, V bf16; dK, dV
+ * fp32) whose addresses in this process are peer_*[g] for group member g (member g owns the
+ * tokens [g*span_len, (g+1)*span_len)). mark (bool [hs][L]) = the keys this rank's span
+ * selected. dsv_scp_pull copies every marked (head, key) row outside [span0, span0+span_len)
+ * from its owner's K/V buffers into k_full / v_full (count += rows, optional);
+ * dsv_scp_push adds the same rows of dk_full / dv_full into the owners' accumulators
+ * (red.add over NVLink). No host round trip: graph-capturable. */
+int dsv_scp_pull(const unsigned char* mark, int hs, int L, int span0, int span_len,
+                 const long long* peer_k, const long long* peer_v, void* k_full, void* v_full,
+                 int D, unsigned long long* count, void* stream);
+int dsv_scp_push(const unsigned char* mark, int hs, int L, int span0, int span_len,
+                 const long long* peer_dk, const long long* peer_dv, void* dk_full, void* dv_full,
+                 int D, void* stream);
+
 /* fp32 [H][L][D] rows -> bf16 rows at tab[h*n + tok/chunk] + (tok % chunk) * D (D = 64 or
  * 128): the dK / dV conversion writing straight into the token owners' buffers. */
 int dsv_f32_to_bf16_rows(const float* in, int H, int L, int D, const long long* tab, int n,

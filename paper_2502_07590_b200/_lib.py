@@ -62,6 +62,10 @@ SIGNATURES = {
                           c_void_p],
     "dsv_critical_counts": [c_void_p, c_longlong, c_int, c_int, ctypes.c_double, ctypes.c_double,
                             c_void_p, c_void_p],
+    "dsv_scp_pull": [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
+                     c_int, c_void_p, c_void_p],
+    "dsv_scp_push": [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
+                     c_int, c_void_p],
     "dsv_peer_alloc": [c_longlong, c_void_p, c_void_p],
     "dsv_peer_open": [c_void_p, c_void_p],
     "dsv_peer_close": [c_void_p],

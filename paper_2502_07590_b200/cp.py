@@ -274,6 +274,67 @@ class _PeerBuffer:
             pass
 
 
+class ScpPeerBuffers:
+    """Selective KV gathering over NVLink for one rank of an SCP group (the g_s ranks holding
+    the same heads; member g owns the tokens [g span, (g+1) span)). Full-length per-head
+    buffers addressed by global token — K, V bf16 and dK, dV fp32 [hs, L, D] — are mapped
+    into every member (CUDA IPC through libdsv). A member pulls the marked remote K/V rows
+    straight from their owners' buffers (dsv_scp_pull, NVLink loads) and pushes the
+    gradients of those rows into the owners' accumulators (dsv_scp_push, red.add over
+    NVLink); device barriers order the phases. Counts stay on the device, so the step is
+    graph-capturable (the all-to-all form in HybridExchange reads them back to size its
+    collectives)."""
+
+    def __init__(self, hs: int, seq_len: int, head_dim: int, d_lr: int, group, device):
+        self.group = group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        n = hs * seq_len * head_dim
+        nl = hs * seq_len * d_lr
+        self.hs, self.L, self.D, self.r = hs, seq_len, head_dim, d_lr
+        self.off = {"k": 0, "v": 2 * n, "dk": 4 * n, "dv": 8 * n, "klr": 12 * n,
+                    "slots": 12 * n + 2 * nl}
+        nbytes = 12 * n + 2 * nl + 4 * (self.world + 1) + 256
+        self.peer = _PeerBuffer(nbytes, group, device)
+        b = self.peer.tensor                                   # bf16 view of the whole buffer
+        shape = (hs, seq_len, head_dim)
+        self.k = b[0:n].view(shape)
+        self.v = b[n:2 * n].view(shape)
+        self.acc = b[2 * n:6 * n].view(torch.float32).view((2,) + shape)   # dK, dV fp32
+        self.klr = b[6 * n:6 * n + nl].view(hs, seq_len, d_lr)            # K_lr, all keys
+        ptrs = np.asarray(self.peer.ptrs, dtype=np.int64)
+        dev = b.device
+        # the peers' K_lr regions as tensors of this process (NVLink reads by torch copies)
+        self.peer_klr = [self.klr if g == self.rank else
+                         torch.as_tensor(_CudaArray(int(ptrs[g]) + self.off["klr"], nl),
+                                         device=dev).view(torch.bfloat16).view(hs, seq_len, d_lr)
+                         for g in range(self.world)]
+        self.peer_tab = {name: torch.from_numpy(ptrs + off).to(dev)
+                         for name, off in self.off.items()}
+        so = self.off["slots"]
+        self._slots_tab = self.peer_tab["slots"]
+        self._my_slots = int(ptrs[self.rank]) + so
+        self._epoch = self._my_slots + 4 * self.world
+        self.pulled = torch.zeros((1,), dtype=torch.int64, device=dev)   # rows fetched (ledger)
+        torch.cuda.synchronize(dev)
+        dist.barrier(group)
+
+    def barrier(self):
+        _lib.call("dsv_peer_barrier", self._slots_tab.data_ptr(), self._my_slots, self._epoch,
+                  self.world, self.rank, torch.cuda.current_stream(self.k.device).cuda_stream)
+
+    def pull(self, mark, span0: int, span_len: int):
+        st = torch.cuda.current_stream(self.k.device).cuda_stream
+        _lib.call("dsv_scp_pull", mark.data_ptr(), self.hs, self.L, span0, span_len,
+                  self.peer_tab["k"].data_ptr(), self.peer_tab["v"].data_ptr(), self.k.data_ptr(),
+                  self.v.data_ptr(), self.D, self.pulled.data_ptr(), st)
+
+    def push(self, mark, span0: int, span_len: int):
+        st = torch.cuda.current_stream(self.k.device).cuda_stream
+        _lib.call("dsv_scp_push", mark.data_ptr(), self.hs, self.L, span0, span_len,
+                  self.peer_tab["dk"].data_ptr(), self.peer_tab["dv"].data_ptr(),
+                  self.acc[0].data_ptr(), self.acc[1].data_ptr(), self.D, st)
+
+
 class PeerExchange:
     """HCP exchange over NVLink peer memory (one process per GPU, B200 NVSwitch).
 
@@ -994,6 +1055,11 @@ class HybridDSV(_PhaseMarks):
             self.peer.ledger = self.ex.ledger
         self._di = torch.tensor(self.dloc, dtype=torch.long, device=self.device)
         self._si = torch.tensor(self.sloc, dtype=torch.long, device=self.device)
+        # selective KV over NVLink (one-sided pulls / pushes, device-side counts); the
+        # all-to-all form (HybridExchange.fetch_kv_dev) stays for transport="all_to_all"
+        self.scp = (ScpPeerBuffers(len(self.sloc), self.L, head_dim, d_lr, self.ex.scp_group,
+                                   self.device)
+                    if transport == "peer" and g_s > 1 and self.sloc else None)
 
     def work(self) -> dict:
         """Algorithmic work of this rank's heads over the whole sequence (sparse heads:
@@ -1014,6 +1080,8 @@ class HybridDSV(_PhaseMarks):
         ex, L, r, D = self.ex, self.L, self.r, self.D
         hs, dev = ql.shape[0], ql.device
         sl = slice(self.s0, self.s0 + self.span_len)
+        if self.scp is not None:
+            return self._sparse_peer(ql, kl, vl, dol, qlr, klr)
         full = lambda t: torch.empty((hs, L, t.shape[2]), dtype=t.dtype, device=dev)
         Qf, Kf, Vf, dOf, Qlr = full(ql), full(kl), full(vl), full(dol), full(qlr)
         for dst, src in ((Qf, ql), (Kf, kl), (Vf, vl), (dOf, dol), (Qlr, qlr)):
@@ -1058,6 +1126,57 @@ class HybridDSV(_PhaseMarks):
             ex.return_grads_dev(dk32, dv32, need, cnt, add_home)
         dk = ops.f32_to_bf16(dk_span.contiguous())
         dv = ops.f32_to_bf16(dv_span.contiguous())
+        self._mark("scp_grad")
+        return out[:, sl].contiguous(), dq[:, sl].contiguous(), dk, dv
+
+    def _sparse_peer(self, ql, kl, vl, dol, qlr, klr):
+        """_sparse over NVLink peer memory: the span's K/V rows go into this rank's peer-mapped
+        full-length buffers, the marked remote rows are pulled from their owners, the
+        gradients of those rows pushed back into the owners' accumulators (dsv_scp_pull /
+        dsv_scp_push between device barriers). No host synchronisation."""
+        from . import ops
+
+        ex, L, r, D, scp = self.ex, self.L, self.r, self.D, self.scp
+        hs, dev = ql.shape[0], ql.device
+        sl = slice(self.s0, self.s0 + self.span_len)
+        Qf = torch.empty((hs, L, D), dtype=ql.dtype, device=dev)
+        dOf = torch.empty_like(Qf)
+        Qlr = torch.empty((hs, L, r), dtype=qlr.dtype, device=dev)
+        Qf[:, sl], dOf[:, sl], Qlr[:, sl] = ql, dol, qlr
+        scp.k[:, sl] = kl
+        scp.v[:, sl] = vl
+        scp.klr[:, sl] = klr
+        scp.barrier()                       # every member's span rows are in place
+        for g in range(ex.g_s):             # every key's K_lr for the selection (NVLink reads)
+            if g != ex.grp:
+                gs_ = slice(g * self.span_len, (g + 1) * self.span_len)
+                scp.klr[:, gs_] = scp.peer_klr[g][:, gs_]
+        Klr = scp.klr
+        self._mark("exchange_in")
+        sel = self.local.select_from_lowrank(Qlr, Klr)
+        self._mark("select")
+        mark = torch.zeros((hs, L), dtype=torch.bool, device=dev)
+        ks = self.local.ks
+        if len(set(ks)) == 1:
+            off = torch.arange(hs, device=dev, dtype=torch.int64)[:, None, None] * L
+            mark.view(-1).index_fill_(0, (sel.idx[:, :, :ks[0]].long() + off).view(-1), True)
+        else:
+            for hi, kh in enumerate(ks):
+                mark[hi].index_fill_(0, sel.idx[hi, :, :kh].reshape(-1).long(), True)
+        scp.pull(mark, self.s0, self.span_len)
+        self._mark("scp_fetch")
+        out, lse = self.local.forward(Qf, scp.k, scp.v, sel, prepare_backward=False)
+        self._mark("fwd")
+        scp.acc.zero_()
+        dq, _, _ = ops.sparse_bwd(Qf, scp.k, scp.v, out, dOf, lse, self.local.grp_rows,
+                                  self.local.grp_size, sel.idx, sel.kcount, self.local.scale,
+                                  scp.acc[0], scp.acc[1], tile_grp=self.local.tile_grp)
+        self._mark("bwd")
+        scp.barrier()                       # every member's accumulators are zeroed and full
+        scp.push(mark, self.s0, self.span_len)
+        scp.barrier()                       # the remote gradients have landed
+        dk = ops.f32_to_bf16(scp.acc[0][:, sl].contiguous())
+        dv = ops.f32_to_bf16(scp.acc[1][:, sl].contiguous())
         self._mark("scp_grad")
         return out[:, sl].contiguous(), dq[:, sl].contiguous(), dk, dv
 

@@ -564,6 +564,71 @@ extern "C" int dsv_peer_barrier(unsigned* const* peer_slots, unsigned* my_slots,
   return cuda_status((int)cudaGetLastError(), "peer_barrier launch");
 }
 
+// ---------------------------------------------------------------- selective KV (SCP) over NVLink
+// Every rank of an SCP group keeps full-length per-head buffers [hs][L][D] (K, V bf16; dK, dV
+// fp32) addressed by global token and mapped into its peers. The critical-key mark of this
+// rank's span (bool [hs][L]) decides, per (head, key row) outside the own span, whether the
+// row is pulled from its owner's buffer (forward) and whether its gradient rows are added
+// into the owner's accumulators (backward). Counts never leave the device.
+namespace {
+template <bool kPush>
+__global__ void __launch_bounds__(256)
+scp_rows_kernel(const unsigned char* __restrict__ mark, int hs, int L, int span0, int span_len,
+                const long long* __restrict__ peer_a, const long long* __restrict__ peer_b,
+                void* __restrict__ own_a, void* __restrict__ own_b, int D,
+                unsigned long long* __restrict__ count) {
+  const long long nrows = (long long)hs * L;
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  unsigned long long got = 0;
+  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < nrows;
+       r += warps) {
+    const int tok = (int)(r % L);
+    if (!mark[r] || (tok >= span0 && tok < span0 + span_len)) continue;
+    const int owner = tok / span_len;
+    ++got;
+    if (!kPush) {                 // K, V rows (bf16) from the owner into the own buffers
+      const uint4* sa = reinterpret_cast<const uint4*>(peer_a[owner]) + r * D / 8;
+      const uint4* sb = reinterpret_cast<const uint4*>(peer_b[owner]) + r * D / 8;
+      uint4* da = reinterpret_cast<uint4*>(own_a) + r * D / 8;
+      uint4* db = reinterpret_cast<uint4*>(own_b) + r * D / 8;
+      for (int i = lane; i < D / 8; i += 32) { da[i] = sa[i]; db[i] = sb[i]; }
+    } else {                      // dK, dV rows (fp32) added into the owner's accumulators
+      const float4* sa = reinterpret_cast<const float4*>(own_a) + r * D / 4;
+      const float4* sb = reinterpret_cast<const float4*>(own_b) + r * D / 4;
+      float* da = reinterpret_cast<float*>(peer_a[owner]) + r * D;
+      float* db = reinterpret_cast<float*>(peer_b[owner]) + r * D;
+      for (int i = lane; i < D / 4; i += 32) {
+        const float4 x = sa[i], y = sb[i];
+        dsv::red_add_v4(da + 4 * i, x.x, x.y, x.z, x.w);
+        dsv::red_add_v4(db + 4 * i, y.x, y.y, y.z, y.w);
+      }
+    }
+  }
+  if (count && lane == 0 && got) atomicAdd(count, got);
+}
+}  // namespace
+
+extern "C" int dsv_scp_pull(const unsigned char* mark, int hs, int L, int span0, int span_len,
+                            const long long* peer_k, const long long* peer_v, void* k_full,
+                            void* v_full, int D, unsigned long long* count, void* stream) {
+  if (hs <= 0 || L <= 0 || span_len <= 0 || L % span_len || D % 8 || !mark || !peer_k || !peer_v)
+    return fail(DSV_EINVAL, "scp_pull: bad arguments");
+  scp_rows_kernel<false><<<148 * 8, 256, 0, S(stream)>>>(mark, hs, L, span0, span_len, peer_k,
+                                                         peer_v, k_full, v_full, D, count);
+  return cuda_status((int)cudaGetLastError(), "scp_pull launch");
+}
+
+extern "C" int dsv_scp_push(const unsigned char* mark, int hs, int L, int span0, int span_len,
+                            const long long* peer_dk, const long long* peer_dv, void* dk_full,
+                            void* dv_full, int D, void* stream) {
+  if (hs <= 0 || L <= 0 || span_len <= 0 || L % span_len || D % 4 || !mark || !peer_dk || !peer_dv)
+    return fail(DSV_EINVAL, "scp_push: bad arguments");
+  scp_rows_kernel<true><<<148 * 8, 256, 0, S(stream)>>>(mark, hs, L, span0, span_len, peer_dk,
+                                                        peer_dv, dk_full, dv_full, D, nullptr);
+  return cuda_status((int)cudaGetLastError(), "scp_push launch");
+}
+
 extern "C" int dsv_gather_rows(const void* src, long long src_stride, const int* rows, int n,
                                int row_bytes, void* out, long long out_stride, void* stream) {
   if (n <= 0) return DSV_OK;

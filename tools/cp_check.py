@@ -67,6 +67,8 @@ def main():
     led = cp.ex.ledger
     if hybrid:
         print(f"rank {rank}: ledger sent {led.sent} received {led.received}")
+        if getattr(cp, "scp", None) is not None:
+            print(f"rank {rank}: SCP rows pulled over NVLink {int(cp.scp.pulled.item())}")
     else:
         got = max(led.sent["hcp_fwd"], led.received["hcp_fwd"])
         # one packed exchange of Q|K|V|Q_lr|K_lr: 3 D + 2 r columns per token
