@@ -179,16 +179,20 @@ DSV_DEV uint32_t ld_peer(const uint32_t* p, uint32_t rank, uint32_t me) {
 DSV_DEV int range_lo(int nt, int S, int s) { return (int)(((long long)nt * s) / S); }
 // i-th sample tile of a range [t0, t1)
 // 1/8 of the range, at least 8 and at most kSampleTiles tiles
-__host__ __device__ __forceinline__ int sample_count(int n) {
-  const int a = n / 8 < kSampleTiles ? n / 8 : kSampleTiles;
+// (a twice denser sample in the single-pass mode shrank the band 27% but its histogram pass,
+// ~2 us per tile on shared-memory atomics, cost more than the band saved: 0.483 vs 0.463 ms)
+__host__ __device__ __forceinline__ int sample_count(int n, int mode = 0) {
+  const int div = 8;
+  (void)mode;
+  const int a = n / div < kSampleTiles ? n / div : kSampleTiles;
   const int b = a > 8 ? a : 8;
   return n < b ? n : b;
 }
 DSV_DEV int sample_tile(int t0, int n, int ns, int i) { return t0 + (int)(((long long)i * n) / ns); }
 
 // tile processed at step i of the current pass
-DSV_DEV int pass_tile(uint32_t pass, int t0, int n, int i) {
-  if (pass == P_MINMAX || pass == P_SHIST) return sample_tile(t0, n, sample_count(n), i);
+DSV_DEV int pass_tile(uint32_t pass, int t0, int n, int i, int mode) {
+  if (pass == P_MINMAX || pass == P_SHIST) return sample_tile(t0, n, sample_count(n, mode), i);
   return t0 + i;
 }
 
@@ -437,7 +441,7 @@ select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       mbar_init(&B.a_full, 1);
       B.pass = P_MINMAX;
       B.nfull = 0;
-      B.ntiles = sample_count(nrange);
+      B.ntiles = sample_count(nrange, mode);
       fence_barrier_init();
     }
     __syncwarp();
@@ -461,7 +465,7 @@ select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   // cluster-wide sample size (valid columns of every CTA's sample tiles)
   uint32_t ns_total = 0;
   for (uint32_t s = 0; s < S; ++s) {
-    const int a0 = range_lo(nt, S, s), n = range_lo(nt, S, s + 1) - a0, cnt = sample_count(n);
+    const int a0 = range_lo(nt, S, s), n = range_lo(nt, S, s + 1) - a0, cnt = sample_count(n, mode);
     for (int i = 0; i < cnt; ++i) ns_total += (uint32_t)min(BN, L - sample_tile(a0, n, cnt, i) * BN);
   }
   uint32_t seq = 0;    // tiles through the pipeline so far (same count in every role)
@@ -482,7 +486,7 @@ select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           tma_load_3d(smem + SL::kA, &tmA, &B.a_full, 0, m0, h);
         }
         for (int i = 0; i < ntl; ++i, ++seq) {
-          const int t = pass_tile(pass, t0, nrange, i);
+          const int t = pass_tile(pass, t0, nrange, i, mode);
           const int s = seq % kStages;
           if (seq >= (uint32_t)kStages) FSEL_WAIT(&B.empty[s], ((seq / kStages) - 1) & 1);
           mbar_arrive_expect_tx(&B.full[s], BN * BK * 2);
@@ -542,7 +546,7 @@ select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       const bool warp_idle = __all_sync(0xffffffffu, st == ST_DONE);
 
       for (int i = 0; i < ntl; ++i, ++seq) {
-        const int t = pass_tile(pass, t0, nrange, i);
+        const int t = pass_tile(pass, t0, nrange, i, mode);
         const int a = seq % kAcc;
         mbar_wait(&B.acc_full[a], (seq / kAcc) & 1);
         tc_fence_after();
@@ -732,7 +736,12 @@ select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             for (int j = 0; j < kCols; ++j) {
               const float s = __uint_as_float(v[j]);
               if (s == s) {
-                const int b = min(max(__float2int_rz(__fmaf_rn(s, va, vb)), 0), kBuckets - 1);
+                // bucket ~ floor(s va + vb) without F2I (a quarter-rate unit shared with the
+                // MUFU): clamp in float, round (t - 0.5) to nearest with the 1.5 * 2^23 add;
+                // an edge value may land one bucket low — the band is an estimate, a miss is
+                // detected and re-run exactly
+                const float t = fminf(fmaxf(__fmaf_rn(s, va, vb), 0.f), (float)kBuckets - 0.5f);
+                const int b = (int)(__float_as_uint(__fadd_rn(t - 0.5f, 12582912.f)) - 0x4B400000u);
                 atomicAdd(hist + b, 1u);
               }
             }
@@ -792,7 +801,7 @@ select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       named_bar_sync(1, kEpiThreads);
       if (et == 0) {
         uint32_t next, n;
-        if (pass == P_MINMAX) { next = P_SHIST; n = sample_count(nrange); }
+        if (pass == P_MINMAX) { next = P_SHIST; n = sample_count(nrange, mode); }
         else if (pass == P_SHIST && mode == M_FAST) { next = P_COLLECT; n = nrange; }
         else if (pass == P_COLLECT) { next = P_EXIT; n = 0; }
         else if (pass == P_SHIST || pass == P_FULL) {
@@ -1122,7 +1131,7 @@ long long dsv_select_fused_ws_bytes(int H, int G, int L, int k_max, int S) {
   using namespace dsv::fsel;
   const int nt = (L + BN - 1) / BN;
   const int n = (nt + S - 1) / S;
-  const double ns = (double)S * sample_count(n) * BN;
+  const double ns = (double)S * sample_count(n, 1) * BN;
   const double pk = fmin((double)k_max, (double)(L - k_max)) / L;
   const double sig = sqrt(fmax(ns * pk * (1.0 - pk), 0.0));
   const double frac = 2.0 * (5.5 * sig + 8.0) / ns + 4.0 / kBuckets;
