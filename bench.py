@@ -337,9 +337,9 @@ def run_gpu(args) -> None:
             if ev is not None:
                 ev[3].record()
             return res
-        # project, proxy gather, (scores gemm + topk | fused select), fwd (persistent + the
-        # list-mode re-run launch), bwd, 2x f32->bf16
-        launches_per_step = 8 if layer.fused_select() else 9
+        # project, proxy gather, (scores gemm + topk | fused select: main + finish + list-mode
+        # re-run launch), fwd (persistent + list-mode re-run), bwd, 2x f32->bf16
+        launches_per_step = 10 if layer.fused_select() else 9
         work = layer.work()
     else:
         from paper_2502_07590_b200.cp import HeadParallelDSV, HybridDSV
