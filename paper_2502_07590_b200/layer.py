@@ -111,7 +111,10 @@ class DSVAttentionLayer:
         H, L, G = self.H, self.L, self.G
         hc = H if return_scores else self.score_heads_per_chunk()
         if not return_scores and self.fused_select():
-            # K1b + K2 fused: scores recomputed on tcgen05 per pass, never stored
+            # K1b + K2 fused: scores recomputed on tcgen05 per pass, never stored; the layer
+            # keeps its single-pass workspace alive (captured graphs hold its address)
+            self.__dict__.setdefault("_sel_ws", ops.select_workspace(H, G, L, self.k_max, 0,
+                                                                     qp.device))
             idx, thr = ops.select_fused(qp, k_lr, self.kcount, self.k_max)
             scores = None
         elif hc >= H:
@@ -261,11 +264,15 @@ class HostPipeline:
                 dst.copy_(src, non_blocking=True)
             self.ready[slot].record(self.copy)
 
-    def _fetch(self, slot, res):
+    def _fetch(self, slot, res, reused: bool = False):
         """D2H of the step's result tensors into pinned host set `slot` on the D2H stream. The
         device tensors stay referenced until the compute stream has waited for the copy (the
-        slot's next step), so the allocator never hands their memory out while it is read."""
+        slot's next step), so the allocator never hands their memory out while it is read.
+        reused: the results are views of buffers the next step overwrites (head-parallel CP
+        returns views of its peer buffers) — they are first copied on the device."""
         res = [t for t in (res if isinstance(res, (tuple, list)) else (res,)) if torch.is_tensor(t)]
+        if reused:
+            res = [t.clone() for t in res]
         if self.host_out[slot] is None:
             self.host_out[slot] = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in res]
             self.d2h_bytes = sum(t.numel() * t.element_size() for t in res)
@@ -283,7 +290,7 @@ class HostPipeline:
         """Make the current stream wait for every issued D2H copy."""
         torch.cuda.current_stream().wait_stream(self.d2h)
 
-    def run(self, step, batches, fetch: bool = True):
+    def run(self, step, batches, fetch: bool = True, reused: bool = False):
         it = iter(batches)
         nxt = next(it, None)
         slot = 0
@@ -302,5 +309,5 @@ class HostPipeline:
             ev = torch.cuda.Event()
             ev.record(cur)
             self.free[slot] = ev
-            yield self._fetch(slot, res) if fetch else res
+            yield self._fetch(slot, res, reused) if fetch else res
             slot ^= 1

@@ -142,6 +142,8 @@ def select_workspace(H: int, G: int, L: int, k_max: int, split: int, device) -> 
     """Device workspace of the single-pass fused selection (cached per shape / device); None
     where the library advises the multi-pass algorithm."""
     key = (H, G, L, k_max, split, str(device))
+    if key not in _WS_CACHE and len(_WS_CACHE) >= 8:     # bounded: a few live shapes at most
+        _WS_CACHE.pop(next(iter(_WS_CACHE)))
     if key not in _WS_CACHE:
         n = int(_lib.load().dsv_select_fused_workspace_size(H, G, L, k_max, split))
         _WS_CACHE[key] = torch.empty((n,), dtype=torch.uint8, device=device) if n > 0 else None
