@@ -137,11 +137,6 @@ __device__ long long g_bwd_prof[kProfCtas][kProfBlocks][kProfEv];
 #define FPROF(j, e) do {} while (0)
 #endif
 
-// Shared-memory base aligned to 1024 B without leaving the shared address space.
-DSV_DEV uint8_t* aligned_smem(uint8_t* raw) {
-  return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
-}
-
 // Softmax pass 1: row max of the raw scores of one S buffer (two TMEM loads in flight,
 // 3-input max).
 template <bool kMasked>

@@ -18,6 +18,11 @@ namespace dsv {
 DSV_DEV uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// Shared-memory base aligned to 1024 B as an offset from the __shared__ array, so the
+// compiler keeps the shared address space (LDS/STS/ATOMS, not generic LD/ST/ATOM).
+DSV_DEV uint8_t* aligned_smem(uint8_t* raw) {
+  return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+}
 DSV_DEV uint32_t lane_id() { return threadIdx.x & 31; }
 DSV_DEV uint32_t warp_id() { return __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0); }
 

@@ -38,7 +38,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             void* __restrict__ C, int M, int N, int K, long long ldc, long long c_bs) {
   using SL = SmemLayout<BN, STAGES, kTmaStore>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = aligned_smem(smem_raw);
   uint8_t* sOut = smem + STAGES * SL::kStage;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SL::kStage + SL::kOut);
   uint64_t* empty = full + STAGES;

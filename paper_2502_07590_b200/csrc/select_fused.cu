@@ -415,7 +415,7 @@ select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                     int mode, uint32_t* __restrict__ bitmap, int nwords, uint2* __restrict__ stash,
                     int cap, uint32_t* __restrict__ counts, const int* __restrict__ tile_fail) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = aligned_smem(smem_raw);
   Bars& B = *reinterpret_cast<Bars*>(smem + SL::kBar);
   uint32_t* U = reinterpret_cast<uint32_t*>(smem + SL::kU);
   uint32_t* stage = reinterpret_cast<uint32_t*>(smem + SL::kStage);
@@ -1065,7 +1065,12 @@ select_finish_kernel(int H, int G, int L, uint32_t S, const int* __restrict__ kc
     if (tid == 0) atomicExch(fail, 1);
     return;
   }
-  int* op = out_idx + row * ldo + (wbase + incl - c);
+  // indices go to shared memory (the band's space, no longer read) when they fit, then out
+  // in coalesced 16-byte stores; a thread's own run of scattered stores would touch a
+  // separate sector per lane
+  int* grow = out_idx + row * ldo;
+  const bool stage_out = (long long)k * 4 <= (long long)smem_cap * 8;
+  int* op = (stage_out ? reinterpret_cast<int*>(sband) : grow) + (wbase + incl - c);
   for (int w = w0; w < w1; ++w) {
     uint32_t word = bits[w];
     const int cb = w * 32;
@@ -1075,6 +1080,17 @@ select_finish_kernel(int H, int G, int L, uint32_t S, const int* __restrict__ kc
     }
   }
   if (tid == 0) out_thr[row] = key2f(T);
+  if (stage_out) {
+    __syncthreads();
+    const int* so = reinterpret_cast<const int*>(sband);
+    if ((reinterpret_cast<uintptr_t>(grow) & 15) == 0) {
+      for (uint32_t i = tid; i < k / 4; i += kFinThreads)
+        reinterpret_cast<int4*>(grow)[i] = reinterpret_cast<const int4*>(so)[i];
+      for (uint32_t i = (k & ~3u) + tid; i < k; i += kFinThreads) grow[i] = so[i];
+    } else {
+      for (uint32_t i = tid; i < k; i += kFinThreads) grow[i] = so[i];
+    }
+  }
 }
 }  // namespace fsel
 }  // namespace dsv
