@@ -138,17 +138,18 @@ class DSVAttentionLayer:
 
     def fused_select(self) -> bool:
         """Fused K1b + K2 (select_fused.cu; r <= 16) where it measured faster than scores
-        GEMM + top-k (tools/select_bench.py on one B200): with >= 48 row tiles of 128 proxies
-        (c2, 24 heads: 0.69 vs 0.88 ms), or >= 24 tiles at L >= 65536 (L = 131072, 4 heads:
-        1.25 vs 2.22 ms). Fewer tiles leave the fused kernel latency-bound (c2, 12 heads:
-        0.69 vs 0.49 ms). DSV_FUSED_SELECT=1 / 0 forces either path."""
+        GEMM + top-k (tools/select_bench.py on one B200, single-pass mode): with >= 32 row
+        tiles of 128 proxies (c2, 24 heads: 0.46 vs 0.87 ms; 12 heads: 0.43 vs 0.48 ms), or
+        >= 16 tiles at L >= 65536 (L = 131072, 2 heads: 0.89 vs 1.24 ms). Fewer tiles leave
+        the fused kernel's sample passes and cluster merges exposed (c2, 6 heads: 0.275 vs
+        0.271 ms; 3 heads: 0.26 vs 0.18 ms). DSV_FUSED_SELECT=1 / 0 forces either path."""
         if self.r > 16:
             return False
         env = os.environ.get("DSV_FUSED_SELECT", "auto")
         if env in ("0", "1"):
             return env == "1"
         tiles = self.H * ((self.G + 127) // 128)
-        return tiles >= 48 or (tiles >= 24 and self.L >= 65536)
+        return tiles >= 32 or (tiles >= 16 and self.L >= 65536)
 
     def score_heads_per_chunk(self) -> int:
         """Heads scored per pass: the fp32 score matrices stay under DSV_SCORE_BYTES (16 GiB)."""
