@@ -359,7 +359,8 @@ def run_gpu(args) -> None:
 
         def step(ev=None):
             return cp.step(x, wt, q, k, v, do)
-        launches_per_step = 8 + 8   # local layer + pack/unpack gathers
+        launches_per_step = (cp.launches_per_step() if getattr(cp, "transport", None) == "peer"
+                             and hasattr(cp, "launches_per_step") else 8 + 8)
         if args.dense_heads:        # ring: per hop attend + merge, grad + 2 accumulations; 2 converts
             launches_per_step += 5 * args.scp + 2
         # the kernel rooflines below are of the sparse kernels (the `fwd` / `bwd` stages);

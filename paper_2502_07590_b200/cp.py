@@ -381,7 +381,8 @@ class PeerExchange:
         big, small, back = nh_max * self.L * self.D, nh_max * self.L * self.r, self.H * self.chunk * self.D
         names = [("q", big), ("k", big), ("v", big), ("do", big), ("qlr", small), ("klr", small),
                  ("o", back), ("dq", back), ("dk", back), ("dv", back),
-                 ("flags", 2 * (self.world + 1))]        # u32 [world] barrier slots + epoch
+                 ("flags", 2 * (self.world + 1)),        # u32 [world] barrier slots + epoch
+                 ("flags2", 2 * (self.world + 1))]       # a second set for the side stream
         self.off, tot = {}, 0
         for n, sz in names:
             self.off[n] = tot
@@ -396,19 +397,25 @@ class PeerExchange:
         self.peer = _PeerBuffer(2 * tot, self.group, dev)
         self.buf = self.peer.tensor
         self.ptrs = np.asarray(self.peer.ptrs, dtype=np.int64)
-        # barrier slots: [world] u32 arrival epochs + one u32 epoch counter (device side)
-        so = 2 * self.off["flags"]
-        self._slots_tab = torch.tensor([int(p) + so for p in self.ptrs], dtype=torch.int64, device=dev)
-        self._my_slots = int(self.ptrs[self.rank]) + so
-        self._epoch = self._my_slots + 4 * self.world
+        # barrier slots: [world] u32 arrival epochs + one u32 epoch counter (device side); set 0
+        # orders the compute stream, set 1 the side stream of the overlapped input exchange
+        # (each set's barriers run in the same order on every rank)
+        self._bars = []
+        for name in ("flags", "flags2"):
+            so = 2 * self.off[name]
+            tab = torch.tensor([int(p) + so for p in self.ptrs], dtype=torch.int64, device=dev)
+            mine = int(self.ptrs[self.rank]) + so
+            self._bars.append((tab, mine, mine + 4 * self.world))
         torch.cuda.synchronize(dev)
         dist.barrier(self.group)
         self._step = 0
 
-    def _barrier(self):
-        """Device barrier over the ranks' peer buffers on the current stream."""
-        _lib.call("dsv_peer_barrier", self._slots_tab.data_ptr(), self._my_slots, self._epoch,
-                  self.world, self.rank, torch.cuda.current_stream(self.buf.device).cuda_stream)
+    def _barrier(self, which: int = 0):
+        """Device barrier over the ranks' peer buffers on the current stream (slot set
+        `which`)."""
+        tab, mine, epoch = self._bars[which]
+        _lib.call("dsv_peer_barrier", tab.data_ptr(), mine, epoch, self.world, self.rank,
+                  torch.cuda.current_stream(self.buf.device).cuda_stream)
 
     # ------------------------------------------------------------------ views
     def region(self, name: str) -> torch.Tensor:
@@ -546,6 +553,34 @@ class PeerExchange:
         self._run(self._table(key, lambda: self._fwd_jobs(q, k, v, do, p)))
         self._account(("hcp_fwd", 3 * self.D + 2 * self.r), ("hcp_bwd_in", self.D), to_heads=True)
         return tuple(self.region(n) for n in ("q", "k", "v", "do", "qlr", "klr"))
+
+    def to_heads_overlapped(self, q, k, v, do, p, side: torch.cuda.Stream):
+        """to_heads with the bulk behind the selection: Q_lr / K_lr travel on the current
+        stream (the selection needs only them), Q, K, V, dO on `side` with a copy grid of about
+        one 256-thread CTA per SM, which fits next to the one-CTA-per-SM selection kernel
+        (registers: 8 K + 55 K of 64 K). Returns the six views and an event the consumer of
+        Q / K / V / dO waits on."""
+        from . import ops
+
+        self._check_in(q, k, v, do, p)
+        dev = self.buf.device
+        cur = torch.cuda.current_stream(dev)
+        key = ("fo",) + tuple(t.data_ptr() for t in (q, k, v, do, p))
+        low = self._table(key + ("lr",), lambda: self._lowrank_jobs(p))
+        big = self._table(key + ("big",), lambda: self._head_jobs((("q", q), ("k", k), ("v", v), ("do", do))),
+                          stream=side)
+        self._barrier()                      # owners are done reading the previous contents
+        ops.copy_jobs(low, self.splits)      # first, at full width: the selection waits on it
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            sm = torch.cuda.get_device_properties(dev).multi_processor_count
+            ops.copy_jobs(big, max(1, -(-sm // big.shape[0])))
+            self._barrier(1)                 # every writer's Q / K / V / dO rows are in place
+            done = torch.cuda.Event()
+            done.record(side)
+        self._barrier()                      # Q_lr / K_lr complete
+        self._account(("hcp_fwd", 3 * self.D + 2 * self.r), ("hcp_bwd_in", self.D), to_heads=True)
+        return tuple(self.region(n) for n in ("q", "k", "v", "do", "qlr", "klr")), done
 
     def _check_in(self, q, k, v, do, p):
         for t in (q, k, v, do, p):
@@ -914,6 +949,9 @@ class HeadParallelDSV(_PhaseMarks):
         self.H, self.D, self.r = heads, head_dim, d_lr
         mine = self.ex.my_heads
         self.local = DSVAttentionLayer(grid, len(mine), head_dim, d_lr, voxel, sp[mine], device)
+        # peer transport: Q / K / V / dO exchanged under the selection (DSV_OVERLAP_IN=0: after)
+        self.overlap_in = transport == "peer" and os.environ.get("DSV_OVERLAP_IN", "1") != "0"
+        self._side = torch.cuda.Stream(torch.device(device)) if self.overlap_in else None
 
     def step(self, x_local, wt, q, k, v, dout):
         """x_local [L/N, H*D]; q, k, v, dout [H, L/N, D] -> (out, dq, dk, dv) [H, L/N, D].
@@ -959,6 +997,16 @@ class HeadParallelDSV(_PhaseMarks):
         self._mark("o_back")
         return (out_local, *grads)
 
+    def launches_per_step(self) -> int:
+        """Kernels one peer-transport step launches: projection, barrier + Q_lr/K_lr copy +
+        barrier, the Q/K/V/dO copy (+ its side-stream barrier when overlapped), proxy gather,
+        selection (fused: main + finish + list-mode re-run; unfused: scores GEMM + top-k),
+        forward (+ list-mode re-run), backward, then with fused outputs two dK/dV converts and
+        a barrier (else the convert pair, then barrier + copy + barrier)."""
+        n = 1 + 3 + (2 if self.overlap_in else 0) + 1 + (3 if self.local.fused_select() else 2)
+        n += 2 + 1 + 2
+        return n + (1 if self.fused_out else 3)
+
     def _step_peer(self, x_local, wt, q, k, v, dout):
         from . import ops
 
@@ -966,9 +1014,17 @@ class HeadParallelDSV(_PhaseMarks):
         self._mark("start")
         p = ops.project(x_local, wt)                                   # [L/N, 2 H r]
         self._mark("project")
-        ql, kl, vl, dout_m, qlr, klr = self.ex.to_heads(q, k, v, dout, p)
-        self._mark("exchange_in")
-        sel = loc.select_from_lowrank(qlr, klr)
+        if self.overlap_in:
+            # the Q / K / V / dO exchange runs on a side stream under the selection
+            (ql, kl, vl, dout_m, qlr, klr), done = self.ex.to_heads_overlapped(q, k, v, dout, p,
+                                                                               self._side)
+            self._mark("exchange_in")
+            sel = loc.select_from_lowrank(qlr, klr)
+            torch.cuda.current_stream(q.device).wait_event(done)
+        else:
+            ql, kl, vl, dout_m, qlr, klr = self.ex.to_heads(q, k, v, dout, p)
+            self._mark("exchange_in")
+            sel = loc.select_from_lowrank(qlr, klr)
         self._mark("select")
         ex = self.ex
         if self.fused_out:
