@@ -375,9 +375,13 @@ def run_gpu(args) -> None:
     eager_step = step
     if args.graph and args.dense_heads:
         args.graph = False   # the ring KV pass issues host-sized NCCL P2P hops
+    graph_evs = None
     if args.graph:
-        # one CUDA graph per step: the host issues one launch instead of ~20 kernels
-        graph = torch.cuda.CUDAGraph()
+        # CUDA graphs: the host issues one launch per step instead of ~10-20 kernels. On one
+        # GPU every timed step gets its own graph (one shared memory pool, replayed in capture
+        # order) whose stage boundaries are external CUDA events — event record nodes on the
+        # launching stream — so the per-stage (and the roofline kernel's) times are measured
+        # live over the whole timed region, not in extra steps outside it
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
@@ -386,16 +390,31 @@ def run_gpu(args) -> None:
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        with torch.cuda.graph(graph):
-            step()
+        graphs, pool = [], None
+        per_step = world == 1 and bool(stage_names)
+        graph_evs = [] if per_step else None
+        for _ in range(args.steps if per_step else 1):
+            g = torch.cuda.CUDAGraph()
+            ev = ([torch.cuda.Event(enable_timing=True, external=True)
+                   for _ in range(len(stage_names) + 1)] if per_step else None)
+            with torch.cuda.graph(g, pool=pool):
+                if ev is not None:
+                    ev[0].record()
+                step(ev[1:] if ev is not None else None)
+            pool = g.pool()
+            graphs.append(g)
+            if per_step:
+                graph_evs.append(ev)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        replay_i = [0]
 
         def step(ev=None):
-            graph.replay()
+            graphs[replay_i[0] % len(graphs)].replay()
+            replay_i[0] += 1
         eager_stage_names, stage_names = stage_names, ()
-        for _ in range(2):
+        for _ in range(len(graphs)):
             step()
         torch.cuda.synchronize()
         if world > 1:
@@ -431,20 +450,13 @@ def run_gpu(args) -> None:
             vals = [(starts[i] if si == 0 else evs[i][si - 1]).elapsed_time(evs[i][si])
                     for i in range(args.steps)]
             stage_ms[name] = sum(vals) / len(vals)
-    if args.graph and world == 1:
-        # per-stage times from extra eager (untimed) steps with events, issued back to back
-        # (the host runs ahead, so no launch gap lands in a stage); median of steps 2..6
-        reps = 6
-        evr = [[torch.cuda.Event(enable_timing=True) for _ in range(len(eager_stage_names) + 1)]
-               for _ in range(reps)]
-        for i in range(reps):
-            evr[i][0].record()
-            eager_step(evr[i][1:])
-        torch.cuda.synchronize()
+    if graph_evs:
+        # per-stage times of the timed replays (each graph's events hold its last replay:
+        # exactly one, inside the timed loop); mean over the K steps
         stage_ms = {}
         for si, name in enumerate(eager_stage_names):
-            vals = sorted(evr[i][si].elapsed_time(evr[i][si + 1]) for i in range(1, reps))
-            stage_ms[name] = vals[len(vals) // 2]
+            vals = [graph_evs[i][si].elapsed_time(graph_evs[i][si + 1]) for i in range(len(graph_evs))]
+            stage_ms[name] = sum(vals) / len(vals)
     if world > 1:
         # extra (untimed) eager steps; per-phase events on the compute stream of the last
         eager_step()
@@ -496,7 +508,7 @@ def run_gpu(args) -> None:
                  "overlap step i; full-duplex PCIe)"}
 
     if args.graph:
-        del graph                        # release the captured graph before the groups go
+        del graphs, step                 # release the captured graphs before the groups go
         torch.cuda.synchronize()
     if rank != 0:
         if world > 1:
