@@ -22,9 +22,18 @@ def _stream() -> int:
 
 
 def _require_cuda(*ts) -> None:
+    cur = None
     for t in ts:
-        if t is not None and not t.is_cuda:
+        if t is None:
+            continue
+        if not t.is_cuda:
             raise _lib.DSVError("libdsv kernels need CUDA tensors (no CPU fallback exists)")
+        if cur is None:
+            cur = torch.cuda.current_device()
+        if t.device.index != cur:
+            # the C ABI launches on the calling thread's current device and stream
+            raise _lib.DSVError(f"tensor on {t.device} while the current device is cuda:{cur}; "
+                                "call under torch.cuda.device(tensor.device)")
 
 
 def _ptr(t) -> int:
