@@ -485,7 +485,7 @@ def run_gpu(args) -> None:
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        n_e2e = max(3, args.steps // 2)
+        n_e2e = max(3, args.steps)        # the same K as the device-timed loop
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         # every step: pinned H2D of its own inputs (overlapping the previous step) and the D2H
         # of its results O, dQ, dK, dV into pinned host buffers (overlapping the next step);
