@@ -3,6 +3,25 @@
 #include "../paper_2502_07590_b200/csrc/dsv_common.cuh"
 using namespace dsv;
 
+// degree-3 minimax 2^x on the FMA pipe (Cody-Waite split via the 1.5 * 2^23 magic add), the
+// variant the kernels once mixed with MUFU ex2 (kept here for the throughput comparison)
+__device__ __forceinline__ f32x2 exp2_poly2(f32x2 x) {
+  float2 v = f2u(x);
+  v.x = fmaxf(v.x, -125.f);
+  v.y = fmaxf(v.y, -125.f);
+  const f32x2 magic = f2(12582912.f, 12582912.f);
+  const f32x2 xc = f2(v.x, v.y);
+  const f32x2 t = fadd2(xc, magic);
+  const f32x2 jf = fadd2(t, f2(-12582912.f, -12582912.f));
+  const f32x2 fr = ffma2(jf, f2(-1.f, -1.f), xc);
+  f32x2 p = ffma2(fr, f2(0.05517044f, 0.05517044f), f2(0.2426081f, 0.2426081f));
+  p = ffma2(fr, p, f2(0.69326096f, 0.69326096f));
+  p = ffma2(fr, p, f2(0.99992834f, 0.99992834f));
+  const float2 q = f2u(p), tt = f2u(t);
+  return f2(__int_as_float(__float_as_int(q.x) + (__float_as_int(tt.x) << 23)),
+            __int_as_float(__float_as_int(q.y) + (__float_as_int(tt.y) << 23)));
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(512) k(float* out, int iters) {
   float a[8];
