@@ -1,11 +1,15 @@
 """Per-source-line instruction and warp-stall shares from an ncu report's source page:
-python tools/ncu_lines.py report.ncu-rep [top]"""
+python tools/ncu_lines.py report.ncu-rep [top] [kernel-name regex] [launch index]"""
 import csv
 import subprocess
 import sys
 
-out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                     capture_output=True, text=True).stdout
+cmd = ["ncu", "-i", sys.argv[1], "--page", "source", "--csv", "--print-source", "cuda,sass"]
+if len(sys.argv) > 3:
+    cmd += ["-k", "regex:" + sys.argv[3]]
+if len(sys.argv) > 4:
+    cmd += ["--launch-skip", sys.argv[4], "--launch-count", "1"]
+out = subprocess.run(cmd, capture_output=True, text=True).stdout
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 rows = [r for r in csv.reader(out.splitlines()) if r and r[0].isdigit()]
 num = lambda x: int(x) if x.isdigit() else 0   # noqa: E731
