@@ -74,7 +74,7 @@ def _args():
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--graph", dest="graph", action="store_true",
                     default=os.environ.get("DSV_GRAPH", "1") == "1",
-                    help="replay the step as one captured CUDA graph (default; DSV_GRAPH=0 or "
+                    help="replay CUDA graphs (default; one per timed step on one GPU; DSV_GRAPH=0 or "
                          "--eager issues the kernels one by one)")
     ap.add_argument("--eager", dest="graph", action="store_false")
     ap.add_argument("--scp", type=int, default=1,
