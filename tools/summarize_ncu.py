@@ -3,7 +3,8 @@
 usage: python tools/summarize_ncu.py <tag> <launches.csv> <full.ncu-rep>
 Writes profiles/<tag>_launches.md (per-kernel device time share, DRAM bytes per
 launch), profiles/<tag>_ncu_full.md (key --set full metrics per kernel) and
-profiles/traffic.json (DRAM bytes per launch of each hot kernel, read by bench.py).
+profiles/traffic.json (DRAM bytes per launch of each hot kernel from the --set full
+capture, else the launch list; read by bench.py as the roofline's `traffic`).
 """
 
 import csv
@@ -69,11 +70,22 @@ def launches(path: Path, tag: str) -> dict:
     return {k: (v[2] + v[3]) / v[0] for k, v in ours.items()}
 
 
-def full(path: Path, tag: str) -> None:
+def full(path: Path, tag: str) -> dict:
+    """Writes the summary; returns DRAM bytes (read + write) per launch of each kernel in the
+    --set full capture (the first launch of each name)."""
     out = subprocess.run(["ncu", "-i", str(path), "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     hdr, units = rows[0], rows[1]
+    dram = {}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for r in rows[2:]:
+        try:
+            b = sum(float(r[hdr.index(m)].replace(",", "")) * scale.get(units[hdr.index(m)], 1)
+                    for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        except ValueError:
+            continue
+        dram.setdefault(short(r[hdr.index("Kernel Name")]), b)
     lines = [f"# {tag}: ncu --set full summary", "",
              f"Source: `{path.name}` (one launch per kernel at the c2 shape, `tools/prof_c2.py`).", ""]
     for r in rows[2:]:
@@ -87,13 +99,15 @@ def full(path: Path, tag: str) -> None:
                 lines.append(f"| {label} (`{m}`) | {r[i]} {units[i]} |")
         lines.append("")
     (PROF / f"{tag}_ncu_full.md").write_text("\n".join(lines))
+    return dram
 
 
 def main():
     tag, lcsv, rep = sys.argv[1], Path(sys.argv[2]), Path(sys.argv[3])
     PROF.mkdir(exist_ok=True)
     traffic = launches(lcsv, tag)
-    full(rep, tag)
+    # per-launch DRAM traffic: the --set full capture where it has the kernel, else the list
+    traffic.update(full(rep, tag))
     tj = {k: int(v) for k, v in traffic.items()}
     # bench.py looks kernels up by base name
     for k in list(tj):
