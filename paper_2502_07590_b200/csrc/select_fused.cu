@@ -849,15 +849,17 @@ constexpr int kFinBuckets = 1 << kFinDigit;
 struct FinShared {
   uint32_t hist[kFinBuckets];
   uint32_t red[2][kFinThreads / 32];
-  uint32_t b, above;
+  uint32_t b, above, cnt;
 };
 
 // m-th largest (1-based) key among n entries passing `keyf`, all keys in [kmin, kmin + range]:
 // radix select on key - kmin with 11-bit digits from the top of the range (two rounds for
-// the band's ~2^22-ulp spread). *rem = m minus the number of entries strictly above it.
+// the band's ~2^22-ulp spread). *rem = m minus the number of entries strictly above it;
+// *eq = the number equal to it (the last round's digit resolves the key exactly, so its
+// bucket count is that number).
 template <typename AtF, typename KeyF>
 DSV_DEV uint32_t block_select(AtF at, uint32_t n, uint32_t m, uint32_t kmin, uint32_t range,
-                              FinShared& F, KeyF keyf, uint32_t* rem) {
+                              FinShared& F, KeyF keyf, uint32_t* rem, uint32_t* eq) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int kPer = kFinBuckets / kFinThreads;    // buckets per thread (8)
   const int top = range ? 31 - __clz(range) : 0;
@@ -899,6 +901,7 @@ DSV_DEV uint32_t block_select(AtF at, uint32_t n, uint32_t m, uint32_t kmin, uin
       while (run + c[j] < remaining) { run += c[j]; ++j; }
       F.b = kFinBuckets - 1 - kPer * tid - j;
       F.above = run;
+      F.cnt = c[j];
     }
     __syncthreads();
     prefix |= F.b << shift;
@@ -906,6 +909,7 @@ DSV_DEV uint32_t block_select(AtF at, uint32_t n, uint32_t m, uint32_t kmin, uin
     __syncthreads();
   }
   *rem = remaining;
+  *eq = F.cnt;
   return prefix + kmin;
 }
 
@@ -931,6 +935,14 @@ DSV_DEV uint32_t block_sum(uint32_t v, FinShared& F) {
 // bitmap, which then holds exactly the k kept keys, emitted ascending by a block scan.
 // A row whose band missed T (or overflowed its stash) flags its row tile for the exact
 // multi-pass re-run (M_LIST launch).
+template <bool kStaged>
+DSV_DEV void finish_row(FinShared& F, uint8_t* fin_smem, long long row, int G, int L,
+                        uint32_t S, const int* __restrict__ kcount,
+                        const uint32_t* __restrict__ bitmap, int nwords,
+                        const uint2* __restrict__ stash, int cap, const uint32_t (&segn)[8],
+                        uint32_t B, const uint2* __restrict__ bandlim, int* __restrict__ out_idx,
+                        long long ldo, float* __restrict__ out_thr, int* fail, int smem_cap);
+
 __global__ void __launch_bounds__(kFinThreads)
 select_finish_kernel(int H, int G, int L, uint32_t S, const int* __restrict__ kcount,
                      const uint32_t* __restrict__ bitmap, int nwords,
@@ -939,15 +951,9 @@ select_finish_kernel(int H, int G, int L, uint32_t S, const int* __restrict__ kc
                      float* __restrict__ out_thr, int* __restrict__ tile_fail, int smem_cap) {
   __shared__ FinShared F;
   extern __shared__ __align__(16) uint8_t fin_smem[];
-  const int tid = threadIdx.x;
-  const int nw4 = (nwords + 3) & ~3;
-  uint32_t* bits = reinterpret_cast<uint32_t*>(fin_smem);
-  uint2* sband = reinterpret_cast<uint2*>(bits + nw4);
   const long long row = blockIdx.x;
   const int h = (int)(row / G), g = (int)(row % G);
   int* fail = tile_fail + h * ((G + BM - 1) / BM) + g / BM;
-  const int kh = kcount[h];
-  const uint32_t k = (uint32_t)(kh < 1 ? 1 : (kh > L ? L : kh));
   uint32_t segn[8];
   uint32_t B = 0;
   bool over = false;
@@ -961,9 +967,32 @@ select_finish_kernel(int H, int G, int L, uint32_t S, const int* __restrict__ kc
     B += segn[s];
   }
   if (over) {
-    if (tid == 0) atomicExch(fail, 1);
+    if (threadIdx.x == 0) atomicExch(fail, 1);
     return;
   }
+  // (the branch is uniform per CTA; each body reads its band entries one way)
+  if (B <= (uint32_t)smem_cap)
+    finish_row<true>(F, fin_smem, row, G, L, S, kcount, bitmap, nwords, stash, cap, segn, B,
+                     bandlim, out_idx, ldo, out_thr, fail, smem_cap);
+  else
+    finish_row<false>(F, fin_smem, row, G, L, S, kcount, bitmap, nwords, stash, cap, segn, B,
+                      bandlim, out_idx, ldo, out_thr, fail, smem_cap);
+}
+
+template <bool kStaged>
+DSV_DEV void finish_row(FinShared& F, uint8_t* fin_smem, long long row, int G, int L,
+                        uint32_t S, const int* __restrict__ kcount,
+                        const uint32_t* __restrict__ bitmap, int nwords,
+                        const uint2* __restrict__ stash, int cap, const uint32_t (&segn)[8],
+                        uint32_t B, const uint2* __restrict__ bandlim, int* __restrict__ out_idx,
+                        long long ldo, float* __restrict__ out_thr, int* fail, int smem_cap) {
+  const int tid = threadIdx.x;
+  const int nw4 = (nwords + 3) & ~3;
+  uint32_t* bits = reinterpret_cast<uint32_t*>(fin_smem);
+  uint2* sband = reinterpret_cast<uint2*>(bits + nw4);
+  const int h = (int)(row / G);
+  const int kh = kcount[h];
+  const uint32_t k = (uint32_t)(kh < 1 ? 1 : (kh > L ? L : kh));
   // stage the bitmap and (when they fit) the band entries in shared memory
   const uint4* brow = reinterpret_cast<const uint4*>(bitmap + row * nwords);
   uint32_t nge = 0;
@@ -982,14 +1011,13 @@ select_finish_kernel(int H, int G, int L, uint32_t S, const int* __restrict__ kc
     }
   }
   const uint2* gbase = stash + row * S * cap;
-  const bool staged = B <= (uint32_t)smem_cap;
   uint32_t sstart[8];
   {
     uint32_t off = 0;
 #pragma unroll
     for (int s = 0; s < 8; ++s) { sstart[s] = off; off += segn[s]; }
   }
-  if (staged) {
+  if (kStaged) {
     // band entries: four loads in flight per thread before their shared-memory stores
     for (uint32_t s = 0; s < S; ++s) {
       const uint2* src = gbase + (size_t)s * cap;
@@ -1010,7 +1038,7 @@ select_finish_kernel(int H, int G, int L, uint32_t S, const int* __restrict__ kc
   }
   // entry i of the row's band: shared copy, or its stash segment (rows too large to stage)
   auto at = [&](uint32_t i) -> uint2 {
-    if (staged) return sband[i];
+    if (kStaged) return sband[i];
     uint32_t s = 0;
     while (s + 1 < S && i >= sstart[s + 1]) ++s;
     return gbase[(size_t)s * cap + (i - sstart[s])];
@@ -1023,18 +1051,17 @@ select_finish_kernel(int H, int G, int L, uint32_t S, const int* __restrict__ kc
   }
   const uint32_t m = k - above;
   const uint2 lim = bandlim[row];
-  uint32_t need;
+  uint32_t need, eq;
   const uint32_t T = block_select(at, B, m, lim.x, lim.y - lim.x, F,
-                                  [](uint2 e, uint32_t& key) { key = e.y; return true; }, &need);
-  uint32_t eq = 0;
-  for (uint32_t i = tid; i < B; i += kFinThreads) eq += at(i).y == T;
-  eq = block_sum(eq, F);
+                                  [](uint2 e, uint32_t& key) { key = e.y; return true; }, &need,
+                                  &eq);
   uint32_t col_max = 0xffffffffu;
   if (eq > need) {
-    uint32_t dummy;
+    uint32_t dummy, dummy2;
     const uint32_t cmin = ~(uint32_t)(L - 1);         // ~col lies in [~(L-1), ~0]
     col_max = ~block_select(at, B, need, cmin, (uint32_t)(L - 1), F,
-                            [T](uint2 e, uint32_t& key) { key = ~e.x; return e.y == T; }, &dummy);
+                            [T](uint2 e, uint32_t& key) { key = ~e.x; return e.y == T; }, &dummy,
+                            &dummy2);
   }
   for (uint32_t i = tid; i < B; i += kFinThreads) {
     const uint2 e = at(i);
