@@ -171,8 +171,15 @@ DSV_DEV uint32_t ld_dsmem(uint32_t addr) {
   asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
   return v;
 }
+DSV_DEV uint32_t ld_shared_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+// a partial of cluster rank `rank` (read after a cluster barrier, which orders it): the own
+// CTA's through a plain shared-memory load, a peer's through DSMEM
 DSV_DEV uint32_t ld_peer(const uint32_t* p, uint32_t rank, uint32_t me) {
-  return rank == me ? *reinterpret_cast<const volatile uint32_t*>(p) : ld_dsmem(dsmem_addr(p, rank));
+  return rank == me ? ld_shared_u32(p) : ld_dsmem(dsmem_addr(p, rank));
 }
 
 // key range of cluster rank s: tiles [s nt / S, (s + 1) nt / S)
@@ -227,16 +234,34 @@ DSV_DEV uint32_t warp_suffix(uint32_t v, int lane) {
   return v;
 }
 
+// Sample-rank band of the SHIST pass around the k-th value's expected rank tgt = k ns / L
+// (the same for every row of a CTA: one head, one k): half-width 4 sigma (+4) when a miss
+// only costs another FULL pass; 5.5 sigma (+8) for the single collect pass, where a miss
+// re-runs the tile. Computed once per CTA and pass (double divisions and a square root).
+struct SampleBand { double hi_rank, lo_rank; };
+DSV_DEV SampleBand sample_band(uint32_t k, uint32_t ns, int L, int mode) {
+  const double tgt = (double)k * ns / L;
+  const double sig = sqrt(fmax(tgt * (1.0 - tgt / ns), 0.0));
+  const double marg = mode == M_FAST ? 5.5 * sig + 8.0 : 4.0 * sig + 4.0;
+  return {tgt - marg, tgt + marg};
+}
+
 DSV_DEV void finalize_row(Rows& R, uint32_t* U, int r, int lane, uint32_t pass, uint32_t S,
-                          uint32_t me, uint32_t ns, int L, int mode) {
+                          uint32_t me, SampleBand band, int L, int mode) {
   const uint32_t st = R.state[r];
   if (pass == P_MINMAX) {
+    // lane s reads CTA s's partials (the cluster's loads in flight together)
+    float a = __int_as_float(0x7f800000), b = __int_as_float(0xff800000);
+    if ((uint32_t)lane < S) {
+      a = __uint_as_float(ld_peer(reinterpret_cast<uint32_t*>(R.cta_min) + r, lane, me));
+      b = __uint_as_float(ld_peer(reinterpret_cast<uint32_t*>(R.cta_max) + r, lane, me));
+    }
+#pragma unroll
+    for (int o = 4; o; o >>= 1) {          // S <= 8
+      a = fminf(a, __shfl_xor_sync(0xffffffffu, a, o));
+      b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
     if (lane == 0) {
-      float a = __int_as_float(0x7f800000), b = __int_as_float(0xff800000);
-      for (uint32_t s = 0; s < S; ++s) {
-        a = fminf(a, __uint_as_float(ld_peer(reinterpret_cast<uint32_t*>(R.cta_min) + r, s, me)));
-        b = fmaxf(b, __uint_as_float(ld_peer(reinterpret_cast<uint32_t*>(R.cta_max) + r, s, me)));
-      }
       R.smin[r] = a;
       R.smax[r] = b;
     }
@@ -246,21 +271,25 @@ DSV_DEV void finalize_row(Rows& R, uint32_t* U, int r, int lane, uint32_t pass, 
   const uint32_t* hrow = U + r * kHistStride + 4 * lane;
   uint32_t c[4] = {0u, 0u, 0u, 0u};
   if (pass == P_SHIST || st == ST_REFINE) {
-    for (uint32_t s = 0; s < S; ++s) {
+    // all of a group of four CTAs' loads issued before any add: each add would otherwise
+    // hold the next DSMEM load behind a full round trip
+    for (uint32_t s0 = 0; s0 < S; s0 += 4) {
+      uint32_t v[4][4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) c[q] += ld_peer(hrow + q, s, me);
+      for (uint32_t s = 0; s < 4; ++s)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[s][q] = s0 + s < S ? ld_peer(hrow + q, s0 + s, me) : 0u;
+#pragma unroll
+      for (uint32_t s = 0; s < 4; ++s)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) c[q] += v[s][q];
     }
   }
   const uint32_t lsum = c[0] + c[1] + c[2] + c[3];
   const uint32_t excl = warp_suffix(lsum, lane) - lsum;     // entries in higher lanes' buckets
   if (pass == P_SHIST) {
     const float lo = R.smin[r], hi = R.smax[r];
-    const double tgt = (double)R.k[r] * ns / L;
-    // band half-width in sample ranks: 4 sigma (+4) when a miss only costs another FULL
-    // pass; 5.5 sigma (+8) for the single collect pass, where a miss re-runs the tile
-    const double sig = sqrt(fmax(tgt * (1.0 - tgt / ns), 0.0));
-    const double marg = mode == M_FAST ? 5.5 * sig + 8.0 : 4.0 * sig + 4.0;
-    const double hi_rank = tgt - marg, lo_rank = tgt + marg;
+    const double hi_rank = band.hi_rank, lo_rank = band.lo_rank;
     // highest bucket with cum > hi_rank / cum >= lo_rank
     int bh = -1, bl = -1;
     uint32_t cum = excl;
@@ -468,6 +497,7 @@ select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     const int a0 = range_lo(nt, S, s), n = range_lo(nt, S, s + 1) - a0, cnt = sample_count(n, mode);
     for (int i = 0; i < cnt; ++i) ns_total += (uint32_t)min(BN, L - sample_tile(a0, n, cnt, i) * BN);
   }
+  const SampleBand band = sample_band(R.k[0], ns_total, L, mode);   // every row: one head's k
   uint32_t seq = 0;    // tiles through the pipeline so far (same count in every role)
   const bool prof = threadIdx.x == 64;
   (void)prof;
@@ -785,7 +815,7 @@ select_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     if (prof) FPROF_AT(np, 4);
     if (warp >= 2 && pass != P_EMIT && pass != P_COLLECT) {
       for (int r = warp - 2; r < BM; r += kEpiWarps)
-        finalize_row(R, U, r, lane, pass, S, me, ns_total, L, mode);
+        finalize_row(R, U, r, lane, pass, S, me, band, L, mode);
     }
     if (prof) FPROF_AT(np, 5);
     if (S > 1) cluster_sync(); else __syncthreads();
