@@ -107,6 +107,9 @@ int dsv_scores_f32(const void* A, long long lda, long long a_bs, const void* B, 
  * The workspace size is 0 where the single pass is not worthwhile (the band would hold too
  * large a share of the keys, or need more than 1 GiB): pass NULL then. */
 long long dsv_select_fused_workspace_size(int H, int G, int L, int k_max, int split);
+/* Clusters of S dsv_select_fused CTAs resident at once on the current device (occupancy
+ * query, cached per device); the automatic split counts waves with it. 0 = no device. */
+int dsv_select_fused_max_clusters(int S);
 int dsv_select_fused(const void* q_prox, long long ldq, long long q_bs, const void* k_lr,
                      long long ldk, long long k_bs, int H, int G, int L, int r,
                      const int* k_per_head, int* out_idx, long long out_ld, float* out_thr,

@@ -37,6 +37,7 @@ SIGNATURES = {
                          c_int, c_int, c_int, c_void_p, c_void_p, c_longlong, c_void_p, c_int,
                          c_void_p, c_longlong, c_void_p],
     "dsv_select_fused_workspace_size": [c_int, c_int, c_int, c_int, c_int],
+    "dsv_select_fused_max_clusters": [c_int],
     "dsv_topk": [c_void_p, c_longlong, c_int, c_int, c_void_p, c_int, c_void_p, c_longlong,
                  c_void_p, c_void_p],
     "dsv_sparse_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_longlong,

@@ -1154,6 +1154,37 @@ DSV_DEV void finish_row(FinShared& F, uint8_t* fin_smem, long long row, int G, i
 
 int dsv_select_fused_smem_bytes() { return dsv::fsel::SL::kBytes; }
 
+// Clusters of S select_fused_kernel CTAs (one per SM: ~221 KB of shared memory) that can be
+// resident at once on the current device (cudaOccupancyMaxActiveClusters: a cluster must fit
+// in one GPC, so 4-CTA clusters leave SMs unused where a GPC's count is not a multiple of 4).
+// 0 when it cannot be queried (no device).
+int dsv_select_fused_clusters_query(int S) {
+  using namespace dsv::fsel;
+  if (S < 1 || S > 8) return 0;
+  if (cudaFuncSetAttribute(select_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           SL::kBytes) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(S * 64), 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = SL::kBytes;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, select_fused_kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
 int dsv_debug_select_timeline_copy(void* dst, int bytes) {
   const int n = (int)sizeof(g_fsel_prof) < bytes ? (int)sizeof(g_fsel_prof) : bytes;
   if (cudaMemcpyFromSymbol(dst, g_fsel_prof, n) != cudaSuccess) return -1;

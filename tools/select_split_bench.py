@@ -10,7 +10,7 @@ from paper_2502_07590_b200 import ops  # noqa: E402
 
 def main():
     dev = torch.device("cuda:0")
-    for L, G, heads in ((32000, 260, (24, 12, 6)), (131072, 1024, (16, 4, 2))):
+    for L, G, heads in ((32000, 260, (24, 12, 6, 3)), (131072, 1024, (16, 4, 2))):
         for H in heads:
             g = torch.Generator(device="cuda").manual_seed(0)
             qp = torch.randn((H, G, 16), device=dev, generator=g).to(torch.bfloat16)
