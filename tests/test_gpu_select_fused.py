@@ -112,3 +112,26 @@ def test_fast_mode_c2_needs_no_fallback():
     ops.select_fused(q, k, kc, 3200, mode="fast")
     torch.cuda.synchronize()
     assert ops.select_fast_fallbacks(24, 260, 32000, 3200, 0, q.device) == 0
+
+
+def test_resident_cluster_query():
+    # the automatic split counts waves with resident clusters: one CTA per SM, fewer S-CTA
+    # clusters than SMs / S where a GPC's SM count is not a multiple of S
+    from paper_2502_07590_b200 import _lib
+
+    lib = _lib.load()
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    n = [lib.dsv_select_fused_max_clusters(s) for s in range(1, 9)]
+    assert n[0] == sms
+    assert all(0 < n[s - 1] <= sms // s for s in range(1, 9))
+    assert lib.dsv_select_fused_max_clusters(0) == 0 and lib.dsv_select_fused_max_clusters(9) == 0
+
+
+@pytest.mark.parametrize("heads", [12, 6])
+def test_auto_split_matches_forced(heads):
+    # whatever split the occupancy rule picks, the selection is the same
+    q, k = _operands(heads, 260, 32000, 16, seed=31)
+    kc = torch.full((heads,), 3200, dtype=torch.int32, device=q.device)
+    a = ops.select_fused(q, k, kc, 3200, split=0)
+    b = ops.select_fused(q, k, kc, 3200, split=1)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
