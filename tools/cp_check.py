@@ -1,7 +1,7 @@
 """HCP on N GPUs vs the single-GPU layer on the same inputs (torchrun, NCCL).
 
 usage: torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/cp_check.py [--skewed] [--hybrid]
-                [--gs=G] [--dense=M] [--transport=peer|all_to_all]
+                [--gs=G] [--dense=M] [--transport=peer|all_to_all] [--voxel=t,h,w]
 (--hybrid: g_h = N/G head groups x g_s = G (default 2) selective-sequence groups, HybridDSV;
  --dense=M: the first M heads are dense residual heads, run by the ring KV pass)
 Every rank builds the same global inputs (seeded), keeps its L/N token chunk, runs
@@ -33,6 +33,9 @@ def main():
     gs = int(next((a.split("=")[1] for a in sys.argv if a.startswith("--gs=")), 2))
     # hybrid: every SCP span must hold whole voxel groups (8 frames deep)
     grid = TokenGrid(8 * gs, 16, 16) if hybrid else TokenGrid(8, 16, 16)
+    # --voxel=t,h,w: ladder shapes of more than 128 queries (128-query tiles sharing an index row)
+    voxel = tuple(int(v) for v in next((a.split("=")[1] for a in sys.argv if a.startswith("--voxel=")),
+                                       "8,4,4").split(","))
     H, D, r = 8, 128, 16
     L = grid.size
     sp = np.linspace(0.5, 0.95, H) if "--skewed" in sys.argv else np.full(H, 0.9)
@@ -45,10 +48,10 @@ def main():
     chunk = L // world
     sl = slice(rank * chunk, (rank + 1) * chunk)
     if hybrid:
-        cp = HybridDSV(grid, H, D, r, (8, 4, 4), sp, world // gs, gs, balanced=True, device=dev)
+        cp = HybridDSV(grid, H, D, r, voxel, sp, world // gs, gs, balanced=True, device=dev)
     else:
         tr = next((a.split("=")[1] for a in sys.argv if a.startswith("--transport=")), "auto")
-        cp = HeadParallelDSV(grid, H, D, r, (8, 4, 4), sp, balanced=True, device=dev, transport=tr)
+        cp = HeadParallelDSV(grid, H, D, r, voxel, sp, balanced=True, device=dev, transport=tr)
     outs = cp.step(x[sl].contiguous(), wt, *(t[:, sl].contiguous() for t in (q, k, v, do)))
     gathered = []
     for t in outs:
@@ -57,7 +60,7 @@ def main():
         gathered.append(torch.cat(buf, dim=1))
     ok = True
     if rank == 0:
-        ref = DSVAttentionLayer(grid, H, D, r, (8, 4, 4), sp, dev).step(x, wt, q, k, v, do)
+        ref = DSVAttentionLayer(grid, H, D, r, voxel, sp, dev).step(x, wt, q, k, v, do)
         for name, a, b in zip(("out", "dq", "dk", "dv"), gathered, ref):
             err = (a.float() - b.float()).abs().max().item()
             rel = ((a.float() - b.float()).norm() / b.float().norm()).item()
