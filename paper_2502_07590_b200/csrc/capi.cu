@@ -537,19 +537,23 @@ namespace {
 __global__ void peer_barrier_kernel(unsigned* const* __restrict__ peer_slots,
                                     unsigned* __restrict__ my_slots, unsigned* __restrict__ epoch,
                                     int world, int rank) {
-  if (threadIdx.x != 0) return;
+  // lane r signals peer r and waits for peer r, all lanes at once (world <= 32): a release
+  // (fence.acq_rel.sys + relaxed store) orders every write issued before this kernel on the
+  // stream — the exchange copies into peer memory — before the flag; the acquire loads make
+  // the peers' writes visible before the kernels after this one. One thread storing and
+  // polling the peers in turn measured 20-25 us per barrier.
+  const int lane = threadIdx.x;
   const unsigned e = *epoch + 1u;
-  __threadfence_system();
-  for (int r = 0; r < world; ++r)
-    asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(peer_slots[r] + rank), "r"(e) : "memory");
-  for (int r = 0; r < world; ++r) {
+  if (lane < world) {
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" :: "l"(peer_slots[lane] + rank), "r"(e) : "memory");
     unsigned v;
     do {
-      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(my_slots + r) : "memory");
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(my_slots + lane) : "memory");
     } while ((int)(v - e) < 0);
   }
-  *epoch = e;
-  __threadfence_system();
+  __syncwarp();
+  if (lane == 0) *epoch = e;
 }
 }  // namespace
 
@@ -584,8 +588,8 @@ extern "C" int dsv_peer_free(void* ptr) { return cuda_status((int)cudaFree(ptr),
 
 extern "C" int dsv_peer_barrier(unsigned* const* peer_slots, unsigned* my_slots, unsigned* epoch,
                                 int world, int rank, void* stream) {
-  if (world < 1 || rank < 0 || rank >= world || !peer_slots || !my_slots || !epoch)
-    return fail(DSV_EINVAL, "peer_barrier: bad arguments");
+  if (world < 1 || world > 32 || rank < 0 || rank >= world || !peer_slots || !my_slots || !epoch)
+    return fail(DSV_EINVAL, "peer_barrier: bad arguments (world 1..32)");
   peer_barrier_kernel<<<1, 32, 0, S(stream)>>>(peer_slots, my_slots, epoch, world, rank);
   return cuda_status((int)cudaGetLastError(), "peer_barrier launch");
 }
