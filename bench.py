@@ -579,7 +579,15 @@ def run_gpu(args) -> None:
             "sparse_bwd_l2": {"fp32_reduction_tbs": red_b / (bwd_ms / 1e3) / 1e12,
                               "frac_of_5.5tbs": red_b / (bwd_ms / 1e3) / 5.5e12,
                               "gather_tbs": gather_b / (bwd_ms / 1e3) / 1e12},
-            "select(project+scores+topk)": {"ms": stage_ms["select"]},
+            "select(project+scores+topk)": {
+                "ms": stage_ms["select"],
+                # SURVEY 8(d)'s selection roofline is the unfused K2's: the fp32 score matrix
+                # read from HBM plus the index lists written (topk_bytes). The fused path
+                # never stores those scores, so this is the bound the design removed, not
+                # one it runs against (its own compulsory HBM traffic is ~0.1 GB)
+                "unfused_k2_hbm_floor_ms": work["topk_bytes"] / (peaks["hbm_gbs"] * 1e9) * 1e3,
+                "frac_of_unfused_k2_floor": (work["topk_bytes"] / (peaks["hbm_gbs"] * 1e9) * 1e3)
+                / stage_ms["select"]},
         }
     if e2e is not None:
         res["e2e"] = e2e
