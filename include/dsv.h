@@ -219,6 +219,10 @@ typedef struct dsv_copy_job {
  * row_bytes must be a multiple of 16 and rows * row_bytes / 16 < 2^31 per job.
  * `splits` blocks cooperate on each job (1..1024). */
 int dsv_copy_jobs(const dsv_copy_job* jobs, int njobs, int splits, void* stream);
+/* The same with `threads` (128 or 256) per block: 128-thread blocks (4 K registers) fit next
+ * to a persistent attention kernel's CTA on its SM, so a copy can run under it. */
+int dsv_copy_jobs_threads(const dsv_copy_job* jobs, int njobs, int splits, int threads,
+                          void* stream);
 
 /* Selective KV gathering (SCP, cpsim.py:164-216) over NVLink, one-sided: each rank of an SCP
  * group holds full-length buffers [hs][L][D] addressed by global token (K, V bf16; dK, dV

@@ -56,6 +56,7 @@ SIGNATURES = {
     "dsv_debug_timeline": [c_void_p, c_int],
     "dsv_debug_select_timeline": [c_void_p, c_int],
     "dsv_copy_jobs": [c_void_p, c_int, c_int, c_void_p],
+    "dsv_copy_jobs_threads": [c_void_p, c_int, c_int, c_int, c_void_p],
     "dsv_pred_pass": [c_int, c_void_p, c_void_p, c_void_p, c_int, c_longlong, c_int, c_int, c_int,
                       c_void_p, c_void_p, c_void_p],
     "dsv_varint_index_bytes": [c_void_p, c_longlong, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p],

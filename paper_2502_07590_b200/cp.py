@@ -555,11 +555,13 @@ class PeerExchange:
         return tuple(self.region(n) for n in ("q", "k", "v", "do", "qlr", "klr"))
 
     def to_heads_overlapped(self, q, k, v, do, p, side: torch.cuda.Stream):
-        """to_heads with the bulk behind the selection: Q_lr / K_lr travel on the current
-        stream (the selection needs only them), Q, K, V, dO on `side` with a copy grid of about
-        one 256-thread CTA per SM, which fits next to the one-CTA-per-SM selection kernel
-        (registers: 8 K + 55 K of 64 K). Returns the six views and an event the consumer of
-        Q / K / V / dO waits on."""
+        """to_heads with the bulk behind the compute: Q_lr / K_lr travel on the current stream
+        (the selection needs only them); on `side`, Q, K, V go under the selection with a
+        copy grid of about one 256-thread CTA per SM (8 K registers, which fit next to the
+        one-CTA-per-SM selection kernel's 55 K), then dO — needed only by the backward —
+        under the forward in 128-thread CTAs (4 K registers: what the persistent forward's
+        800 x 72 leave). Returns the six views and two events: Q / K / V in place, dO in
+        place."""
         from . import ops
 
         self._check_in(q, k, v, do, p)
@@ -567,20 +569,25 @@ class PeerExchange:
         cur = torch.cuda.current_stream(dev)
         key = ("fo",) + tuple(t.data_ptr() for t in (q, k, v, do, p))
         low = self._table(key + ("lr",), lambda: self._lowrank_jobs(p))
-        big = self._table(key + ("big",), lambda: self._head_jobs((("q", q), ("k", k), ("v", v), ("do", do))),
+        qkv = self._table(key + ("qkv",), lambda: self._head_jobs((("q", q), ("k", k), ("v", v))),
                           stream=side)
+        dsj = self._table(key + ("do",), lambda: self._head_jobs((("do", do),)), stream=side)
         self._barrier()                      # owners are done reading the previous contents
         ops.copy_jobs(low, self.splits)      # first, at full width: the selection waits on it
         side.wait_stream(cur)
+        sm = torch.cuda.get_device_properties(dev).multi_processor_count
         with torch.cuda.stream(side):
-            sm = torch.cuda.get_device_properties(dev).multi_processor_count
-            ops.copy_jobs(big, max(1, -(-sm // big.shape[0])))
-            self._barrier(1)                 # every writer's Q / K / V / dO rows are in place
-            done = torch.cuda.Event()
-            done.record(side)
+            ops.copy_jobs(qkv, max(1, -(-sm // qkv.shape[0])))
+            self._barrier(1)                 # every writer's Q / K / V rows are in place
+            done_qkv = torch.cuda.Event()
+            done_qkv.record(side)
+            ops.copy_jobs(dsj, max(1, -(-sm // dsj.shape[0])), threads=128)
+            self._barrier(1)                 # ... and dO
+            done_do = torch.cuda.Event()
+            done_do.record(side)
         self._barrier()                      # Q_lr / K_lr complete
         self._account(("hcp_fwd", 3 * self.D + 2 * self.r), ("hcp_bwd_in", self.D), to_heads=True)
-        return tuple(self.region(n) for n in ("q", "k", "v", "do", "qlr", "klr")), done
+        return tuple(self.region(n) for n in ("q", "k", "v", "do", "qlr", "klr")), (done_qkv, done_do)
 
     def _check_in(self, q, k, v, do, p):
         for t in (q, k, v, do, p):
@@ -999,11 +1006,12 @@ class HeadParallelDSV(_PhaseMarks):
 
     def launches_per_step(self) -> int:
         """Kernels one peer-transport step launches: projection, barrier + Q_lr/K_lr copy +
-        barrier, the Q/K/V/dO copy (+ its side-stream barrier when overlapped), proxy gather,
+        barrier, the Q/K/V/dO copy (overlapped: Q/K/V and dO copies, each with a side-stream
+        barrier), proxy gather,
         selection (fused: main + finish + list-mode re-run; unfused: scores GEMM + top-k),
         forward (+ list-mode re-run), backward, then with fused outputs two dK/dV converts and
         a barrier (else the convert pair, then barrier + copy + barrier)."""
-        n = 1 + 3 + (2 if self.overlap_in else 0) + 1 + (3 if self.local.fused_select() else 2)
+        n = 1 + 3 + (4 if self.overlap_in else 0) + 1 + (3 if self.local.fused_select() else 2)
         n += 2 + 1 + 2
         return n + (1 if self.fused_out else 3)
 
@@ -1014,13 +1022,14 @@ class HeadParallelDSV(_PhaseMarks):
         self._mark("start")
         p = ops.project(x_local, wt)                                   # [L/N, 2 H r]
         self._mark("project")
+        done_do = None
         if self.overlap_in:
-            # the Q / K / V / dO exchange runs on a side stream under the selection
-            (ql, kl, vl, dout_m, qlr, klr), done = self.ex.to_heads_overlapped(q, k, v, dout, p,
-                                                                               self._side)
+            # Q / K / V travel on a side stream under the selection, dO under the forward
+            (ql, kl, vl, dout_m, qlr, klr), (done_qkv, done_do) = self.ex.to_heads_overlapped(
+                q, k, v, dout, p, self._side)
             self._mark("exchange_in")
             sel = loc.select_from_lowrank(qlr, klr)
-            torch.cuda.current_stream(q.device).wait_event(done)
+            torch.cuda.current_stream(q.device).wait_event(done_qkv)
         else:
             ql, kl, vl, dout_m, qlr, klr = self.ex.to_heads(q, k, v, dout, p)
             self._mark("exchange_in")
@@ -1033,6 +1042,8 @@ class HeadParallelDSV(_PhaseMarks):
             # there directly (NVLink peer stores), then one device barrier
             out, lse = loc.forward(ql, kl, vl, sel, out_rows=ex.rows("o"))
             self._mark("fwd")
+            if done_do is not None:
+                torch.cuda.current_stream(q.device).wait_event(done_do)
             loc.backward(ql, kl, vl, out, lse, dout_m, sel, dq_rows=ex.rows("dq"),
                          dkdv_rows=(ex.rows("dk"), ex.rows("dv")))
             self._mark("bwd")
@@ -1041,6 +1052,8 @@ class HeadParallelDSV(_PhaseMarks):
             return res
         out, lse = loc.forward(ql, kl, vl, sel)
         self._mark("fwd")
+        if done_do is not None:
+            torch.cuda.current_stream(q.device).wait_event(done_do)
         dq, dk, dv = loc.backward(ql, kl, vl, out, lse, dout_m, sel)
         self._mark("bwd")
         res = ex.to_tokens(out, dq, dk, dv)

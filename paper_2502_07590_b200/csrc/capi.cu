@@ -517,6 +517,16 @@ extern "C" int dsv_critical_counts(const float* scores, long long ld, int rows, 
                      "critical_counts launch");
 }
 
+extern "C" int dsv_copy_jobs_threads(const dsv_copy_job* jobs, int njobs, int splits, int threads,
+                                     void* stream) {
+  if (njobs <= 0) return DSV_OK;
+  if (!jobs || splits < 1 || splits > 1024 || (threads != 128 && threads != 256))
+    return fail(DSV_EINVAL, "copy_jobs_threads: bad job table, split count or block size");
+  dim3 grid(njobs, splits);
+  copy_jobs_kernel<<<grid, threads, 0, S(stream)>>>(jobs);
+  return cuda_status((int)cudaGetLastError(), "copy_jobs launch");
+}
+
 extern "C" int dsv_copy_jobs(const dsv_copy_job* jobs, int njobs, int splits, void* stream) {
   if (njobs <= 0) return DSV_OK;
   if (!jobs || splits < 1 || splits > 1024)

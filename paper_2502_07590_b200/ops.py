@@ -347,13 +347,18 @@ def critical_counts(scores: torch.Tensor, sqrt_d: float, theta: float) -> torch.
     return out
 
 
-def copy_jobs(jobs: torch.Tensor, splits: int = 16) -> None:
+def copy_jobs(jobs: torch.Tensor, splits: int = 16, threads: int = 256) -> None:
     """Run a [njobs, 6] int64 device job table (src, dst, src_stride, dst_stride, rows,
-    row_bytes) in one launch (dsv_copy_jobs); addresses may be NVLink peer pointers."""
+    row_bytes) in one launch (dsv_copy_jobs); addresses may be NVLink peer pointers.
+    threads = 128: blocks small enough to share an SM with a persistent attention CTA."""
     _require_cuda(jobs)
     if jobs.dtype != torch.int64 or jobs.dim() != 2 or jobs.shape[1] != 6 or not jobs.is_contiguous():
         raise ValueError("copy_jobs: expected a contiguous [njobs, 6] int64 table")
-    _lib.call("dsv_copy_jobs", _ptr(jobs), jobs.shape[0], int(splits), _stream())
+    if threads == 256:
+        _lib.call("dsv_copy_jobs", _ptr(jobs), jobs.shape[0], int(splits), _stream())
+    else:
+        _lib.call("dsv_copy_jobs_threads", _ptr(jobs), jobs.shape[0], int(splits), int(threads),
+                  _stream())
 
 
 def f32_to_bf16_rows(x: torch.Tensor, rows) -> None:
