@@ -158,6 +158,21 @@ int dsv_sparse_bwd(const void* q, const void* k, const void* v, const void* out,
                    int G, int Lq, int Lk, int D, float scale, void* dq, float* dk_acc,
                    float* dv_acc, unsigned* work, const int* tile_grp, int n_groups,
                    const long long* dq_tab, int dq_n, int dq_chunk, void* stream);
+/* dsv_sparse_bwd plus the dK/dV conversion to bf16 in the kernel's tail: once the tile queue
+ * is exhausted the persistent CTAs convert slices of every head whose tiles are all done
+ * (what a separate conversion pass over the accumulators would do, without the CTAs idling
+ * while the last tiles finish). Outputs: dkdv_out bf16 [2][H][Lk][D] (dK then dV), or the
+ * token owners' rows dk_tab / dv_tab[h*kv_n + tok/kv_chunk] + (tok % kv_chunk)*D.
+ * conv_ws: H + 1 device ints (zeroed by the call). conv_ws == NULL: no conversion. */
+int dsv_sparse_bwd_convert(const void* q, const void* k, const void* v, const void* out,
+                           const void* dout, const float* lse, const int* grp_rows,
+                           const int* grp_size, const int* idx, long long ldk, const int* kcount,
+                           const int* kcount_hg, int H, int G, int Lq, int Lk, int D, float scale,
+                           void* dq, float* dk_acc, float* dv_acc, unsigned* work,
+                           const int* tile_grp, int n_groups, const long long* dq_tab, int dq_n,
+                           int dq_chunk, void* dkdv_out, const long long* dk_tab,
+                           const long long* dv_tab, int kv_n, int kv_chunk, int* conv_ws,
+                           void* stream);
 
 /* Ragged per-(head, query) CSR sparse attention on CUDA cores (fp32 math), any D <= 256.
  * ptr: [H*Lq + 1] int64 offsets into cols (int32 key ids); cols == NULL selects every key

@@ -48,6 +48,11 @@ SIGNATURES = {
                        c_void_p, c_void_p, c_longlong, c_void_p, c_void_p, c_int, c_int, c_int,
                        c_int, c_int, c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                        c_int, c_void_p, c_int, c_int, c_void_p],
+    "dsv_sparse_bwd_convert": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                               c_void_p, c_void_p, c_void_p, c_longlong, c_void_p, c_void_p,
+                               c_int, c_int, c_int, c_int, c_int, c_float, c_void_p, c_void_p,
+                               c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int, c_int,
+                               c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p],
     "dsv_rows_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int,
                      c_int, c_float, c_int, c_void_p, c_void_p, c_void_p],
     "dsv_rows_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

@@ -253,6 +253,20 @@ DSV_DEV long long sel_row(int tile, int G, const int* tile_grp, int Gs) {
   return (long long)h * Gs + (tile_grp ? __ldg(tile_grp + g) : g);
 }
 
+// Backward: the dK/dV fp32 -> bf16 conversion done by the persistent CTAs once the tile
+// queue is exhausted (the kernel's tail, where CTAs would otherwise idle while the last
+// tiles finish). head_done[h] counts the finished tiles of head h (scatter warps publish
+// them after a fence); a CTA converts a slice of head h once all its tiles are done.
+// head_done == nullptr: no conversion (the caller converts).
+struct KvOut {
+  __nv_bfloat16* dk;        // bf16 [H, Lk, D] (local outputs), or
+  __nv_bfloat16* dv;
+  RowOut dk_rows, dv_rows;  // row addresses at the token owners (tab != nullptr)
+  int* head_done;           // [H] finished tiles per head; [H] = slice counter (zeroed)
+  int H, tiles_per_head;
+};
+constexpr int kConvSlices = 32;   // conversion work items per head
+
 template <int D>
 __global__ void __launch_bounds__(kFwdThreads, 1)
 sparse_fwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __restrict__ Kg,
@@ -672,7 +686,7 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
                   float scale_log2,
                   __nv_bfloat16* __restrict__ dQ, float* __restrict__ dK, float* __restrict__ dV,
                   int n_tiles, unsigned* __restrict__ sched, const int* __restrict__ tile_grp,
-                  int Gs, RowOut dqremote) {
+                  int Gs, RowOut dqremote, KvOut kv) {
   using SL = BwdSmem<D>;
   using GT = Gather<D, kBwdLoadThreads>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -758,8 +772,19 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
     const int pw = warp - kBwdScatWarp0;            // rows [RPW pw, RPW pw + RPW)
     const int stid = threadIdx.x - kBwdScatWarp0 * 32;
     int gj = 0;
+    int prev_h = -1, pending = 0;
+    // publish the finished tiles of head prev_h: every scatter thread's reductions are
+    // performed (fence), then one release add (the tail conversion acquires it)
+    auto flush = [&]() {
+      __threadfence();
+      named_bar_sync(2, kBwdScatThreads);
+      if (stid == 0) red_release_add(kv.head_done + prev_h, pending);
+      pending = 0;
+    };
     for (int it = 0;; ++it) {
     DSV_BWD_TILE();
+    if (kv.head_done != nullptr && prev_h >= 0 && h != prev_h) flush();
+    prev_h = h;
     const long long hoff = (long long)h * Lk * D;
     for (int jb = 0; jb < nblk; ++jb, ++gj) {
       const int kv = min(BKV, kh - jb * BKV);
@@ -798,7 +823,9 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
       }
       if (stid == 0) PROF(jb, 10);
     }
+    ++pending;
     }
+    if (kv.head_done != nullptr && pending > 0) flush();
   } else if (warp >= kBwdLoadWarp0) {
     // ------------------------------------------------------------ gather producers
     const int ptid = threadIdx.x - kBwdLoadWarp0 * 32;
@@ -1033,6 +1060,42 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
   tc_fence_before();
   __syncthreads();
   if (warp == kBwdMmaWarp) tmem_dealloc(tmem, 512);
+  if (kv.head_done == nullptr) return;
+  // ---- tail: convert dK / dV slices of finished heads (items handed out in head order)
+  volatile int* s_item = reinterpret_cast<volatile int*>(sLse);
+  const int total = kv.H * kConvSlices;
+  const int rps = (Lk + kConvSlices - 1) / kConvSlices;
+  constexpr int kC4 = D / 4;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      const int item = atomicAdd(kv.head_done + kv.H, 1);
+      if (item < total) {
+        const int* done = kv.head_done + item / kConvSlices;
+        const unsigned long long t0 = globaltimer_ns();
+        while (ld_acquire_gpu(done) < kv.tiles_per_head) {
+          __nanosleep(256);
+          if (globaltimer_ns() - t0 > 4000000000ull) __trap();   // watchdog
+        }
+      }
+      *s_item = item;
+    }
+    __syncthreads();
+    const int item = *s_item;
+    __syncthreads();
+    if (item >= total) break;
+    const int hh = item / kConvSlices, sl = item - hh * kConvSlices;
+    const int r0 = sl * rps, r1 = min(Lk, r0 + rps);
+    const long long base = (long long)hh * Lk * D;
+    for (int i = threadIdx.x; i < (r1 - r0) * kC4; i += kBwdThreads) {
+      const int row = r0 + i / kC4, c = (i % kC4) * 4;
+      const float4 a = __ldcg(reinterpret_cast<const float4*>(dK + base + (long long)row * D + c));
+      const float4 b = __ldcg(reinterpret_cast<const float4*>(dV + base + (long long)row * D + c));
+      __nv_bfloat16* ok = kv.dk_rows.tab ? row_out<D>(kv.dk_rows, hh, row) : kv.dk + base + (long long)row * D;
+      __nv_bfloat16* ov = kv.dv_rows.tab ? row_out<D>(kv.dv_rows, hh, row) : kv.dv + base + (long long)row * D;
+      *reinterpret_cast<uint2*>(ok + c) = make_uint2(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w));
+      *reinterpret_cast<uint2*>(ov + c) = make_uint2(pack_bf16(b.x, b.y), pack_bf16(b.z, b.w));
+    }
+  }
 }
 
 __global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
@@ -1133,7 +1196,7 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* O
                       long long ldk, const int* kcount, const int* kcount_hg, int H, int G, int Lq,
                       int Lk, float scale,
                       float scale_log2, void* dQ, float* dK, float* dV, unsigned* sched,
-                      const int* tile_grp, int Gs, RowOut dqremote, cudaStream_t st) {
+                      const int* tile_grp, int Gs, RowOut dqremote, KvOut kv, cudaStream_t st) {
   auto kern = sparse_bwd_kernel<D>;
   const int smem = BwdSmem<D>::kBytes;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1150,12 +1213,17 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* O
   }
   const int grid = per_tile ? n_tiles : (n_tiles < sms ? n_tiles : sms);
   cudaMemsetAsync(sched, 0, sizeof(unsigned), st);
+  if (kv.head_done != nullptr) {
+    kv.H = H;
+    kv.tiles_per_head = G;
+    cudaMemsetAsync(kv.head_done, 0, (H + 1) * sizeof(int), st);
+  }
   kern<<<grid, kBwdThreads, smem, st>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)dO,
                                       (const __nv_bfloat16*)k, (const __nv_bfloat16*)v,
                                       (const __nv_bfloat16*)O, lse, grp_rows, grp_size, idx, ldk,
                                       kcount, kcount_hg, G, Lq, Lk, scale, scale_log2,
                                       (__nv_bfloat16*)dQ, dK, dV, n_tiles, sched, tile_grp, Gs,
-                                      dqremote);
+                                      dqremote, kv);
   return (int)cudaGetLastError();
 }
 
@@ -1165,14 +1233,25 @@ int dsv_attn_bwd_tc_launch(const void* q, const void* k, const void* v, const vo
                            const int* kcount_hg, int H, int G, int Lq, int Lk, int D, float scale,
                            float scale_log2, void* dQ, float* dK, float* dV, unsigned* sched,
                            const int* tile_grp, int Gs, const long long* dq_tab, int dq_n,
-                           int dq_chunk, cudaStream_t st) {
+                           int dq_chunk, void* dkdv_out, const long long* dk_tab,
+                           const long long* dv_tab, int kv_n, int kv_chunk, int* conv_ws,
+                           cudaStream_t st) {
   const RowOut ro{dq_tab, dq_n, dq_chunk};
+  KvOut kv{};
+  if (conv_ws != nullptr && (dkdv_out != nullptr || (dk_tab != nullptr && dv_tab != nullptr))) {
+    kv.dk = reinterpret_cast<__nv_bfloat16*>(dkdv_out);
+    kv.dv = kv.dk ? kv.dk + (long long)H * Lk * D : nullptr;
+    kv.dk_rows = RowOut{dk_tab, kv_n, kv_chunk};
+    kv.dv_rows = RowOut{dv_tab, kv_n, kv_chunk};
+    kv.head_done = conv_ws;
+  }
   if (D == 128)
     return bwd_launch<128>(q, k, v, O, dO, lse, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H,
-                           G, Lq, Lk, scale, scale_log2, dQ, dK, dV, sched, tile_grp, Gs, ro, st);
+                           G, Lq, Lk, scale, scale_log2, dQ, dK, dV, sched, tile_grp, Gs, ro, kv,
+                           st);
   if (D == 64)
     return bwd_launch<64>(q, k, v, O, dO, lse, grp_rows, grp_size, idx, ldk, kcount, kcount_hg, H,
-                          G, Lq, Lk, scale, scale_log2, dQ, dK, dV, sched, tile_grp, Gs, ro, st);
+                          G, Lq, Lk, scale, scale_log2, dQ, dK, dV, sched, tile_grp, Gs, ro, kv, st);
   return 1;
 }
 

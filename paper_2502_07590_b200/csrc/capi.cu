@@ -38,6 +38,7 @@ int dsv_attn_bwd_tc_launch(const void*, const void*, const void*, const void*, c
                            const float*, const int*, const int*, const int*, long long,
                            const int*, const int*, int, int, int, int, int, float, float, void*,
                            float*, float*, unsigned*, const int*, int, const long long*, int, int,
+                           void*, const long long*, const long long*, int, int, int*,
                            cudaStream_t);
 int dsv_f32_to_bf16_rows_launch(const float*, int, int, int, const long long*, int, int,
                                 cudaStream_t);
@@ -333,13 +334,23 @@ int dsv_sparse_fwd(const void* q, const void* k, const void* v, const int* grp_r
                      "sparse_fwd launch");
 }
 
-int dsv_sparse_bwd(const void* q, const void* k, const void* v, const void* out,
-                   const void* dout, const float* lse, const int* grp_rows, const int* grp_size,
-                   const int* idx, long long ldk, const int* kcount, const int* kcount_hg, int H,
-                   int G, int Lq, int Lk, int D, float scale, void* dq, float* dk_acc,
-                   float* dv_acc, unsigned* work, const int* tile_grp, int n_groups,
-                   const long long* dq_tab, int dq_n, int dq_chunk, void* stream) {
+int dsv_sparse_bwd_convert(const void* q, const void* k, const void* v, const void* out,
+                           const void* dout, const float* lse, const int* grp_rows,
+                           const int* grp_size, const int* idx, long long ldk, const int* kcount,
+                           const int* kcount_hg, int H, int G, int Lq, int Lk, int D, float scale,
+                           void* dq, float* dk_acc, float* dv_acc, unsigned* work,
+                           const int* tile_grp, int n_groups, const long long* dq_tab, int dq_n,
+                           int dq_chunk, void* dkdv_out, const long long* dk_tab,
+                           const long long* dv_tab, int kv_n, int kv_chunk, int* conv_ws,
+                           void* stream) {
   if (D != 64 && D != 128) return fail(DSV_EUNSUPPORTED, "sparse_bwd: head dim %d not 64/128", D);
+  if (conv_ws) {
+    if (!dkdv_out && !(dk_tab && dv_tab))
+      return fail(DSV_EINVAL, "sparse_bwd: conversion needs dkdv_out or both row tables");
+    if (dkdv_out && !al16(dkdv_out)) return fail(DSV_EINVAL, "sparse_bwd: dkdv_out must be 16-byte aligned");
+    if (!dkdv_out && (kv_n < 1 || kv_chunk < 1 || (long long)kv_n * kv_chunk < Lk))
+      return fail(DSV_EINVAL, "sparse_bwd: dk/dv tables need n * chunk >= Lk");
+  }
   if (dq_tab && (dq_n < 1 || dq_chunk < 1 || (long long)dq_n * dq_chunk < Lq))
     return fail(DSV_EINVAL, "sparse_bwd: dq_tab needs n * chunk >= Lq");
   if (tile_grp && n_groups <= 0) return fail(DSV_EINVAL, "sparse_bwd: tile_grp needs n_groups > 0");
@@ -354,8 +365,21 @@ int dsv_sparse_bwd(const void* q, const void* k, const void* v, const void* out,
                                             kcount, kcount_hg, H, G, Lq, Lk, D, scale, scale_log2,
                                             dq, dk_acc, dv_acc, work, tile_grp,
                                             tile_grp ? n_groups : G, dq_tab, dq_n, dq_chunk,
+                                            dkdv_out, dk_tab, dv_tab, kv_n, kv_chunk, conv_ws,
                                             S(stream)),
                      "sparse_bwd launch");
+}
+
+int dsv_sparse_bwd(const void* q, const void* k, const void* v, const void* out,
+                   const void* dout, const float* lse, const int* grp_rows, const int* grp_size,
+                   const int* idx, long long ldk, const int* kcount, const int* kcount_hg, int H,
+                   int G, int Lq, int Lk, int D, float scale, void* dq, float* dk_acc,
+                   float* dv_acc, unsigned* work, const int* tile_grp, int n_groups,
+                   const long long* dq_tab, int dq_n, int dq_chunk, void* stream) {
+  return dsv_sparse_bwd_convert(q, k, v, out, dout, lse, grp_rows, grp_size, idx, ldk, kcount,
+                                kcount_hg, H, G, Lq, Lk, D, scale, dq, dk_acc, dv_acc, work,
+                                tile_grp, n_groups, dq_tab, dq_n, dq_chunk, nullptr, nullptr,
+                                nullptr, 0, 0, nullptr, stream);
 }
 
 int dsv_rows_fwd(const void* q, const void* k, const void* v, const long long* ptr,

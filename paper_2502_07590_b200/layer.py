@@ -185,6 +185,21 @@ class DSVAttentionLayer:
         else:
             dk_acc.zero_()
             dv_acc.zero_()
+        if os.environ.get("DSV_BWD_CONVERT", "1") != "0":
+            # the backward kernel converts dK / dV to bf16 itself, in its tail (CTAs that run
+            # out of tiles convert the heads already finished); DSV_BWD_CONVERT=0: separately
+            dkdv = None
+            if dkdv_rows is None:
+                dkdv = torch.empty((2, self.H, k.shape[1], self.D), device=k.device,
+                                   dtype=torch.bfloat16)
+            dq, _, _ = ops.sparse_bwd(q, k, v, out, dout, lse, self.grp_rows, self.grp_size,
+                                      sel.idx, sel.kcount, self.scale, dk_acc, dv_acc,
+                                      tile_grp=self.tile_grp, dq_rows=dq_rows, dkdv_out=dkdv,
+                                      dkdv_rows=dkdv_rows)
+            if kernel_done is not None:
+                kernel_done.record()
+            dq = None if dq_rows is not None else dq
+            return (dq, None, None) if dkdv is None else (dq, dkdv[0], dkdv[1])
         dq, dk32, dv32 = ops.sparse_bwd(q, k, v, out, dout, lse, self.grp_rows, self.grp_size,
                                         sel.idx, sel.kcount, self.scale, dk_acc, dv_acc,
                                         tile_grp=self.tile_grp, dq_rows=dq_rows)

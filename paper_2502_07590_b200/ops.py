@@ -262,8 +262,13 @@ def _rows_args(rows):
 
 
 def sparse_bwd(q, k, v, out, dout, lse, grp_rows, grp_size, idx, kcount, scale=None,
-               dk_acc=None, dv_acc=None, kcount_hg=None, tile_grp=None, dq_rows=None):
-    """Backward of sparse_fwd. Returns (dq bf16, dk_acc fp32, dv_acc fp32)."""
+               dk_acc=None, dv_acc=None, kcount_hg=None, tile_grp=None, dq_rows=None,
+               dkdv_out=None, dkdv_rows=None):
+    """Backward of sparse_fwd. Returns (dq bf16, dk_acc fp32, dv_acc fp32).
+
+    dkdv_out (bf16 [2, H, Lk, D]) or dkdv_rows ((tab, n, chunk) for dK and for dV): the
+    kernel also converts the accumulators to bf16 there in its tail
+    (dsv_sparse_bwd_convert)."""
     _require_cuda(q, k, v, out, dout, lse)
     H, Lq, D = q.shape
     Lk = k.shape[1]
@@ -276,11 +281,29 @@ def sparse_bwd(q, k, v, out, dout, lse, grp_rows, grp_size, idx, kcount, scale=N
     if dv_acc is None:
         dv_acc = torch.zeros((H, Lk, D), device=q.device, dtype=torch.float32)
     work = torch.empty((4,), device=q.device, dtype=torch.int32)
-    _lib.call("dsv_sparse_bwd", _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(dout), _ptr(lse),
-              _ptr(grp_rows), _ptr(grp_size), _ptr(idx), idx.stride(1), _ptr(kcount),
-              _ptr(kcount_hg), H, G, Lq, Lk, D, float(scale), _ptr(dq), _ptr(dk_acc), _ptr(dv_acc),
-              _ptr(work), _ptr(tile_grp), 0 if tile_grp is None else idx.shape[1],
-              *_rows_args(dq_rows), _stream())
+    if dkdv_out is None and dkdv_rows is None:
+        _lib.call("dsv_sparse_bwd", _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(dout), _ptr(lse),
+                  _ptr(grp_rows), _ptr(grp_size), _ptr(idx), idx.stride(1), _ptr(kcount),
+                  _ptr(kcount_hg), H, G, Lq, Lk, D, float(scale), _ptr(dq), _ptr(dk_acc),
+                  _ptr(dv_acc), _ptr(work), _ptr(tile_grp), 0 if tile_grp is None else idx.shape[1],
+                  *_rows_args(dq_rows), _stream())
+        return dq, dk_acc, dv_acc
+    if dkdv_out is not None:
+        _require_cuda(dkdv_out)
+        if (dkdv_out.dtype != torch.bfloat16 or dkdv_out.shape != (2, H, Lk, D)
+                or not dkdv_out.is_contiguous()):
+            raise ValueError("sparse_bwd: dkdv_out must be a contiguous bf16 [2, H, Lk, D] tensor")
+        ktab, vtab, kv_n, kv_chunk = 0, 0, 0, 0
+    else:
+        ktab, kv_n, kv_chunk = _rows_args(dkdv_rows[0])
+        vtab = _rows_args(dkdv_rows[1])[0]
+    conv = torch.empty((H + 1,), device=q.device, dtype=torch.int32)
+    _lib.call("dsv_sparse_bwd_convert", _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(dout),
+              _ptr(lse), _ptr(grp_rows), _ptr(grp_size), _ptr(idx), idx.stride(1), _ptr(kcount),
+              _ptr(kcount_hg), H, G, Lq, Lk, D, float(scale), _ptr(dq), _ptr(dk_acc),
+              _ptr(dv_acc), _ptr(work), _ptr(tile_grp), 0 if tile_grp is None else idx.shape[1],
+              *_rows_args(dq_rows), _ptr(dkdv_out), ktab, vtab, kv_n, kv_chunk, _ptr(conv),
+              _stream())
     return dq, dk_acc, dv_acc
 
 
