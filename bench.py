@@ -338,8 +338,10 @@ def run_gpu(args) -> None:
                 ev[3].record()
             return res
         # project, proxy gather, (scores gemm + topk | fused select: main + finish + list-mode
-        # re-run launch), fwd (persistent + list-mode re-run), bwd, 2x f32->bf16
-        launches_per_step = 10 if layer.fused_select() else 9
+        # re-run launch), fwd (persistent + list-mode re-run), bwd (+ 2x f32->bf16 unless the
+        # backward converts in its tail)
+        launches_per_step = (8 if layer.fused_select() else 7) + (
+            0 if os.environ.get("DSV_BWD_CONVERT", "1") != "0" else 2)
         work = layer.work()
     else:
         from paper_2502_07590_b200.cp import HeadParallelDSV, HybridDSV

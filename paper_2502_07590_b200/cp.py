@@ -1005,14 +1005,14 @@ class HeadParallelDSV(_PhaseMarks):
         return (out_local, *grads)
 
     def launches_per_step(self) -> int:
-        """Kernels one peer-transport step launches: projection, barrier + Q_lr/K_lr copy +
-        barrier, the Q/K/V/dO copy (overlapped: Q/K/V and dO copies, each with a side-stream
-        barrier), proxy gather,
-        selection (fused: main + finish + list-mode re-run; unfused: scores GEMM + top-k),
-        forward (+ list-mode re-run), backward, then with fused outputs two dK/dV converts and
-        a barrier (else the convert pair, then barrier + copy + barrier)."""
+        """Kernels one peer-transport step launches: projection; barrier, one copy of all
+        inputs, barrier (overlapped: barrier, Q_lr/K_lr copy, barrier, plus on the side stream
+        the Q/K/V and dO copies with a barrier each); proxy gather; selection (fused: main +
+        finish + list-mode re-run; unfused: scores GEMM + top-k); forward (+ list-mode re-run);
+        backward (converting dK/dV in its tail, or two separate converts); then with fused
+        outputs a barrier (else barrier + copy + barrier)."""
         n = 1 + 3 + (4 if self.overlap_in else 0) + 1 + (3 if self.local.fused_select() else 2)
-        n += 2 + 1 + 2
+        n += 2 + 1 + (0 if os.environ.get("DSV_BWD_CONVERT", "1") != "0" else 2)
         return n + (1 if self.fused_out else 3)
 
     def _step_peer(self, x_local, wt, q, k, v, dout):
