@@ -30,7 +30,9 @@ def main(which):
     q, kk, v, do = (torch.randn((H, L, D), device=dev, generator=g).to(torch.bfloat16) for _ in range(4))
     rows, size = plan.tables(dev)
     o, lse = ops.sparse_fwd(q, kk, v, rows, size, idx, kp)
-    ops.sparse_bwd(q, kk, v, o, do, lse, rows, size, idx, kp)
+    # as the layer runs it: dK / dV converted to bf16 in the kernel's tail
+    dkdv = torch.empty((2, H, L, D), device=dev, dtype=torch.bfloat16)
+    ops.sparse_bwd(q, kk, v, o, do, lse, rows, size, idx, kp, dkdv_out=dkdv)
     torch.cuda.synchronize()
     print("ok")
 
