@@ -329,3 +329,27 @@ def test_layer_backward_accumulators_zeroed_by_forward_or_itself(cuda):
     for x1, x2, x3 in zip(a, b, c):
         assert _rel_l2(x2.float().cpu().numpy(), x1.float().cpu().numpy()) < 1e-3
         assert _rel_l2(x3.float().cpu().numpy(), x1.float().cpu().numpy()) < 1e-3
+
+
+@pytest.mark.parametrize("D", [128, 64])
+def test_backward_tail_conversion_equals_separate_pass(cuda, D):
+    # the backward's tail conversion (dsv_sparse_bwd_convert: per-head completion counters,
+    # CTAs out of tiles convert finished heads) must give the bits of the separate fp32 ->
+    # bf16 pass over the same accumulators — at 512 tiles on 148 persistent CTAs, so heads
+    # finish while other CTAs are still on earlier ones
+    H, k = 4, 1024
+    plan = build_groups(TokenGrid(16, 16, 32), (8, 4, 4))
+    L, G = plan.grid.size, plan.n_groups
+    g = torch.Generator(device="cpu").manual_seed(33 + D)
+    idx = torch.stack([torch.randperm(L, generator=g)[:k].sort().values for _ in range(H * G)])
+    idx = idx.to(torch.int32).reshape(H, G, k).to(cuda)
+    q, kk, v, do = (torch.randn((H, L, D), generator=g).to(torch.bfloat16).to(cuda) for _ in range(4))
+    rows, size = plan.tables(cuda)
+    kc = torch.full((H,), k, dtype=torch.int32, device=cuda)
+    out, lse = ops.sparse_fwd(q, kk, v, rows, size, idx, kc)
+    dkdv = torch.empty((2, H, L, D), device=cuda, dtype=torch.bfloat16)
+    dq1, dk32, dv32 = ops.sparse_bwd(q, kk, v, out, do, lse, rows, size, idx, kc, dkdv_out=dkdv)
+    torch.cuda.synchronize()
+    assert torch.equal(dkdv[0], ops.f32_to_bf16(dk32)) and torch.equal(dkdv[1], ops.f32_to_bf16(dv32))
+    dq2, _, _ = ops.sparse_bwd(q, kk, v, out, do, lse, rows, size, idx, kc)
+    assert torch.equal(dq1, dq2)
