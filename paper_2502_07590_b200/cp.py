@@ -229,11 +229,29 @@ class HeadParallelExchange:
 
 
 class _CudaArray:
-    """Minimal __cuda_array_interface__ view of raw device memory (int16 elements)."""
+    """Minimal __cuda_array_interface__ view of raw device memory (int16 elements). `owner`
+    is kept alive as long as any tensor made from this view (torch holds the interface object
+    until the tensor's storage is released)."""
 
-    def __init__(self, ptr: int, n: int):
+    def __init__(self, ptr: int, n: int, owner=None):
+        self._owner = owner
         self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i2", "data": (ptr, False),
                                          "version": 3, "strides": None}
+
+
+class _PeerAlloc:
+    """This rank's dsv_peer_alloc buffer; freed (after the device is idle) when the last
+    tensor view of it is gone — step() results are views of it and may outlive the layer."""
+
+    def __init__(self, ptr: int, device):
+        self.ptr, self.device = ptr, device
+
+    def __del__(self):
+        try:
+            torch.cuda.synchronize(self.device)
+            _lib.load().dsv_peer_free(self.ptr)
+        except Exception:
+            pass
 
 
 class _PeerBuffer:
@@ -262,14 +280,19 @@ class _PeerBuffer:
                 self.ptrs.append(int(p.value))
                 self._opened.append(int(p.value))
         self._own = int(ptr.value)
-        self.tensor = torch.as_tensor(_CudaArray(self._own, nbytes // 2), device=device).view(torch.bfloat16)
+        self._device = torch.device(device)
+        alloc = _PeerAlloc(self._own, self._device)
+        self.tensor = torch.as_tensor(_CudaArray(self._own, nbytes // 2, owner=alloc),
+                                      device=device).view(torch.bfloat16)
 
     def __del__(self):
+        # kernels already queued may still read or write the peers' buffers: unmap them only
+        # once the device is idle (the own buffer goes with its last tensor view)
         try:
+            torch.cuda.synchronize(self._device)
             for p in self._opened:
                 _lib.load().dsv_peer_close(p)
             self.tensor = None
-            _lib.load().dsv_peer_free(self._own)
         except Exception:
             pass
 

@@ -108,3 +108,27 @@ def test_measured_sparsity_drives_the_head_plan(cuda, pg):
     out = cp.step(x, wt, q, k, v, do)
     torch.cuda.synchronize()
     assert all(torch.isfinite(t.float()).all() for t in out)
+
+
+@pytest.mark.parametrize("overlap,fused_out,convert", [("0", "1", "1"), ("1", "0", "1"),
+                                                       ("1", "1", "0")])
+def test_head_parallel_peer_variants_world1(cuda, pg, monkeypatch, overlap, fused_out, convert):
+    # the peer transport's switches — input exchange under the selection / forward
+    # (DSV_OVERLAP_IN), outputs stored by the kernels' epilogues (DSV_FUSED_OUT), dK/dV
+    # converted in the backward's tail (DSV_BWD_CONVERT) — each turned off against the default
+    from paper_2502_07590_b200.cp import HeadParallelDSV
+
+    grid, H, D, r = TokenGrid(8, 16, 16), 4, 128, 16
+    sp = np.array([0.5, 0.75, 0.9, 0.95])
+    x, wt, q, k, v, do = _inputs(grid, H, D, r, cuda, seed=3)
+    base = [t.clone() for t in HeadParallelDSV(grid, H, D, r, (8, 4, 4), sp, device=cuda,
+                                               transport="peer").step(x, wt, q, k, v, do)]
+    monkeypatch.setenv("DSV_OVERLAP_IN", overlap)
+    monkeypatch.setenv("DSV_FUSED_OUT", fused_out)
+    monkeypatch.setenv("DSV_BWD_CONVERT", convert)
+    cp = HeadParallelDSV(grid, H, D, r, (8, 4, 4), sp, device=cuda, transport="peer")
+    got = [t.clone() for t in cp.step(x, wt, q, k, v, do)]
+    torch.cuda.synchronize()
+    assert torch.equal(got[0], base[0]) and torch.equal(got[1], base[1])
+    for a, b in zip(got[2:], base[2:]):
+        assert _rel(a, b) <= 1e-5                    # dK / dV: fp32 atomic order only
