@@ -456,10 +456,12 @@ class PeerExchange:
         memory (kept alive with the table), so a step can be captured in a CUDA graph.
         stream: the stream that will read the table (default: the current one); the upload
         is ordered on it and the allocator told, so an evicted table is not reused while
-        that stream may still read it."""
+        that stream may still read it. A captured graph keeps using its tables' addresses, so
+        the cache drops tables only after 64 distinct input-pointer sets (a double-buffered
+        host pipeline uses a handful)."""
         t = self._tables.get(key)
         if t is None:
-            if len(self._tables) >= 16:
+            if len(self._tables) >= 64:
                 self._tables.clear()
             host = torch.from_numpy(build()).pin_memory()
             st = stream or torch.cuda.current_stream(self.buf.device)
@@ -554,7 +556,7 @@ class PeerExchange:
     def _host_table(self, key, build):
         t = self._tables.get(key)
         if t is None:
-            if len(self._tables) >= 16:
+            if len(self._tables) >= 64:
                 self._tables.clear()
             t = build()
             self._tables[key] = t
