@@ -980,6 +980,10 @@ class HeadParallelDSV(_PhaseMarks):
             self.ex = HeadParallelExchange(heads, grid.size, self.assignment, group)
         self.H, self.D, self.r = heads, head_dim, d_lr
         mine = self.ex.my_heads
+        if len(mine) == 0:
+            # cpmodel.solve_hybrid's rule: with fewer heads than ranks use g_s > 1 (HybridDSV)
+            raise ValueError(f"head-parallel CP over {self.world} ranks left rank {dist.get_rank(group)} "
+                             f"without heads ({heads} heads): use HybridDSV with g_s > 1")
         self.local = DSVAttentionLayer(grid, len(mine), head_dim, d_lr, voxel, sp[mine], device)
         # peer transport: Q / K / V / dO exchanged under the selection (DSV_OVERLAP_IN=0: after)
         self.overlap_in = transport == "peer" and os.environ.get("DSV_OVERLAP_IN", "1") != "0"
