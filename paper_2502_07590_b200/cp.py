@@ -964,6 +964,11 @@ class HeadParallelDSV(_PhaseMarks):
         self.world = dist.get_world_size(group)
         sp = np.broadcast_to(np.asarray(sparsity, dtype=np.float64), (heads,)).copy()
         self.assignment = plan_heads(sp, grid.size, head_dim, self.world, balanced)
+        if np.bincount(self.assignment, minlength=self.world).min() == 0:
+            # every rank sees the same plan, so all of them raise (no rank left in a collective);
+            # cpmodel.solve_hybrid's rule: fewer heads than ranks needs g_s > 1 (HybridDSV)
+            raise ValueError(f"head-parallel CP: {heads} heads leave a rank of {self.world} without "
+                             "heads; use HybridDSV with g_s > 1")
         if transport == "auto":
             transport = "peer" if torch.device(device).type == "cuda" else "all_to_all"
         if transport not in ("peer", "all_to_all"):
@@ -980,10 +985,6 @@ class HeadParallelDSV(_PhaseMarks):
             self.ex = HeadParallelExchange(heads, grid.size, self.assignment, group)
         self.H, self.D, self.r = heads, head_dim, d_lr
         mine = self.ex.my_heads
-        if len(mine) == 0:
-            # cpmodel.solve_hybrid's rule: with fewer heads than ranks use g_s > 1 (HybridDSV)
-            raise ValueError(f"head-parallel CP over {self.world} ranks left rank {dist.get_rank(group)} "
-                             f"without heads ({heads} heads): use HybridDSV with g_s > 1")
         self.local = DSVAttentionLayer(grid, len(mine), head_dim, d_lr, voxel, sp[mine], device)
         # peer transport: Q / K / V / dO exchanged under the selection (DSV_OVERLAP_IN=0: after)
         self.overlap_in = transport == "peer" and os.environ.get("DSV_OVERLAP_IN", "1") != "0"
