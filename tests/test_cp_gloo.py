@@ -123,3 +123,35 @@ def test_plan_heads_from_measured_profile():
     assert max(loads[assign == r].sum() for r in range(4)) <= max(loads[naive == r].sum() for r in range(4))
     with pytest.raises(ValueError):
         plan_heads_from_profile(prof, 7, 4096, 64, 4)
+
+
+def _worker_no_heads(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2502_07590_b200.cp import HeadParallelDSV
+        from paper_2502_07590_b200.grid import TokenGrid
+
+        try:
+            HeadParallelDSV(TokenGrid(8, 4, 4), 1, 64, 16, (8, 4, 4), 0.9, device="cpu",
+                            transport="all_to_all")
+            q.put((rank, "no error"))
+        except ValueError as e:
+            q.put((rank, "ValueError" if "HybridDSV" in str(e) else repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_head_parallel_fewer_heads_than_ranks_raises_on_every_rank():
+    # one head over two ranks: both raise before any collective (none is left waiting)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_no_heads, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    results = dict(q.get(timeout=5) for _ in range(2))
+    assert results == {0: "ValueError", 1: "ValueError"}, results
