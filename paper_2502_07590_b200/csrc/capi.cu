@@ -238,8 +238,8 @@ extern "C" int dsv_select_fused_max_clusters(int S) {
 }
 
 static int select_split(int H, int G, int L, int split) {
-  // key-range split per 128-row tile (a cluster of `split` CTAs): fewest waves per unit of
-  // per-CTA work, at least one 128-key tile per CTA. Waves count the clusters that can be
+  // key-range split per 128-row tile (a cluster of `split` CTAs, 1..6): fewest waves per
+  // unit of per-CTA work, at least one 128-key tile per CTA. Waves count the clusters that can be
   // resident at once (a cluster fits in one GPC; measured: 36 4-CTA clusters at c2 with 12
   // heads took two waves, 0.40 ms against 0.375 at S = 2); ties keep the smaller split
   // (fewer cross-CTA merges)
@@ -249,7 +249,7 @@ static int select_split(int H, int G, int L, int split) {
     int sms = dsv_device_sm_count();
     if (sms <= 0) sms = 148;        // no device visible: size for a B200
     double best = 1e30;
-    for (int s = 1; s <= 4 && s <= nt; ++s) {
+    for (int s = 1; s <= 6 && s <= nt; ++s) {
       const int mc = dsv_select_fused_max_clusters(s);
       const int per_wave = mc > 0 ? mc : sms / s;
       const double cost = (double)((n_mt + per_wave - 1) / per_wave) / s;

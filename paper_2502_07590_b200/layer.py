@@ -138,11 +138,12 @@ class DSVAttentionLayer:
 
     def fused_select(self) -> bool:
         """Fused K1b + K2 (select_fused.cu; r <= 16) where it measured faster than scores
-        GEMM + top-k (tools/select_bench.py on one B200, single-pass mode): with >= 32 row
-        tiles of 128 proxies (c2, 24 heads: 0.46 vs 0.87 ms; 12 heads: 0.43 vs 0.48 ms), or
-        >= 16 tiles at L >= 65536 (L = 131072, 2 heads: 0.89 vs 1.24 ms). Fewer tiles leave
-        the fused kernel's sample passes and cluster merges exposed (c2, 6 heads: 0.275 vs
-        0.271 ms; 3 heads: 0.26 vs 0.18 ms). DSV_FUSED_SELECT=1 / 0 forces either path."""
+        GEMM + top-k (tools/select_bench.py on one B200, single-pass mode, occupancy-sized
+        key-range split): from 32 row tiles of 128 proxies (c2: 24 heads 0.47 vs 0.87 ms, 12
+        heads 0.34 vs 0.48), or 16 at L >= 65536 (L = 131072, 2 heads: 0.73 vs 1.24 ms). With
+        fewer tiles the fused kernel's sample passes and cluster merges are exposed (c2, 6
+        heads: 0.28 vs 0.28 ms alone, and 2.12 vs 2.09 ms per 4-GPU step; 3 heads: 0.26 vs
+        0.17 ms). DSV_FUSED_SELECT=1 / 0 forces either path."""
         if self.r > 16:
             return False
         env = os.environ.get("DSV_FUSED_SELECT", "auto")

@@ -17,12 +17,12 @@ def main():
     lib = _lib.load()
     print("max resident clusters per split:",
           {s: lib.dsv_select_fused_max_clusters(s) for s in range(1, 9)}, flush=True)
-    for H in (24, 12, 6, 3):
+    for H in (24, 12, 6, 3, 2, 1):
         g = torch.Generator(device="cuda").manual_seed(0)
         qp = torch.randn((H, G, 16), device=dev, generator=g).to(torch.bfloat16)
         klr = torch.randn((H, L, 16), device=dev, generator=g).to(torch.bfloat16)
         kp = torch.full((H,), k, dtype=torch.int32, device=dev)
-        for sp in (0, 1, 2, 3, 4, 8):
+        for sp in (0, 2, 3, 4, 5, 6, 7, 8):
             for _ in range(2):
                 ops.select_fused(qp, klr, kp, k, split=sp, mode="fast")
             ts = []
