@@ -13,24 +13,30 @@
 // [H, G, ldk] ascending, k per head int32 [H]; LSE fp32 [H, L] in the log2
 // domain of the scaled logits (lse2 = max + log2(sum)).
 //
-// Both kernels run one CTA per (head, group), head-major so the K/V of the two
-// or three heads in flight stay L2-resident. Gather producers issue 16-byte
-// cp.async copies of the selected K/V rows straight into 128B-swizzled UMMA tiles
-// (measured on B200: ~50 B/clk/SM for random 256 B rows, vs ~8 for TMA
-// tile::gather4). Forward, 800 threads: warps 0-15 softmax (4 warps per TMEM lane
-// quarter, one 32-key slice each), warp 16 tcgen05.mma issuer + TMEM owner, warps
-// 17-24 producers (K ring 2-deep, V ring 3-deep, three S/P buffers in TMEM).
-// Backward, 864 threads: warps 0-15 row workers (4 per TMEM lane quarter), warp 16
-// MMA issuer, warps 17-18 producers, warps 19-26 dK/dV scatter.
-// Forward: S_j = Q K_j^T into one of two TMEM S buffers; softmax workers take
-// the row max in a first TMEM pass, write P (bf16) over S in a second, rescale
-// O in TMEM only when the max grows by > 2^8; O += P_{j-1} V_{j-1} reads P from
-// TMEM (A operand) and V from shared memory (MN-major B).
-// Backward (transposed, keys in TMEM lanes): S^T = K_j Q^T, dP^T = V_j dO^T;
-// workers (one key per thread) form P^T, dS^T in TMEM and dS in smem; then
-// dQ += dS K_j, dV_j = P^T dO, dK_j = dS^T Q; dV_j / dK_j rows are staged
-// through shared memory and scatter-added with row-contiguous red.v4 (coalesced:
-// 2x the L2 reduction rate of row-per-thread atomics) by dedicated warps.
+// Both kernels are persistent: one CTA per SM draws 128-query tiles (a voxel group, or a
+// 128-query slice of a larger ladder group sharing its index row) from a global atomic
+// counter in head-major order, so the K/V of the one or two heads in flight stay
+// L2-resident; every role keeps running block counters for its barrier parities, so the
+// next tile's loads and first MMAs overlap the current tile's tail. Gather producers issue
+// 16-byte cp.async copies of the selected K/V rows straight into 128B-swizzled UMMA tiles
+// (measured on B200: ~50 B/clk/SM for random 256 B rows, vs ~8 for TMA tile::gather4).
+// Forward, 800 threads: warps 0-15 softmax (4 per TMEM lane quarter, one 32-key slice
+// each), warp 16 tcgen05.mma issuer + TMEM owner, warps 17-24 producers (K ring and V ring
+// 3 deep each, three S/P buffers in TMEM, S issued three blocks ahead). The row max is
+// exchanged for key block 0 only (lazy max: later blocks exponentiate against it, a tile
+// whose scores exceed it by 2^64 is flagged and re-run with the per-block exchange); P
+// (bf16) overwrites the warp's own S columns; O += P V reads P from TMEM (A operand) and
+// V from shared memory (MN-major B); the producers also zero the backward's dK/dV
+// accumulators for this tile's share.
+// Backward, 864 threads: warps 0-15 row workers (4 per TMEM lane quarter), warp 16 MMA
+// issuer, warps 17-18 producers, warps 19-26 dK/dV scatter. Transposed (keys in TMEM
+// lanes): S^T = K_j Q^T, dP^T = V_j dO^T; workers (one key per thread) form P^T, dS^T in
+// TMEM and dS in smem; then dQ += dS K_j, dV_j = P^T dO, dK_j = dS^T Q; dV_j / dK_j rows
+// are staged through shared memory and scatter-added with row-contiguous red.v4 (the fp32
+// L2 reduction rate bounds the kernel). Once the tile queue is exhausted the CTAs convert
+// the finished heads' dK/dV accumulators to bf16 (per-head completion counters).
+// Optional row-address tables send O / dQ / dK / dV rows to their token owners' peer
+// buffers (head-parallel CP) from the same epilogue stores.
 
 #include <cuda.h>
 #include "dsv_common.cuh"
