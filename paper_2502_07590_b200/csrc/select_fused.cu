@@ -17,8 +17,9 @@
 // resident — and each pass touches only TMEM, registers and shared memory.
 //
 // CTA = one 128-row tile of one head's proxy rows x a contiguous key range; a cluster
-// of S CTAs splits the key range of one row tile (S chosen so the grid fills the SMs;
-// per-pass partials are combined through distributed shared memory). Warp 0: TMA
+// of S CTAs splits the key range of one row tile (S = 1..6, the fewest waves of resident
+// clusters per unit of per-CTA work; per-pass partials are combined through distributed
+// shared memory). Warp 0: TMA
 // producer (B ring), warp 1: MMA issuer (4 TMEM accumulators x 128 columns), warps 2..:
 // epilogue, each TMEM lane quadrant covered by kEpiWarps/4 warps that split a tile's
 // 128 columns. Per row, passes over the key range (all rows advance together):
@@ -30,6 +31,11 @@
 //   EMIT: bit masks (s > T) and (s == T) per 32 columns staged in shared memory, then a
 //       warp per row emits ascending column indices, ties at T in column order up to the
 //       row's quota (ties resolve toward lower indices), coalesced per row.
+// Single-pass mode (a workspace is given; the default): after the sample passes, ONE
+// COLLECT pass writes per row a bitmap of the keys at or above the band and stashes the
+// band entries (column, order key); select_finish_kernel (a CTA per row) finds T among
+// the band by radix select and emits from the bitmap; row tiles whose band missed T are
+// re-run with the passes above (list mode).
 // Scores are compared as floats: with the order key f2key (-0.0 == +0.0, monotone) every
 // band edge is converted to the float with that key (the one key without a float, the
 // image of -0.0, is handled explicitly). Columns past L are NaN (no comparison holds).
