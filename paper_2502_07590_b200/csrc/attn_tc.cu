@@ -643,6 +643,8 @@ constexpr int kBwdScatWarp0 = kBwdLoadWarp0 + kBwdLoadWarps;
 #define DSV_BWD_SCAT_WARPS 8
 #endif
 constexpr int kBwdScatWarps = DSV_BWD_SCAT_WARPS;
+static_assert(kBwdWork % 4 == 0 && 128 % kBwdScatWarps == 0,
+              "worker warps: a multiple of 4 (TMEM lane quarters); scatter warps divide 128 rows");
 constexpr int kBwdScatThreads = kBwdScatWarps * 32;
 constexpr int kBwdThreads = (kBwdScatWarp0 + kBwdScatWarps) * 32;   // 864 by default
 
@@ -1044,7 +1046,7 @@ sparse_bwd_kernel(const __nv_bfloat16* __restrict__ Qg, const __nv_bfloat16* __r
     __nv_bfloat16* qrow = dqremote.tab ? row_out<D>(dqremote, h, tok)   // the token owner
                                        : dQ + ((long long)h * Lq + tok) * D;
 #pragma unroll 1
-    for (int c = cg; c < D / 32; c += 4) {
+    for (int c = cg; c < D / 32; c += kBwdWPQ) {
       uint32_t r[32];
       tmem_ld32(tDq + lane_off + c * 32, r);
       tmem_ld_wait();
