@@ -87,6 +87,8 @@ constexpr int kFwdSBufs = 3;                                     // S/P buffers 
 #define DSV_FWD_SOFT_WGS 4
 #endif
 constexpr int kFwdSoftWGs = DSV_FWD_SOFT_WGS;                    // warps 0-15
+// each softmax warp owns one 32-key slice of a 128-key block per TMEM lane quarter
+static_assert(kFwdSoftWGs * 32 == BKV, "forward: four softmax warpgroups (32-key slices)");
 constexpr int kFwdSoftThreads = kFwdSoftWGs * 128;
 constexpr int kFwdMmaWarp = kFwdSoftWGs * 4;
 constexpr int kFwdProdWarp0 = kFwdMmaWarp + 1;
