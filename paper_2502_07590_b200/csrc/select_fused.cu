@@ -64,6 +64,8 @@ constexpr int kAcc = 4;                       // TMEM accumulators (4 x 128 colu
 constexpr int kEpiWarps = DSV_FSEL_EPI_WARPS;
 constexpr int kParts = kEpiWarps / 4;         // threads per row
 constexpr int kCols = BN / kParts;            // columns per thread per tile
+static_assert(kEpiWarps == 4 || kEpiWarps == 8 || kEpiWarps == 16,
+              "epilogue warps: 1, 2 or 4 per TMEM lane quadrant (32-column multiples, part_above)");
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kThreads = 64 + kEpiThreads;
 constexpr int kBuckets = 128;
