@@ -17,6 +17,11 @@
  *   dsv_sparse_fwd       attention.py:153-187  sparse_attention (uniform/group-shared sets)
  *                        grouping.py:196-216   grouped_sparse_attention
  *   dsv_sparse_bwd       trainer.py:110-117    autograd of the sparse attention (dQ, dK, dV)
+ *   dsv_sparse_bwd_convert  the same, dK / dV also converted to the caller's dtype (bf16)
+ *                        in the kernel's tail (trainer.py:110-117 returns them in it)
+ *   dsv_select_fused     grouping.py:184-193 + selection.py:118-175 proxy scores and exact
+ *                        top-k fused (no score matrix); dsv_select_fused_workspace_size /
+ *                        dsv_select_fused_max_clusters size its workspace and key split
  *   dsv_rows_fwd/_bwd    attention.py:176-183  ragged per-query index sets (CSR)
  *   dsv_gather_rows      cpsim.py:147-156/195-216 pack/unpack of head slices and KV rows
  *   dsv_pred_pass        predictor.py:103-194 (predictor training step: row statistics and the
@@ -25,7 +30,12 @@
  *   dsv_critical_counts  profiler.py:48-79 + attention.py:118-140 (sampled sparsity profiler:
  *                        critical-KV prefix length per scored row)
  *   dsv_copy_jobs        cpsim.py:147-156/284-299 HCP head exchange written straight into
- *                        the owners' buffers (peer pointers over NVLink)
+ *                        the owners' buffers (peer pointers over NVLink); _threads: the
+ *                        same with 128-thread blocks (runs beside a persistent kernel)
+ *   dsv_peer_*           cpsim.py:125-161/284-299 transport: CUDA-IPC peer buffers and the
+ *                        device barrier that orders each exchange phase
+ *   dsv_scp_pull/_push   cpsim.py:164-216 selective_comm_scp (critical rows pulled from the
+ *                        owners; their gradients added back)
  *   dsv_ring_*           ring KV pass for dense residual heads under SCP (no reference
  *                        counterpart; dense semantics of attention.py:95-109)
  * Reference-precision (fp64) path for host fp64/fp32 callers (validate.py:10-25 computes in
